@@ -1,0 +1,138 @@
+/*
+ * spanpipe — C ABI of the B200-native span-forward hot path of
+ * Petals / swarmpipe (arXiv 2312.08361).
+ *
+ * Plain pointers and sizes only; device pointers are CUDA device addresses
+ * on the span's device, `stream` is a cudaStream_t (NULL = legacy stream).
+ * Every call returns SP_OK (0) or a negative SP_ERR_* code; sp_last_error()
+ * returns the message of the most recent failure on the calling thread.
+ *
+ * Reference interfaces replaced (SP/ = /root/reference/pkg/src/swarmpipe/):
+ *   sp_quantize_blockwise    <- quantize_hidden        SP/quantize.py:36-49
+ *   sp_dequantize_blockwise  <- dequantize_hidden      SP/quantize.py:52-58
+ *   sp_weights_generate      <- _uniform_weights       SP/model.py:55-60
+ *   sp_span_create           <- RealServerEngine.__init__ / init_model
+ *                                                      SP/server.py:80-82, SP/model.py:178-199
+ *   sp_kv_create             <- RealServerEngine.make_caches  SP/server.py:84-85
+ *   sp_kv_length             <- RealServerEngine.cache_length SP/server.py:87-91
+ *   sp_span_forward          <- RealServerEngine.run_cached   SP/server.py:93-100
+ *                               (block_forward_batched + KVCache.append,
+ *                                SP/model.py:244-280, :163-167)
+ *   sp_span_forward_stateless<- RealServerEngine.forward      SP/server.py:106-125
+ *   sp_kv_reorder            <- RealServerEngine.reorder / KVCache.gather
+ *                                                      SP/server.py:102-104, SP/model.py:169-175
+ *   sp_kv_read               <- KVCache.keys / .values views (test access,
+ *                                T/test_server.py:173-178)
+ *   sp_fnv1a64               <- fnv1a64 / RealServerEngine.blob_checksum
+ *                                SP/wire.py:39-44, SP/server.py:141-142
+ */
+#ifndef SPANPIPE_H_
+#define SPANPIPE_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SP_OK 0
+#define SP_ERR_ARG (-1)
+#define SP_ERR_CUDA (-2)
+#define SP_ERR_CAPACITY (-3)
+#define SP_ERR_STATE (-4)
+#define SP_ERR_OOM (-5)
+
+/* model families / dtypes (paper_2312_08361_b200/config.py) */
+#define SP_FAMILY_TOY 0
+#define SP_FAMILY_LLAMA 1
+#define SP_FAMILY_BLOOM 2
+#define SP_W_F32 0
+#define SP_W_BF16 1
+#define SP_W_I8 2
+#define SP_KV_F32 0
+#define SP_KV_BF16 1
+
+typedef struct sp_config {
+  int32_t n_blocks;
+  int32_t hidden_dim;
+  int32_t n_heads;
+  int32_t n_kv_heads;
+  int32_t ffn_dim;
+  int32_t vocab_size;
+  int32_t max_seq_len;
+  int32_t family;
+  int32_t weight_dtype;
+  int32_t kv_dtype;
+  uint64_t seed;
+  double rope_theta;
+} sp_config;
+
+typedef struct sp_span sp_span; /* weights + KV pool of blocks [start, end) on one device */
+typedef struct sp_kv sp_kv;     /* one session's paged attention caches over the span */
+
+const char* sp_last_error(void);
+int sp_version(void);
+
+/* ---- hidden-state codec (bit-exact with SP/quantize.py) ---------------- */
+/* n elements of x (f32) -> codes int8 [n], scales f32 [ceil(n/64)] */
+int sp_quantize_blockwise(const float* x, int8_t* codes, float* scales, int64_t n, void* stream);
+int sp_dequantize_blockwise(const int8_t* codes, const float* scales, float* x, int64_t n,
+                            void* stream);
+
+/* ---- deterministic weights (bit-exact with SP/model.py:55-60) ----------- */
+/* dst[i] = element i of the row-major [d_in, d_out] tensor of (seed, block, role_id) */
+int sp_weights_generate(uint64_t seed, int32_t block, int32_t role_id, int64_t n_elements,
+                        double scale, float* dst, void* stream);
+/* splitmix64 stream seed of (seed, block, role_id) — SP/model.py:49-52 */
+uint64_t sp_stream_seed(uint64_t seed, int32_t block, int32_t role_id);
+
+/* ---- span lifecycle ----------------------------------------------------- */
+/* kv_pool_tokens: KV capacity of the span's page pool, in positions
+ * (summed over all sessions and beam slots). */
+int sp_span_create(const sp_config* cfg, int32_t start, int32_t end, int32_t device,
+                   int64_t kv_pool_tokens, sp_span** out);
+int sp_span_destroy(sp_span* span);
+int64_t sp_span_weight_bytes(const sp_span* span);
+int64_t sp_span_free_pages(const sp_span* span);
+/* copy block `block`'s matrix `role_id` back as f32 [d_in, d_out] (effective
+ * values: bf16/int8 dequantised) — test access only */
+int sp_span_read_weight(sp_span* span, int32_t block, int32_t role_id, float* dst_host);
+
+/* ---- sessions ------------------------------------------------------------ */
+int sp_kv_create(sp_span* span, int32_t width, sp_kv** out);
+int sp_kv_destroy(sp_kv* kv);
+int32_t sp_kv_length(const sp_kv* kv);
+int32_t sp_kv_width(const sp_kv* kv);
+/* new slot i <- old slot parents0[i]; new width = new_width (pages are shared
+ * copy-on-write; only a shared partial tail page is copied) */
+int sp_kv_reorder(sp_kv* kv, const int32_t* parents0, int32_t new_width, void* stream);
+/* keys/values of one block (absolute block id) and slot, as f32
+ * [length, n_kv_heads, head_dim] into host memory */
+int sp_kv_read(sp_kv* kv, int32_t block, int32_t slot, float* keys_host, float* values_host);
+
+/* ---- the hot path ----------------------------------------------------------
+ * x: device f32 [width * n_new, hidden] (rows ordered slot-major), or NULL when
+ * x_codes/x_scales carry the int8 codec form (dequantised in-kernel);
+ * y: device f32 [width * n_new, hidden]; if y_codes != NULL the output is also
+ * quantised (SP/server.py:100 with quantized=True) into y_codes/y_scales.
+ * Appends n_new positions per slot to kv. */
+int sp_span_forward(sp_span* span, sp_kv* kv, int32_t block_begin, int32_t block_end,
+                    const float* x, const int8_t* x_codes, const float* x_scales, float* y,
+                    int8_t* y_codes, float* y_scales, int32_t width, int32_t n_new,
+                    void* stream);
+/* stateless causal forward of `batch` independent sequences of `tokens`
+ * (no cache kept), SP/server.py:106-125.  If record != NULL it receives the
+ * input of every block: f32 [block_end - block_begin][batch * tokens][hidden]
+ * (the `record` list of SP/server.py:113-121). */
+int sp_span_forward_stateless(sp_span* span, int32_t block_begin, int32_t block_end,
+                              const float* x, float* y, float* record, int32_t batch,
+                              int32_t tokens, void* stream);
+
+/* FNV-1a 64 over host bytes — SP/wire.py:39-44 (relay checksums,
+ * SP/server.py:141-142); host-side helper */
+uint64_t sp_fnv1a64(const uint8_t* data, int64_t n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPANPIPE_H_ */

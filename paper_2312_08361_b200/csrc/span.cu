@@ -1,0 +1,616 @@
+// Span runtime: weights, paged KV pool, sessions and the per-block kernel
+// schedule of RealServerEngine.run_cached (SP/server.py:93-100).
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace {
+thread_local std::string g_err;
+}
+
+void sp_set_error(const char* file, int line, const char* msg) {
+  char buf[512];
+  snprintf(buf, sizeof(buf), "%s:%d: %s", file, line, msg);
+  g_err = buf;
+}
+
+#define SP_FAIL(code, msg)                     \
+  do {                                         \
+    sp_set_error(__FILE__, __LINE__, (msg));   \
+    return (code);                             \
+  } while (0)
+
+#define SP_CHECK_LAUNCH() SP_CUDA_TRY(cudaGetLastError())
+
+using namespace sp;
+
+namespace {
+
+constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ull;
+constexpr uint64_t kRoleMix = 0xC2B2AE3D27D4EB4Full;
+
+enum Role { R_WQ = 1, R_WK = 2, R_WV = 3, R_WO = 4, R_W1 = 5, R_W2 = 6, R_W3 = 13 };
+
+struct BlockW {
+  void* qkv; float* s_qkv;
+  void* o; float* s_o;
+  void* up; float* s_up;      // llama: gate/up interleaved [2F]; else w1 [F]
+  void* down; float* s_down;
+  float *ln1_g, *ln1_b, *ln2_g, *ln2_b;
+};
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+}  // namespace
+
+struct sp_span {
+  sp_config cfg;
+  int start, end, device;
+  int d, H, kvh, hd, F, kv;
+  int64_t n_qkv, n_up;
+  int64_t weight_bytes = 0;
+  char* wmem = nullptr;
+  std::vector<BlockW> blocks;
+  float* rope_cos = nullptr;
+  float* rope_sin = nullptr;
+  float* alibi = nullptr;
+  // KV pool
+  char* pool = nullptr;
+  int64_t n_pages = 0;
+  int64_t page_bytes = 0;        // one page, one block: 2*kvh*64*hd*elt
+  int64_t block_stride = 0;      // bytes per block pool
+  std::vector<int> refcount;
+  std::vector<int> free_pages;
+  int max_pages = 0;
+  // scratch
+  int64_t cap_rows = 0;
+  float *h = nullptr, *qkvb = nullptr, *ctx = nullptr, *mlp = nullptr, *mlp_raw = nullptr;
+  float* gemv_ws = nullptr;
+  int* gemv_cnt = nullptr;
+  int64_t attn_ws_floats = 0;
+  float* attn_ws = nullptr;
+  std::mutex mu;
+};
+
+struct sp_kv {
+  sp_span* span;
+  int width;
+  int length;
+  std::vector<std::vector<int>> pages;
+  int* d_table = nullptr;
+  int table_cap_width = 0;
+  std::vector<int> h_table;
+};
+
+namespace {
+
+uint64_t stream_seed(uint64_t seed, int block, int role) {
+  uint64_t key = seed ^ ((uint64_t)(block + 1) * kGolden) ^ ((uint64_t)role * kRoleMix);
+  return splitmix64_at(key, 0);
+}
+
+int wdtype_ktile(int wd) { return wd == kI8 ? 32 : 16; }
+
+int elt_bytes(int wd) { return wd == kF32 ? 4 : (wd == kBF16 ? 2 : 1); }
+
+int validate(const sp_config* c) {
+  if (c->n_blocks < 1 || c->hidden_dim < 1 || c->n_heads < 1) return SP_ERR_ARG;
+  if (c->hidden_dim % c->n_heads) return SP_ERR_ARG;
+  int kvh = c->n_kv_heads ? c->n_kv_heads : c->n_heads;
+  if (c->n_heads % kvh) return SP_ERR_ARG;
+  int hd = c->hidden_dim / c->n_heads;
+  if (!(hd == 4 || hd == 16 || hd == 32 || hd == 64 || hd == 128)) return SP_ERR_ARG;
+  int F = c->ffn_dim ? c->ffn_dim : 4 * c->hidden_dim;
+  int d = c->hidden_dim, kv = kvh * hd;
+  if (c->weight_dtype != kF32) {
+    int kt = wdtype_ktile(c->weight_dtype) * 8;
+    if (d % kt || F % kt) return SP_ERR_ARG;
+    if ((d + 2 * kv) % 32 || d % 32 || F % 32) return SP_ERR_ARG;
+  } else {
+    if (d % 16 || F % 16 || kv % 16) return SP_ERR_ARG;
+  }
+  return SP_OK;
+}
+
+int ensure_scratch(sp_span* s, int64_t rows) {
+  if (rows <= s->cap_rows) return SP_OK;
+  int64_t cap = rows < 64 ? 64 : rows;
+  cudaFree(s->h); cudaFree(s->qkvb); cudaFree(s->ctx); cudaFree(s->mlp); cudaFree(s->mlp_raw);
+  s->h = s->qkvb = s->ctx = s->mlp = s->mlp_raw = nullptr;
+  int64_t wmax = s->d > s->F ? s->d : s->F;
+  SP_CUDA_TRY(cudaMalloc(&s->h, cap * wmax * sizeof(float)));
+  SP_CUDA_TRY(cudaMalloc(&s->qkvb, cap * s->n_qkv * sizeof(float)));
+  SP_CUDA_TRY(cudaMalloc(&s->ctx, cap * s->d * sizeof(float)));
+  SP_CUDA_TRY(cudaMalloc(&s->mlp, cap * s->F * sizeof(float)));
+  SP_CUDA_TRY(cudaMalloc(&s->mlp_raw, cap * s->n_up * sizeof(float)));
+  s->cap_rows = cap;
+  return SP_OK;
+}
+
+int ensure_attn_ws(sp_span* s, int width) {
+  int64_t need = attn_workspace_floats(width, s->H, s->hd, s->cfg.max_seq_len);
+  if (need <= s->attn_ws_floats) return SP_OK;
+  cudaFree(s->attn_ws);
+  SP_CUDA_TRY(cudaMalloc(&s->attn_ws, need * sizeof(float)));
+  s->attn_ws_floats = need;
+  return SP_OK;
+}
+
+int alloc_page(sp_span* s) {
+  if (s->free_pages.empty()) return -1;
+  int p = s->free_pages.back();
+  s->free_pages.pop_back();
+  s->refcount[p] = 1;
+  return p;
+}
+
+void release_page(sp_span* s, int p) {
+  if (--s->refcount[p] == 0) s->free_pages.push_back(p);
+}
+
+int upload_table(sp_kv* kv, cudaStream_t st) {
+  sp_span* s = kv->span;
+  if (kv->table_cap_width < kv->width) {
+    cudaFree(kv->d_table);
+    kv->d_table = nullptr;
+    SP_CUDA_TRY(cudaMalloc(&kv->d_table, (size_t)kv->width * s->max_pages * sizeof(int)));
+    kv->table_cap_width = kv->width;
+  }
+  kv->h_table.assign((size_t)kv->width * s->max_pages, 0);
+  for (int i = 0; i < kv->width; ++i)
+    for (size_t p = 0; p < kv->pages[i].size(); ++p)
+      kv->h_table[(size_t)i * s->max_pages + p] = kv->pages[i][p];
+  SP_CUDA_TRY(cudaMemcpyAsync(kv->d_table, kv->h_table.data(), kv->h_table.size() * sizeof(int),
+                              cudaMemcpyHostToDevice, st));
+  SP_CUDA_TRY(cudaStreamSynchronize(st));
+  return SP_OK;
+}
+
+// make pages for positions [length, length + n_new) writable for every slot
+int prepare_pages(sp_kv* kv, int n_new, cudaStream_t st) {
+  sp_span* s = kv->span;
+  bool changed = false;
+  for (int i = 0; i < kv->width; ++i) {
+    auto& pg = kv->pages[i];
+    if (kv->length % kPageTokens && !pg.empty()) {
+      int tail = pg.back();
+      if (s->refcount[tail] > 1) {  // copy-on-write of a shared partial tail page
+        int np = alloc_page(s);
+        if (np < 0) SP_FAIL(SP_ERR_CAPACITY, "KV page pool exhausted");
+        launch_page_copy(s->pool, s->block_stride, s->end - s->start, s->page_bytes, tail, np,
+                         st);
+        SP_CHECK_LAUNCH();
+        release_page(s, tail);
+        pg.back() = np;
+        changed = true;
+      }
+    }
+    int need = (kv->length + n_new + kPageTokens - 1) / kPageTokens;
+    while ((int)pg.size() < need) {
+      int np = alloc_page(s);
+      if (np < 0) SP_FAIL(SP_ERR_CAPACITY, "KV page pool exhausted");
+      pg.push_back(np);
+      changed = true;
+    }
+  }
+  if (changed) return upload_table(kv, st);
+  return SP_OK;
+}
+
+void linear(sp_span* s, int wd, void* w, float* sc, int64_t N, int64_t K, const float* x,
+            float* y, int64_t ldy, const float* res, int epi, int64_t R, bool decode,
+            cudaStream_t st) {
+  LinearArgs a{};
+  a.w = w; a.wscale = sc; a.wdtype = wd; a.N = N; a.K = K;
+  a.x = x; a.ldx = K; a.y = y; a.ldy = ldy; a.res = res; a.epi = epi; a.R = (int)R;
+  a.workspace = s->gemv_ws; a.counters = s->gemv_cnt;
+  if (decode) {
+    launch_gemv(a, st);
+  } else if (epi == EPI_SWIGLU) {
+    a.epi = EPI_STORE;
+    a.y = s->mlp_raw;
+    a.ldy = N;
+    launch_gemm(a, st);
+    launch_swiglu_rows(s->mlp_raw, y, R, N / 2, st);
+  } else {
+    launch_gemm(a, st);
+  }
+}
+
+int run_span(sp_span* s, sp_kv* kv, int b0, int b1, float* y, float* record, int width,
+             int n_new, cudaStream_t st) {
+  const int64_t R = (int64_t)width * n_new;
+  const bool decode = (n_new == 1);
+  const int wd = s->cfg.weight_dtype;
+  const int fam = s->cfg.family;
+  int rc = ensure_scratch(s, R);
+  if (rc) return rc;
+  rc = ensure_attn_ws(s, width);
+  if (rc) return rc;
+  AttnArgs at{};
+  at.family = fam; at.kv_dtype = s->cfg.kv_dtype;
+  at.width = width; at.n_new = n_new; at.t0 = kv->length;
+  at.H = s->H; at.kvh = s->kvh; at.hd = s->hd;
+  at.qkv = s->qkvb; at.ldqkv = s->n_qkv;
+  at.page_table = kv->d_table; at.max_pages = s->max_pages;
+  at.rope_cos = s->rope_cos; at.rope_sin = s->rope_sin; at.alibi = s->alibi;
+  at.ctx = s->ctx; at.workspace = s->attn_ws;
+  const int64_t d = s->d, F = s->F;
+  for (int b = b0 - s->start; b < b1 - s->start; ++b) {
+    BlockW& W = s->blocks[b];
+    at.kv_pool = s->pool + (int64_t)b * s->block_stride;
+    if (record)
+      SP_CUDA_TRY(cudaMemcpyAsync(record + (int64_t)(b - (b0 - s->start)) * R * d, y,
+                                  R * d * sizeof(float), cudaMemcpyDeviceToDevice, st));
+    launch_norm(fam, y, W.ln1_g, W.ln1_b, s->h, R, d, st);
+    linear(s, wd, W.qkv, W.s_qkv, s->n_qkv, d, s->h, s->qkvb, s->n_qkv, nullptr, EPI_STORE, R,
+           decode, st);
+    launch_rope_append(at, st);
+    if (decode) launch_attention_decode(at, st);
+    else launch_attention_prefill(at, st);
+    linear(s, wd, W.o, W.s_o, d, d, s->ctx, y, d, y, EPI_RESID, R, decode, st);
+    launch_norm(fam, y, W.ln2_g, W.ln2_b, s->h, R, d, st);
+    if (fam == kLlama)
+      linear(s, wd, W.up, W.s_up, s->n_up, d, s->h, s->mlp, F, nullptr, EPI_SWIGLU, R, decode,
+             st);
+    else
+      linear(s, wd, W.up, W.s_up, s->n_up, d, s->h, s->mlp, F, nullptr, EPI_GELU, R, decode, st);
+    linear(s, wd, W.down, W.s_down, d, F, s->mlp, y, d, y, EPI_RESID, R, decode, st);
+  }
+  SP_CHECK_LAUNCH();
+  return SP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sp_last_error(void) { return g_err.c_str(); }
+int sp_version(void) { return 1; }
+
+uint64_t sp_stream_seed(uint64_t seed, int32_t block, int32_t role_id) {
+  return stream_seed(seed, block, role_id);
+}
+
+int sp_quantize_blockwise(const float* x, int8_t* codes, float* scales, int64_t n,
+                          void* stream) {
+  if (n < 0) SP_FAIL(SP_ERR_ARG, "negative length");
+  launch_quantize(x, codes, scales, n, (cudaStream_t)stream);
+  SP_CHECK_LAUNCH();
+  return SP_OK;
+}
+
+int sp_dequantize_blockwise(const int8_t* codes, const float* scales, float* x, int64_t n,
+                            void* stream) {
+  if (n < 0) SP_FAIL(SP_ERR_ARG, "negative length");
+  launch_dequantize(codes, scales, x, n, (cudaStream_t)stream);
+  SP_CHECK_LAUNCH();
+  return SP_OK;
+}
+
+int sp_weights_generate(uint64_t seed, int32_t block, int32_t role_id, int64_t n_elements,
+                        double scale, float* dst, void* stream) {
+  launch_gen_stream(stream_seed(seed, block, role_id), n_elements, scale, dst,
+                    (cudaStream_t)stream);
+  SP_CHECK_LAUNCH();
+  return SP_OK;
+}
+
+int sp_span_create(const sp_config* cfg, int32_t start, int32_t end, int32_t device,
+                   int64_t kv_pool_tokens, sp_span** out) {
+  if (!cfg || !out) SP_FAIL(SP_ERR_ARG, "null argument");
+  if (validate(cfg) != SP_OK) SP_FAIL(SP_ERR_ARG, "unsupported config shape");
+  if (!(0 <= start && start < end && end <= cfg->n_blocks)) SP_FAIL(SP_ERR_ARG, "bad span");
+  SP_CUDA_TRY(cudaSetDevice(device));
+  sp_span* s = new sp_span();
+  s->cfg = *cfg;
+  s->start = start; s->end = end; s->device = device;
+  s->d = cfg->hidden_dim; s->H = cfg->n_heads;
+  s->kvh = cfg->n_kv_heads ? cfg->n_kv_heads : cfg->n_heads;
+  s->hd = s->d / s->H;
+  s->F = cfg->ffn_dim ? cfg->ffn_dim : 4 * s->d;
+  s->kv = s->kvh * s->hd;
+  s->n_qkv = s->d + 2 * s->kv;
+  s->n_up = cfg->family == kLlama ? 2 * (int64_t)s->F : s->F;
+  const int wd = cfg->weight_dtype;
+  const int64_t eb = elt_bytes(wd);
+  const int nb = end - start;
+  const int64_t d = s->d, F = s->F;
+
+  // ---- weights: one allocation per span ----
+  auto mat_bytes = [&](int64_t N, int64_t K) { return align_up((size_t)(N * K * eb), 256); };
+  auto sc_bytes = [&](int64_t N) { return wd == kI8 ? align_up((size_t)N * 4, 256) : 0; };
+  size_t per_block = mat_bytes(s->n_qkv, d) + sc_bytes(s->n_qkv) + mat_bytes(d, d) + sc_bytes(d) +
+                     mat_bytes(s->n_up, d) + sc_bytes(s->n_up) + mat_bytes(d, F) + sc_bytes(d) +
+                     4 * align_up((size_t)d * 4, 256);
+  s->weight_bytes = (int64_t)per_block * nb;
+  cudaError_t e = cudaMalloc(&s->wmem, s->weight_bytes);
+  if (e != cudaSuccess) {
+    delete s;
+    SP_FAIL(SP_ERR_OOM, "weight allocation failed");
+  }
+  cudaStream_t st = 0;
+  const double scale = 1.0 / std::sqrt((double)d);   // SP/model.py:181
+  std::vector<float> ones(d, 1.0f);
+  char* p = s->wmem;
+  for (int b = start; b < end; ++b) {
+    BlockW W{};
+    auto take = [&](size_t bytes) { char* r = p; p += bytes; return (void*)r; };
+    W.qkv = take(mat_bytes(s->n_qkv, d)); W.s_qkv = (float*)take(sc_bytes(s->n_qkv));
+    W.o = take(mat_bytes(d, d)); W.s_o = (float*)take(sc_bytes(d));
+    W.up = take(mat_bytes(s->n_up, d)); W.s_up = (float*)take(sc_bytes(s->n_up));
+    W.down = take(mat_bytes(d, F)); W.s_down = (float*)take(sc_bytes(d));
+    W.ln1_g = (float*)take(align_up(d * 4, 256)); W.ln1_b = (float*)take(align_up(d * 4, 256));
+    W.ln2_g = (float*)take(align_up(d * 4, 256)); W.ln2_b = (float*)take(align_up(d * 4, 256));
+    uint64_t seed = cfg->seed;
+    launch_gen_matrix(wd, stream_seed(seed, b, R_WQ), d, d, scale, MatPlace{0, 1, 0}, W.qkv, W.s_qkv, st);
+    launch_gen_matrix(wd, stream_seed(seed, b, R_WK), d, s->kv, scale, MatPlace{d, 1, 0}, W.qkv, W.s_qkv, st);
+    launch_gen_matrix(wd, stream_seed(seed, b, R_WV), d, s->kv, scale, MatPlace{d + s->kv, 1, 0}, W.qkv, W.s_qkv, st);
+    launch_gen_matrix(wd, stream_seed(seed, b, R_WO), d, d, scale, MatPlace{0, 1, 0}, W.o, W.s_o, st);
+    if (cfg->family == kLlama) {
+      launch_gen_matrix(wd, stream_seed(seed, b, R_W1), d, F, scale, MatPlace{0, 2, 0}, W.up, W.s_up, st);
+      launch_gen_matrix(wd, stream_seed(seed, b, R_W3), d, F, scale, MatPlace{0, 2, 1}, W.up, W.s_up, st);
+    } else {
+      launch_gen_matrix(wd, stream_seed(seed, b, R_W1), d, F, scale, MatPlace{0, 1, 0}, W.up, W.s_up, st);
+    }
+    launch_gen_matrix(wd, stream_seed(seed, b, R_W2), F, d, scale, MatPlace{0, 1, 0}, W.down, W.s_down, st);
+    SP_CUDA_TRY(cudaMemcpy(W.ln1_g, ones.data(), d * 4, cudaMemcpyHostToDevice));
+    SP_CUDA_TRY(cudaMemcpy(W.ln2_g, ones.data(), d * 4, cudaMemcpyHostToDevice));
+    SP_CUDA_TRY(cudaMemset(W.ln1_b, 0, d * 4));
+    SP_CUDA_TRY(cudaMemset(W.ln2_b, 0, d * 4));
+    s->blocks.push_back(W);
+  }
+  SP_CHECK_LAUNCH();
+
+  // ---- constant tables ----
+  if (cfg->family == kLlama) {
+    int half = s->hd / 2;
+    std::vector<float> c((size_t)cfg->max_seq_len * half), sn((size_t)cfg->max_seq_len * half);
+    for (int pos = 0; pos < cfg->max_seq_len; ++pos)
+      for (int j = 0; j < half; ++j) {
+        double inv = std::pow(cfg->rope_theta, -((double)(2 * j) / (double)s->hd));
+        double ang = (double)pos * inv;
+        c[(size_t)pos * half + j] = (float)std::cos(ang);
+        sn[(size_t)pos * half + j] = (float)std::sin(ang);
+      }
+    SP_CUDA_TRY(cudaMalloc(&s->rope_cos, c.size() * 4));
+    SP_CUDA_TRY(cudaMalloc(&s->rope_sin, sn.size() * 4));
+    SP_CUDA_TRY(cudaMemcpy(s->rope_cos, c.data(), c.size() * 4, cudaMemcpyHostToDevice));
+    SP_CUDA_TRY(cudaMemcpy(s->rope_sin, sn.data(), sn.size() * 4, cudaMemcpyHostToDevice));
+  }
+  if (cfg->family == kBloom) {
+    int n = s->H;
+    auto pow2 = [](int m) {
+      std::vector<double> v;
+      double start = std::pow(2.0, -std::pow(2.0, -(std::log2((double)m) - 3)));
+      for (int i = 0; i < m; ++i) v.push_back(start * std::pow(start, i));
+      return v;
+    };
+    int p2 = 1;
+    while (p2 * 2 <= n) p2 *= 2;
+    std::vector<double> sl = pow2(p2);
+    if (p2 < n) {
+      std::vector<double> ex = pow2(2 * p2);
+      for (int i = 0; i < n - p2; ++i) sl.push_back(ex[2 * i]);
+    }
+    std::vector<float> f(sl.begin(), sl.end());
+    SP_CUDA_TRY(cudaMalloc(&s->alibi, f.size() * 4));
+    SP_CUDA_TRY(cudaMemcpy(s->alibi, f.data(), f.size() * 4, cudaMemcpyHostToDevice));
+  }
+
+  // ---- KV pool ----
+  const int kvel = cfg->kv_dtype == kKVBF16 ? 2 : 4;
+  s->page_bytes = (int64_t)2 * s->kvh * kPageTokens * s->hd * kvel;
+  s->n_pages = (kv_pool_tokens + kPageTokens - 1) / kPageTokens;
+  if (s->n_pages < 1) s->n_pages = 1;
+  s->block_stride = s->n_pages * s->page_bytes;
+  s->max_pages = (cfg->max_seq_len + kPageTokens - 1) / kPageTokens;
+  e = cudaMalloc(&s->pool, (size_t)s->block_stride * nb);
+  if (e != cudaSuccess) {
+    sp_span_destroy(s);
+    SP_FAIL(SP_ERR_OOM, "KV pool allocation failed");
+  }
+  s->refcount.assign(s->n_pages, 0);
+  for (int64_t i = s->n_pages - 1; i >= 0; --i) s->free_pages.push_back((int)i);
+
+  // ---- split-K workspace for the decode GEMVs ----
+  if (wd != kF32) {
+    int64_t ws = 0, cnt = 0;
+    int64_t shapes[4][2] = {{s->n_qkv, d}, {d, d}, {s->n_up, d}, {d, F}};
+    for (auto& sh : shapes) {
+      int64_t w = gemv_workspace_floats(sh[0], sh[1], wd);
+      ws = w > ws ? w : ws;
+      int64_t c = gemv_counter_ints(sh[0]);
+      cnt = c > cnt ? c : cnt;
+    }
+    SP_CUDA_TRY(cudaMalloc(&s->gemv_ws, (ws + 1) * sizeof(float)));
+    SP_CUDA_TRY(cudaMalloc(&s->gemv_cnt, cnt * sizeof(int)));
+    SP_CUDA_TRY(cudaMemset(s->gemv_cnt, 0, cnt * sizeof(int)));
+  }
+  SP_CUDA_TRY(cudaDeviceSynchronize());
+  *out = s;
+  return SP_OK;
+}
+
+int sp_span_destroy(sp_span* s) {
+  if (!s) return SP_OK;
+  cudaSetDevice(s->device);
+  cudaFree(s->wmem); cudaFree(s->rope_cos); cudaFree(s->rope_sin); cudaFree(s->alibi);
+  cudaFree(s->pool); cudaFree(s->h); cudaFree(s->qkvb); cudaFree(s->ctx); cudaFree(s->mlp);
+  cudaFree(s->mlp_raw); cudaFree(s->gemv_ws); cudaFree(s->gemv_cnt); cudaFree(s->attn_ws);
+  delete s;
+  return SP_OK;
+}
+
+int64_t sp_span_weight_bytes(const sp_span* s) { return s ? s->weight_bytes : 0; }
+int64_t sp_span_free_pages(const sp_span* s) { return s ? (int64_t)s->free_pages.size() : 0; }
+
+int sp_span_read_weight(sp_span* s, int32_t block, int32_t role, float* dst_host) {
+  if (!s || block < s->start || block >= s->end) SP_FAIL(SP_ERR_ARG, "block outside span");
+  SP_CUDA_TRY(cudaSetDevice(s->device));
+  BlockW& W = s->blocks[block - s->start];
+  const int64_t d = s->d, F = s->F;
+  void* src = nullptr; float* sc = nullptr; int64_t K = 0, N = 0; MatPlace pl{0, 1, 0};
+  int64_t bufK = 0;
+  switch (role) {
+    case R_WQ: src = W.qkv; sc = W.s_qkv; K = d; N = d; pl = {0, 1, 0}; break;
+    case R_WK: src = W.qkv; sc = W.s_qkv; K = d; N = s->kv; pl = {d, 1, 0}; break;
+    case R_WV: src = W.qkv; sc = W.s_qkv; K = d; N = s->kv; pl = {d + s->kv, 1, 0}; break;
+    case R_WO: src = W.o; sc = W.s_o; K = d; N = d; break;
+    case R_W1: src = W.up; sc = W.s_up; K = d; N = F;
+      pl = (s->cfg.family == kLlama) ? MatPlace{0, 2, 0} : MatPlace{0, 1, 0}; break;
+    case R_W3: if (s->cfg.family != kLlama) SP_FAIL(SP_ERR_ARG, "no w3");
+      src = W.up; sc = W.s_up; K = d; N = F; pl = {0, 2, 1}; break;
+    case R_W2: src = W.down; sc = W.s_down; K = F; N = d; break;
+    default: SP_FAIL(SP_ERR_ARG, "unknown role");
+  }
+  (void)bufK;
+  float* tmp = nullptr;
+  SP_CUDA_TRY(cudaMalloc(&tmp, K * N * sizeof(float)));
+  launch_read_matrix(s->cfg.weight_dtype, src, sc, K, N, pl, tmp, 0);
+  SP_CHECK_LAUNCH();
+  SP_CUDA_TRY(cudaMemcpy(dst_host, tmp, K * N * sizeof(float), cudaMemcpyDeviceToHost));
+  cudaFree(tmp);
+  return SP_OK;
+}
+
+int sp_kv_create(sp_span* s, int32_t width, sp_kv** out) {
+  if (!s || !out || width < 1) SP_FAIL(SP_ERR_ARG, "bad kv args");
+  sp_kv* kv = new sp_kv();
+  kv->span = s;
+  kv->width = width;
+  kv->length = 0;
+  kv->pages.assign(width, {});
+  *out = kv;
+  return SP_OK;
+}
+
+int sp_kv_destroy(sp_kv* kv) {
+  if (!kv) return SP_OK;
+  sp_span* s = kv->span;
+  {
+    std::lock_guard<std::mutex> g(s->mu);
+    for (auto& pg : kv->pages)
+      for (int p : pg) release_page(s, p);
+  }
+  cudaSetDevice(s->device);
+  cudaFree(kv->d_table);
+  delete kv;
+  return SP_OK;
+}
+
+int32_t sp_kv_length(const sp_kv* kv) { return kv ? kv->length : -1; }
+int32_t sp_kv_width(const sp_kv* kv) { return kv ? kv->width : -1; }
+
+int sp_kv_reorder(sp_kv* kv, const int32_t* parents0, int32_t new_width, void* stream) {
+  if (!kv || new_width < 1) SP_FAIL(SP_ERR_ARG, "bad reorder args");
+  for (int i = 0; i < new_width; ++i)
+    if (parents0[i] < 0 || parents0[i] >= kv->width)
+      SP_FAIL(SP_ERR_ARG, "reorder index out of range");
+  sp_span* s = kv->span;
+  std::lock_guard<std::mutex> g(s->mu);
+  std::vector<std::vector<int>> np(new_width);
+  for (int i = 0; i < new_width; ++i) {
+    np[i] = kv->pages[parents0[i]];
+    for (int p : np[i]) s->refcount[p]++;
+  }
+  for (auto& pg : kv->pages)
+    for (int p : pg) release_page(s, p);
+  kv->pages.swap(np);
+  kv->width = new_width;
+  SP_CUDA_TRY(cudaSetDevice(s->device));
+  return upload_table(kv, (cudaStream_t)stream);
+}
+
+int sp_kv_read(sp_kv* kv, int32_t block, int32_t slot, float* keys_host, float* values_host) {
+  if (!kv) SP_FAIL(SP_ERR_ARG, "null kv");
+  sp_span* s = kv->span;
+  if (block < s->start || block >= s->end || slot < 0 || slot >= kv->width)
+    SP_FAIL(SP_ERR_ARG, "block/slot out of range");
+  block -= s->start;
+  SP_CUDA_TRY(cudaSetDevice(s->device));
+  int64_t n = (int64_t)kv->length * s->kvh * s->hd;
+  if (n == 0) return SP_OK;
+  float *k = nullptr, *v = nullptr;
+  SP_CUDA_TRY(cudaMalloc(&k, n * 4));
+  SP_CUDA_TRY(cudaMalloc(&v, n * 4));
+  launch_kv_gather_slot(s->pool + (int64_t)block * s->block_stride, s->cfg.kv_dtype,
+                        kv->d_table + (int64_t)slot * s->max_pages, kv->length, s->kvh, s->hd, k,
+                        v, 0);
+  SP_CHECK_LAUNCH();
+  SP_CUDA_TRY(cudaMemcpy(keys_host, k, n * 4, cudaMemcpyDeviceToHost));
+  SP_CUDA_TRY(cudaMemcpy(values_host, v, n * 4, cudaMemcpyDeviceToHost));
+  cudaFree(k);
+  cudaFree(v);
+  return SP_OK;
+}
+
+static int forward_impl(sp_span* s, sp_kv* kv, int32_t b0, int32_t b1, const float* x,
+                        const int8_t* x_codes, const float* x_scales, float* y, float* record,
+                        int8_t* y_codes, float* y_scales, int32_t width, int32_t n_new,
+                        void* stream) {
+  if (!s || !kv || !y) SP_FAIL(SP_ERR_ARG, "null argument");
+  if (!(s->start <= b0 && b0 < b1 && b1 <= s->end)) SP_FAIL(SP_ERR_ARG, "blocks outside span");
+  if (width != kv->width) SP_FAIL(SP_ERR_STATE, "width mismatch");
+  if (n_new < 1) SP_FAIL(SP_ERR_ARG, "n_new must be >= 1");
+  if (kv->length + n_new > s->cfg.max_seq_len) SP_FAIL(SP_ERR_CAPACITY, "exceeds max_seq_len");
+  cudaStream_t st = (cudaStream_t)stream;
+  SP_CUDA_TRY(cudaSetDevice(s->device));
+  std::lock_guard<std::mutex> g(s->mu);
+  int rc = prepare_pages(kv, n_new, st);
+  if (rc) return rc;
+  const int64_t n = (int64_t)width * n_new * s->d;
+  if (x_codes) {
+    launch_dequantize(x_codes, x_scales, y, n, st);
+  } else if (x != y) {
+    SP_CUDA_TRY(cudaMemcpyAsync(y, x, n * sizeof(float), cudaMemcpyDeviceToDevice, st));
+  }
+  rc = run_span(s, kv, b0, b1, y, record, width, n_new, st);
+  if (rc) return rc;
+  kv->length += n_new;
+  if (y_codes) launch_quantize(y, y_codes, y_scales, n, st);
+  SP_CHECK_LAUNCH();
+  return SP_OK;
+}
+
+int sp_span_forward(sp_span* s, sp_kv* kv, int32_t b0, int32_t b1, const float* x,
+                    const int8_t* x_codes, const float* x_scales, float* y, int8_t* y_codes,
+                    float* y_scales, int32_t width, int32_t n_new, void* stream) {
+  return forward_impl(s, kv, b0, b1, x, x_codes, x_scales, y, nullptr, y_codes, y_scales, width,
+                      n_new, stream);
+}
+
+int sp_span_forward_stateless(sp_span* s, int32_t b0, int32_t b1, const float* x, float* y,
+                              float* record, int32_t batch, int32_t tokens, void* stream) {
+  sp_kv* kv = nullptr;
+  int rc = sp_kv_create(s, batch, &kv);
+  if (rc) return rc;
+  rc = forward_impl(s, kv, b0, b1, x, nullptr, nullptr, y, record, nullptr, nullptr, batch,
+                    tokens, stream);
+  if (rc == SP_OK) {
+    cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+    if (e != cudaSuccess) {
+      sp_set_error(__FILE__, __LINE__, cudaGetErrorString(e));
+      rc = SP_ERR_CUDA;
+    }
+  }
+  sp_kv_destroy(kv);
+  return rc;
+}
+
+uint64_t sp_fnv1a64(const uint8_t* data, int64_t n) {
+  uint64_t h = 0xCBF29CE484222325ull;  // SP/wire.py:35-44
+  for (int64_t i = 0; i < n; ++i) {
+    h ^= data[i];
+    h *= 0x100000001B3ull;
+  }
+  return h;
+}
+
+}  // extern "C"

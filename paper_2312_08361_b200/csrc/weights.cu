@@ -1,0 +1,154 @@
+// Deterministic weight generation on the GPU, bit-identical to the reference
+// recipe (SP/model.py:40-60 splitmix64 streams, f64 affine map, f64->f32 RN),
+// plus the bf16 / int8 roundings defined in oracle/model.py:
+//   bf16: round-to-nearest-even of the f32 value
+//   int8: per output channel scale = f32(absmax/127), code = rint(w/scale)
+//         (the SP/quantize.py:43-47 arithmetic, one channel = one block)
+//
+// Reference orientation is x @ W with W [d_in = K, d_out = N] row-major, i.e.
+// element (k, n) is stream index k*N + n.  Storage here is output-major
+// [N][K] (row per output channel), f32 plain or bf16/int8 fragment-tiled.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace sp {
+
+__global__ void gen_stream_kernel(uint64_t stream, int64_t n, double scale, float* dst) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = uniform_value(stream, (uint64_t)i, scale);
+}
+
+// buffer row of output channel n for a matrix placed at `row0` with 16-row
+// tiles interleaved every `tstride` tiles at tile offset `toff`
+__device__ __forceinline__ int64_t buf_row(int64_t n, const MatPlace& p) {
+  return p.row0 + ((n >> 4) * p.tstride + p.toff) * 16 + (n & 15);
+}
+
+// f32 storage, row-major [rows][K]
+__global__ void gen_f32_rows_kernel(uint64_t stream, int64_t K, int64_t N, double scale,
+                                    MatPlace place, float* dst) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= K * N) return;
+  int64_t n = i / K, k = i % K;
+  dst[buf_row(n, place) * K + k] = uniform_value(stream, (uint64_t)(k * N + n), scale);
+}
+
+// int8 pass 1: per-output-channel absmax -> scale (warp per channel)
+__global__ void gen_i8_scales_kernel(uint64_t stream, int64_t K, int64_t N, double scale,
+                                     MatPlace place, float* scales) {
+  int64_t n = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  int lane = threadIdx.x & 31;
+  if (n >= N) return;
+  float m = 0.f;
+  for (int64_t k = lane; k < K; k += 32)
+    m = fmaxf(m, fabsf(uniform_value(stream, (uint64_t)(k * N + n), scale)));
+  m = warp_max(m);
+  if (lane == 0) scales[buf_row(n, place)] = __fdiv_rn(m, 127.0f);
+}
+
+// int8 pass 2: one thread writes one lane-chunk (16 B) of a 16x32 tile
+__global__ void gen_i8_pack_kernel(uint64_t stream, int64_t K, int64_t N, double scale,
+                                   MatPlace place, const float* __restrict__ scales,
+                                   uint8_t* dst) {
+  int64_t chunk = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // (rt, kt, lane)
+  int64_t KT = K >> 5;
+  int64_t total = (N >> 4) * KT * 32;
+  if (chunk >= total) return;
+  int lane = (int)(chunk & 31);
+  int64_t kt = (chunk >> 5) % KT;
+  int64_t rt = (chunk >> 5) / KT;
+  int g = lane >> 2, c = (lane & 3) * 2;
+  uint8_t out[16];
+#pragma unroll
+  for (int ks = 0; ks < 2; ++ks) {
+#pragma unroll
+    for (int p = 0; p < 8; ++p) {
+      int k8 = p >> 2, hi = (p >> 1) & 1, jj = p & 1;
+      int64_t n = rt * 16 + g + hi * 8;
+      int64_t k = kt * 32 + ks * 16 + k8 * 8 + c + jj;
+      float w = uniform_value(stream, (uint64_t)(k * N + n), scale);
+      float s = scales[buf_row(n, place)];
+      int q = (s > 0.f) ? __float2int_rn(__fdiv_rn(w, s)) : 0;
+      out[ks * 8 + p] = (uint8_t)(q + 128);
+    }
+  }
+  int64_t brt = (place.row0 >> 4) + rt * place.tstride + place.toff;  // buffer row tile
+  uint4* d = reinterpret_cast<uint4*>(dst + ((brt * KT + kt) << 9) + lane * 16);
+  *d = *reinterpret_cast<uint4*>(out);
+}
+
+// bf16: one thread writes one lane-chunk (16 B = 8 bf16) of a 16x16 tile
+__global__ void gen_bf16_pack_kernel(uint64_t stream, int64_t K, int64_t N, double scale,
+                                     MatPlace place, __nv_bfloat16* dst) {
+  int64_t chunk = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t KT = K >> 4;
+  int64_t total = (N >> 4) * KT * 32;
+  if (chunk >= total) return;
+  int lane = (int)(chunk & 31);
+  int64_t kt = (chunk >> 5) % KT;
+  int64_t rt = (chunk >> 5) / KT;
+  int g = lane >> 2, c = (lane & 3) * 2;
+  __align__(16) __nv_bfloat16 out[8];
+#pragma unroll
+  for (int p = 0; p < 8; ++p) {
+    int k8 = p >> 2, hi = (p >> 1) & 1, jj = p & 1;
+    int64_t n = rt * 16 + g + hi * 8;
+    int64_t k = kt * 16 + k8 * 8 + c + jj;
+    out[p] = __float2bfloat16_rn(uniform_value(stream, (uint64_t)(k * N + n), scale));
+  }
+  int64_t brt = (place.row0 >> 4) + rt * place.tstride + place.toff;
+  uint4* d = reinterpret_cast<uint4*>(dst + ((brt * KT + kt) << 8) + lane * 8);
+  *d = *reinterpret_cast<uint4*>(out);
+}
+
+void launch_gen_stream(uint64_t stream, int64_t n, double scale, float* dst, cudaStream_t st) {
+  if (n <= 0) return;
+  gen_stream_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(stream, n, scale, dst);
+}
+
+void launch_gen_matrix(int wdtype, uint64_t stream, int64_t K, int64_t N, double scale,
+                       MatPlace place, void* dst, float* scales, cudaStream_t st) {
+  if (wdtype == kF32) {
+    int64_t n = K * N;
+    gen_f32_rows_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(stream, K, N, scale, place,
+                                                                      (float*)dst);
+  } else if (wdtype == kBF16) {
+    int64_t chunks = (N / 16) * (K / 16) * 32;
+    gen_bf16_pack_kernel<<<(unsigned)((chunks + 255) / 256), 256, 0, st>>>(
+        stream, K, N, scale, place, (__nv_bfloat16*)dst);
+  } else {
+    gen_i8_scales_kernel<<<(unsigned)((N + 7) / 8), 256, 0, st>>>(stream, K, N, scale, place,
+                                                                   scales);
+    int64_t chunks = (N / 16) * (K / 32) * 32;
+    gen_i8_pack_kernel<<<(unsigned)((chunks + 255) / 256), 256, 0, st>>>(
+        stream, K, N, scale, place, scales, (uint8_t*)dst);
+  }
+}
+
+// read back: dst [K][N] f32 (reference orientation), effective values
+__global__ void read_matrix_kernel(int wdtype, const void* src, const float* scales, int64_t K,
+                                   int64_t N, int64_t bufK, MatPlace place, float* dst) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= K * N) return;
+  int64_t k = i / N, n = i % N;
+  int64_t r = buf_row(n, place);
+  float v;
+  if (wdtype == kF32) {
+    v = ((const float*)src)[r * bufK + k];
+  } else if (wdtype == kBF16) {
+    v = __bfloat162float(((const __nv_bfloat16*)src)[frag_offset_bf16(r, k, bufK)]);
+  } else {
+    int q = (int)((const uint8_t*)src)[frag_offset_i8(r, k, bufK)] - 128;
+    v = __fmul_rn((float)q, scales[r]);
+  }
+  dst[i] = v;
+}
+
+void launch_read_matrix(int wdtype, const void* src, const float* scales, int64_t K, int64_t N,
+                        MatPlace place, float* dst, cudaStream_t st) {
+  int64_t n = K * N;
+  read_matrix_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(wdtype, src, scales, K, N, K,
+                                                                   place, dst);
+}
+
+}  // namespace sp

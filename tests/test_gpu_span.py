@@ -1,0 +1,215 @@
+"""Span forward on the GPU vs the CPU oracle (and the reference's golden
+vectors) through the engine protocol of SP/server.py:77-142.
+
+Tolerances (written here):
+* toy family (f32 end to end): max-abs 1e-5 — the reference's own bound
+  (T/test_server.py:42-58, :123-136);
+* interleaving / micro-batching: array_equal (T/test_server.py:91-119, :247-255);
+* bf16/int8-weight Llama/BLOOM shapes: decode max-abs <= 2e-3 * max|y|
+  (f32-class hi/lo tensor-core GEMV), prefill <= 2e-2 * max|y| (f32 SIMT
+  GEMM with bf16 KV), measured against the oracle on the same rounded weights.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import model as om
+from paper_2312_08361_b200.config import SpanConfig, toy
+
+pytestmark = pytest.mark.gpu
+
+
+def _engine(cfg):
+    from paper_2312_08361_b200.engine import B200ServerEngine
+    return B200ServerEngine(cfg)
+
+
+def _blob(a, quantized=False):
+    from paper_2312_08361_b200.blob import HiddenBlob
+    return HiddenBlob.from_array(a, quantized)
+
+
+def test_toy_stack_matches_reference_golden(golden_toy):
+    """prefill 3 rows then 6 decode rows through all 8 blocks (reference run)."""
+    eng = _engine(toy(seed=1))
+    xs = golden_toy["default__stack_in"]
+    want = golden_toy["default__stack_out"]
+    caches = eng.make_caches(0, 8, 1)
+    outs = [eng.run_cached(0, 8, caches, _blob(xs[:3]), 1, 3, False).array()]
+    for i in range(3, 9):
+        outs.append(eng.run_cached(0, 8, caches, _blob(xs[i:i + 1]), 1, 1, False).array())
+    got = np.concatenate(outs)
+    assert eng.cache_length(caches) == 9
+    assert np.abs(got - want).max() < 1e-5
+
+
+def test_toy_greedy_tokens_match_reference(golden_toy):
+    """reference_generate(ModelConfig(seed=1), [3,1,4], 32) with the GPU span
+    and the oracle's tied head (client side stays on the host here)."""
+    cfg = toy(seed=1)
+    eng = _engine(cfg)
+    emb = golden_toy["default__embedding"]
+    caches = eng.make_caches(0, 8, 1)
+    toks = [3, 1, 4]
+    x = emb[toks]
+    for _ in range(32):
+        y = eng.run_cached(0, 8, caches, _blob(x), 1, x.shape[0], False).array()
+        t = om.greedy_pick(om.logits_for(emb, y[-1]))
+        toks.append(t)
+        x = emb[[t]]
+    assert toks == list(golden_toy["default__greedy32"])
+
+
+def test_five_steps_match_local_stage():
+    """T/test_server.py:42-58 on blocks [2, 5)."""
+    cfg = toy(seed=1)
+    eng = _engine(cfg)
+    rng = np.random.default_rng(0)
+    x_all = rng.standard_normal((5, 64)).astype(np.float32)
+    runner = om.SpanRunner(cfg, 2, 5)
+    caches = eng.make_caches(2, 5, 1)
+    for i in range(5):
+        got = eng.run_cached(2, 5, caches, _blob(x_all[i:i + 1]), 1, 1, False).array()
+        want = runner.step(x_all[i:i + 1][None])[0]
+        assert np.abs(got - want).max() < 1e-5
+    assert eng.cache_length(caches) == 5
+
+
+def test_interleaved_sessions_bit_identical():
+    """T/test_server.py:91-119."""
+    eng = _engine(toy(seed=1))
+    rng = np.random.default_rng(1)
+    xa = rng.standard_normal((6, 64)).astype(np.float32)
+    xb = rng.standard_normal((6, 64)).astype(np.float32)
+
+    def serial(xs):
+        c = eng.make_caches(0, 4, 1)
+        return np.concatenate([eng.run_cached(0, 4, c, _blob(xs[i:i + 1]), 1, 1, False).array()
+                               for i in range(6)])
+
+    sa, sb = serial(xa), serial(xb)
+    ca, cb = eng.make_caches(0, 4, 1), eng.make_caches(0, 4, 1)
+    ia, ib = [], []
+    for i in range(6):
+        ia.append(eng.run_cached(0, 4, ca, _blob(xa[i:i + 1]), 1, 1, False).array())
+        ib.append(eng.run_cached(0, 4, cb, _blob(xb[i:i + 1]), 1, 1, False).array())
+    assert np.array_equal(np.concatenate(ia), sa)
+    assert np.array_equal(np.concatenate(ib), sb)
+
+
+def test_restore_then_continue():
+    """T/test_server.py:123-136: replay of 10 rows then 1 step == uninterrupted."""
+    eng = _engine(toy(seed=1))
+    rng = np.random.default_rng(2)
+    x = rng.standard_normal((11, 64)).astype(np.float32)
+    c1 = eng.make_caches(0, 4, 1)
+    direct = [eng.run_cached(0, 4, c1, _blob(x[i:i + 1]), 1, 1, False).array() for i in range(11)]
+    c2 = eng.make_caches(0, 4, 1)
+    eng.run_cached(0, 4, c2, _blob(x[:10]), 1, 10, False)
+    res = eng.run_cached(0, 4, c2, _blob(x[10:11]), 1, 1, False).array()
+    assert np.abs(res - direct[10]).max() < 1e-5
+
+
+def test_reorder_paper_example():
+    """T/test_server.py:167-178: new slot i <- old slot idx[i]-1."""
+    eng = _engine(toy(seed=1))
+    rng = np.random.default_rng(3)
+    c = eng.make_caches(0, 4, 5)
+    x = rng.standard_normal((5, 64)).astype(np.float32)
+    eng.run_cached(0, 4, c, _blob(x), 5, 1, False)
+    old = [blk.keys.copy() for blk in c]
+    eng.reorder(c, [1, 1, 0, 2, 1])
+    for before, blk in zip(old, c):
+        keys = blk.keys
+        for new_slot, old_slot in enumerate([2, 2, 1, 3, 2]):
+            assert np.array_equal(keys[new_slot], before[old_slot - 1])
+    # widening from a prefill, then stepping the clones (copy-on-write tail)
+    c = eng.make_caches(0, 4, 1)
+    eng.run_cached(0, 4, c, _blob(x[:3]), 1, 3, False)
+    eng.reorder(c, [0, 0, 0, 0])
+    assert c.width == 4 and all(b.width == 4 and b.length == 3 for b in c)
+    y = eng.run_cached(0, 4, c, _blob(x[:4]), 4, 1, False).array()
+    runner = om.SpanRunner(toy(seed=1), 0, 4)
+    runner.step(x[:3][None])
+    runner.reorder([0, 0, 0, 0])
+    want = runner.step(x[:4][:, None, :])[:, 0]
+    assert np.abs(y - want).max() < 1e-5
+
+
+def test_micro_batch_split_bit_identical():
+    """T/test_server.py:247-255."""
+    eng = _engine(toy(seed=1))
+    rng = np.random.default_rng(4)
+    x = rng.standard_normal((4, 512, 64)).astype(np.float32)
+    blob = _blob(x.reshape(-1, 64))
+    whole = eng.forward(0, 2, blob, 4, 512, micro_batch_tokens=10**9, record=None).array()
+    split = eng.forward(0, 2, blob, 4, 512, micro_batch_tokens=1024, record=None).array()
+    assert np.array_equal(whole, split)
+    runner = om.SpanRunner(toy(seed=1), 0, 2, width=4)
+    want = runner.step(x)
+    assert np.abs(whole.reshape(4, 512, 64) - want).max() < 1e-5
+
+
+def test_quantized_output_equals_codec_of_output():
+    eng = _engine(toy(seed=1))
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal((3, 64)).astype(np.float32)
+    c1, c2 = eng.make_caches(0, 8, 1), eng.make_caches(0, 8, 1)
+    raw = eng.run_cached(0, 8, c1, _blob(x), 1, 3, False).array()
+    q = eng.run_cached(0, 8, c2, _blob(x), 1, 3, True)
+    from oracle import codec as oc
+    codes, scales = oc.quantize(raw)
+    assert np.array_equal(q.quant.codes, codes) and np.array_equal(q.quant.scales, scales)
+    # quantized input path: dequant in-kernel == host dequant
+    c3, c4 = eng.make_caches(4, 8, 1), eng.make_caches(4, 8, 1)
+    a = eng.run_cached(4, 8, c3, q, 1, 3, False).array()
+    b = eng.run_cached(4, 8, c4, _blob(oc.dequantize(codes, scales, raw.shape)), 1, 3,
+                       False).array()
+    assert np.array_equal(a, b)
+
+
+SMALL = {
+    "llama_int8": SpanConfig(n_blocks=3, hidden_dim=512, n_heads=4, n_kv_heads=2, ffn_dim=1024,
+                             vocab_size=64, max_seq_len=512, family="llama",
+                             weight_dtype="int8", kv_dtype="bf16", seed=5),
+    "llama_bf16": SpanConfig(n_blocks=3, hidden_dim=512, n_heads=4, ffn_dim=768,
+                             vocab_size=64, max_seq_len=512, family="llama",
+                             weight_dtype="bf16", kv_dtype="bf16", seed=6),
+    "bloom_int8": SpanConfig(n_blocks=2, hidden_dim=512, n_heads=4, vocab_size=64,
+                             max_seq_len=512, family="bloom", weight_dtype="int8",
+                             kv_dtype="bf16", seed=7),
+    "llama_f32": SpanConfig(n_blocks=2, hidden_dim=256, n_heads=2, n_kv_heads=1, ffn_dim=512,
+                            vocab_size=64, max_seq_len=512, family="llama", seed=8),
+}
+
+
+@pytest.mark.parametrize("name", sorted(SMALL))
+def test_extended_families_vs_oracle(name):
+    cfg = SMALL[name]
+    eng = _engine(cfg)
+    rng = np.random.default_rng(11)
+    d = cfg.hidden_dim
+    t_pre, n_dec = 70, 6        # crosses a 64-position page boundary
+    x = rng.standard_normal((t_pre + n_dec, d)).astype(np.float32)
+    runner = om.SpanRunner(cfg, 0, cfg.n_blocks)
+    c = eng.make_caches(0, cfg.n_blocks, 1)
+    got = eng.run_cached(0, cfg.n_blocks, c, _blob(x[:t_pre]), 1, t_pre, False).array()
+    want = runner.step(x[None, :t_pre])[0]
+    tol_pre = 2e-2 if cfg.weight_dtype != "f32" else 1e-4
+    scale = np.abs(want).max()
+    assert np.abs(got - want).max() <= tol_pre * scale, np.abs(got - want).max() / scale
+    for i in range(t_pre, t_pre + n_dec):
+        g = eng.run_cached(0, cfg.n_blocks, c, _blob(x[i:i + 1]), 1, 1, False).array()
+        w = runner.step(x[None, i:i + 1])[0]
+        tol = 2e-3 if cfg.weight_dtype != "f32" else 1e-4
+        s = np.abs(w).max()
+        assert np.abs(g - w).max() <= tol * s, (i, np.abs(g - w).max() / s)
+
+
+def test_engine_blocks_params_hash_matches_reference(golden_toy):
+    """`params_hash(engine.blocks)` (T/test_server.py:228) reads the GPU
+    weights back; for the toy config they equal the reference arrays."""
+    eng = _engine(toy(seed=1))
+    arrs = eng.blocks[0].arrays()
+    assert np.array_equal(arrs[0], golden_toy["default__w_wq_0"])
+    assert np.array_equal(arrs[5], golden_toy["default__w_w2_0"])

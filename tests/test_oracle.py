@@ -1,0 +1,130 @@
+"""The oracle is pinned before it is trusted: bit-exact against the
+reference's golden vectors (tests/golden/make_golden.py) and, when
+/root/reference is importable, against the live reference."""
+
+import json
+import os
+import sys
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, REFERENCE_SRC, reference_available
+from oracle import codec as oc
+from oracle import model as om
+from paper_2312_08361_b200.config import SpanConfig, toy
+
+
+def test_codec_golden_bit_exact(golden_codec):
+    keys = sorted({k.split("__")[0] for k in golden_codec.files})
+    for k in keys:
+        h = golden_codec[f"{k}__in"]
+        codes, scales = oc.quantize(h)
+        assert np.array_equal(codes, golden_codec[f"{k}__codes"]), k
+        assert np.array_equal(scales, golden_codec[f"{k}__scales"]), k
+        assert np.array_equal(oc.dequantize(codes, scales, h.shape), golden_codec[f"{k}__deq"]), k
+
+
+def test_codec_kats():
+    """T/test_quantize_wire.py:16-29."""
+    codes, scales = oc.quantize(np.zeros((4, 64), np.float32))
+    assert (scales == 0).all() and (codes == 0).all()
+    h = np.ones(128, np.float32)
+    h[7] = 127.0
+    codes, scales = oc.quantize(h, block=128)
+    assert scales[0] == pytest.approx(1.0)
+    assert np.abs(oc.dequantize(codes, scales, h.shape, block=128) - h).max() <= 1.0
+
+
+@pytest.mark.parametrize("name,cfg", [("default", toy(seed=1)),
+                                      ("tiny", SpanConfig(n_blocks=2, hidden_dim=8, n_heads=2,
+                                                          vocab_size=16, max_seq_len=64, seed=3))])
+def test_toy_weights_and_forward_golden(golden_toy, name, cfg):
+    g = golden_toy
+    for role in ("wq", "wk", "wv", "wo", "w1", "w2"):
+        for b in (0, cfg.n_blocks - 1):
+            w = om.init_block(cfg, b)[role]
+            assert np.array_equal(w, g[f"{name}__w_{role}_{b}"]), (role, b)
+    assert np.array_equal(om.init_embedding(cfg), g[f"{name}__embedding"])
+    p0 = om.init_block(cfg, 0)
+    for tag in ("prefill", "decode", "fresh"):
+        y, kn, vn = om.block_forward_batched(cfg, p0, g[f"{name}__{tag}_x"], g[f"{name}__{tag}_pk"],
+                                             g[f"{name}__{tag}_pv"])
+        assert np.array_equal(y, g[f"{name}__{tag}_y"]), tag
+        assert np.array_equal(kn, g[f"{name}__{tag}_kn"]), tag
+        assert np.array_equal(vn, g[f"{name}__{tag}_vn"]), tag
+    prefix = [3, 1, 4] if cfg.vocab_size > 4 else [1, 2, 3]
+    assert om.reference_generate(cfg, prefix, 32) == list(g[f"{name}__greedy32"])
+
+
+def test_toy_stack_golden(golden_toy):
+    cfg = toy(seed=1)
+    r = om.SpanRunner(cfg)
+    xs = golden_toy["default__stack_in"]
+    outs = [r.step(xs[None, :3])[0]] + [r.step(xs[None, i:i + 1])[0] for i in range(3, 9)]
+    assert np.array_equal(np.concatenate(outs), golden_toy["default__stack_out"])
+
+
+def test_kv_gather_example():
+    """T/test_model.py:222-234: new slot i <- old slot idx[i]."""
+    cfg = toy(seed=1)
+    c = om.KVCache(cfg, 5)
+    k = np.arange(5 * 2 * 4 * 16, dtype=np.float32).reshape(5, 2, 4, 16)
+    c.append(k, -k)
+    c.gather([1, 1, 0, 2, 1])
+    for i, j in enumerate([1, 1, 0, 2, 1]):
+        assert np.array_equal(c.keys[i], k[j])
+
+
+def test_extension_families_consistent():
+    """Unpinned extensions: stepwise == full prefill (KV-equivalence, the
+    property of T/test_model.py:103-135) for llama/bloom restatements."""
+    for cfg in (SpanConfig(n_blocks=2, hidden_dim=64, n_heads=4, n_kv_heads=2, ffn_dim=96,
+                           family="llama", seed=2, max_seq_len=64),
+                SpanConfig(n_blocks=2, hidden_dim=64, n_heads=4, family="bloom", seed=2,
+                           max_seq_len=64)):
+        rng = np.random.default_rng(0)
+        x = rng.standard_normal((1, 9, 64)).astype(np.float32)
+        full = om.SpanRunner(cfg).step(x)
+        r = om.SpanRunner(cfg)
+        step = np.concatenate([r.step(x[:, i:i + 1]) for i in range(9)], axis=1)
+        assert np.abs(full - step).max() < 1e-5
+
+
+def test_int8_weight_rounding_is_codec_per_column():
+    rng = np.random.default_rng(1)
+    w = rng.uniform(-1, 1, (256, 32)).astype(np.float32)
+    codes, scales = om.quantize_columns_int8(w)
+    for j in range(32):
+        c2, s2 = oc.quantize(w[:, j], block=256)
+        assert np.array_equal(codes[j], c2) and scales[j] == s2[0]
+
+
+@pytest.mark.skipif(not reference_available(), reason="reference not mounted")
+def test_live_reference_matches_oracle():
+    sys.path.insert(0, REFERENCE_SRC)
+    import swarmpipe.model as R
+    import swarmpipe.quantize as Q
+    rc = R.ModelConfig(seed=4)
+    cfg = toy(seed=4)
+    blocks, client = R.init_model(rc)
+    for b in range(rc.n_blocks):
+        p = om.init_block(cfg, b)
+        for k in ("wq", "wk", "wv", "wo", "w1", "w2"):
+            assert np.array_equal(p[k], getattr(blocks[b], k))
+    assert R.reference_generate(rc, [5, 9], 24) == om.reference_generate(cfg, [5, 9], 24)
+    rng = np.random.default_rng(9)
+    for n in (1, 63, 64, 65, 1000):
+        h = (rng.standard_normal(n) * 3).astype(np.float32)
+        q = Q.quantize_hidden(h)
+        c, s = oc.quantize(h)
+        assert np.array_equal(q.codes, c) and np.array_equal(q.scales, s)
+
+
+def test_swarm_trace_fixture_is_self_consistent():
+    with open(os.path.join(GOLDEN, "swarm_traces.json")) as f:
+        traces = json.load(f)
+    for t in traces:
+        assert t["tokens"] == t["oracle"]
+        for (_, _, tt, nbytes) in t["restore_events"]:
+            assert nbytes == tt * 64 * 4
