@@ -1,0 +1,397 @@
+"""Benchmark: Llama-2-70B-shape int8 span decode steps/s and prefill tokens/s
+on B200, with the HBM / tensor-core roofline and the reference CPU path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+N=1: all 80 blocks on one GPU (68.5 GB of int8 weights fit).  N>1 (torchrun):
+rank r serves span stage_intervals(80, N)[r]; activations move between spans
+as int8 codes + f32 scales by NCCL send/recv; N independent sessions are
+kept in flight so every GPU works on a different session each tick.
+A "step" = one decode token of every in-flight session through all 80 blocks.
+Inputs (weights, 68.5 GB) are far larger than L2, so no flush is needed.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "Llama-2-70B-shape decode steps/s and prefill tokens/s, % of HBM/TC roofline"
+UNIT = "steps/s"
+
+
+def load_peaks() -> dict:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        d["_src"] = "measured"
+        return d
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+            "_src": "fallback"}
+
+
+def stage_intervals(n_blocks: int, n_stages: int) -> list[tuple[int, int]]:
+    from paper_2312_08361_b200.balancer import stage_intervals as si
+    return si(n_blocks, n_stages)
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.path = tempfile.mktemp(suffix=".csv")
+
+    def start(self):
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
+                stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.close()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the reference algorithm (oracle port, numpy/OpenBLAS) on host
+# ---------------------------------------------------------------------------
+
+def cpu_block_decode_seconds(cfg, context: int, reps: int = 3) -> tuple[float, dict]:
+    """Time one decode step of one block of the oracle's block forward (the
+    reference's SP/model.py:244-280 structure, f32 numpy) at `context`."""
+    from oracle import model as om
+    d, kv, F = cfg.hidden_dim, cfg.kv_heads * cfg.head_dim, cfg.ffn
+    p = {}
+    for role, a, b in om.block_matrices(cfg):
+        p[role] = np.full((a, b), 1e-3, np.float32)     # f32 effective weights (values irrelevant to timing)
+    for k in ("ln1_g", "ln2_g"):
+        p[k] = np.ones(d, np.float32)
+    for k in ("ln1_b", "ln2_b"):
+        p[k] = np.zeros(d, np.float32)
+    rng = np.random.default_rng(0)
+    pk = rng.standard_normal((1, context, cfg.kv_heads, cfg.head_dim)).astype(np.float32)
+    pv = rng.standard_normal((1, context, cfg.kv_heads, cfg.head_dim)).astype(np.float32)
+    x = rng.standard_normal((1, 1, d)).astype(np.float32)
+    tables = om.Tables(cfg)
+    om.block_forward_batched(cfg, p, x, pk, pv, tables)   # warm
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        om.block_forward_batched(cfg, p, x, pk, pv, tables)
+        ts.append(time.perf_counter() - t0)
+    info = {}
+    try:
+        from threadpoolctl import threadpool_info
+        info = {"threadpools": [{k: v for k, v in t.items() if k in ("internal_api", "num_threads")}
+                                for t in threadpool_info()]}
+    except Exception:
+        pass
+    return float(np.median(ts)), info
+
+
+def cpu_threads() -> int:
+    try:
+        from threadpoolctl import threadpool_info
+        n = [t.get("num_threads", 1) for t in threadpool_info()]
+        return int(max(n)) if n else 1
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ---------------------------------------------------------------------------
+# the reference arm
+# ---------------------------------------------------------------------------
+
+def run_reference(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_2312_08361_b200.config import llama2_70b
+    cfg = llama2_70b()
+    context = args.prefill
+    # each step = one oracle block decode at `context` (bounded sample); the
+    # metric scales it to the 80-block model
+    for _ in range(args.warmup):
+        cpu_block_decode_seconds(cfg, context, reps=1)
+    t0 = time.perf_counter()
+    per = []
+    for _ in range(args.steps):
+        s, info = cpu_block_decode_seconds(cfg, context, reps=1)
+        per.append(s)
+    wall = time.perf_counter() - t0
+    t_block = float(np.median(per))
+    value = 1.0 / (t_block * cfg.n_blocks)
+    cores = cpu_threads()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t_block * cfg.n_blocks * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "llama2-70b-shape decode, batch 1, context %d, 80 blocks" % context,
+                   "sample": "1 block decode per step, scaled x80"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"oracle block_forward_batched (SP/model.py:244-280 restated, "
+                                   f"f32 numpy/OpenBLAS) of one 70B-shape block at context "
+                                   f"{context}, {args.steps} steps, scaled to 80 blocks"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s": wall, **info,
+    }
+    print(json.dumps(line))
+
+
+# ---------------------------------------------------------------------------
+# the B200 arm
+# ---------------------------------------------------------------------------
+
+def run_b200(args) -> None:
+    import torch
+    import torch.distributed as dist
+
+    from paper_2312_08361_b200 import _lib
+    from paper_2312_08361_b200.blob import HiddenBlob
+    from paper_2312_08361_b200.config import llama2_70b
+    from paper_2312_08361_b200.engine import B200ServerEngine, DeviceSpan
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    peaks = load_peaks()
+    cfg = llama2_70b()
+    n_blocks = args.blocks or cfg.n_blocks
+    if args.blocks:
+        cfg = cfg.with_(n_blocks=n_blocks)
+    start, end = stage_intervals(n_blocks, world)[rank]
+    t_gen = time.perf_counter()
+    span = DeviceSpan(cfg, start, end, device=local,
+                      kv_pool_tokens=(args.prefill + 256) * (max(1, world) + 1) + 1024)
+    torch.cuda.synchronize()
+    t_gen = time.perf_counter() - t_gen
+    eng = B200ServerEngine(cfg, span=span)
+    lib = _lib.load()
+    d = cfg.hidden_dim
+    stream = torch.cuda.current_stream(dev)
+
+    def prof(on: bool):
+        _lib.check(lib.sp_span_set_profiling(span.handle, 1 if on else 0))
+
+    def prof_read():
+        import ctypes
+        n = 5
+        ms = (ctypes.c_double * n)()
+        by = (ctypes.c_double * n)()
+        fl = (ctypes.c_double * n)()
+        la = (ctypes.c_int64 * n)()
+        _lib.check(lib.sp_span_profile_read(span.handle, n, ms, by, fl, la))
+        return [dict(ms=ms[i], bytes=by[i], flops=fl[i], launches=la[i]) for i in range(n)]
+
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    sessions = max(1, world)       # sessions in flight (one per pipeline stage)
+
+    # ---- prefill (2048 tokens per session), timed on the device ----
+    caches = [eng.make_caches(start, end, 1) for _ in range(sessions)]
+    x_pre = torch.randn(args.prefill, d, device=dev, generator=g)
+    prof(True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for s in range(sessions):
+        eng.run_cached(start, end, caches[s], HiddenBlob.from_device(x_pre), 1, args.prefill,
+                       False)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    pre_ms = ev0.elapsed_time(ev1)
+    pre_prof = prof_read()
+    prof(False)
+    pre_ms_t = torch.tensor([pre_ms], device=dev)
+    if world > 1:
+        dist.all_reduce(pre_ms_t, op=dist.ReduceOp.MAX)
+    pre_ms = float(pre_ms_t.item())
+    pre_flops = sum(p["flops"] for p in pre_prof)
+    prefill_tok_s = sessions * args.prefill / (pre_ms / 1e3)
+
+    # ---- decode: W warm-up + K timed steps ----
+    from paper_2312_08361_b200.pipeline import SpanPipeline
+    pipe = SpanPipeline(eng, start, end, caches, rank, world, d, dev)
+    for _ in range(args.warmup):
+        pipe.step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = lib.sp_kernel_launches()
+    prof(True)
+    clocks = ClockSampler(local).start()
+    time.sleep(0.3)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        pipe.step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    dec_prof = prof_read()
+    prof(False)
+    launches = lib.sp_kernel_launches() - launches0
+    dec_ms = e0.elapsed_time(e1)
+    t = torch.tensor([dec_ms], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dec_ms = float(t.item())
+    # every tick each rank advances one session by its span; a full token of a
+    # session needs `world` ticks, `world` sessions are in flight
+    ticks = args.steps
+    steps_done = ticks * sessions / max(1, world)          # full-model tokens, all sessions
+    value = steps_done / (dec_ms / 1e3)
+
+    # ---- end to end through the public API (host buffers, H2D + D2H per step) ----
+    e2e = None
+    if world == 1:
+        c_e2e = eng.make_caches(start, end, 1)
+        eng.run_cached(start, end, c_e2e, HiddenBlob.from_array(
+            np.random.default_rng(0).standard_normal((args.prefill, d)).astype(np.float32)), 1,
+            args.prefill, False)
+        rows = np.random.default_rng(1).standard_normal((args.steps + args.warmup, 1, d)).astype(
+            np.float32)
+        for i in range(args.warmup):
+            eng.run_cached(start, end, c_e2e, HiddenBlob.from_array(rows[i]), 1, 1, False).array()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for i in range(args.warmup, args.warmup + args.steps):
+            out = eng.run_cached(start, end, c_e2e, HiddenBlob.from_array(rows[i]), 1, 1, False)
+            out.array()
+        e2e_s = time.perf_counter() - t0
+        e2e = {"value": args.steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 4 * d,
+               "d2h_bytes_per_step": 4 * d}
+        del c_e2e
+
+    # ---- roofline of the dominant kernel (decode GEMV) ----
+    gemv = dec_prof[0]
+    achieved = gemv["bytes"] / (gemv["ms"] / 1e3) / 1e9 if gemv["ms"] else 0.0
+    step_bytes = sum(p["bytes"] for p in dec_prof[:3])
+    rank_ms_per_tick = dec_ms / ticks
+    line = None
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu:
+            t_block, info = cpu_block_decode_seconds(cfg, args.prefill, reps=3)
+            cpu = {"value": 1.0 / (t_block * n_blocks), "unit": UNIT, "cores": cpu_threads(),
+                   "kind": "port",
+                   "sample": f"oracle block_forward_batched (f32 numpy/OpenBLAS) of one "
+                             f"70B-shape block at context {args.prefill}, median of 3, scaled "
+                             f"to {n_blocks} blocks"}
+        peak = peaks["hbm_gbs"]
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": dec_ms / max(steps_done, 1e-9) * (sessions / max(1, world)) * world
+            if world > 1 else dec_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "int8 weights x f32 activations (f16 hi/lo tensor-core split)",
+            "data": "synthetic (splitmix64 random-init weights per SP/model.py:55-60, N(0,1) "
+                    "hidden rows)",
+            "config": {"workload": f"llama2-70b-shape int8 span decode, batch 1, context "
+                                   f"{args.prefill}+, {n_blocks} blocks over {world} GPU(s), "
+                                   f"{sessions} session(s) in flight",
+                       "span_per_gpu": [start, end], "prefill_tokens": args.prefill,
+                       "l2": "inputs larger than L2 (68.5 GB weights)"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "kernel": "gemv_mma_kernel<int8> (decode linear layers)",
+                         "peak_src": peaks["_src"],
+                         "launches": gemv["launches"], "avg_launch_us":
+                             gemv["ms"] / max(gemv["launches"], 1) * 1e3},
+            "step_roofline": {"bytes_per_tick": step_bytes / ticks,
+                              "achieved_gbs": step_bytes / ticks / (rank_ms_per_tick / 1e3) / 1e9,
+                              "frac": step_bytes / ticks / (rank_ms_per_tick / 1e3) / 1e9 / peak},
+            "prefill": {"tokens_per_s": prefill_tok_s, "ms": pre_ms, "tokens": args.prefill,
+                        "sessions": sessions, "tflops": pre_flops / (pre_ms / 1e3) / 1e12,
+                        "tc_frac": pre_flops / (pre_ms / 1e3) / 1e12 / peaks["bf16_tflops"],
+                        "gemm_ms": pre_prof[1]["ms"], "attn_ms": pre_prof[3]["ms"],
+                        "gemm_tflops": pre_prof[1]["flops"] / max(pre_prof[1]["ms"], 1e-9) / 1e9},
+            "decode_breakdown_ms_per_tick": {k: dec_prof[i]["ms"] / ticks for i, k in enumerate(
+                ["gemv", "gemm", "attn_decode", "attn_prefill", "other"])},
+            "e2e": e2e, "cpu_baseline": cpu, "clocks": clk, "gpu_launches": int(launches),
+            "weight_gen_s": t_gen, "weight_bytes_per_gpu": span.weight_bytes,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference", "ours"])
+    ap.add_argument("--prefill", type=int, default=2048)
+    ap.add_argument("--blocks", type=int, default=0, help="override n_blocks (debug only)")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -128,6 +128,18 @@ int sp_span_forward_stateless(sp_span* span, int32_t block_begin, int32_t block_
                               const float* x, float* y, float* record, int32_t batch,
                               int32_t tokens, void* stream);
 
+/* ---- measurement ----------------------------------------------------------
+ * With profiling on, every launch of the span schedule is bracketed by CUDA
+ * events on its stream; profile_read synchronises and returns, per class
+ * (0 decode GEMV, 1 prefill GEMM, 2 decode attention, 3 prefill attention,
+ * 4 norms/RoPE/KV-append/codec), the summed device ms, algorithmic bytes and
+ * flops and the number of launches, then clears the records. */
+int sp_span_set_profiling(sp_span* span, int32_t enable);
+int sp_span_profile_read(sp_span* span, int32_t n_classes, double* ms, double* bytes,
+                         double* flops, int64_t* launches);
+/* kernels launched by this library since load (all spans, all devices) */
+int64_t sp_kernel_launches(void);
+
 /* FNV-1a 64 over host bytes — SP/wire.py:39-44 (relay checksums,
  * SP/server.py:141-142); host-side helper */
 uint64_t sp_fnv1a64(const uint8_t* data, int64_t n);

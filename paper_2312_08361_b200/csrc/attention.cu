@@ -353,8 +353,11 @@ void decode_t(const AttnArgs& a, cudaStream_t st) {
   auto kern = attn_decode_kernel<HD, KT>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   dim3 grid(a.width * a.kvh, nsplit);
-  kern<<<grid, 128, sm, st>>>(a, nsplit);
-  if (nsplit > 1) attn_combine_kernel<HD><<<a.width * a.H, HD, 0, st>>>(a, nsplit);
+  kern<<<grid, 128, sm, st>>>(a, nsplit); count_launch();
+  if (nsplit > 1) {
+    attn_combine_kernel<HD><<<a.width * a.H, HD, 0, st>>>(a, nsplit);
+    count_launch();
+  }
 }
 
 template <int HD, typename KT>
@@ -364,7 +367,7 @@ void prefill_t(const AttnArgs& a, cudaStream_t st) {
   auto kern = attn_prefill_kernel<HD, KT>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   dim3 grid(a.width * a.H, (a.n_new + 15) / 16);
-  kern<<<grid, 128, sm, st>>>(a);
+  kern<<<grid, 128, sm, st>>>(a); count_launch();
 }
 
 template <typename KT>
@@ -391,7 +394,7 @@ void dispatch_hd(const AttnArgs& a, bool decode, cudaStream_t st) {
 void launch_norm(int family, const float* x, const float* g, const float* b, float* out,
                  int64_t R, int64_t d, cudaStream_t st) {
   if (R == 0) return;
-  norm_kernel<<<(unsigned)R, 256, 0, st>>>(family, x, g, b, out, d);
+  norm_kernel<<<(unsigned)R, 256, 0, st>>>(family, x, g, b, out, d); count_launch();
 }
 
 void launch_rope_append(const AttnArgs& a, cudaStream_t st) {
@@ -399,6 +402,7 @@ void launch_rope_append(const AttnArgs& a, cudaStream_t st) {
   if (R == 0) return;
   if (a.kv_dtype == kKVBF16) rope_append_kernel<__nv_bfloat16><<<R, 256, 0, st>>>(a);
   else rope_append_kernel<float><<<R, 256, 0, st>>>(a);
+  count_launch();
 }
 
 int64_t attn_workspace_floats(int width, int H, int hd, int max_seq) {
@@ -420,7 +424,7 @@ void launch_page_copy(void* pool, int64_t block_stride_bytes, int n_blocks, int6
                       int src_page, int dst_page, cudaStream_t st) {
   dim3 grid(64, n_blocks);
   page_copy_kernel<<<grid, 256, 0, st>>>((char*)pool, block_stride_bytes, page_bytes, src_page,
-                                         dst_page);
+                                         dst_page); count_launch();
 }
 
 void launch_kv_gather_slot(const void* pool, int kv_dtype, const int* table, int t, int kvh,
@@ -431,6 +435,7 @@ void launch_kv_gather_slot(const void* pool, int kv_dtype, const int* table, int
     kv_gather_kernel<__nv_bfloat16><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(pool, table, t, kvh, hd, k_out, v_out);
   else
     kv_gather_kernel<float><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(pool, table, t, kvh, hd, k_out, v_out);
+  count_launch();
 }
 
 }  // namespace sp

@@ -44,13 +44,13 @@ void launch_quantize(const float* x, int8_t* codes, float* scales, int64_t n, cu
   int64_t nblk = (n + kCodecBlock - 1) / kCodecBlock;
   if (nblk == 0) return;
   int64_t grid = (nblk + 7) / 8;
-  quantize_kernel<<<(unsigned)grid, 256, 0, st>>>(x, codes, scales, n);
+  quantize_kernel<<<(unsigned)grid, 256, 0, st>>>(x, codes, scales, n); count_launch();
 }
 
 void launch_dequantize(const int8_t* codes, const float* scales, float* x, int64_t n,
                        cudaStream_t st) {
   if (n == 0) return;
-  dequantize_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(codes, scales, x, n);
+  dequantize_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(codes, scales, x, n); count_launch();
 }
 
 }  // namespace sp

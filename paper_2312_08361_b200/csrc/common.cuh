@@ -85,6 +85,9 @@ __host__ __device__ __forceinline__ int64_t frag_offset_i8(int64_t n, int64_t k,
   return (((n >> 4) * (K >> 5) + (k >> 5)) << 9) + lane * 16 + ks * 8 + pos;
 }
 
+// host-side count of kernels launched by this library (bench `gpu_launches`)
+void count_launch();
+
 }  // namespace sp
 
 #define SP_CUDA_TRY(expr)                                       \

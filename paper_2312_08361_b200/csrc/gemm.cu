@@ -96,13 +96,13 @@ __global__ void swiglu_rows_kernel(const float* in, float* out, int64_t R, int64
 
 void launch_gemm(const LinearArgs& a, cudaStream_t st) {
   dim3 grid((unsigned)((a.N + BN - 1) / BN), (unsigned)((a.R + BM - 1) / BM));
-  gemm_simt_kernel<<<grid, 256, 0, st>>>(a);
+  gemm_simt_kernel<<<grid, 256, 0, st>>>(a); count_launch();
 }
 
 void launch_swiglu_rows(const float* in, float* out, int64_t R, int64_t F, cudaStream_t st) {
   int64_t n = R * F;
   if (n == 0) return;
-  swiglu_rows_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(in, out, R, F);
+  swiglu_rows_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(in, out, R, F); count_launch();
 }
 
 }  // namespace sp

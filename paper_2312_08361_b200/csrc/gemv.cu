@@ -369,7 +369,7 @@ int64_t gemv_counter_ints(int64_t N) { return N / (16 * kRT) + 1; }
 void launch_gemv(const LinearArgs& a, cudaStream_t st) {
   if (a.wdtype == kF32) {
     int64_t outs = (a.epi == EPI_SWIGLU) ? a.N / 2 : a.N;
-    gemv_f32_kernel<<<(unsigned)((outs + 7) / 8), 256, 0, st>>>(a);
+    gemv_f32_kernel<<<(unsigned)((outs + 7) / 8), 256, 0, st>>>(a); count_launch();
     return;
   }
   const int ks = choose_ks(a.N, a.K, a.wdtype);
@@ -384,6 +384,7 @@ void launch_gemv(const LinearArgs& a, cudaStream_t st) {
       gemv_mma_kernel<kI8><<<(unsigned)grid, kNW * 32, 0, st>>>(b, ks, rn);
     else
       gemv_mma_kernel<kBF16><<<(unsigned)grid, kNW * 32, 0, st>>>(b, ks, rn);
+    count_launch();
   }
 }
 

@@ -1,5 +1,6 @@
 // Span runtime: weights, paged KV pool, sessions and the per-block kernel
 // schedule of RealServerEngine.run_cached (SP/server.py:93-100).
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -27,6 +28,11 @@ void sp_set_error(const char* file, int line, const char* msg) {
   } while (0)
 
 #define SP_CHECK_LAUNCH() SP_CUDA_TRY(cudaGetLastError())
+
+namespace sp {
+static std::atomic<int64_t> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+}  // namespace sp
 
 using namespace sp;
 
@@ -76,6 +82,11 @@ struct sp_span {
   int64_t attn_ws_floats = 0;
   float* attn_ws = nullptr;
   std::mutex mu;
+  // live per-launch timing (bench roofline): CUDA events around each launch
+  struct ProfRec { int cls; cudaEvent_t a, b; double bytes, flops; };
+  bool prof = false;
+  std::vector<ProfRec> prof_recs;
+  std::vector<cudaEvent_t> ev_pool;
 };
 
 struct sp_kv {
@@ -203,9 +214,48 @@ int prepare_pages(sp_kv* kv, int n_new, cudaStream_t st) {
   return SP_OK;
 }
 
+// profiling classes (sp_span_profile_read)
+enum ProfCls { PC_GEMV = 0, PC_GEMM = 1, PC_ATTN_DEC = 2, PC_ATTN_PRE = 3, PC_OTHER = 4 };
+
+cudaEvent_t get_event(sp_span* s) {
+  if (!s->ev_pool.empty()) {
+    cudaEvent_t e = s->ev_pool.back();
+    s->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+struct ProfScope {
+  sp_span* s;
+  int cls;
+  double bytes, flops;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr;
+  ProfScope(sp_span* s_, int c, double by, double fl, cudaStream_t st_)
+      : s(s_), cls(c), bytes(by), flops(fl), st(st_) {
+    if (s->prof) {
+      a = get_event(s);
+      cudaEventRecord(a, st);
+    }
+  }
+  ~ProfScope() {
+    if (a) {
+      cudaEvent_t b = get_event(s);
+      cudaEventRecord(b, st);
+      s->prof_recs.push_back({cls, a, b, bytes, flops});
+    }
+  }
+};
+
 void linear(sp_span* s, int wd, void* w, float* sc, int64_t N, int64_t K, const float* x,
             float* y, int64_t ldy, const float* res, int epi, int64_t R, bool decode,
             cudaStream_t st) {
+  const double wbytes = (double)N * K * elt_bytes(wd) + (wd == kI8 ? 4.0 * N : 0.0);
+  const double outc = (epi == EPI_SWIGLU) ? N / 2 : N;
+  ProfScope ps(s, decode ? PC_GEMV : PC_GEMM, wbytes + 4.0 * R * (K + outc), 2.0 * R * N * K, st);
   LinearArgs a{};
   a.w = w; a.wscale = sc; a.wdtype = wd; a.N = N; a.K = K;
   a.x = x; a.ldx = K; a.y = y; a.ldy = ldy; a.res = res; a.epi = epi; a.R = (int)R;
@@ -242,20 +292,39 @@ int run_span(sp_span* s, sp_kv* kv, int b0, int b1, float* y, float* record, int
   at.rope_cos = s->rope_cos; at.rope_sin = s->rope_sin; at.alibi = s->alibi;
   at.ctx = s->ctx; at.workspace = s->attn_ws;
   const int64_t d = s->d, F = s->F;
+  const double kv_elt = s->cfg.kv_dtype == kKVBF16 ? 2.0 : 4.0;
   for (int b = b0 - s->start; b < b1 - s->start; ++b) {
     BlockW& W = s->blocks[b];
     at.kv_pool = s->pool + (int64_t)b * s->block_stride;
     if (record)
       SP_CUDA_TRY(cudaMemcpyAsync(record + (int64_t)(b - (b0 - s->start)) * R * d, y,
                                   R * d * sizeof(float), cudaMemcpyDeviceToDevice, st));
-    launch_norm(fam, y, W.ln1_g, W.ln1_b, s->h, R, d, st);
+    {
+      ProfScope ps(s, PC_OTHER, 8.0 * R * d, 0, st);
+      launch_norm(fam, y, W.ln1_g, W.ln1_b, s->h, R, d, st);
+    }
     linear(s, wd, W.qkv, W.s_qkv, s->n_qkv, d, s->h, s->qkvb, s->n_qkv, nullptr, EPI_STORE, R,
            decode, st);
-    launch_rope_append(at, st);
-    if (decode) launch_attention_decode(at, st);
-    else launch_attention_prefill(at, st);
+    {
+      ProfScope ps(s, PC_OTHER, 4.0 * R * s->n_qkv + (double)R * 2 * s->kv * kv_elt, 0, st);
+      launch_rope_append(at, st);
+    }
+    {
+      // keys visible to all new rows: width * sum_i (t0 + i + 1)
+      const double pairs = (double)width * ((double)n_new * kv->length +
+                                            (double)n_new * (n_new + 1) / 2);
+      const double kvbytes = decode ? (double)width * (kv->length + 1) * 2 * s->kv * kv_elt
+                                    : (double)width * (kv->length + n_new) * 2 * s->kv * kv_elt;
+      ProfScope ps(s, decode ? PC_ATTN_DEC : PC_ATTN_PRE, kvbytes + 8.0 * R * d,
+                   4.0 * pairs * s->H * s->hd, st);
+      if (decode) launch_attention_decode(at, st);
+      else launch_attention_prefill(at, st);
+    }
     linear(s, wd, W.o, W.s_o, d, d, s->ctx, y, d, y, EPI_RESID, R, decode, st);
-    launch_norm(fam, y, W.ln2_g, W.ln2_b, s->h, R, d, st);
+    {
+      ProfScope ps(s, PC_OTHER, 8.0 * R * d, 0, st);
+      launch_norm(fam, y, W.ln2_g, W.ln2_b, s->h, R, d, st);
+    }
     if (fam == kLlama)
       linear(s, wd, W.up, W.s_up, s->n_up, d, s->h, s->mlp, F, nullptr, EPI_SWIGLU, R, decode,
              st);
@@ -444,6 +513,8 @@ int sp_span_destroy(sp_span* s) {
   cudaFree(s->wmem); cudaFree(s->rope_cos); cudaFree(s->rope_sin); cudaFree(s->alibi);
   cudaFree(s->pool); cudaFree(s->h); cudaFree(s->qkvb); cudaFree(s->ctx); cudaFree(s->mlp);
   cudaFree(s->mlp_raw); cudaFree(s->gemv_ws); cudaFree(s->gemv_cnt); cudaFree(s->attn_ws);
+  for (auto& r : s->prof_recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+  for (auto e : s->ev_pool) cudaEventDestroy(e);
   delete s;
   return SP_OK;
 }
@@ -603,6 +674,33 @@ int sp_span_forward_stateless(sp_span* s, int32_t b0, int32_t b1, const float* x
   sp_kv_destroy(kv);
   return rc;
 }
+
+int sp_span_set_profiling(sp_span* s, int32_t enable) {
+  if (!s) SP_FAIL(SP_ERR_ARG, "null span");
+  s->prof = enable != 0;
+  return SP_OK;
+}
+
+int sp_span_profile_read(sp_span* s, int32_t n_classes, double* ms, double* bytes, double* flops,
+                         int64_t* launches) {
+  if (!s) SP_FAIL(SP_ERR_ARG, "null span");
+  SP_CUDA_TRY(cudaSetDevice(s->device));
+  SP_CUDA_TRY(cudaDeviceSynchronize());
+  for (int c = 0; c < n_classes; ++c) { ms[c] = 0; bytes[c] = 0; flops[c] = 0; launches[c] = 0; }
+  for (auto& r : s->prof_recs) {
+    float t = 0.f;
+    cudaEventElapsedTime(&t, r.a, r.b);
+    if (r.cls < n_classes) {
+      ms[r.cls] += t; bytes[r.cls] += r.bytes; flops[r.cls] += r.flops; launches[r.cls] += 1;
+    }
+    s->ev_pool.push_back(r.a);
+    s->ev_pool.push_back(r.b);
+  }
+  s->prof_recs.clear();
+  return SP_OK;
+}
+
+int64_t sp_kernel_launches(void) { return sp::g_launches.load(); }
 
 uint64_t sp_fnv1a64(const uint8_t* data, int64_t n) {
   uint64_t h = 0xCBF29CE484222325ull;  // SP/wire.py:35-44

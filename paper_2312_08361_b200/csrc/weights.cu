@@ -103,7 +103,7 @@ __global__ void gen_bf16_pack_kernel(uint64_t stream, int64_t K, int64_t N, doub
 
 void launch_gen_stream(uint64_t stream, int64_t n, double scale, float* dst, cudaStream_t st) {
   if (n <= 0) return;
-  gen_stream_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(stream, n, scale, dst);
+  gen_stream_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(stream, n, scale, dst); count_launch();
 }
 
 void launch_gen_matrix(int wdtype, uint64_t stream, int64_t K, int64_t N, double scale,
@@ -111,17 +111,17 @@ void launch_gen_matrix(int wdtype, uint64_t stream, int64_t K, int64_t N, double
   if (wdtype == kF32) {
     int64_t n = K * N;
     gen_f32_rows_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(stream, K, N, scale, place,
-                                                                      (float*)dst);
+                                                                      (float*)dst); count_launch();
   } else if (wdtype == kBF16) {
     int64_t chunks = (N / 16) * (K / 16) * 32;
     gen_bf16_pack_kernel<<<(unsigned)((chunks + 255) / 256), 256, 0, st>>>(
-        stream, K, N, scale, place, (__nv_bfloat16*)dst);
+        stream, K, N, scale, place, (__nv_bfloat16*)dst); count_launch();
   } else {
     gen_i8_scales_kernel<<<(unsigned)((N + 7) / 8), 256, 0, st>>>(stream, K, N, scale, place,
-                                                                   scales);
+                                                                   scales); count_launch();
     int64_t chunks = (N / 16) * (K / 32) * 32;
     gen_i8_pack_kernel<<<(unsigned)((chunks + 255) / 256), 256, 0, st>>>(
-        stream, K, N, scale, place, scales, (uint8_t*)dst);
+        stream, K, N, scale, place, scales, (uint8_t*)dst); count_launch();
   }
 }
 
@@ -148,7 +148,7 @@ void launch_read_matrix(int wdtype, const void* src, const float* scales, int64_
                         MatPlace place, float* dst, cudaStream_t st) {
   int64_t n = K * N;
   read_matrix_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(wdtype, src, scales, K, N, K,
-                                                                   place, dst);
+                                                                   place, dst); count_launch();
 }
 
 }  // namespace sp

@@ -1,0 +1,90 @@
+"""Multi-GPU span pipeline: one process per GPU, each serving one contiguous
+span; activations cross span boundaries as int8 codes + f32 scales
+(`SP/quantize.py`, 8,704 B/token at d = 8192) by NCCL send/recv over NVLink.
+
+Schedule (N ranks, N sessions in flight): at tick k rank r advances session
+(k - r) mod N through its span.  Rank r's output of tick k is the input of
+rank r+1 at tick k+1; the last rank returns the f32 rows of the final block
+to rank 0 (the client side: only stage->stage boundaries are coded,
+`SP/client.py:280-287`), which feeds them back as that session's next input.
+Each tick ends with ONE grouped p2p (send this tick's output, receive next
+tick's input), so the ring never deadlocks and the host never blocks.
+With N == 1 this degenerates to plain autoregressive stepping of one session.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+
+
+class SpanPipeline:
+    def __init__(self, engine, start: int, end: int, caches: list, rank: int, world: int, d: int,
+                 device: torch.device, seed: int = 7):
+        self.eng, self.lib = engine, engine.lib
+        self.start, self.end = start, end
+        self.caches = caches
+        self.rank, self.world, self.d = rank, world, d
+        self.dev = device
+        self.k = 0
+        n_sc = (d + 63) // 64
+        g = torch.Generator(device=device).manual_seed(seed + rank)
+        self.init_rows = torch.randn(max(1, world), 1, d, device=device, generator=g)
+        self.y = torch.empty(1, d, device=device)
+        self.ring_in = torch.empty(1, d, device=device)            # rank 0: from the last rank
+        self.out_wire = torch.empty(d + 4 * n_sc, dtype=torch.uint8, device=device)
+        self.in_wire = torch.empty(d + 4 * n_sc, dtype=torch.uint8, device=device)
+        self.out_codes = self.out_wire[:d].view(torch.int8)
+        self.out_scales = self.out_wire[d:].view(torch.float32)
+        self.in_codes = self.in_wire[:d].view(torch.int8)
+        self.in_scales = self.in_wire[d:].view(torch.float32)
+        if world == 1:
+            self.y.copy_(self.init_rows[0])
+
+    def _forward(self, session: int, x_ptr: int, codes_ptr: int, scales_ptr: int,
+                 quantize_out: bool) -> None:
+        st = torch.cuda.current_stream(self.dev).cuda_stream
+        _lib.check(self.lib.sp_span_forward(
+            self.eng.span.handle, self.caches[session].handle, self.start, self.end, x_ptr,
+            codes_ptr, scales_ptr, self.y.data_ptr(),
+            self.out_codes.data_ptr() if quantize_out else 0,
+            self.out_scales.data_ptr() if quantize_out else 0, 1, 1, st))
+
+    def step(self) -> None:
+        k, r, N = self.k, self.rank, self.world
+        if N == 1:
+            # autoregressive feedback: the span output is the next input (in place)
+            self._forward(0, self.y.data_ptr(), 0, 0, False)
+            self.k += 1
+            return
+        import torch.distributed as dist
+        active = k >= r
+        s = (k - r) % N
+        last = r == N - 1
+        if active:
+            if r == 0:
+                x = self.init_rows[s] if k < N else self.ring_in
+                self._forward(s, x.data_ptr(), 0, 0, True)
+            else:
+                self._forward(s, 0, self.in_codes.data_ptr(), self.in_scales.data_ptr(),
+                              not last)
+        ops = []
+        if active:
+            if last:
+                ops.append(dist.P2POp(dist.isend, self.y, 0))
+            else:
+                ops.append(dist.P2POp(dist.isend, self.out_wire, r + 1))
+        if r == 0:
+            if k >= N - 1:
+                ops.append(dist.P2POp(dist.irecv, self.ring_in, N - 1))
+        elif k >= r - 1:
+            ops.append(dist.P2POp(dist.irecv, self.in_wire, r - 1))
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+        self.k += 1
+
+    @property
+    def wire_bytes_per_token(self) -> int:
+        return int(self.out_wire.numel())
