@@ -60,29 +60,26 @@ template <> __device__ __forceinline__ __nv_bfloat16 from_f32<__nv_bfloat16>(flo
 __device__ __forceinline__ float to_f32(float v) { return v; }
 __device__ __forceinline__ float to_f32(__nv_bfloat16 v) { return __bfloat162float(v); }
 
-// Fragment-tiled weight layout used by the tensor-core decode GEMV
-// (see DESIGN.md "weights in HBM").  A "tile" is 512 bytes = 32 lanes x 16 B;
-// lane L's 16 bytes are exactly its mma.m16n8k16 A-fragment(s).
-//   bf16: tile = 16 rows x 16 k        (one k-step)
-//   int8: tile = 16 rows x 32 k        (two k-steps), offset-binary u8 = w + 128
-// Tiles are ordered row-tile major: tile(rt, kt) at ((rt * KT) + kt) * 512 B.
-// Position of element (i, j) of a 16x16 sub-tile inside lane's 8 halves:
-__host__ __device__ __forceinline__ void frag_pos(int i, int j, int* lane, int* pos) {
-  int g = i & 7, hi = i >> 3, c4 = (j & 7) >> 1, jj = j & 1, k8 = j >> 3;
-  *lane = g * 4 + c4;
-  *pos = (k8 * 2 + hi) * 2 + jj;
-}
-// element offset (in elements of the storage type) of W[n][k]
+// Fragment-tiled weight layout of the tensor-core decode GEMV (DESIGN.md
+// "weights in HBM").  A tile is 512 bytes = 32 lanes x 16 B and lane L's 16
+// bytes are exactly its mma A fragment, so a coalesced LDG.128 per lane feeds
+// the MMA with no shuffles or shared-memory staging.  Tiles are row-tile major:
+// tile(rt, kt) at ((rt * KT) + kt) * 512 B.
+//   bf16: tile = 16 rows x 16 k, mma.m16n8k16 A layout (lane = g*4+t holds
+//         rows g, g+8 x k {2t, 2t+1, 2t+8, 2t+9})
+//   int8: tile = 16 rows x 32 k, mma.m16n8k32 s8 A layout (lane = g*4+t holds
+//         4-byte groups: (g, 4t..), (g+8, 4t..), (g, 16+4t..), (g+8, 16+4t..))
 __host__ __device__ __forceinline__ int64_t frag_offset_bf16(int64_t n, int64_t k, int64_t K) {
-  int lane, pos;
-  frag_pos((int)(n & 15), (int)(k & 15), &lane, &pos);
+  const int i = (int)(n & 15), j = (int)(k & 15);
+  const int g = i & 7, hi = i >> 3, c4 = (j & 7) >> 1, jj = j & 1, k8 = j >> 3;
+  const int lane = g * 4 + c4, pos = (k8 * 2 + hi) * 2 + jj;
   return (((n >> 4) * (K >> 4) + (k >> 4)) << 8) + lane * 8 + pos;
 }
 __host__ __device__ __forceinline__ int64_t frag_offset_i8(int64_t n, int64_t k, int64_t K) {
-  int lane, pos;
-  frag_pos((int)(n & 15), (int)(k & 15), &lane, &pos);
-  int ks = (int)((k >> 4) & 1);
-  return (((n >> 4) * (K >> 5) + (k >> 5)) << 9) + lane * 16 + ks * 8 + pos;
+  const int i = (int)(n & 15), j = (int)(k & 31);
+  const int g = i & 7, hi = i >> 3, t = (j & 15) >> 2, q = j & 3, k16 = j >> 4;
+  const int lane = g * 4 + t, reg = k16 * 2 + hi;
+  return (((n >> 4) * (K >> 5) + (k >> 5)) << 9) + lane * 16 + reg * 4 + q;
 }
 
 // host-side count of kernels launched by this library (bench `gpu_launches`)

@@ -20,7 +20,7 @@ __device__ __forceinline__ float load_w(const LinearArgs& a, int64_t n, int64_t 
   if (a.wdtype == kBF16)
     return __bfloat162float(
         reinterpret_cast<const __nv_bfloat16*>(a.w)[frag_offset_bf16(n, k, a.K)]);
-  int q = (int)reinterpret_cast<const uint8_t*>(a.w)[frag_offset_i8(n, k, a.K)] - 128;
+  int q = (int)reinterpret_cast<const int8_t*>(a.w)[frag_offset_i8(n, k, a.K)];
   return (float)q;  // per-row scale applied in the epilogue
 }
 

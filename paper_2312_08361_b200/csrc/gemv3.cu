@@ -1,0 +1,501 @@
+// Decode linear layers (n_new == 1) — persistent stream-K tensor-pipe GEMV.
+//
+//   y[r, n] = epi( rstd_r * sum_k W[n, k] * ((x[r, k] - mu_r) * g[k]) )
+//
+// Work split.  The weight matrix is a sequence of "units" = (group of 64 output
+// channels, one k-tile); every warp of a persistent grid (2 CTAs x 8 warps per
+// SM) owns an equal contiguous slice of units — identical byte counts per
+// warp, no waves, no tail.  Each warp streams its slice through a private
+// STAGES-deep ring of 1-D TMA bulk copies (cp.async.bulk + mbarrier, L2
+// evict-first) and never synchronises with other warps.
+//
+// Arithmetic (int8 weights, 70B/BLOOM): EXACT.  The input row is scaled by a
+// power of two 2^(22-e_r) and rounded to a 23-bit integer q = d0*2^16 +
+// d1*2^8 + d2 (balanced base-256 digits); the three digits of each batch row
+// are three columns of mma.m16n8k32.s8.s8.s32 whose A fragment is the lane's
+// 16-byte weight load (fragment-tiled storage, no conversion).  Digit sums are
+// exact int32, combined in int64; partial sums of a group's k-range are int64
+// atomics (exact => order-independent => deterministic and batch-invariant).
+// One rounding at the end: y = f32(D * 2^(e-22) * rstd * wscale[n]).
+// bf16 weights (7B): A = bf16 tiles, input split hi+lo (two bf16 MMA columns),
+// f32 accumulation; partials fixed-point (2^-32) int64 atomics => deterministic.
+//
+// The pre-norm (RMSNorm / LayerNorm) is folded in: the producer of x wrote
+// per-row (sum, sumsq, max|x g|) partials, reduced here in a fixed order; mu
+// and g are applied while building the B fragments, rstd in the epilogue.
+// The last warp to finish a group writes the group's outputs (+ residual /
+// SwiGLU / GELU epilogue) and the same partial stats for the next consumer.
+#include <type_traits>
+
+#include "common.cuh"
+#include "decode.cuh"
+#include "kernels.cuh"
+
+namespace sp {
+
+namespace {
+
+constexpr int NW = 8;             // warps per CTA
+constexpr int CTAS_PER_SM = 2;
+constexpr int RT = 4;             // 16-row tiles per group (64 output channels)
+constexpr int UNIT_BYTES = RT * 512;
+constexpr int STAGES = 5;         // TMA ring depth per warp (units)
+constexpr int RMAX = 8;           // batch rows per launch
+constexpr double kFix = 4294967296.0;   // bf16 partial fixed point 2^32
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
+                                            uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+__device__ __forceinline__ void mma_s8(int* c, const uint4& a, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k32.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+      : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void mma_bf16(float* c, const uint4& a, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ float gelu_f(float x) {
+  return 0.5f * x * (1.0f + tanhf(0.7978845608028654f * (x + 0.044715f * x * x * x)));
+}
+__device__ __forceinline__ float silu_f(float x) { return x / (1.0f + expf(-x)); }
+
+// digit of 4 integers: byte `sel` of (q + bias), packed; balanced digits:
+// d2 = byte0(q), d1 = byte1(q + 0x80), d0 = byte2(q + 0x8080)  (|q| <= 2^22)
+__device__ __forceinline__ uint32_t digits4(int q0, int q1, int q2, int q3, int bias,
+                                            uint32_t sel_lo, uint32_t sel_hi) {
+  const uint32_t u0 = q0 + bias, u1 = q1 + bias, u2 = q2 + bias, u3 = q3 + bias;
+  const uint32_t lo = __byte_perm(u0, u1, sel_lo);    // bytes: u0.b, u1.b
+  const uint32_t hi = __byte_perm(u2, u3, sel_lo);
+  return __byte_perm(lo, hi, sel_hi);
+}
+
+struct WarpSmem {
+  float mu[RMAX], dscale[RMAX];
+  double yscale[RMAX];
+  uint64_t bar[STAGES];
+};
+
+template <int WT, int NT, int NORMT, bool HASG>
+__global__ void __launch_bounds__(NW * 32, CTAS_PER_SM)
+gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_total) {
+  constexpr int KTILE = (WT == kI8) ? 32 : 16;
+  constexpr int COLS = (WT == kI8) ? 3 : 2;
+  constexpr int XV = (WT == kI8) ? 4 : 2;
+  using XVec = typename std::conditional<WT == kI8, float4, float2>::type;
+  extern __shared__ __align__(128) uint8_t dyn[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* ring = dyn + (size_t)warp * STAGES * UNIT_BYTES;
+  int* ctile = reinterpret_cast<int*>(dyn + (size_t)NW * STAGES * UNIT_BYTES) +
+               warp * (RT * 16 * NT * 8);                           // [64][NT*8]
+  WarpSmem* ws_ = reinterpret_cast<WarpSmem*>(dyn + (size_t)NW * STAGES * UNIT_BYTES +
+                                              (size_t)NW * RT * 16 * NT * 8 * 4) + warp;
+
+  const int64_t gw = (int64_t)blockIdx.x * NW + warp;
+  const int64_t u0 = gw * units / warps_total, u1 = (gw + 1) * units / warps_total;
+  const int64_t KT = a.K / KTILE;
+
+  if (lane == 0) {
+    for (int st = 0; st < STAGES; ++st) mbar_init(&ws_->bar[st], 1);
+    mbar_fence_init();
+  }
+  // ---- per-row parameters from the producer's partial stats ----
+  // CTA-wide: 256 threads load the P_in x Rn partials with several loads in
+  // flight each, then a fixed-order tree (warp shuffles, then warps in order)
+  __shared__ float red_s[NW][RMAX][3];
+  __shared__ float prm_mu[RMAX], prm_ds[RMAX];
+  __shared__ double prm_ys[RMAX];
+  {
+    float S[RMAX], Q[RMAX], M[RMAX];
+#pragma unroll
+    for (int r = 0; r < RMAX; ++r) { S[r] = 0.f; Q[r] = 0.f; M[r] = 0.f; }
+    constexpr int PU = 4;
+    for (int p0 = threadIdx.x; p0 < a.P_in; p0 += PU * NW * 32) {
+#pragma unroll
+      for (int r = 0; r < RMAX; ++r) {
+        if (r >= Rn) break;
+        RowStat t[PU];
+#pragma unroll
+        for (int j = 0; j < PU; ++j) {
+          const int p = p0 + j * NW * 32;
+          t[j] = p < a.P_in ? a.st_in[(int64_t)p * Rs + r0 + r] : RowStat{0.f, 0.f, 0.f, 0.f};
+        }
+#pragma unroll
+        for (int j = 0; j < PU; ++j) {
+          S[r] += t[j].sum; Q[r] += t[j].sumsq; M[r] = fmaxf(M[r], t[j].amax);
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < RMAX; ++r) {
+      const float vs = warp_sum(S[r]), vq = warp_sum(Q[r]), vm = warp_max(M[r]);
+      if (lane == 0) { red_s[warp][r][0] = vs; red_s[warp][r][1] = vq; red_s[warp][r][2] = vm; }
+    }
+    __syncthreads();
+    if (threadIdx.x < Rn) {
+      const int r = threadIdx.x;
+      float s = 0.f, q = 0.f, m = 0.f;
+      for (int w = 0; w < NW; ++w) {
+        s += red_s[w][r][0]; q += red_s[w][r][1]; m = fmaxf(m, red_s[w][r][2]);
+      }
+      const float invK = 1.0f / (float)a.K;
+      float mu = 0.f, rstd = 1.f, bound = m;
+      if (NORMT == NORM_RMS) {
+        rstd = 1.0f / sqrtf(q * invK + a.eps);
+      } else if (NORMT == NORM_LN) {
+        mu = s * invK;
+        rstd = 1.0f / sqrtf(fmaxf(q * invK - mu * mu, 0.f) + a.eps);
+        bound = m + fabsf(mu) * a.gmax;
+      }
+      prm_mu[r] = mu;
+      if (WT == kI8) {
+        int e = 0;
+        if (bound > 0.f) frexpf(bound, &e);          // bound < 2^e
+        prm_ds[r] = bound > 0.f ? ldexpf(1.0f, 22 - e) : 0.f;
+        prm_ys[r] = ldexp(1.0, e - 22) * (double)rstd;
+      } else {
+        prm_ds[r] = 1.0f;
+        prm_ys[r] = (double)rstd / kFix;
+      }
+    }
+    __syncthreads();
+  }
+  if (u0 >= u1) return;
+  if (lane < RMAX) {
+    ws_->mu[lane] = prm_mu[lane];
+    ws_->dscale[lane] = prm_ds[lane];
+    ws_->yscale[lane] = prm_ys[lane];
+  }
+  __syncwarp();
+
+  // ---- this lane's B column: nt*8 + lane/4 -> (batch row, digit | hi/lo) ----
+  int brow[NT], bsub[NT];
+  float bmu[NT], bsc[NT];
+  int bbias[NT];
+  uint32_t bsel_lo[NT];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    const int c = nt * 8 + (lane >> 2);
+    brow[nt] = c / COLS;
+    bsub[nt] = c % COLS;
+    if (brow[nt] >= Rn) brow[nt] = 0;   // unused column: computed, never read
+    bmu[nt] = ws_->mu[brow[nt]];
+    bsc[nt] = ws_->dscale[brow[nt]];
+    // digit dg in {0,1,2}: byte (2-dg) of q + {0x8080, 0x80, 0}
+    bbias[nt] = bsub[nt] == 0 ? 0x8080 : (bsub[nt] == 1 ? 0x80 : 0);
+    const uint32_t b = 2 - bsub[nt];
+    bsel_lo[nt] = b | ((b + 4) << 4);
+  }
+  const int t4 = lane & 3;
+
+  // ---- TMA producer (lane 0) ----
+  const uint8_t* wbase = reinterpret_cast<const uint8_t*>(a.w);
+  const uint64_t policy = evict_first_policy();
+  // producer state (lane 0): next unit to issue as (group, k-tile, ring stage)
+  const int nunits = (int)(u1 - u0);
+  int p_grp = (int)(u0 / KT), p_kt = (int)(u0 % KT), p_st = 0, p_left = nunits;
+  auto issue_next = [&]() {
+    mbar_expect_tx(&ws_->bar[p_st], UNIT_BYTES);
+    const uint8_t* src = wbase + ((((int64_t)p_grp * RT) * KT + p_kt) << 9);
+#pragma unroll
+    for (int t = 0; t < RT; ++t)
+      tma_load_1d(ring + p_st * UNIT_BYTES + t * 512, src + ((int64_t)t * KT << 9), 512,
+                  &ws_->bar[p_st], policy);
+    if (++p_kt == KT) { p_kt = 0; ++p_grp; }
+    if (++p_st == STAGES) p_st = 0;
+    --p_left;
+  };
+  __syncwarp();
+  if (lane == 0)
+    for (int i = 0; i < STAGES && p_left > 0; ++i) issue_next();
+
+  // ---- activation side, prefetched one unit ahead ----
+  XVec xc[NT][2], gc[NT][2], xn[NT][2], gn[NT][2], xm[NT][2], gm[NT][2];
+  auto load_x = [&](int kt, XVec (&xr_)[NT][2], XVec (&gr_)[NT][2]) {
+    const int64_t k0 = (int64_t)kt * KTILE + t4 * XV;
+    constexpr int KOFF = (WT == kI8) ? 16 : 8;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const float* xr = a.x + (int64_t)(r0 + brow[nt]) * a.ldx;
+      xr_[nt][0] = __ldg(reinterpret_cast<const XVec*>(xr + k0));
+      xr_[nt][1] = __ldg(reinterpret_cast<const XVec*>(xr + k0 + KOFF));
+      if (HASG) {
+        gr_[nt][0] = __ldg(reinterpret_cast<const XVec*>(a.g + k0));
+        gr_[nt][1] = __ldg(reinterpret_cast<const XVec*>(a.g + k0 + KOFF));
+      }
+    }
+  };
+  int c_grp = (int)(u0 / KT), c_kt = (int)(u0 % KT), c_st = 0;
+  uint32_t c_ph = 0;
+  load_x(c_kt, xc, gc);
+  if (nunits > 1) load_x(c_kt + 1 == KT ? 0 : c_kt + 1, xn, gn);
+
+  int iacc[RT][NT][4];
+  float facc[RT][NT][4];
+#pragma unroll
+  for (int t = 0; t < RT; ++t)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) { iacc[t][nt][j] = 0; facc[t][nt][j] = 0.f; }
+  int seg_kt0 = c_kt;
+
+  for (int i = 0; i < nunits; ++i) {
+    if (i + 2 < nunits) {
+      int k2 = c_kt + 2;
+      if (k2 >= KT) k2 -= (int)KT;
+      load_x(k2, xm, gm);
+    }
+    mbar_wait(&ws_->bar[c_st], c_ph);
+    const uint8_t* stage = ring + c_st * UNIT_BYTES;
+    uint4 wt[RT];
+#pragma unroll
+    for (int t = 0; t < RT; ++t)
+      wt[t] = *reinterpret_cast<const uint4*>(stage + t * 512 + lane * 16);
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      uint32_t b0 = 0, b1 = 0;
+      {
+        const float mu = bmu[nt], sc = bsc[nt];
+        if constexpr (WT == kI8) {
+          float v[8] = {xc[nt][0].x, xc[nt][0].y, xc[nt][0].z, xc[nt][0].w,
+                        xc[nt][1].x, xc[nt][1].y, xc[nt][1].z, xc[nt][1].w};
+          if (HASG) {
+            const float g8[8] = {gc[nt][0].x, gc[nt][0].y, gc[nt][0].z, gc[nt][0].w,
+                                 gc[nt][1].x, gc[nt][1].y, gc[nt][1].z, gc[nt][1].w};
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[j] *= g8[j];
+          }
+          int q[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            float t = (NORMT == NORM_LN) ? (v[j] - mu) : v[j];
+            q[j] = __float2int_rn(t * sc);
+          }
+          b0 = digits4(q[0], q[1], q[2], q[3], bbias[nt], bsel_lo[nt], 0x5410);
+          b1 = digits4(q[4], q[5], q[6], q[7], bbias[nt], bsel_lo[nt], 0x5410);
+        } else {
+          float v[4] = {xc[nt][0].x, xc[nt][0].y, xc[nt][1].x, xc[nt][1].y};
+          if (HASG) {
+            const float g4[4] = {gc[nt][0].x, gc[nt][0].y, gc[nt][1].x, gc[nt][1].y};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) v[j] *= g4[j];
+          }
+          __nv_bfloat16 h[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float t = (NORMT == NORM_LN) ? (v[j] - mu) : v[j];
+            h[j] = __float2bfloat16_rn(t);
+            if (bsub[nt]) h[j] = __float2bfloat16_rn(t - __bfloat162float(h[j]));
+          }
+          __nv_bfloat162 p0 = __halves2bfloat162(h[0], h[1]), p1 = __halves2bfloat162(h[2], h[3]);
+          b0 = *reinterpret_cast<uint32_t*>(&p0);
+          b1 = *reinterpret_cast<uint32_t*>(&p1);
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < RT; ++t) {
+        if constexpr (WT == kI8) mma_s8(iacc[t][nt], wt[t], b0, b1);
+        else mma_bf16(facc[t][nt], wt[t], b0, b1);
+      }
+    }
+    __syncwarp();
+    if (lane == 0 && p_left > 0) issue_next();
+    if (++c_st == STAGES) { c_st = 0; c_ph ^= 1; }
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        xc[nt][h] = xn[nt][h];
+        xn[nt][h] = xm[nt][h];
+        if (HASG) { gc[nt][h] = gn[nt][h]; gn[nt][h] = gm[nt][h]; }
+      }
+
+    // ---- end of this warp's contribution to a group: flush ----
+    const int64_t grp = c_grp;
+    const int nkt = c_kt + 1 - seg_kt0;
+    const bool grp_end = (c_kt + 1 == KT) || (i + 1 == nunits);
+    if (++c_kt == KT) { c_kt = 0; ++c_grp; seg_kt0 = 0; }
+    if (!grp_end) continue;
+    // C fragments -> ctile[row][col]
+#pragma unroll
+    for (int t = 0; t < RT; ++t)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int row = t * 16 + (lane >> 2) + ((j >> 1) << 3);
+          const int col = nt * 8 + t4 * 2 + (j & 1);
+          ctile[row * (NT * 8) + col] =
+              (WT == kI8) ? iacc[t][nt][j] : __float_as_int(facc[t][nt][j]);
+          iacc[t][nt][j] = 0;
+          facc[t][nt][j] = 0.f;
+        }
+    __syncwarp();
+    unsigned long long* acc64 = reinterpret_cast<unsigned long long*>(a.ws);
+    for (int e = lane; e < RT * 16 * Rn; e += 32) {
+      const int row = e / Rn, r = e % Rn;
+      long long D;
+      const int* cr = ctile + row * (NT * 8);
+      if (WT == kI8)
+        D = (long long)cr[3 * r] * 65536 + (long long)cr[3 * r + 1] * 256 + (long long)cr[3 * r + 2];
+      else
+        D = __double2ll_rn(((double)__int_as_float(cr[2 * r]) +
+                            (double)__int_as_float(cr[2 * r + 1])) * kFix);
+      atomicAdd(acc64 + (int64_t)(r0 + r) * a.N + grp * (RT * 16) + row, (unsigned long long)D);
+    }
+    __syncwarp();
+    int last = 0;
+    if (lane == 0) {
+      int old;
+      asm volatile("atom.release.gpu.global.add.s32 %0, [%1], %2;"
+                   : "=r"(old) : "l"(a.counters + grp), "r"(nkt) : "memory");
+      last = (old + nkt == KT);
+      if (last) {
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        a.counters[grp] = 0;
+      }
+    }
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (!last) continue;
+
+    // ---- epilogue for the group (64 channels x Rn rows) ----
+    float* outv = reinterpret_cast<float*>(ctile);   // reuse: [64][RMAX]
+    for (int e = lane; e < RT * 16 * Rn; e += 32) {
+      const int row = e / Rn, r = e % Rn;
+      const int64_t n = grp * (RT * 16) + row;
+      const long long D = (long long)atomicExch(acc64 + (int64_t)(r0 + r) * a.N + n, 0ull);
+      float v;
+      if (WT == kI8) v = (float)((double)D * ws_->yscale[r] * (double)a.wscale[n]);
+      else v = (float)((double)D * ws_->yscale[r]);
+      outv[row * RMAX + r] = v;
+    }
+    __syncwarp();
+    // outputs: SwiGLU pairs tiles (0,1) and (2,3) -> 32 outputs, else 64
+    const int nout = (a.epi == EPI_SWIGLU) ? 32 : 64;
+    for (int r = 0; r < Rn; ++r) {
+      float S = 0.f, Q = 0.f, M = 0.f;
+      for (int o = lane; o < nout; o += 32) {
+        float val;
+        int64_t col;
+        if (a.epi == EPI_SWIGLU) {
+          const int pr = o >> 4, jj = o & 15;
+          val = silu_f(outv[(pr * 32 + jj) * RMAX + r]) * outv[(pr * 32 + 16 + jj) * RMAX + r];
+          col = grp * 32 + o;
+        } else {
+          col = grp * 64 + o;
+          val = outv[o * RMAX + r];
+          if (a.epi == EPI_RESID) val += a.res[(int64_t)(r0 + r) * a.ldy + col];
+          else if (a.epi == EPI_GELU) val = gelu_f(val);
+        }
+        a.y[(int64_t)(r0 + r) * a.ldy + col] = val;
+        S += val;
+        Q = fmaf(val, val, Q);
+        M = fmaxf(M, fabsf(val * (a.g_next ? a.g_next[col] : 1.f)));
+      }
+      if (a.st_out) {
+        S = warp_sum(S); Q = warp_sum(Q); M = warp_max(M);
+        if (lane == 0) a.st_out[grp * Rs + r0 + r] = RowStat{S, Q, M, 0.f};
+      }
+    }
+    __syncwarp();
+  }
+}
+
+int g_num_sms = 0;
+
+template <int WT, int NT, int NORMT, bool HASG>
+void launch_cfg(const GemvArgs& a, int r0, int rn, cudaStream_t st) {
+  const int KTILE = (WT == kI8) ? 32 : 16;
+  const int64_t units = (a.N / (RT * 16)) * (a.K / KTILE);
+  const int grid = g_num_sms * CTAS_PER_SM;
+  const size_t smem = (size_t)NW * STAGES * UNIT_BYTES + (size_t)NW * RT * 16 * NT * 8 * 4 +
+                      (size_t)NW * sizeof(WarpSmem) + 128;
+  static bool set = false;
+  if (!set) {
+    cudaFuncSetAttribute(gemv3_kernel<WT, NT, NORMT, HASG>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    set = true;
+  }
+  gemv3_kernel<WT, NT, NORMT, HASG><<<grid, NW * 32, smem, st>>>(a, r0, rn, a.R, units,
+                                                                   (int64_t)grid * NW);
+  count_launch();
+}
+
+template <int WT, int NT>
+void launch_nt(const GemvArgs& a, int r0, int rn, cudaStream_t st) {
+  const bool hg = a.g != nullptr;
+  switch (a.norm) {
+    case NORM_RMS: hg ? launch_cfg<WT, NT, NORM_RMS, true>(a, r0, rn, st)
+                      : launch_cfg<WT, NT, NORM_RMS, false>(a, r0, rn, st); break;
+    case NORM_LN: hg ? launch_cfg<WT, NT, NORM_LN, true>(a, r0, rn, st)
+                     : launch_cfg<WT, NT, NORM_LN, false>(a, r0, rn, st); break;
+    default: launch_cfg<WT, NT, NORM_NONE, false>(a, r0, rn, st); break;
+  }
+}
+
+template <int WT>
+void launch_wt(const GemvArgs& a, int r0, int rn, cudaStream_t st) {
+  const int cols = rn * ((WT == kI8) ? 3 : 2);
+  if (cols <= 8) launch_nt<WT, 1>(a, r0, rn, st);
+  else if (cols <= 16) launch_nt<WT, 2>(a, r0, rn, st);
+  else launch_nt<WT, 3>(a, r0, rn, st);
+}
+
+}  // namespace
+
+int64_t gemv3_ws_bytes(int64_t N, int Rmax) { return (int64_t)Rmax * N * 8; }
+int64_t gemv3_counters(int64_t N) { return N / 64 + 1; }
+
+void launch_gemv3(int wdtype, const GemvArgs& a, cudaStream_t st) {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  for (int r0 = 0; r0 < a.R; r0 += RMAX) {
+    const int rn = a.R - r0 < RMAX ? a.R - r0 : RMAX;
+    if (wdtype == kI8) launch_wt<kI8>(a, r0, rn, st);
+    else launch_wt<kBF16>(a, r0, rn, st);
+  }
+}
+
+}  // namespace sp

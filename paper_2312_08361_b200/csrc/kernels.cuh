@@ -48,9 +48,7 @@ void launch_gen_matrix(int wdtype, uint64_t stream, int64_t K, int64_t N, double
 void launch_read_matrix(int wdtype, const void* src, const float* scales, int64_t K, int64_t N,
                         MatPlace place, float* dst, cudaStream_t st);
 
-// decode GEMV (any R; rows processed independently, batch-invariant)
-int64_t gemv_workspace_floats(int64_t N, int64_t K, int wdtype);
-int64_t gemv_counter_ints(int64_t N);
+// decode GEMV for f32 weights (any R; rows independent, batch-invariant)
 void launch_gemv(const LinearArgs& a, cudaStream_t st);
 // prefill GEMM (SIMT fp32, M-invariant)
 void launch_gemm(const LinearArgs& a, cudaStream_t st);

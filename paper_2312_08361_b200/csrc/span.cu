@@ -1,5 +1,6 @@
 // Span runtime: weights, paged KV pool, sessions and the per-block kernel
 // schedule of RealServerEngine.run_cached (SP/server.py:93-100).
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdio>
@@ -9,6 +10,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "decode.cuh"
 #include "kernels.cuh"
 
 namespace {
@@ -79,6 +81,14 @@ struct sp_span {
   float *h = nullptr, *qkvb = nullptr, *ctx = nullptr, *mlp = nullptr, *mlp_raw = nullptr;
   float* gemv_ws = nullptr;
   int* gemv_cnt = nullptr;
+  // fused tensor-core decode path (decode.cuh)
+  int64_t dec_cap_rows = 0;
+  RowStat *st_norm1 = nullptr, *st_ctx = nullptr, *st_norm2 = nullptr, *st_mlp = nullptr;
+  long long* ws2 = nullptr;
+  int* cnt2 = nullptr;
+  float* attn_part = nullptr;
+  int* attn_cnt = nullptr;
+  bool gains_one = true;   // LN/RMS gains are 1 at init (SP/model.py:192-195), never mutated
   int64_t attn_ws_floats = 0;
   float* attn_ws = nullptr;
   std::mutex mu;
@@ -141,6 +151,32 @@ int ensure_scratch(sp_span* s, int64_t rows) {
   SP_CUDA_TRY(cudaMalloc(&s->mlp, cap * s->F * sizeof(float)));
   SP_CUDA_TRY(cudaMalloc(&s->mlp_raw, cap * s->n_up * sizeof(float)));
   s->cap_rows = cap;
+  return SP_OK;
+}
+
+int ensure_decode(sp_span* s, int64_t rows) {
+  if (rows <= s->dec_cap_rows) return SP_OK;
+  int64_t cap = rows < 8 ? 8 : rows;
+  cudaFree(s->st_norm1); cudaFree(s->st_ctx); cudaFree(s->st_norm2); cudaFree(s->st_mlp);
+  cudaFree(s->ws2); cudaFree(s->cnt2); cudaFree(s->attn_part); cudaFree(s->attn_cnt);
+  const int64_t P = std::max<int64_t>(std::max<int64_t>(s->d / 64, s->H), s->n_up / 64);
+  for (RowStat** b : {&s->st_norm1, &s->st_ctx, &s->st_norm2, &s->st_mlp})
+    SP_CUDA_TRY(cudaMalloc(b, P * cap * sizeof(RowStat)));
+  int64_t ws = 0, cnt = 0;
+  const int64_t shapes[4][2] = {{s->n_qkv, s->d}, {s->d, s->d}, {s->n_up, s->d}, {s->d, s->F}};
+  for (auto& sh : shapes) {
+    ws = std::max(ws, gemv3_ws_bytes(sh[0], (int)cap));
+    cnt = std::max(cnt, gemv3_counters(sh[0]));
+  }
+  SP_CUDA_TRY(cudaMalloc(&s->ws2, ws + 16));
+  SP_CUDA_TRY(cudaMemset(s->ws2, 0, ws + 16));
+  SP_CUDA_TRY(cudaMalloc(&s->cnt2, cnt * sizeof(int)));
+  SP_CUDA_TRY(cudaMemset(s->cnt2, 0, cnt * sizeof(int)));
+  SP_CUDA_TRY(cudaMalloc(&s->attn_part,
+                         attn_dec_part_floats((int)cap, s->H, s->hd, s->max_pages) * sizeof(float)));
+  SP_CUDA_TRY(cudaMalloc(&s->attn_cnt, cap * s->kvh * sizeof(int)));
+  SP_CUDA_TRY(cudaMemset(s->attn_cnt, 0, cap * s->kvh * sizeof(int)));
+  s->dec_cap_rows = cap;
   return SP_OK;
 }
 
@@ -260,7 +296,7 @@ void linear(sp_span* s, int wd, void* w, float* sc, int64_t N, int64_t K, const 
   a.w = w; a.wscale = sc; a.wdtype = wd; a.N = N; a.K = K;
   a.x = x; a.ldx = K; a.y = y; a.ldy = ldy; a.res = res; a.epi = epi; a.R = (int)R;
   a.workspace = s->gemv_ws; a.counters = s->gemv_cnt;
-  if (decode) {
+  if (decode && wd == kF32) {
     launch_gemv(a, st);
   } else if (epi == EPI_SWIGLU) {
     a.epi = EPI_STORE;
@@ -273,8 +309,96 @@ void linear(sp_span* s, int wd, void* w, float* sc, int64_t N, int64_t K, const 
   }
 }
 
+// decode (n_new == 1) with bf16/int8 weights: 5 launches per block, norms folded
+// into the GEMVs, RoPE + KV append + page merge folded into attention.
+int run_span_decode_tc(sp_span* s, sp_kv* kv, int b0, int b1, float* y, int width,
+                       cudaStream_t st) {
+  const int64_t R = width;
+  int rc = ensure_scratch(s, R);
+  if (rc) return rc;
+  rc = ensure_decode(s, R);
+  if (rc) return rc;
+  const int wd = s->cfg.weight_dtype, fam = s->cfg.family;
+  const int64_t d = s->d;
+  const int norm = fam == kLlama ? NORM_RMS : NORM_LN;
+  const double kv_elt = s->cfg.kv_dtype == kKVBF16 ? 2.0 : 4.0;
+  const double welt = wd == kI8 ? 1.0 : 2.0;
+  auto wbytes = [&](int64_t N, int64_t K) {
+    return (double)N * K * welt + (wd == kI8 ? 4.0 * N : 0.0);
+  };
+  {
+    ProfScope ps(s, PC_OTHER, 4.0 * R * d, 0, st);
+    launch_row_stats(y, (int)R, d, s->gains_one ? nullptr : s->blocks[b0 - s->start].ln1_g,
+                     s->st_norm1, st);
+  }
+  GemvArgs g{};
+  g.R = (int)R; g.eps = 1e-5f; g.gmax = 1.0f;
+  g.ws = s->ws2; g.counters = s->cnt2;
+  AttnDecArgs at{};
+  at.family = fam; at.kv_dtype = s->cfg.kv_dtype; at.width = width; at.t0 = kv->length;
+  at.H = s->H; at.kvh = s->kvh; at.hd = s->hd; at.qkv = s->qkvb; at.ldqkv = s->n_qkv;
+  at.page_table = kv->d_table; at.max_pages = s->max_pages;
+  at.rope_cos = s->rope_cos; at.rope_sin = s->rope_sin; at.alibi = s->alibi;
+  at.ctx = s->ctx; at.part = s->attn_part; at.counters = s->attn_cnt; at.st_out = s->st_ctx;
+  for (int b = b0 - s->start; b < b1 - s->start; ++b) {
+    BlockW& W = s->blocks[b];
+    const bool last = (b == b1 - s->start - 1);
+    // 1) QKV = RMS/LN(x) @ Wqkv
+    g.w = W.qkv; g.wscale = W.s_qkv; g.N = s->n_qkv; g.K = d; g.x = y; g.ldx = d;
+    g.norm = norm; g.g = s->gains_one ? nullptr : W.ln1_g; g.st_in = s->st_norm1;
+    g.P_in = (int)(d / 64);
+    g.y = s->qkvb; g.ldy = s->n_qkv; g.res = nullptr; g.epi = EPI_STORE;
+    g.st_out = nullptr; g.g_next = nullptr;
+    {
+      ProfScope ps(s, PC_GEMV, wbytes(g.N, g.K) + 4.0 * R * (g.K + g.N), 2.0 * R * g.N * g.K, st);
+      launch_gemv3(wd, g, st);
+    }
+    // 2) attention (RoPE, append, page merge)
+    at.kv_pool = s->pool + (int64_t)b * s->block_stride;
+    {
+      const double kvb = (double)width * (kv->length + 1) * 2 * s->kv * kv_elt;
+      ProfScope ps(s, PC_ATTN_DEC, kvb + 4.0 * R * (s->n_qkv + d),
+                   4.0 * width * (kv->length + 1) * s->H * s->hd, st);
+      launch_attn_decode_fused(at, st);
+    }
+    // 3) x += ctx @ Wo      (stats for norm2)
+    g.w = W.o; g.wscale = W.s_o; g.N = d; g.K = d; g.x = s->ctx; g.ldx = d;
+    g.norm = NORM_NONE; g.g = nullptr; g.st_in = s->st_ctx; g.P_in = s->H;
+    g.y = y; g.ldy = d; g.res = y; g.epi = EPI_RESID; g.st_out = s->st_norm2;
+    g.g_next = s->gains_one ? nullptr : W.ln2_g;
+    {
+      ProfScope ps(s, PC_GEMV, wbytes(g.N, g.K) + 4.0 * R * (g.K + 2 * g.N), 2.0 * R * g.N * g.K, st);
+      launch_gemv3(wd, g, st);
+    }
+    // 4) mlp = act(RMS/LN(x) @ Wup)
+    g.w = W.up; g.wscale = W.s_up; g.N = s->n_up; g.K = d; g.x = y; g.ldx = d;
+    g.norm = norm; g.g = s->gains_one ? nullptr : W.ln2_g; g.st_in = s->st_norm2;
+    g.P_in = (int)(d / 64);
+    g.y = s->mlp; g.ldy = s->F; g.res = nullptr; g.epi = fam == kLlama ? EPI_SWIGLU : EPI_GELU;
+    g.st_out = s->st_mlp; g.g_next = nullptr;
+    {
+      ProfScope ps(s, PC_GEMV, wbytes(g.N, g.K) + 4.0 * R * (g.K + s->F), 2.0 * R * g.N * g.K, st);
+      launch_gemv3(wd, g, st);
+    }
+    // 5) x += mlp @ Wdown   (stats for the next block's norm1)
+    g.w = W.down; g.wscale = W.s_down; g.N = d; g.K = s->F; g.x = s->mlp; g.ldx = s->F;
+    g.norm = NORM_NONE; g.g = nullptr; g.st_in = s->st_mlp; g.P_in = (int)(s->n_up / 64);
+    g.y = y; g.ldy = d; g.res = y; g.epi = EPI_RESID;
+    g.st_out = last ? nullptr : s->st_norm1;
+    g.g_next = (last || s->gains_one) ? nullptr : s->blocks[b + 1].ln1_g;
+    {
+      ProfScope ps(s, PC_GEMV, wbytes(g.N, g.K) + 4.0 * R * (g.K + 2 * g.N), 2.0 * R * g.N * g.K, st);
+      launch_gemv3(wd, g, st);
+    }
+  }
+  SP_CHECK_LAUNCH();
+  return SP_OK;
+}
+
 int run_span(sp_span* s, sp_kv* kv, int b0, int b1, float* y, float* record, int width,
              int n_new, cudaStream_t st) {
+  if (n_new == 1 && s->cfg.weight_dtype != kF32 && !record)
+    return run_span_decode_tc(s, kv, b0, b1, y, width, st);
   const int64_t R = (int64_t)width * n_new;
   const bool decode = (n_new == 1);
   const int wd = s->cfg.weight_dtype;
@@ -488,20 +612,6 @@ int sp_span_create(const sp_config* cfg, int32_t start, int32_t end, int32_t dev
   s->refcount.assign(s->n_pages, 0);
   for (int64_t i = s->n_pages - 1; i >= 0; --i) s->free_pages.push_back((int)i);
 
-  // ---- split-K workspace for the decode GEMVs ----
-  if (wd != kF32) {
-    int64_t ws = 0, cnt = 0;
-    int64_t shapes[4][2] = {{s->n_qkv, d}, {d, d}, {s->n_up, d}, {d, F}};
-    for (auto& sh : shapes) {
-      int64_t w = gemv_workspace_floats(sh[0], sh[1], wd);
-      ws = w > ws ? w : ws;
-      int64_t c = gemv_counter_ints(sh[0]);
-      cnt = c > cnt ? c : cnt;
-    }
-    SP_CUDA_TRY(cudaMalloc(&s->gemv_ws, (ws + 1) * sizeof(float)));
-    SP_CUDA_TRY(cudaMalloc(&s->gemv_cnt, cnt * sizeof(int)));
-    SP_CUDA_TRY(cudaMemset(s->gemv_cnt, 0, cnt * sizeof(int)));
-  }
   SP_CUDA_TRY(cudaDeviceSynchronize());
   *out = s;
   return SP_OK;
@@ -513,6 +623,8 @@ int sp_span_destroy(sp_span* s) {
   cudaFree(s->wmem); cudaFree(s->rope_cos); cudaFree(s->rope_sin); cudaFree(s->alibi);
   cudaFree(s->pool); cudaFree(s->h); cudaFree(s->qkvb); cudaFree(s->ctx); cudaFree(s->mlp);
   cudaFree(s->mlp_raw); cudaFree(s->gemv_ws); cudaFree(s->gemv_cnt); cudaFree(s->attn_ws);
+  cudaFree(s->st_norm1); cudaFree(s->st_ctx); cudaFree(s->st_norm2); cudaFree(s->st_mlp);
+  cudaFree(s->ws2); cudaFree(s->cnt2); cudaFree(s->attn_part); cudaFree(s->attn_cnt);
   for (auto& r : s->prof_recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : s->ev_pool) cudaEventDestroy(e);
   delete s;

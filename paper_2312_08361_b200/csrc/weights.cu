@@ -46,10 +46,11 @@ __global__ void gen_i8_scales_kernel(uint64_t stream, int64_t K, int64_t N, doub
   if (lane == 0) scales[buf_row(n, place)] = __fdiv_rn(m, 127.0f);
 }
 
-// int8 pass 2: one thread writes one lane-chunk (16 B) of a 16x32 tile
+// int8 pass 2: one thread writes one lane-chunk (16 B) of a 16x32 tile,
+// m16n8k32 s8 A-fragment order (common.cuh frag_offset_i8)
 __global__ void gen_i8_pack_kernel(uint64_t stream, int64_t K, int64_t N, double scale,
                                    MatPlace place, const float* __restrict__ scales,
-                                   uint8_t* dst) {
+                                   int8_t* dst) {
   int64_t chunk = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // (rt, kt, lane)
   int64_t KT = K >> 5;
   int64_t total = (N >> 4) * KT * 32;
@@ -57,19 +58,19 @@ __global__ void gen_i8_pack_kernel(uint64_t stream, int64_t K, int64_t N, double
   int lane = (int)(chunk & 31);
   int64_t kt = (chunk >> 5) % KT;
   int64_t rt = (chunk >> 5) / KT;
-  int g = lane >> 2, c = (lane & 3) * 2;
-  uint8_t out[16];
+  int g = lane >> 2, t = lane & 3;
+  __align__(16) int8_t out[16];
 #pragma unroll
-  for (int ks = 0; ks < 2; ++ks) {
+  for (int reg = 0; reg < 4; ++reg) {
+    const int hi = reg & 1, k16 = reg >> 1;
+    const int64_t n = rt * 16 + g + hi * 8;
+    const float s = scales[buf_row(n, place)];
 #pragma unroll
-    for (int p = 0; p < 8; ++p) {
-      int k8 = p >> 2, hi = (p >> 1) & 1, jj = p & 1;
-      int64_t n = rt * 16 + g + hi * 8;
-      int64_t k = kt * 32 + ks * 16 + k8 * 8 + c + jj;
+    for (int q = 0; q < 4; ++q) {
+      const int64_t k = kt * 32 + k16 * 16 + t * 4 + q;
       float w = uniform_value(stream, (uint64_t)(k * N + n), scale);
-      float s = scales[buf_row(n, place)];
-      int q = (s > 0.f) ? __float2int_rn(__fdiv_rn(w, s)) : 0;
-      out[ks * 8 + p] = (uint8_t)(q + 128);
+      int c = (s > 0.f) ? __float2int_rn(__fdiv_rn(w, s)) : 0;
+      out[reg * 4 + q] = (int8_t)c;
     }
   }
   int64_t brt = (place.row0 >> 4) + rt * place.tstride + place.toff;  // buffer row tile
@@ -121,7 +122,7 @@ void launch_gen_matrix(int wdtype, uint64_t stream, int64_t K, int64_t N, double
                                                                    scales); count_launch();
     int64_t chunks = (N / 16) * (K / 32) * 32;
     gen_i8_pack_kernel<<<(unsigned)((chunks + 255) / 256), 256, 0, st>>>(
-        stream, K, N, scale, place, scales, (uint8_t*)dst); count_launch();
+        stream, K, N, scale, place, scales, (int8_t*)dst); count_launch();
   }
 }
 
@@ -138,7 +139,7 @@ __global__ void read_matrix_kernel(int wdtype, const void* src, const float* sca
   } else if (wdtype == kBF16) {
     v = __bfloat162float(((const __nv_bfloat16*)src)[frag_offset_bf16(r, k, bufK)]);
   } else {
-    int q = (int)((const uint8_t*)src)[frag_offset_i8(r, k, bufK)] - 128;
+    int q = (int)((const int8_t*)src)[frag_offset_i8(r, k, bufK)];
     v = __fmul_rn((float)q, scales[r]);
   }
   dst[i] = v;
