@@ -137,6 +137,12 @@ int sp_span_forward_stateless(sp_span* span, int32_t block_begin, int32_t block_
 int sp_span_set_profiling(sp_span* span, int32_t enable);
 int sp_span_profile_read(sp_span* span, int32_t n_classes, double* ms, double* bytes,
                          double* flops, int64_t* launches);
+/* measurement helper: only the 4 decode GEMVs of every block in [b0, b1)
+ * (tensor-core path), reading the activations/statistics left by the last
+ * decode step; *weight_bytes = algorithmic weight bytes of the sequence.
+ * Used by bench.py to time the dominant kernel back to back with CUDA events. */
+int sp_span_decode_gemv_only(sp_span* span, sp_kv* kv, int32_t block_begin, int32_t block_end,
+                             float* y, int32_t width, void* stream, double* weight_bytes);
 /* kernels launched by this library since load (all spans, all devices) */
 int64_t sp_kernel_launches(void);
 

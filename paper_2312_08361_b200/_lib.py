@@ -31,6 +31,7 @@ EXPORTS = (
     "sp_kv_destroy", "sp_kv_length", "sp_kv_width", "sp_kv_reorder", "sp_kv_read",
     "sp_span_forward", "sp_span_forward_stateless", "sp_fnv1a64",
     "sp_span_set_profiling", "sp_span_profile_read", "sp_kernel_launches",
+    "sp_span_decode_gemv_only",
 )
 
 
@@ -90,6 +91,7 @@ def load() -> ctypes.CDLL:
         "sp_span_set_profiling": (I32, [P, I32]),
         "sp_span_profile_read": (I32, [P, I32, P, P, P, P]),
         "sp_kernel_launches": (I64, []),
+        "sp_span_decode_gemv_only": (I32, [P, P, I32, I32, P, I32, P, P]),
     }
     for name in EXPORTS:
         fn = getattr(lib, name)

@@ -42,8 +42,119 @@ __device__ __forceinline__ float rope_val(const float* x, int dd, int half, cons
                    : __fadd_rn(__fmul_rn(x[j + half], c), __fmul_rn(x[j], s));
 }
 
-template <int HD, typename KT>
+// merge the 4 warp partials (fixed order) into this chunk's partial; the
+// last-arriving CTA of (slot, kv head) merges all chunks in ascending order,
+// writes ctx and the per-head partial stats of ctx
+template <int HD>
+__device__ void merge_tail(const AttnDecArgs& a, int G, int slot, int kh, int chunk, int nchunk,
+                           int T, const float (*wm)[GMAX], const float (*wl)[GMAX], float* wo,
+                           float* pm, float* pl, int* last_flag) {
+  __shared__ float wf[4][GMAX];        // per (warp, head) rescale factors
+  __shared__ float hM[GMAX], hL[GMAX];
+  // ---- merge the 4 warps (fixed order) -> chunk partial ----
+  if (threadIdx.x < G) {
+    const int g = threadIdx.x;
+    float M = -INFINITY;
+    for (int w = 0; w < 4; ++w)
+      if (chunk * CHUNK + w * 32 < T) M = fmaxf(M, wm[w][g]);
+    float L = 0.f;
+    for (int w = 0; w < 4; ++w) {
+      const float f = (chunk * CHUNK + w * 32 < T) ? expf(wm[w][g] - M) : 0.f;  // empty warp: 0
+      wf[w][g] = f;
+      L = fmaf(wl[w][g] * (f > 0.f ? 1.f : 0.f), f, L);
+    }
+    hM[g] = M;
+    hL[g] = L;
+  }
+  __syncthreads();
+  const int64_t pstride = (int64_t)G * (HD + 2);
+  float* part = a.part + ((int64_t)(slot * a.kvh + kh) * a.max_pages + chunk) * pstride;
+  for (int i = threadIdx.x; i < G * HD; i += NTH) {
+    const int g = i / HD, dd = i % HD;
+    float O = 0.f;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) O = fmaf(wo[(w * G + g) * HD + dd], wf[w][g], O);
+    part[g * (HD + 2) + dd] = O;
+  }
+  if (threadIdx.x < G) {
+    part[threadIdx.x * (HD + 2) + HD] = hM[threadIdx.x];
+    part[threadIdx.x * (HD + 2) + HD + 1] = hL[threadIdx.x];
+  }
+
+  // ---- last CTA of this (slot, kv head): merge chunks in ascending order ----
+  if (nchunk > 1) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int old;
+      asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;"
+                   : "=r"(old) : "l"(a.counters + slot * a.kvh + kh) : "memory");
+      *last_flag = (old == nchunk - 1);
+    }
+    __syncthreads();
+    if (!*last_flag) return;
+  } else {
+    __syncthreads();
+  }
+  const float* pall = a.part + (int64_t)(slot * a.kvh + kh) * a.max_pages * pstride;
+  for (int e = threadIdx.x; e < nchunk * G; e += NTH) {
+    const int c = e / G, g = e % G;
+    pm[c * GMAX + g] = __ldcg(pall + c * pstride + g * (HD + 2) + HD);
+    pl[c * GMAX + g] = __ldcg(pall + c * pstride + g * (HD + 2) + HD + 1);
+  }
+  __syncthreads();
+  // per head: global max, then per-chunk factor f_c = exp(m_c - M) (in pm), 1/L
+  if (threadIdx.x < G) {
+    const int g = threadIdx.x;
+    float M = -INFINITY;
+    for (int c = 0; c < nchunk; ++c) M = fmaxf(M, pm[c * GMAX + g]);
+    float L = 0.f;
+    for (int c = 0; c < nchunk; ++c) {
+      const float f = expf(pm[c * GMAX + g] - M);
+      pm[c * GMAX + g] = f;
+      L = fmaf(pl[c * GMAX + g], f, L);
+    }
+    hL[g] = L;
+  }
+  __syncthreads();
+  float* outh = wo;
+  for (int i = threadIdx.x; i < G * HD; i += NTH) {
+    const int g = i / HD, dd = i % HD;
+    float O = 0.f;
+    for (int c0 = 0; c0 < nchunk; c0 += 8) {
+      float wv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        wv[u] = (c0 + u < nchunk) ? __ldcg(pall + (c0 + u) * pstride + g * (HD + 2) + dd) : 0.f;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (c0 + u < nchunk) O = fmaf(wv[u], pm[(c0 + u) * GMAX + g], O);
+    }
+    const float c = O / hL[g];
+    outh[i] = c;
+    a.ctx[(int64_t)slot * a.H * HD + (kh * G + g) * HD + dd] = c;
+  }
+  if (threadIdx.x == 0 && nchunk > 1) a.counters[slot * a.kvh + kh] = 0;
+  __syncthreads();
+  if (a.st_out) {
+    // one warp per head, fixed shuffle tree (deterministic)
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int g = warp; g < G; g += NTH / 32) {
+      float S = 0.f, Q = 0.f, Mx = 0.f;
+      for (int dd = lane; dd < HD; dd += 32) {
+        const float c = outh[g * HD + dd];
+        S += c;
+        Q = fmaf(c, c, Q);
+        Mx = fmaxf(Mx, fabsf(c));
+      }
+      S = warp_sum(S); Q = warp_sum(Q); Mx = warp_max(Mx);
+      if (lane == 0) a.st_out[(int64_t)(kh * G + g) * a.width + slot] = RowStat{S, Q, Mx, 0.f};
+    }
+  }
+}
+
+template <int HD, typename KT, int GT>
 __global__ void __launch_bounds__(NTH) attn_dec2_kernel(AttnDecArgs a) {
+  constexpr int GC = GT ? GT : GMAX;              // compile-time bound on heads per kv head
   constexpr int DPL = HD >= 32 ? HD / 32 : 1;     // dims per lane in P.V
   constexpr int ACT = HD >= 32 ? 32 : HD;         // lanes active in P.V
   __shared__ __align__(16) float qT[HD][GMAX];    // [dim][head]
@@ -51,7 +162,7 @@ __global__ void __launch_bounds__(NTH) attn_dec2_kernel(AttnDecArgs a) {
   __shared__ float wm[4][GMAX], wl[4][GMAX];
   __shared__ int last_flag;
   extern __shared__ __align__(16) float dsm[];
-  const int G = a.H / a.kvh;
+  const int G = GT ? GT : a.H / a.kvh;
   float* wo = dsm;                                // [4][G][HD]
   float* pm = dsm + 4 * G * HD;                   // [max_pages][GMAX] chunk maxima
   float* pl = pm + a.max_pages * GMAX;            // [max_pages][GMAX] chunk sums
@@ -117,15 +228,15 @@ __global__ void __launch_bounds__(NTH) attn_dec2_kernel(AttnDecArgs a) {
   }
   // ---- scores: lane = position (its K row read straight from the page, 16 B
   // at a time: whole sectors), G accumulators ----
-  float s[GMAX];
+  float s[((GC + 3) / 4) * 4];
 #pragma unroll
-  for (int g = 0; g < GMAX; ++g) s[g] = 0.f;
+  for (int g = 0; g < ((GC + 3) / 4) * 4; ++g) s[g] = 0.f;
   if (lane < nv) {
     constexpr int VE = 16 / sizeof(KT) < HD ? 16 / sizeof(KT) : HD;   // elements per load
     constexpr int NCH = HD / VE;
-    constexpr int BLK = NCH < 8 ? NCH : 8;                             // loads in flight
+    constexpr int BLK = NCH < 2 ? NCH : 2;                             // loads in flight
     const KT* krow = kbase + lane * HD;
-#pragma unroll
+#pragma unroll 1
     for (int c0 = 0; c0 < NCH; c0 += BLK) {
       KT kv[BLK][VE];
 #pragma unroll
@@ -144,7 +255,7 @@ __global__ void __launch_bounds__(NTH) attn_dec2_kernel(AttnDecArgs a) {
           const float k = to_f32(kv[c][e]);
           const float4* q4 = reinterpret_cast<const float4*>(qT[dd]);
 #pragma unroll
-          for (int g4 = 0; g4 < GMAX / 4; ++g4) {
+          for (int g4 = 0; g4 < (GC + 3) / 4; ++g4) {
             if (g4 * 4 >= G) break;
             const float4 qv = q4[g4];
             s[g4 * 4 + 0] = fmaf(qv.x, k, s[g4 * 4 + 0]);
@@ -158,7 +269,7 @@ __global__ void __launch_bounds__(NTH) attn_dec2_kernel(AttnDecArgs a) {
   const float rs = sqrtf((float)HD);
   const int pos = p0 + lane;
 #pragma unroll
-  for (int g = 0; g < GMAX; ++g) {
+  for (int g = 0; g < GC; ++g) {
     if (g >= G) break;
     float sc = -INFINITY;
     if (lane < nv) {
@@ -176,16 +287,16 @@ __global__ void __launch_bounds__(NTH) attn_dec2_kernel(AttnDecArgs a) {
 
   // ---- P.V: lane = dims, G x DPL accumulators ----
   if (lane < ACT && nv > 0) {
-    float o[GMAX][DPL];
+    float o[((GC + 3) / 4) * 4][DPL];
 #pragma unroll
-    for (int g = 0; g < GMAX; ++g)
+    for (int g = 0; g < ((GC + 3) / 4) * 4; ++g)
 #pragma unroll
       for (int e = 0; e < DPL; ++e) o[g][e] = 0.f;
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
       const float4* p4 = reinterpret_cast<const float4*>(ps[warp][j]);
 #pragma unroll
-      for (int g4 = 0; g4 < GMAX / 4; ++g4) {
+      for (int g4 = 0; g4 < (GC + 3) / 4; ++g4) {
         if (g4 * 4 >= G) break;
         const float4 pv = p4[g4];
 #pragma unroll
@@ -198,7 +309,7 @@ __global__ void __launch_bounds__(NTH) attn_dec2_kernel(AttnDecArgs a) {
       }
     }
 #pragma unroll
-    for (int g = 0; g < GMAX; ++g) {
+    for (int g = 0; g < GC; ++g) {
       if (g >= G) break;
 #pragma unroll
       for (int e = 0; e < DPL; ++e) wo[(warp * G + g) * HD + lane * DPL + e] = o[g][e];
@@ -206,99 +317,262 @@ __global__ void __launch_bounds__(NTH) attn_dec2_kernel(AttnDecArgs a) {
   }
   __syncthreads();
 
-  // ---- merge the 4 warps (fixed order) -> chunk partial ----
-  const int64_t pstride = (int64_t)G * (HD + 2);
-  float* part = a.part + ((int64_t)(slot * a.kvh + kh) * a.max_pages + chunk) * pstride;
-  for (int i = threadIdx.x; i < G * HD; i += NTH) {
-    const int g = i / HD, dd = i % HD;
-    float M = -INFINITY;
-    for (int w = 0; w < 4; ++w) M = fmaxf(M, wm[w][g]);
-    float L = 0.f, O = 0.f;
-    for (int w = 0; w < 4; ++w) {
-      if (chunk * CHUNK + w * 32 >= T) continue;      // warp had no positions
-      const float f = expf(wm[w][g] - M);
-      L = fmaf(wl[w][g], f, L);
-      O = fmaf(wo[(w * G + g) * HD + dd], f, O);
-    }
-    part[g * (HD + 2) + dd] = O;
-    if (dd == 0) {
-      part[g * (HD + 2) + HD] = M;
-      part[g * (HD + 2) + HD + 1] = L;
-    }
-  }
-
-  // ---- last CTA of this (slot, kv head): merge chunks in ascending order ----
-  if (nchunk > 1) {
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0)
-      last_flag = (atomicAdd(a.counters + slot * a.kvh + kh, 1) == nchunk - 1);
-    __syncthreads();
-    if (!last_flag) return;
-    __threadfence();
-  } else {
-    __syncthreads();
-  }
-  const float* pall = a.part + (int64_t)(slot * a.kvh + kh) * a.max_pages * pstride;
-  for (int e = threadIdx.x; e < nchunk * G; e += NTH) {
-    const int c = e / G, g = e % G;
-    pm[c * GMAX + g] = __ldcg(pall + c * pstride + g * (HD + 2) + HD);
-    pl[c * GMAX + g] = __ldcg(pall + c * pstride + g * (HD + 2) + HD + 1);
-  }
-  __syncthreads();
-  float* outh = wo;
-  for (int i = threadIdx.x; i < G * HD; i += NTH) {
-    const int g = i / HD, dd = i % HD;
-    float M = -INFINITY;
-    for (int c = 0; c < nchunk; ++c) M = fmaxf(M, pm[c * GMAX + g]);
-    float L = 0.f, O = 0.f;
-    for (int c0 = 0; c0 < nchunk; c0 += 8) {
-      float wv[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        wv[u] = (c0 + u < nchunk) ? __ldcg(pall + (c0 + u) * pstride + g * (HD + 2) + dd) : 0.f;
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        if (c0 + u < nchunk) {
-          const float f = expf(pm[(c0 + u) * GMAX + g] - M);
-          L = fmaf(pl[(c0 + u) * GMAX + g], f, L);
-          O = fmaf(wv[u], f, O);
-        }
-      }
-    }
-    const float c = O / L;
-    outh[i] = c;
-    a.ctx[(int64_t)slot * a.H * HD + (kh * G + g) * HD + dd] = c;
-  }
-  if (threadIdx.x == 0 && nchunk > 1) a.counters[slot * a.kvh + kh] = 0;
-  __syncthreads();
-  if (a.st_out && threadIdx.x < G) {
-    const int g = threadIdx.x;
-    float S = 0.f, Q = 0.f, Mx = 0.f;
-    for (int dd = 0; dd < HD; ++dd) {
-      const float c = outh[g * HD + dd];
-      S += c;
-      Q = fmaf(c, c, Q);
-      Mx = fmaxf(Mx, fabsf(c));
-    }
-    a.st_out[(int64_t)(kh * G + g) * a.width + slot] = RowStat{S, Q, Mx, 0.f};
-  }
+  merge_tail<HD>(a, G, slot, kh, chunk, nchunk, T, wm, wl, wo, pm, pl, &last_flag);
 }
 
-template <int HD, typename KT>
-void launch_t(const AttnDecArgs& a, cudaStream_t st) {
+
+// ---------------------------------------------------------------------------
+// tensor-core variant (bf16 KV, hd % 16 == 0, G <= 8): per warp 32 positions,
+// S = K.q^T and O^T = V^T.P on mma.m16n8k16 (q and P split hi+lo in bf16, so
+// the products keep ~16 mantissa bits; K/V are exact cache values), K/V tiles
+// staged by cp.async and fed by ldmatrix (.trans for V^T).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void mma_bf16_16816(float* c, uint32_t a0, uint32_t a1, uint32_t a2,
+                                               uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t* r, const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"((uint32_t)__cvta_generic_to_shared(p)));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t* r, const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"((uint32_t)__cvta_generic_to_shared(p)));
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(valid ? 16 : 0));
+}
+
+template <int HD>
+__global__ void __launch_bounds__(NTH) attn_dec_mma_kernel(AttnDecArgs a) {
+  constexpr int RS = HD + 8;                      // padded smem row (bf16), breaks ldmatrix conflicts
+  __shared__ __align__(16) __nv_bfloat16 qh[8][RS], ql[8][RS];      // [head][dim]
+  __shared__ __align__(16) __nv_bfloat16 ph[4][8][40], pl_[4][8][40]; // [warp][head][pos]
+  __shared__ float wm[4][GMAX], wl[4][GMAX];
+  __shared__ int last_flag;
+  extern __shared__ __align__(16) float dsm[];
+  const int G = a.H / a.kvh;
+  typedef __nv_bfloat16 Row[RS];
+  Row* Kt = reinterpret_cast<Row*>(dsm);          // [4*32][RS]
+  Row* Vt = Kt + 4 * 32;                          // [4*32][RS]
+  float* wo = reinterpret_cast<float*>(Vt + 4 * 32);   // [4][G][HD]
+  float* pmv = wo + 4 * G * HD;
+  float* plv = pmv + a.max_pages * GMAX;
+
+  const int slot = blockIdx.x / a.kvh, kh = blockIdx.x % a.kvh;
+  const int chunk = blockIdx.y;
+  const int T = a.t0 + 1;
+  const int nchunk = (T + CHUNK - 1) / CHUNK;
+  if (chunk >= nchunk) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g8 = lane >> 2, t4 = lane & 3;
+  const int half = HD / 2;
+  const float* qrow = a.qkv + (int64_t)slot * a.ldqkv;
+  const float* cs = a.rope_cos ? a.rope_cos + (int64_t)a.t0 * half : nullptr;
+  const float* sn = a.rope_sin ? a.rope_sin + (int64_t)a.t0 * half : nullptr;
+
+  // ---- q (RoPE) -> bf16 hi/lo, [head][dim]; unused heads zero.  All loads
+  // of the thread are issued before any arithmetic (one latency, not eight) ----
+  {
+    constexpr int PER = 8 * HD / NTH;
+    float x1[PER], x2[PER], c[PER], sg[PER];
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int i = threadIdx.x + u * NTH, g = i / HD, dd = i % HD, j = dd % half;
+      const float* q = qrow + (kh * min(G - 1, g) + 0) * 0 + (kh * G + min(g, G - 1)) * HD;
+      x1[u] = q[j];
+      x2[u] = q[j + half];
+      c[u] = cs ? cs[j] : 1.f;
+      sg[u] = sn ? sn[j] : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int i = threadIdx.x + u * NTH, g = i / HD, dd = i % HD;
+      float v = 0.f;
+      if (g < G) {
+        if (a.family == kLlama)
+          v = dd < half ? __fsub_rn(__fmul_rn(x1[u], c[u]), __fmul_rn(x2[u], sg[u]))
+                        : __fadd_rn(__fmul_rn(x2[u], c[u]), __fmul_rn(x1[u], sg[u]));
+        else
+          v = dd < half ? x1[u] : x2[u];
+      }
+      const __nv_bfloat16 h = __float2bfloat16_rn(v);
+      qh[g][dd] = h;
+      ql[g][dd] = __float2bfloat16_rn(v - __bfloat162float(h));
+    }
+  }
+  // ---- append the new position ----
+  if (a.t0 / CHUNK == chunk) {
+    const int page = a.page_table[slot * a.max_pages + a.t0 / kPageTokens];
+    __nv_bfloat16* kp = page_ptr<__nv_bfloat16>(a.kv_pool, page, 0, a.kvh, kh, HD) + (a.t0 % kPageTokens) * HD;
+    __nv_bfloat16* vp = page_ptr<__nv_bfloat16>(a.kv_pool, page, 1, a.kvh, kh, HD) + (a.t0 % kPageTokens) * HD;
+    const float* kn = qrow + a.H * HD + kh * HD;
+    const float* vn = qrow + a.H * HD + a.kvh * HD + kh * HD;
+    for (int dd = threadIdx.x; dd < HD; dd += NTH) {
+      kp[dd] = __float2bfloat16_rn((a.family == kLlama) ? rope_val(kn, dd, half, cs, sn) : kn[dd]);
+      vp[dd] = __float2bfloat16_rn(vn[dd]);
+    }
+  }
+  __syncthreads();
+
+  // ---- stage this warp's 32 K/V rows (cp.async, zero-fill past T) ----
+  const int p0 = chunk * CHUNK + warp * 32;
+  const int nv = max(0, min(32, T - p0));
+  const int page = a.page_table[slot * a.max_pages + min(p0, T - 1) / kPageTokens];
+  const __nv_bfloat16* kbase = page_ptr<__nv_bfloat16>(a.kv_pool, page, 0, a.kvh, kh, HD) + (p0 % kPageTokens) * HD;
+  const __nv_bfloat16* vbase = page_ptr<__nv_bfloat16>(a.kv_pool, page, 1, a.kvh, kh, HD) + (p0 % kPageTokens) * HD;
+  constexpr int CPR = HD / 8;                     // 16-byte chunks per row
+  for (int c = lane; c < 32 * CPR; c += 32) {
+    const int j = c / CPR, e = (c % CPR) * 8;
+    const bool ok = j < nv;
+    cp_async16(&Kt[warp * 32 + j][e], kbase + (ok ? j : 0) * HD + e, ok);
+    cp_async16(&Vt[warp * 32 + j][e], vbase + (ok ? j : 0) * HD + e, ok);
+  }
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+  __syncwarp();
+
+  // ---- S[32 x 8] = K . q^T ----
+  float sacc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+  for (int ks = 0; ks < HD / 16; ++ks) {
+    const uint32_t bh0 = *reinterpret_cast<const uint32_t*>(&qh[g8][ks * 16 + 2 * t4]);
+    const uint32_t bh1 = *reinterpret_cast<const uint32_t*>(&qh[g8][ks * 16 + 2 * t4 + 8]);
+    const uint32_t bl0 = *reinterpret_cast<const uint32_t*>(&ql[g8][ks * 16 + 2 * t4]);
+    const uint32_t bl1 = *reinterpret_cast<const uint32_t*>(&ql[g8][ks * 16 + 2 * t4 + 8]);
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      uint32_t af[4];
+      ldsm_x4(af, &Kt[warp * 32 + mt * 16 + (lane & 15)][ks * 16 + (lane >> 4) * 8]);
+      mma_bf16_16816(sacc[mt], af[0], af[1], af[2], af[3], bh0, bh1);
+      mma_bf16_16816(sacc[mt], af[0], af[1], af[2], af[3], bl0, bl1);
+    }
+  }
+  // ---- softmax per head over the warp's 32 positions ----
+  // lane holds S[pos mt*16 + g8 (+8)][head 2*t4 + {0,1}]
+  const float rs = sqrtf((float)HD);
+  float m2[2], l2[2];
+#pragma unroll
+  for (int hc = 0; hc < 2; ++hc) {
+    const int head = 2 * t4 + hc;
+    float mx = -INFINITY;
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        const int pos = mt * 16 + g8 + hh * 8;
+        float v = sacc[mt][hh * 2 + hc] / rs;
+        if (a.family == kBloom && head < G) v += a.alibi[kh * G + head] * (float)(p0 + pos - (T - 1));
+        if (pos >= nv) v = -INFINITY;
+        sacc[mt][hh * 2 + hc] = v;
+        mx = fmaxf(mx, v);
+      }
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+    float sum = 0.f;
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        const int pos = mt * 16 + g8 + hh * 8;
+        const float e = (pos < nv) ? expf(sacc[mt][hh * 2 + hc] - mx) : 0.f;
+        sum += e;
+        const __nv_bfloat16 h = __float2bfloat16_rn(e);
+        ph[warp][head][pos] = h;
+        pl_[warp][head][pos] = __float2bfloat16_rn(e - __bfloat162float(h));
+      }
+    sum += __shfl_xor_sync(0xffffffffu, sum, 4);
+    sum += __shfl_xor_sync(0xffffffffu, sum, 8);
+    sum += __shfl_xor_sync(0xffffffffu, sum, 16);
+    m2[hc] = mx;
+    l2[hc] = sum;
+  }
+  if (g8 == 0) {
+#pragma unroll
+    for (int hc = 0; hc < 2; ++hc) {
+      const int head = 2 * t4 + hc;
+      if (head < G) { wm[warp][head] = m2[hc]; wl[warp][head] = l2[hc]; }
+    }
+  }
+  __syncwarp();
+
+  // ---- O^T[HD x 8] = V^T . P ----
+  const int jrow = (lane & 7) + ((lane >> 4) << 3);      // ldmatrix.trans source row (pos)
+  const int dcol = ((lane >> 3) & 1) * 8;                // +8 dims for matrices 1 and 3
+#pragma unroll
+  for (int mt = 0; mt < HD / 16; ++mt) {
+    float oacc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      uint32_t af[4];
+      ldsm_x4_t(af, &Vt[warp * 32 + ks * 16 + jrow][mt * 16 + dcol]);
+      const uint32_t bh0 = *reinterpret_cast<const uint32_t*>(&ph[warp][g8][ks * 16 + 2 * t4]);
+      const uint32_t bh1 = *reinterpret_cast<const uint32_t*>(&ph[warp][g8][ks * 16 + 2 * t4 + 8]);
+      const uint32_t bl0 = *reinterpret_cast<const uint32_t*>(&pl_[warp][g8][ks * 16 + 2 * t4]);
+      const uint32_t bl1 = *reinterpret_cast<const uint32_t*>(&pl_[warp][g8][ks * 16 + 2 * t4 + 8]);
+      mma_bf16_16816(oacc, af[0], af[1], af[2], af[3], bh0, bh1);
+      mma_bf16_16816(oacc, af[0], af[1], af[2], af[3], bl0, bl1);
+    }
+    // oacc: O^T[dim mt*16 + g8 (+8)][head 2*t4 + {0,1}]
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int head = 2 * t4 + (j & 1);
+      const int dim = mt * 16 + g8 + ((j >> 1) << 3);
+      if (head < G) wo[(warp * G + head) * HD + dim] = oacc[j];
+    }
+  }
+  __syncthreads();
+  merge_tail<HD>(a, G, slot, kh, chunk, nchunk, T, wm, wl, wo, pmv, plv, &last_flag);
+}
+
+template <int HD>
+void launch_mma(const AttnDecArgs& a, cudaStream_t st) {
+  const int T = a.t0 + 1;
+  dim3 grid(a.width * a.kvh, (T + CHUNK - 1) / CHUNK);
+  const int G = a.H / a.kvh;
+  const size_t smem = (size_t)2 * 4 * 32 * (HD + 8) * 2 +
+                      (size_t)(4 * G * HD + 2 * a.max_pages * GMAX) * sizeof(float);
+  static size_t set = 0;
+  if (smem > set) {
+    cudaFuncSetAttribute(attn_dec_mma_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    set = smem;
+  }
+  attn_dec_mma_kernel<HD><<<grid, NTH, smem, st>>>(a);
+  count_launch();
+}
+
+template <int HD, typename KT, int GT>
+void launch_g(const AttnDecArgs& a, cudaStream_t st) {
   const int T = a.t0 + 1;
   dim3 grid(a.width * a.kvh, (T + CHUNK - 1) / CHUNK);
   const int G = a.H / a.kvh;
   const size_t smem = (size_t)(4 * G * HD + 2 * a.max_pages * GMAX) * sizeof(float);
   static size_t set = 0;
   if (smem > set) {
-    cudaFuncSetAttribute(attn_dec2_kernel<HD, KT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(attn_dec2_kernel<HD, KT, GT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
     set = smem;
   }
-  attn_dec2_kernel<HD, KT><<<grid, NTH, smem, st>>>(a);
+  attn_dec2_kernel<HD, KT, GT><<<grid, NTH, smem, st>>>(a);
   count_launch();
+}
+
+template <int HD, typename KT>
+void launch_t(const AttnDecArgs& a, cudaStream_t st) {
+  switch (a.H / a.kvh) {
+    case 1: launch_g<HD, KT, 1>(a, st); break;
+    case 8: launch_g<HD, KT, 8>(a, st); break;
+    default: launch_g<HD, KT, 0>(a, st); break;
+  }
 }
 
 template <typename KT>
@@ -319,6 +593,12 @@ int64_t attn_dec_part_floats(int width, int H, int hd, int max_pages) {
 }
 
 void launch_attn_decode_fused(const AttnDecArgs& a, cudaStream_t st) {
+  const int G = a.H / a.kvh;
+  if (a.kv_dtype == kKVBF16 && G <= 8 && (a.hd == 64 || a.hd == 128)) {
+    if (a.hd == 128) launch_mma<128>(a, st);
+    else launch_mma<64>(a, st);
+    return;
+  }
   if (a.kv_dtype == kKVBF16) dispatch<__nv_bfloat16>(a, st);
   else dispatch<float>(a, st);
 }

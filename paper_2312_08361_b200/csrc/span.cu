@@ -312,7 +312,7 @@ void linear(sp_span* s, int wd, void* w, float* sc, int64_t N, int64_t K, const 
 // decode (n_new == 1) with bf16/int8 weights: 5 launches per block, norms folded
 // into the GEMVs, RoPE + KV append + page merge folded into attention.
 int run_span_decode_tc(sp_span* s, sp_kv* kv, int b0, int b1, float* y, int width,
-                       cudaStream_t st) {
+                       cudaStream_t st, bool gemv_only = false) {
   const int64_t R = width;
   int rc = ensure_scratch(s, R);
   if (rc) return rc;
@@ -326,7 +326,7 @@ int run_span_decode_tc(sp_span* s, sp_kv* kv, int b0, int b1, float* y, int widt
   auto wbytes = [&](int64_t N, int64_t K) {
     return (double)N * K * welt + (wd == kI8 ? 4.0 * N : 0.0);
   };
-  {
+  if (!gemv_only) {
     ProfScope ps(s, PC_OTHER, 4.0 * R * d, 0, st);
     launch_row_stats(y, (int)R, d, s->gains_one ? nullptr : s->blocks[b0 - s->start].ln1_g,
                      s->st_norm1, st);
@@ -355,7 +355,7 @@ int run_span_decode_tc(sp_span* s, sp_kv* kv, int b0, int b1, float* y, int widt
     }
     // 2) attention (RoPE, append, page merge)
     at.kv_pool = s->pool + (int64_t)b * s->block_stride;
-    {
+    if (!gemv_only) {
       const double kvb = (double)width * (kv->length + 1) * 2 * s->kv * kv_elt;
       ProfScope ps(s, PC_ATTN_DEC, kvb + 4.0 * R * (s->n_qkv + d),
                    4.0 * width * (kv->length + 1) * s->H * s->hd, st);
@@ -813,6 +813,20 @@ int sp_span_profile_read(sp_span* s, int32_t n_classes, double* ms, double* byte
 }
 
 int64_t sp_kernel_launches(void) { return sp::g_launches.load(); }
+
+int sp_span_decode_gemv_only(sp_span* s, sp_kv* kv, int32_t b0, int32_t b1, float* y,
+                             int32_t width, void* stream, double* weight_bytes) {
+  if (!s || !kv || !y) SP_FAIL(SP_ERR_ARG, "null argument");
+  if (s->cfg.weight_dtype == kF32) SP_FAIL(SP_ERR_ARG, "tensor-core decode path only");
+  SP_CUDA_TRY(cudaSetDevice(s->device));
+  const double welt = s->cfg.weight_dtype == kI8 ? 1.0 : 2.0;
+  const int64_t d = s->d;
+  double wb = 0;
+  const int64_t shapes[4][2] = {{s->n_qkv, d}, {d, d}, {s->n_up, d}, {d, s->F}};
+  for (auto& sh : shapes) wb += (double)sh[0] * sh[1] * welt + (welt == 1.0 ? 4.0 * sh[0] : 0.0);
+  if (weight_bytes) *weight_bytes = wb * (b1 - b0);
+  return run_span_decode_tc(s, kv, b0, b1, y, width, (cudaStream_t)stream, true);
+}
 
 uint64_t sp_fnv1a64(const uint8_t* data, int64_t n) {
   uint64_t h = 0xCBF29CE484222325ull;  // SP/wire.py:35-44
