@@ -69,6 +69,7 @@ typedef struct sp_config {
 
 typedef struct sp_span sp_span; /* weights + KV pool of blocks [start, end) on one device */
 typedef struct sp_kv sp_kv;     /* one session's paged attention caches over the span */
+typedef struct sp_head sp_head; /* client head: tied embedding + greedy pick */
 
 const char* sp_last_error(void);
 int sp_version(void);
@@ -127,6 +128,16 @@ int sp_span_forward(sp_span* span, sp_kv* kv, int32_t block_begin, int32_t block
 int sp_span_forward_stateless(sp_span* span, int32_t block_begin, int32_t block_end,
                               const float* x, float* y, float* record, int32_t batch,
                               int32_t tokens, void* stream);
+
+/* ---- client head (SP/model.py:388-400) -------------
+ * embedding generated on the device bit-identically (role 11, block n_blocks);
+ * embed = row gather; greedy = argmax(row @ E^T), ties to the lowest id */
+int sp_head_create(const sp_config* cfg, int32_t device, sp_head** out);
+int sp_head_destroy(sp_head* head);
+int sp_head_embed(sp_head* head, const int32_t* tokens_host, int32_t n, float* out_dev,
+                  void* stream);
+int sp_head_greedy(sp_head* head, const float* row_dev, int32_t* token_host, void* stream);
+int sp_head_read_embedding(sp_head* head, float* dst_host);
 
 /* ---- measurement ----------------------------------------------------------
  * With profiling on, every launch of the span schedule is bracketed by CUDA

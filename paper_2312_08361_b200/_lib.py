@@ -31,7 +31,8 @@ EXPORTS = (
     "sp_kv_destroy", "sp_kv_length", "sp_kv_width", "sp_kv_reorder", "sp_kv_read",
     "sp_span_forward", "sp_span_forward_stateless", "sp_fnv1a64",
     "sp_span_set_profiling", "sp_span_profile_read", "sp_kernel_launches",
-    "sp_span_decode_gemv_only",
+    "sp_span_decode_gemv_only", "sp_head_create", "sp_head_destroy", "sp_head_embed",
+    "sp_head_greedy", "sp_head_read_embedding",
 )
 
 
@@ -92,6 +93,11 @@ def load() -> ctypes.CDLL:
         "sp_span_profile_read": (I32, [P, I32, P, P, P, P]),
         "sp_kernel_launches": (I64, []),
         "sp_span_decode_gemv_only": (I32, [P, P, I32, I32, P, I32, P, P]),
+        "sp_head_create": (I32, [ctypes.POINTER(SpConfig), I32, ctypes.POINTER(P)]),
+        "sp_head_destroy": (I32, [P]),
+        "sp_head_embed": (I32, [P, P, I32, P, P]),
+        "sp_head_greedy": (I32, [P, P, P, P]),
+        "sp_head_read_embedding": (I32, [P, P]),
     }
     for name in EXPORTS:
         fn = getattr(lib, name)
