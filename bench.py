@@ -372,7 +372,7 @@ def run_b200(args) -> None:
             "ms_per_step": dec_ms / max(steps_done, 1e-9) * (sessions / max(1, world)) * world
             if world > 1 else dec_ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "int8 weights x f32 activations (f16 hi/lo tensor-core split)",
+            "dtype": "int8 (weights x 23-bit int digit activations, exact int32 tensor-core MMA; f32 residual)",
             "data": "synthetic (splitmix64 random-init weights per SP/model.py:55-60, N(0,1) "
                     "hidden rows)",
             "config": {"workload": f"llama2-70b-shape int8 span decode, batch 1, context "

@@ -60,26 +60,23 @@ template <> __device__ __forceinline__ __nv_bfloat16 from_f32<__nv_bfloat16>(flo
 __device__ __forceinline__ float to_f32(float v) { return v; }
 __device__ __forceinline__ float to_f32(__nv_bfloat16 v) { return __bfloat162float(v); }
 
-// Fragment-tiled weight layout of the tensor-core decode GEMV (DESIGN.md
-// "weights in HBM").  A tile is 512 bytes = 32 lanes x 16 B and lane L's 16
-// bytes are exactly its mma A fragment, so a coalesced LDG.128 per lane feeds
-// the MMA with no shuffles or shared-memory staging.  Tiles are row-tile major:
-// tile(rt, kt) at ((rt * KT) + kt) * 512 B.
-//   bf16: tile = 16 rows x 16 k, mma.m16n8k16 A layout (lane = g*4+t holds
-//         rows g, g+8 x k {2t, 2t+1, 2t+8, 2t+9})
-//   int8: tile = 16 rows x 32 k, mma.m16n8k32 s8 A layout (lane = g*4+t holds
-//         4-byte groups: (g, 4t..), (g+8, 4t..), (g, 16+4t..), (g+8, 16+4t..))
-__host__ __device__ __forceinline__ int64_t frag_offset_bf16(int64_t n, int64_t k, int64_t K) {
-  const int i = (int)(n & 15), j = (int)(k & 15);
-  const int g = i & 7, hi = i >> 3, c4 = (j & 7) >> 1, jj = j & 1, k8 = j >> 3;
-  const int lane = g * 4 + c4, pos = (k8 * 2 + hi) * 2 + jj;
-  return (((n >> 4) * (K >> 4) + (k >> 4)) << 8) + lane * 8 + pos;
-}
-__host__ __device__ __forceinline__ int64_t frag_offset_i8(int64_t n, int64_t k, int64_t K) {
-  const int i = (int)(n & 15), j = (int)(k & 31);
-  const int g = i & 7, hi = i >> 3, t = (j & 15) >> 2, q = j & 3, k16 = j >> 4;
-  const int lane = g * 4 + t, reg = k16 * 2 + hi;
-  return (((n >> 4) * (K >> 5) + (k >> 5)) << 9) + lane * 16 + reg * 4 + q;
+// Weight layout in HBM for bf16 / int8 ("core-matrix tiles", DESIGN.md
+// "weights in HBM").  Rows (output channels) come in groups of 128; within a
+// group the K dimension is cut into units of 32 bytes, each unit stored as
+// 2 x 16 core matrices of 8 rows x 16 bytes (128 contiguous bytes):
+//   offset(n, kb) = ((g*KT + kt)*2 + kc)*2048 + r8*128 + rr*16 + b
+//   g = n/128, r8 = (n%128)/8, rr = n%8, kt = kb/32, kc = (kb%32)/16, b = kb%16
+// (kb = byte offset along K: k for int8, 2k for bf16; KT = K bytes / 32).
+// One decode unit (128 rows x 32 B = 4 KB) is contiguous -> one TMA bulk copy;
+// ldmatrix.x4 on it yields mma.m16n8k32 (int8) / m16n8k16 (bf16) A fragments;
+// and the same bytes are the UMMA canonical K-major SWIZZLE_NONE layout
+// (LBO = 2048 B between K-adjacent core matrices, SBO = 128 B between
+// row-adjacent ones) for the tcgen05 prefill GEMM.
+constexpr int kGroupRows = 128;
+__host__ __device__ __forceinline__ int64_t cm_offset(int64_t n, int64_t kb, int64_t Kbytes) {
+  const int64_t g = n >> 7, r8 = (n & 127) >> 3, rr = n & 7;
+  const int64_t kt = kb >> 5, kc = (kb & 31) >> 4, b = kb & 15;
+  return ((g * (Kbytes >> 5) + kt) * 2 + kc) * 2048 + r8 * 128 + rr * 16 + b;
 }
 
 // host-side count of kernels launched by this library (bench `gpu_launches`)

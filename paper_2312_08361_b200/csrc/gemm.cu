@@ -18,9 +18,9 @@ constexpr int BM = 64, BN = 64, BK = 16;
 __device__ __forceinline__ float load_w(const LinearArgs& a, int64_t n, int64_t k) {
   if (a.wdtype == kF32) return reinterpret_cast<const float*>(a.w)[n * a.K + k];
   if (a.wdtype == kBF16)
-    return __bfloat162float(
-        reinterpret_cast<const __nv_bfloat16*>(a.w)[frag_offset_bf16(n, k, a.K)]);
-  int q = (int)reinterpret_cast<const int8_t*>(a.w)[frag_offset_i8(n, k, a.K)];
+    return __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(
+        reinterpret_cast<const uint8_t*>(a.w) + cm_offset(n, 2 * k, 2 * a.K)));
+  int q = (int)reinterpret_cast<const int8_t*>(a.w)[cm_offset(n, k, a.K)];
   return (float)q;  // per-row scale applied in the epilogue
 }
 
@@ -87,8 +87,8 @@ __global__ void swiglu_rows_kernel(const float* in, float* out, int64_t R, int64
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= R * F) return;
   int64_t r = i / F, j = i % F;
-  int64_t ng = (j >> 4) * 32 + (j & 15);
-  float g = in[r * 2 * F + ng], u = in[r * 2 * F + ng + 16];
+  int64_t ng = (j / 64) * 128 + (j % 64);
+  float g = in[r * 2 * F + ng], u = in[r * 2 * F + ng + 64];
   out[i] = silu_f(g) * u;
 }
 

@@ -28,7 +28,7 @@ __global__ void __launch_bounds__(256) gemv_f32_kernel(LinearArgs a) {
   if (a.epi == EPI_SWIGLU) {
     const int64_t F = a.N / 2;
     if (o >= F) return;
-    const int64_t ng = (o >> 4) * 32 + (o & 15), nu = ng + 16;
+    const int64_t ng = (o / 64) * 128 + (o % 64), nu = ng + 64;
     for (int r = 0; r < a.R; ++r) {
       const float* x = a.x + (int64_t)r * a.ldx;
       float sg = 0.f, su = 0.f;

@@ -543,19 +543,19 @@ void launch_wt(const GemvArgs& a, int ks, int r0, int rn, int Rs, cudaStream_t s
   count_launch();
 }
 
-// ---- span-input statistics: P = d/64 partials (the layout GEMV outputs use) ----
+// ---- span-input statistics: P = d/128 partials (the layout GEMV outputs use) ----
 __global__ void row_stats_kernel(const float* x, int64_t d, const float* g, RowStat* st, int Rs) {
   const int p = blockIdx.x, r = blockIdx.y;
-  const int lane = threadIdx.x;   // 64 threads: one element each
-  __shared__ float vs[64], vg[64];
-  const int64_t k = (int64_t)p * 64 + lane;
+  const int t = threadIdx.x;   // 128 threads: one element each
+  __shared__ float vs[128], vg[128];
+  const int64_t k = (int64_t)p * 128 + t;
   float v = x[(int64_t)r * d + k];
-  vs[lane] = v;
-  vg[lane] = fabsf(v * (g ? g[k] : 1.f));
+  vs[t] = v;
+  vg[t] = fabsf(v * (g ? g[k] : 1.f));
   __syncthreads();
-  if (lane == 0) {
+  if (t == 0) {
     float S = 0.f, Q = 0.f, M = 0.f;
-    for (int i = 0; i < 64; ++i) {
+    for (int i = 0; i < 128; ++i) {
       S += vs[i];
       Q = fmaf(vs[i], vs[i], Q);
       M = fmaxf(M, vg[i]);
@@ -585,8 +585,8 @@ void launch_gemv2(int wdtype, const GemvArgs& a, cudaStream_t st) {
 
 void launch_row_stats(const float* x, int R, int64_t d, const float* g_next, RowStat* st_out,
                       cudaStream_t st) {
-  dim3 grid((unsigned)(d / 64), (unsigned)R);
-  row_stats_kernel<<<grid, 64, 0, st>>>(x, d, g_next, st_out, R);
+  dim3 grid((unsigned)(d / 128), (unsigned)R);
+  row_stats_kernel<<<grid, 128, 0, st>>>(x, d, g_next, st_out, R);
   count_launch();
 }
 

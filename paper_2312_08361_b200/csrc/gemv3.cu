@@ -37,9 +37,15 @@ namespace {
 
 constexpr int NW = 8;             // warps per CTA
 constexpr int CTAS_PER_SM = 2;
-constexpr int RT = 4;             // 16-row tiles per group (64 output channels)
-constexpr int UNIT_BYTES = RT * 512;
-constexpr int STAGES = 5;         // TMA ring depth per warp (units)
+constexpr int RT = 8;             // 16-row tiles per group (128 output channels)
+constexpr int UNIT_BYTES = 4096;  // one unit = 128 rows x 32 bytes of K (common.cuh cm_offset)
+constexpr int XSLOT = 128;        // per batch row: the unit's activation chunk (<= 32 f32)
+// stage = weights + the activation chunks of the rows one launch handles
+// (NT MMA column tiles hold 8*NT/3 int8 digit rows / 8*NT/2 bf16 hi-lo rows)
+__host__ __device__ constexpr int stage_bytes(int nt) {
+  return UNIT_BYTES + (nt == 1 ? 4 : (nt == 2 ? 8 : 8)) * XSLOT;
+}
+constexpr int STAGES = 3;         // TMA ring depth per warp (units)
 constexpr int RMAX = 8;           // batch rows per launch
 constexpr double kFix = 4294967296.0;   // bf16 partial fixed point 2^32
 
@@ -76,6 +82,12 @@ __device__ __forceinline__ uint64_t evict_first_policy() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
+}
+
+__device__ __forceinline__ void ldsm_x4(uint4& r, const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "r"(smem_u32(p)));
 }
 
 __device__ __forceinline__ void mma_s8(int* c, const uint4& a, uint32_t b0, uint32_t b1) {
@@ -123,11 +135,9 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
   using XVec = typename std::conditional<WT == kI8, float4, float2>::type;
   extern __shared__ __align__(128) uint8_t dyn[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint8_t* ring = dyn + (size_t)warp * STAGES * UNIT_BYTES;
-  int* ctile = reinterpret_cast<int*>(dyn + (size_t)NW * STAGES * UNIT_BYTES) +
-               warp * (RT * 16 * NT * 8);                           // [64][NT*8]
-  WarpSmem* ws_ = reinterpret_cast<WarpSmem*>(dyn + (size_t)NW * STAGES * UNIT_BYTES +
-                                              (size_t)NW * RT * 16 * NT * 8 * 4) + warp;
+  constexpr int STAGE_BYTES = stage_bytes(NT);
+  uint8_t* ring = dyn + (size_t)warp * STAGES * STAGE_BYTES;
+  WarpSmem* ws_ = reinterpret_cast<WarpSmem*>(dyn + (size_t)NW * STAGES * STAGE_BYTES) + warp;
 
   const int64_t gw = (int64_t)blockIdx.x * NW + warp;
   const int64_t u0 = gw * units / warps_total, u1 = (gw + 1) * units / warps_total;
@@ -229,16 +239,22 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
   // ---- TMA producer (lane 0) ----
   const uint8_t* wbase = reinterpret_cast<const uint8_t*>(a.w);
   const uint64_t policy = evict_first_policy();
+  uint64_t policy_x;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(policy_x));
   // producer state (lane 0): next unit to issue as (group, k-tile, ring stage)
   const int nunits = (int)(u1 - u0);
   int p_grp = (int)(u0 / KT), p_kt = (int)(u0 % KT), p_st = 0, p_left = nunits;
   auto issue_next = [&]() {
-    mbar_expect_tx(&ws_->bar[p_st], UNIT_BYTES);
-    const uint8_t* src = wbase + ((((int64_t)p_grp * RT) * KT + p_kt) << 9);
-#pragma unroll
-    for (int t = 0; t < RT; ++t)
-      tma_load_1d(ring + p_st * UNIT_BYTES + t * 512, src + ((int64_t)t * KT << 9), 512,
-                  &ws_->bar[p_st], policy);
+    // the unit's weights and, alongside, each batch row's activation chunk:
+    // both arrive on the same mbarrier (no separate activation-load latency)
+    constexpr int XB = KTILE * 4;
+    mbar_expect_tx(&ws_->bar[p_st], UNIT_BYTES + Rn * XB);
+    uint8_t* dstg = ring + p_st * STAGE_BYTES;
+    tma_load_1d(dstg, wbase + ((int64_t)p_grp * KT + p_kt) * UNIT_BYTES, UNIT_BYTES,
+                &ws_->bar[p_st], policy);
+    for (int r = 0; r < Rn; ++r)
+      tma_load_1d(dstg + UNIT_BYTES + r * XSLOT, a.x + (int64_t)(r0 + r) * a.ldx + p_kt * KTILE,
+                  XB, &ws_->bar[p_st], policy_x);
     if (++p_kt == KT) { p_kt = 0; ++p_grp; }
     if (++p_st == STAGES) p_st = 0;
     --p_left;
@@ -247,49 +263,38 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
   if (lane == 0)
     for (int i = 0; i < STAGES && p_left > 0; ++i) issue_next();
 
-  // ---- activation side, prefetched one unit ahead ----
-  XVec xc[NT][2], gc[NT][2], xn[NT][2], gn[NT][2], xm[NT][2], gm[NT][2];
-  auto load_x = [&](int kt, XVec (&xr_)[NT][2], XVec (&gr_)[NT][2]) {
-    const int64_t k0 = (int64_t)kt * KTILE + t4 * XV;
-    constexpr int KOFF = (WT == kI8) ? 16 : 8;
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      const float* xr = a.x + (int64_t)(r0 + brow[nt]) * a.ldx;
-      xr_[nt][0] = __ldg(reinterpret_cast<const XVec*>(xr + k0));
-      xr_[nt][1] = __ldg(reinterpret_cast<const XVec*>(xr + k0 + KOFF));
-      if (HASG) {
-        gr_[nt][0] = __ldg(reinterpret_cast<const XVec*>(a.g + k0));
-        gr_[nt][1] = __ldg(reinterpret_cast<const XVec*>(a.g + k0 + KOFF));
-      }
-    }
-  };
+  // ---- activation side: read from the stage (arrived with the weights) ----
+  XVec xc[NT][2], gc[NT][2];
+  constexpr int KOFF = (WT == kI8) ? 16 : 8;
   int c_grp = (int)(u0 / KT), c_kt = (int)(u0 % KT), c_st = 0;
   uint32_t c_ph = 0;
-  load_x(c_kt, xc, gc);
-  if (nunits > 1) load_x(c_kt + 1 == KT ? 0 : c_kt + 1, xn, gn);
 
-  int iacc[RT][NT][4];
-  float facc[RT][NT][4];
+  using AccT = typename std::conditional<WT == kI8, int, float>::type;
+  AccT acc[RT][NT][4];
 #pragma unroll
   for (int t = 0; t < RT; ++t)
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) { iacc[t][nt][j] = 0; facc[t][nt][j] = 0.f; }
+      for (int j = 0; j < 4; ++j) acc[t][nt][j] = 0;
   int seg_kt0 = c_kt;
 
   for (int i = 0; i < nunits; ++i) {
-    if (i + 2 < nunits) {
-      int k2 = c_kt + 2;
-      if (k2 >= KT) k2 -= (int)KT;
-      load_x(k2, xm, gm);
-    }
     mbar_wait(&ws_->bar[c_st], c_ph);
-    const uint8_t* stage = ring + c_st * UNIT_BYTES;
-    uint4 wt[RT];
+    const uint8_t* stage = ring + c_st * STAGE_BYTES;
 #pragma unroll
-    for (int t = 0; t < RT; ++t)
-      wt[t] = *reinterpret_cast<const uint4*>(stage + t * 512 + lane * 16);
+    for (int nt = 0; nt < NT; ++nt) {
+      const float* xs = reinterpret_cast<const float*>(stage + UNIT_BYTES + brow[nt] * XSLOT) + t4 * XV;
+      xc[nt][0] = *reinterpret_cast<const XVec*>(xs);
+      xc[nt][1] = *reinterpret_cast<const XVec*>(xs + KOFF);
+      if (HASG) {
+        const int64_t k0 = (int64_t)c_kt * KTILE + t4 * XV;
+        gc[nt][0] = __ldg(reinterpret_cast<const XVec*>(a.g + k0));
+        gc[nt][1] = __ldg(reinterpret_cast<const XVec*>(a.g + k0 + KOFF));
+      }
+    }
+    // ldmatrix.x4: lane i addresses row (i%8) of core matrix (kc = i/16, r8 = 2t + (i/8)%2)
+    const uint8_t* lrow = stage + (lane >> 4) * 2048 + ((lane >> 3) & 1) * 128 + (lane & 7) * 16;
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
       uint32_t b0 = 0, b1 = 0;
@@ -333,21 +338,15 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
       }
 #pragma unroll
       for (int t = 0; t < RT; ++t) {
-        if constexpr (WT == kI8) mma_s8(iacc[t][nt], wt[t], b0, b1);
-        else mma_bf16(facc[t][nt], wt[t], b0, b1);
+        uint4 wt;
+        ldsm_x4(wt, lrow + t * 256);
+        if constexpr (WT == kI8) mma_s8(reinterpret_cast<int*>(acc[t][nt]), wt, b0, b1);
+        else mma_bf16(reinterpret_cast<float*>(acc[t][nt]), wt, b0, b1);
       }
     }
     __syncwarp();
     if (lane == 0 && p_left > 0) issue_next();
     if (++c_st == STAGES) { c_st = 0; c_ph ^= 1; }
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        xc[nt][h] = xn[nt][h];
-        xn[nt][h] = xm[nt][h];
-        if (HASG) { gc[nt][h] = gn[nt][h]; gn[nt][h] = gm[nt][h]; }
-      }
 
     // ---- end of this warp's contribution to a group: flush ----
     const int64_t grp = c_grp;
@@ -355,32 +354,44 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
     const bool grp_end = (c_kt + 1 == KT) || (i + 1 == nunits);
     if (++c_kt == KT) { c_kt = 0; ++c_grp; seg_kt0 = 0; }
     if (!grp_end) continue;
-    // C fragments -> ctile[row][col]
+    // combine this segment's digit/hi-lo columns per (row, batch row) in registers
+    unsigned long long* acc64 = reinterpret_cast<unsigned long long*>(a.ws);
+    const int g8 = lane >> 2;
 #pragma unroll
-    for (int t = 0; t < RT; ++t)
+    for (int t = 0; t < RT; ++t) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t n = grp * 128 + t * 16 + g8 + h * 8;
+        for (int r = 0; r < Rn; ++r) {
+          long long D = 0;
+          if constexpr (WT == kI8) {
+#pragma unroll
+            for (int dg = 0; dg < 3; ++dg) {
+              const int c = 3 * r + dg, nt = c >> 3, cw = c & 7;
+              int val = 0;
+#pragma unroll
+              for (int q = 0; q < NT; ++q)
+                if (q == nt) val = (cw & 1) ? (int)acc[t][q][1 + 2 * h] : (int)acc[t][q][2 * h];
+              val = __shfl_sync(0xffffffffu, val, g8 * 4 + (cw >> 1));
+              D += (long long)val << (16 - 8 * dg);
+            }
+          } else {
+            const int c = 2 * r, nt = c >> 3, cw = c & 7;
+            float hi = 0.f, lo = 0.f;
+#pragma unroll
+            for (int q = 0; q < NT; ++q)
+              if (q == nt) { hi = (float)acc[t][q][2 * h]; lo = (float)acc[t][q][2 * h + 1]; }
+            hi = __shfl_sync(0xffffffffu, hi, g8 * 4 + (cw >> 1));
+            lo = __shfl_sync(0xffffffffu, lo, g8 * 4 + (cw >> 1));
+            D = __double2ll_rn(((double)hi + (double)lo) * kFix);
+          }
+          if (t4 == 0) atomicAdd(acc64 + (int64_t)(r0 + r) * a.N + n, (unsigned long long)D);
+        }
+      }
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int row = t * 16 + (lane >> 2) + ((j >> 1) << 3);
-          const int col = nt * 8 + t4 * 2 + (j & 1);
-          ctile[row * (NT * 8) + col] =
-              (WT == kI8) ? iacc[t][nt][j] : __float_as_int(facc[t][nt][j]);
-          iacc[t][nt][j] = 0;
-          facc[t][nt][j] = 0.f;
-        }
-    __syncwarp();
-    unsigned long long* acc64 = reinterpret_cast<unsigned long long*>(a.ws);
-    for (int e = lane; e < RT * 16 * Rn; e += 32) {
-      const int row = e / Rn, r = e % Rn;
-      long long D;
-      const int* cr = ctile + row * (NT * 8);
-      if (WT == kI8)
-        D = (long long)cr[3 * r] * 65536 + (long long)cr[3 * r + 1] * 256 + (long long)cr[3 * r + 2];
-      else
-        D = __double2ll_rn(((double)__int_as_float(cr[2 * r]) +
-                            (double)__int_as_float(cr[2 * r + 1])) * kFix);
-      atomicAdd(acc64 + (int64_t)(r0 + r) * a.N + grp * (RT * 16) + row, (unsigned long long)D);
+        for (int j = 0; j < 4; ++j) acc[t][nt][j] = 0;
     }
     __syncwarp();
     int last = 0;
@@ -397,32 +408,28 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
     last = __shfl_sync(0xffffffffu, last, 0);
     if (!last) continue;
 
-    // ---- epilogue for the group (64 channels x Rn rows) ----
-    float* outv = reinterpret_cast<float*>(ctile);   // reuse: [64][RMAX]
-    for (int e = lane; e < RT * 16 * Rn; e += 32) {
-      const int row = e / Rn, r = e % Rn;
-      const int64_t n = grp * (RT * 16) + row;
-      const long long D = (long long)atomicExch(acc64 + (int64_t)(r0 + r) * a.N + n, 0ull);
-      float v;
-      if (WT == kI8) v = (float)((double)D * ws_->yscale[r] * (double)a.wscale[n]);
-      else v = (float)((double)D * ws_->yscale[r]);
-      outv[row * RMAX + r] = v;
-    }
-    __syncwarp();
-    // outputs: SwiGLU pairs tiles (0,1) and (2,3) -> 32 outputs, else 64
-    const int nout = (a.epi == EPI_SWIGLU) ? 32 : 64;
+    // ---- epilogue for the group (128 channels x Rn rows), last warp only ----
+    const int nout = (a.epi == EPI_SWIGLU) ? 64 : 128;
     for (int r = 0; r < Rn; ++r) {
+      unsigned long long* accr = acc64 + (int64_t)(r0 + r) * a.N + grp * 128;
+      const double ys = ws_->yscale[r];
       float S = 0.f, Q = 0.f, M = 0.f;
       for (int o = lane; o < nout; o += 32) {
         float val;
         int64_t col;
+        auto fetch = [&](int row) {
+          const long long D = (long long)atomicExch(accr + row, 0ull);
+          if (WT == kI8) return (float)((double)D * ys * (double)a.wscale[grp * 128 + row]);
+          return (float)((double)D * ys);
+        };
         if (a.epi == EPI_SWIGLU) {
-          const int pr = o >> 4, jj = o & 15;
-          val = silu_f(outv[(pr * 32 + jj) * RMAX + r]) * outv[(pr * 32 + 16 + jj) * RMAX + r];
-          col = grp * 32 + o;
-        } else {
+          // group = [gate 64 rows | up 64 rows] of outputs grp*64 + o
+          const float gt = fetch(o), up = fetch(64 + o);
+          val = silu_f(gt) * up;
           col = grp * 64 + o;
-          val = outv[o * RMAX + r];
+        } else {
+          col = grp * 128 + o;
+          val = fetch(o);
           if (a.epi == EPI_RESID) val += a.res[(int64_t)(r0 + r) * a.ldy + col];
           else if (a.epi == EPI_GELU) val = gelu_f(val);
         }
@@ -445,10 +452,9 @@ int g_num_sms = 0;
 template <int WT, int NT, int NORMT, bool HASG>
 void launch_cfg(const GemvArgs& a, int r0, int rn, cudaStream_t st) {
   const int KTILE = (WT == kI8) ? 32 : 16;
-  const int64_t units = (a.N / (RT * 16)) * (a.K / KTILE);
+  const int64_t units = (a.N / 128) * (a.K / KTILE);
   const int grid = g_num_sms * CTAS_PER_SM;
-  const size_t smem = (size_t)NW * STAGES * UNIT_BYTES + (size_t)NW * RT * 16 * NT * 8 * 4 +
-                      (size_t)NW * sizeof(WarpSmem) + 128;
+  const size_t smem = (size_t)NW * STAGES * stage_bytes(NT) + (size_t)NW * sizeof(WarpSmem) + 128;
   static bool set = false;
   if (!set) {
     cudaFuncSetAttribute(gemv3_kernel<WT, NT, NORMT, HASG>,
@@ -483,7 +489,7 @@ void launch_wt(const GemvArgs& a, int r0, int rn, cudaStream_t st) {
 }  // namespace
 
 int64_t gemv3_ws_bytes(int64_t N, int Rmax) { return (int64_t)Rmax * N * 8; }
-int64_t gemv3_counters(int64_t N) { return N / 64 + 1; }
+int64_t gemv3_counters(int64_t N) { return N / 128 + 1; }
 
 void launch_gemv3(int wdtype, const GemvArgs& a, cudaStream_t st) {
   if (!g_num_sms) {

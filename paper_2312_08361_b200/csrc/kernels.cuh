@@ -6,12 +6,14 @@
 namespace sp {
 
 // Where a [K x N] matrix lives inside a fused weight buffer: output channel n
-// goes to buffer row  row0 + ((n/16)*tstride + toff)*16 + n%16.
+// goes to buffer row  row0 + ((n/64)*tstride + toff)*64 + n%64
+// (tstride 2 interleaves gate/up in 64-row halves of each 128-row group).
 struct MatPlace {
   int64_t row0;
   int64_t tstride;
   int64_t toff;
 };
+constexpr int kPlaceGranule = 64;
 
 // GEMV / GEMM epilogues
 enum Epi {

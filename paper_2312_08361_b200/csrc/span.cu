@@ -130,9 +130,10 @@ int validate(const sp_config* c) {
   int F = c->ffn_dim ? c->ffn_dim : 4 * c->hidden_dim;
   int d = c->hidden_dim, kv = kvh * hd;
   if (c->weight_dtype != kF32) {
-    int kt = wdtype_ktile(c->weight_dtype) * 8;
-    if (d % kt || F % kt) return SP_ERR_ARG;
-    if ((d + 2 * kv) % 32 || d % 32 || F % 32) return SP_ERR_ARG;
+    // core-matrix layout: 128-row groups, K in 32-byte units (common.cuh)
+    if (d % 32 || F % 32) return SP_ERR_ARG;
+    if ((d + 2 * kv) % 128 || d % 128 || F % 64) return SP_ERR_ARG;
+    if (c->family != kLlama && F % 128) return SP_ERR_ARG;
   } else {
     if (d % 16 || F % 16 || kv % 16) return SP_ERR_ARG;
   }
@@ -346,7 +347,7 @@ int run_span_decode_tc(sp_span* s, sp_kv* kv, int b0, int b1, float* y, int widt
     // 1) QKV = RMS/LN(x) @ Wqkv
     g.w = W.qkv; g.wscale = W.s_qkv; g.N = s->n_qkv; g.K = d; g.x = y; g.ldx = d;
     g.norm = norm; g.g = s->gains_one ? nullptr : W.ln1_g; g.st_in = s->st_norm1;
-    g.P_in = (int)(d / 64);
+    g.P_in = (int)(d / 128);
     g.y = s->qkvb; g.ldy = s->n_qkv; g.res = nullptr; g.epi = EPI_STORE;
     g.st_out = nullptr; g.g_next = nullptr;
     {
@@ -373,7 +374,7 @@ int run_span_decode_tc(sp_span* s, sp_kv* kv, int b0, int b1, float* y, int widt
     // 4) mlp = act(RMS/LN(x) @ Wup)
     g.w = W.up; g.wscale = W.s_up; g.N = s->n_up; g.K = d; g.x = y; g.ldx = d;
     g.norm = norm; g.g = s->gains_one ? nullptr : W.ln2_g; g.st_in = s->st_norm2;
-    g.P_in = (int)(d / 64);
+    g.P_in = (int)(d / 128);
     g.y = s->mlp; g.ldy = s->F; g.res = nullptr; g.epi = fam == kLlama ? EPI_SWIGLU : EPI_GELU;
     g.st_out = s->st_mlp; g.g_next = nullptr;
     {
@@ -382,7 +383,7 @@ int run_span_decode_tc(sp_span* s, sp_kv* kv, int b0, int b1, float* y, int widt
     }
     // 5) x += mlp @ Wdown   (stats for the next block's norm1)
     g.w = W.down; g.wscale = W.s_down; g.N = d; g.K = s->F; g.x = s->mlp; g.ldx = s->F;
-    g.norm = NORM_NONE; g.g = nullptr; g.st_in = s->st_mlp; g.P_in = (int)(s->n_up / 64);
+    g.norm = NORM_NONE; g.g = nullptr; g.st_in = s->st_mlp; g.P_in = (int)(s->n_up / 128);
     g.y = y; g.ldy = d; g.res = y; g.epi = EPI_RESID;
     g.st_out = last ? nullptr : s->st_norm1;
     g.g_next = (last || s->gains_one) ? nullptr : s->blocks[b + 1].ln1_g;

@@ -21,7 +21,7 @@ __global__ void gen_stream_kernel(uint64_t stream, int64_t n, double scale, floa
 // buffer row of output channel n for a matrix placed at `row0` with 16-row
 // tiles interleaved every `tstride` tiles at tile offset `toff`
 __device__ __forceinline__ int64_t buf_row(int64_t n, const MatPlace& p) {
-  return p.row0 + ((n >> 4) * p.tstride + p.toff) * 16 + (n & 15);
+  return p.row0 + ((n / kPlaceGranule) * p.tstride + p.toff) * kPlaceGranule + (n % kPlaceGranule);
 }
 
 // f32 storage, row-major [rows][K]
@@ -46,60 +46,41 @@ __global__ void gen_i8_scales_kernel(uint64_t stream, int64_t K, int64_t N, doub
   if (lane == 0) scales[buf_row(n, place)] = __fdiv_rn(m, 127.0f);
 }
 
-// int8 pass 2: one thread writes one lane-chunk (16 B) of a 16x32 tile,
-// m16n8k32 s8 A-fragment order (common.cuh frag_offset_i8)
+// int8 pass 2: one thread writes one 16-byte core-matrix row (16 k of one
+// output channel), layout common.cuh cm_offset
 __global__ void gen_i8_pack_kernel(uint64_t stream, int64_t K, int64_t N, double scale,
                                    MatPlace place, const float* __restrict__ scales,
                                    int8_t* dst) {
-  int64_t chunk = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // (rt, kt, lane)
-  int64_t KT = K >> 5;
-  int64_t total = (N >> 4) * KT * 32;
-  if (chunk >= total) return;
-  int lane = (int)(chunk & 31);
-  int64_t kt = (chunk >> 5) % KT;
-  int64_t rt = (chunk >> 5) / KT;
-  int g = lane >> 2, t = lane & 3;
+  const int64_t chunk = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // (n, k16)
+  const int64_t KC = K >> 4;
+  if (chunk >= N * KC) return;
+  const int64_t n = chunk / KC, k0 = (chunk % KC) * 16;
+  const int64_t r = buf_row(n, place);
+  const float s = scales[r];
   __align__(16) int8_t out[16];
 #pragma unroll
-  for (int reg = 0; reg < 4; ++reg) {
-    const int hi = reg & 1, k16 = reg >> 1;
-    const int64_t n = rt * 16 + g + hi * 8;
-    const float s = scales[buf_row(n, place)];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int64_t k = kt * 32 + k16 * 16 + t * 4 + q;
-      float w = uniform_value(stream, (uint64_t)(k * N + n), scale);
-      int c = (s > 0.f) ? __float2int_rn(__fdiv_rn(w, s)) : 0;
-      out[reg * 4 + q] = (int8_t)c;
-    }
+  for (int q = 0; q < 16; ++q) {
+    const int64_t k = k0 + q;
+    const float w = uniform_value(stream, (uint64_t)(k * N + n), scale);
+    out[q] = (int8_t)((s > 0.f) ? __float2int_rn(__fdiv_rn(w, s)) : 0);
   }
-  int64_t brt = (place.row0 >> 4) + rt * place.tstride + place.toff;  // buffer row tile
-  uint4* d = reinterpret_cast<uint4*>(dst + ((brt * KT + kt) << 9) + lane * 16);
-  *d = *reinterpret_cast<uint4*>(out);
+  *reinterpret_cast<uint4*>(dst + cm_offset(r, k0, K)) = *reinterpret_cast<uint4*>(out);
 }
 
-// bf16: one thread writes one lane-chunk (16 B = 8 bf16) of a 16x16 tile
+// bf16: one thread writes one 16-byte core-matrix row (8 k of one channel)
 __global__ void gen_bf16_pack_kernel(uint64_t stream, int64_t K, int64_t N, double scale,
                                      MatPlace place, __nv_bfloat16* dst) {
-  int64_t chunk = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  int64_t KT = K >> 4;
-  int64_t total = (N >> 4) * KT * 32;
-  if (chunk >= total) return;
-  int lane = (int)(chunk & 31);
-  int64_t kt = (chunk >> 5) % KT;
-  int64_t rt = (chunk >> 5) / KT;
-  int g = lane >> 2, c = (lane & 3) * 2;
+  const int64_t chunk = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // (n, k8)
+  const int64_t KC = K >> 3;
+  if (chunk >= N * KC) return;
+  const int64_t n = chunk / KC, k0 = (chunk % KC) * 8;
+  const int64_t r = buf_row(n, place);
   __align__(16) __nv_bfloat16 out[8];
 #pragma unroll
-  for (int p = 0; p < 8; ++p) {
-    int k8 = p >> 2, hi = (p >> 1) & 1, jj = p & 1;
-    int64_t n = rt * 16 + g + hi * 8;
-    int64_t k = kt * 16 + k8 * 8 + c + jj;
-    out[p] = __float2bfloat16_rn(uniform_value(stream, (uint64_t)(k * N + n), scale));
-  }
-  int64_t brt = (place.row0 >> 4) + rt * place.tstride + place.toff;
-  uint4* d = reinterpret_cast<uint4*>(dst + ((brt * KT + kt) << 8) + lane * 8);
-  *d = *reinterpret_cast<uint4*>(out);
+  for (int q = 0; q < 8; ++q)
+    out[q] = __float2bfloat16_rn(uniform_value(stream, (uint64_t)((k0 + q) * N + n), scale));
+  *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(dst) + cm_offset(r, 2 * k0, 2 * K)) =
+      *reinterpret_cast<uint4*>(out);
 }
 
 void launch_gen_stream(uint64_t stream, int64_t n, double scale, float* dst, cudaStream_t st) {
@@ -114,13 +95,13 @@ void launch_gen_matrix(int wdtype, uint64_t stream, int64_t K, int64_t N, double
     gen_f32_rows_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(stream, K, N, scale, place,
                                                                       (float*)dst); count_launch();
   } else if (wdtype == kBF16) {
-    int64_t chunks = (N / 16) * (K / 16) * 32;
+    int64_t chunks = N * (K / 8);
     gen_bf16_pack_kernel<<<(unsigned)((chunks + 255) / 256), 256, 0, st>>>(
         stream, K, N, scale, place, (__nv_bfloat16*)dst); count_launch();
   } else {
     gen_i8_scales_kernel<<<(unsigned)((N + 7) / 8), 256, 0, st>>>(stream, K, N, scale, place,
                                                                    scales); count_launch();
-    int64_t chunks = (N / 16) * (K / 32) * 32;
+    int64_t chunks = N * (K / 16);
     gen_i8_pack_kernel<<<(unsigned)((chunks + 255) / 256), 256, 0, st>>>(
         stream, K, N, scale, place, scales, (int8_t*)dst); count_launch();
   }
@@ -137,9 +118,10 @@ __global__ void read_matrix_kernel(int wdtype, const void* src, const float* sca
   if (wdtype == kF32) {
     v = ((const float*)src)[r * bufK + k];
   } else if (wdtype == kBF16) {
-    v = __bfloat162float(((const __nv_bfloat16*)src)[frag_offset_bf16(r, k, bufK)]);
+    v = __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(
+        (const uint8_t*)src + cm_offset(r, 2 * k, 2 * bufK)));
   } else {
-    int q = (int)((const int8_t*)src)[frag_offset_i8(r, k, bufK)];
+    int q = (int)((const int8_t*)src)[cm_offset(r, k, bufK)];
     v = __fmul_rn((float)q, scales[r]);
   }
   dst[i] = v;
