@@ -146,6 +146,9 @@ int sp_head_read_embedding(sp_head* head, float* dst_host);
  * 4 norms/RoPE/KV-append/codec), the summed device ms, algorithmic bytes and
  * flops and the number of launches, then clears the records. */
 int sp_span_set_profiling(sp_span* span, int32_t enable);
+/* options: 0 = use the tcgen05 prefill GEMM when the shape allows (default 1;
+ * 0 selects the exact-f32 SIMT GEMM, used by parity tests as a cross-check) */
+int sp_span_set_option(sp_span* span, int32_t option, int32_t value);
 int sp_span_profile_read(sp_span* span, int32_t n_classes, double* ms, double* bytes,
                          double* flops, int64_t* launches);
 /* measurement helper: only the 4 decode GEMVs of every block in [b0, b1)

@@ -1,0 +1,340 @@
+// Prefill / replay linear layers on the 5th-gen tensor cores (tcgen05 + TMEM).
+//
+//   Y[m, n] = epi( 2^(e_m - 14) * wscale[n] * sum_k (d0[m,k]*256 + d1[m,k]) * W[n,k] )
+//
+// * Activations are two int8 "digit planes" of a per-row 15-bit fixed-point
+//   code (q = rint(x * 2^(14-e)), q = 256*d0 + d1): written by the digitize
+//   kernel below in the same UMMA-canonical core-matrix layout as the weights
+//   (common.cuh cm_offset), so both operands reach shared memory as plain 1-D
+//   TMA bulk copies (cp.async.bulk + mbarrier complete_tx).
+// * int8 weights are consumed as stored (no dequantisation pass): the MMA is
+//   tcgen05.mma.cta_group::1.kind::i8, M = 128 tokens x N = 128 channels x
+//   K = 32, both operands K-major SWIZZLE_NONE (LBO = 2048 B along K, SBO = 128 B
+//   per 8 rows).  One CTA owns a 128 x 256 output tile = 2 planes x 2 weight
+//   groups = 4 int32 accumulators = all 512 TMEM columns.
+// * Accumulation is exact (int32 per plane, int64 when the planes combine), so
+//   every output row is independent of M and of its tile position — the
+//   micro-batch invariance the reference pins (T/test_server.py:247-255) holds.
+// * Warp roles: warp 0 = TMA producer (one lane), warp 1 = MMA issuer (one
+//   lane), warp 2 = TMEM allocator, warps 4..7 = epilogue (tcgen05.ld, scale,
+//   residual / GELU / SwiGLU, store).  3-stage smem ring of 64 KB stages.
+#include "common.cuh"
+#include "kernels.cuh"
+#include "prefill.cuh"
+
+namespace sp {
+
+namespace {
+
+constexpr int BM = 128;                 // tokens per tile
+constexpr int NGRP = 2;                 // 128-channel weight groups per tile (N = 256)
+constexpr int KU = 4;                   // 32-byte K units per stage (128 B of K)
+constexpr int STAGES = 3;
+constexpr int UNIT = 4096;              // one 128-row x 32-byte unit (common.cuh)
+constexpr int A_BYTES = 2 * KU * UNIT;  // two digit planes
+constexpr int B_BYTES = NGRP * KU * UNIT;
+constexpr int STAGE = A_BYTES + B_BYTES;   // 64 KB
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// UMMA shared-memory descriptor, K-major, SWIZZLE_NONE (cute::UMMA::SmemDescriptor)
+__device__ __forceinline__ uint64_t umma_desc(const void* smem, uint32_t lbo, uint32_t sbo) {
+  const uint32_t addr = smem_u32(smem);
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;             // version = 1 (sm100)
+  // base_offset = 0, lbo_mode = 0, layout_type = 0 (SWIZZLE_NONE)
+  return d;
+}
+
+// instruction descriptor: kind::i8, D = s32, A = B = s8, K-major, M = 128, N = 128
+constexpr uint32_t kIdescI8 = (2u << 4) | (1u << 7) | (1u << 10) | ((128u >> 3) << 17) |
+                              ((128u >> 4) << 24);
+
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(kIdescI8), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::
+                   "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, int* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+        "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+        "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ float gelu_f(float x) {
+  return 0.5f * x * (1.0f + tanhf(0.7978845608028654f * (x + 0.044715f * x * x * x)));
+}
+__device__ __forceinline__ float silu_f(float x) { return x / (1.0f + expf(-x)); }
+
+__global__ void __launch_bounds__(256, 1) gemm_i8_tc_kernel(TcGemmArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], tmem_full;
+  __shared__ uint32_t tmem_base;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ng0 = blockIdx.x * NGRP;         // first weight group of this tile
+  const int mt = blockIdx.y;                 // token tile (128 rows)
+  const int64_t KT = a.K >> 5;               // 32-byte units along K
+  const int KB = (int)(KT / KU);             // stages along K
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    mbar_init(&tmem_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(&tmem_base))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tbase = tmem_base;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer ----------------
+    const uint8_t* pa0 = a.planes;
+    const uint8_t* pa1 = a.planes + a.plane_stride;
+    const uint8_t* wb = reinterpret_cast<const uint8_t*>(a.w);
+    for (int kb = 0; kb < KB; ++kb) {
+      const int s = kb % STAGES;
+      if (kb >= STAGES) mbar_wait(&empty[s], ((kb / STAGES) - 1) & 1);
+      uint8_t* st = smem + (size_t)s * STAGE;
+      mbar_expect_tx(&full[s], STAGE);
+      const int64_t ua = ((int64_t)mt * KT + (int64_t)kb * KU) * UNIT;
+      tma_load_1d(st, pa0 + ua, KU * UNIT, &full[s]);
+      tma_load_1d(st + KU * UNIT, pa1 + ua, KU * UNIT, &full[s]);
+      for (int j = 0; j < NGRP; ++j) {
+        const int64_t ub = ((int64_t)(ng0 + j) * KT + (int64_t)kb * KU) * UNIT;
+        tma_load_1d(st + A_BYTES + j * KU * UNIT, wb + ub, KU * UNIT, &full[s]);
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer ----------------
+    for (int kb = 0; kb < KB; ++kb) {
+      const int s = kb % STAGES;
+      mbar_wait(&full[s], (kb / STAGES) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint8_t* st = smem + (size_t)s * STAGE;
+#pragma unroll
+      for (int u = 0; u < KU; ++u) {
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+          const uint64_t ad = umma_desc(st + p * KU * UNIT + u * UNIT, 2048, 128);
+#pragma unroll
+          for (int j = 0; j < NGRP; ++j) {
+            const uint64_t bd = umma_desc(st + A_BYTES + j * KU * UNIT + u * UNIT, 2048, 128);
+            mma_i8(tbase + (uint32_t)((p * NGRP + j) * 128), ad, bd, (kb | u) ? 1u : 0u);
+          }
+        }
+      }
+      mma_commit(&empty[s]);          // frees the stage when these MMAs complete
+    }
+    mma_commit(&tmem_full);
+  } else if (warp >= 4) {
+    // ---------------- epilogue ----------------
+    const int q = warp - 4;                          // TMEM lane quarter
+    const int row = q * 32 + lane;
+    const int64_t m = (int64_t)mt * BM + row;
+    mbar_wait(&tmem_full, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const bool valid = m < a.M;
+    const double ys = valid ? ldexp(1.0, a.exps[m] - 14) : 0.0;
+    const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
+    for (int j = 0; j < NGRP; ++j) {
+      const int64_t n0 = (int64_t)(ng0 + j) * 128;
+      if (a.epi == EPI_SWIGLU) {
+        // group = [gate 64 | up 64] of outputs (ng0+j)*64 + c
+        for (int c0 = 0; c0 < 64; c0 += 32) {
+          int g0[32], g1[32], u0[32], u1[32];
+          tmem_ld32(tbase + lane_addr + (uint32_t)((0 * NGRP + j) * 128 + c0), g0);
+          tmem_ld32(tbase + lane_addr + (uint32_t)((1 * NGRP + j) * 128 + c0), g1);
+          tmem_ld32(tbase + lane_addr + (uint32_t)((0 * NGRP + j) * 128 + 64 + c0), u0);
+          tmem_ld32(tbase + lane_addr + (uint32_t)((1 * NGRP + j) * 128 + 64 + c0), u1);
+          if (!valid) continue;
+          float* out = a.y + m * a.ldy + (ng0 + j) * 64 + c0;
+#pragma unroll
+          for (int c = 0; c < 32; c += 4) {
+            float o4[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int cc = c + e;
+              const double gd = (double)((long long)g0[cc] * 256 + g1[cc]) * ys *
+                                (double)a.wscale[n0 + c0 + cc];
+              const double ud = (double)((long long)u0[cc] * 256 + u1[cc]) * ys *
+                                (double)a.wscale[n0 + 64 + c0 + cc];
+              o4[e] = silu_f((float)gd) * (float)ud;
+            }
+            *reinterpret_cast<float4*>(out + c) = make_float4(o4[0], o4[1], o4[2], o4[3]);
+          }
+        }
+      } else {
+        for (int c0 = 0; c0 < 128; c0 += 32) {
+          int v0[32], v1[32];
+          tmem_ld32(tbase + lane_addr + (uint32_t)((0 * NGRP + j) * 128 + c0), v0);
+          tmem_ld32(tbase + lane_addr + (uint32_t)((1 * NGRP + j) * 128 + c0), v1);
+          if (!valid) continue;
+          float* out = a.y + m * a.ldy + n0 + c0;
+          const float* res = a.res ? a.res + m * a.ldy + n0 + c0 : nullptr;
+#pragma unroll
+          for (int c = 0; c < 32; c += 4) {
+            float o4[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int cc = c + e;
+              float v = (float)((double)((long long)v0[cc] * 256 + v1[cc]) * ys *
+                                (double)a.wscale[n0 + c0 + cc]);
+              if (a.epi == EPI_RESID) v += res[cc];
+              else if (a.epi == EPI_GELU) v = gelu_f(v);
+              o4[e] = v;
+            }
+            *reinterpret_cast<float4*>(out + c) = make_float4(o4[0], o4[1], o4[2], o4[3]);
+          }
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 2)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tbase)
+                 : "memory");
+}
+
+// ---- activation digit planes: one CTA per (padded) row -----------------------
+// norm: 0 none, 1 RMSNorm, 2 LayerNorm (gains g, bias b; eps 1e-5)
+__global__ void __launch_bounds__(256) digitize_kernel(const float* __restrict__ x, int64_t ldx,
+                                                       int64_t M, int64_t K, int norm,
+                                                       const float* g, const float* b,
+                                                       uint8_t* planes, int64_t plane_stride,
+                                                       int* exps) {
+  __shared__ float sh[3][9];
+  const int64_t m = blockIdx.x;
+  const float* xr = x + m * ldx;
+  const bool valid = m < M;
+  float mu = 0.f, rstd = 1.f;
+  auto bsum = [&](float v, int slot) {
+    v = warp_sum(v);
+    if ((threadIdx.x & 31) == 0) sh[slot][threadIdx.x >> 5] = v;
+    __syncthreads();
+    float t = 0.f;
+    for (int w = 0; w < 8; ++w) t += sh[slot][w];
+    __syncthreads();
+    return t;
+  };
+  if (valid && norm != 0) {
+    float s = 0.f, s2 = 0.f;
+    for (int64_t k = threadIdx.x; k < K; k += 256) { s += xr[k]; s2 = fmaf(xr[k], xr[k], s2); }
+    if (norm == 2) {
+      mu = bsum(s, 0) / (float)K;
+      float q = 0.f;
+      for (int64_t k = threadIdx.x; k < K; k += 256) { float c = xr[k] - mu; q = fmaf(c, c, q); }
+      rstd = 1.0f / sqrtf(bsum(q, 1) / (float)K + 1e-5f);
+    } else {
+      rstd = 1.0f / sqrtf(bsum(s2, 1) / (float)K + 1e-5f);
+    }
+  }
+  auto val = [&](int64_t k) -> float {
+    if (!valid) return 0.f;
+    float v = xr[k];
+    if (norm == 1) v = v * rstd * g[k];
+    else if (norm == 2) v = (v - mu) * rstd * g[k] + b[k];
+    return v;
+  };
+  float amax = 0.f;
+  for (int64_t k = threadIdx.x; k < K; k += 256) amax = fmaxf(amax, fabsf(val(k)));
+  amax = warp_max(amax);
+  if ((threadIdx.x & 31) == 0) sh[2][threadIdx.x >> 5] = amax;
+  __syncthreads();
+  amax = 0.f;
+  for (int w = 0; w < 8; ++w) amax = fmaxf(amax, sh[2][w]);
+  int e = 0;
+  if (amax > 0.f) frexpf(amax, &e);                 // |v| < 2^e
+  const float sc = amax > 0.f ? ldexpf(1.0f, 14 - e) : 0.f;
+  if (threadIdx.x == 0 && valid) exps[m] = e;
+  // 16 consecutive k per thread -> one 16-byte core-matrix row per plane
+  for (int64_t k0 = (int64_t)threadIdx.x * 16; k0 < K; k0 += 256 * 16) {
+    __align__(16) int8_t d0[16], d1[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int q = __float2int_rn(val(k0 + i) * sc);      // |q| <= 2^14
+      const int lo = (int)(int8_t)(q & 0xFF);
+      d1[i] = (int8_t)lo;
+      d0[i] = (int8_t)((q - lo) >> 8);
+    }
+    const int64_t off = cm_offset(m, k0, K);
+    *reinterpret_cast<uint4*>(planes + off) = *reinterpret_cast<uint4*>(d0);
+    *reinterpret_cast<uint4*>(planes + plane_stride + off) = *reinterpret_cast<uint4*>(d1);
+  }
+}
+
+}  // namespace
+
+void launch_digitize(const float* x, int64_t ldx, int64_t M, int64_t K, int norm, const float* g,
+                     const float* b, uint8_t* planes, int64_t plane_stride, int* exps,
+                     cudaStream_t st) {
+  const int64_t Mp = (M + 127) / 128 * 128;
+  digitize_kernel<<<(unsigned)Mp, 256, 0, st>>>(x, ldx, M, K, norm, g, b, planes, plane_stride,
+                                                exps);
+  count_launch();
+}
+
+void launch_gemm_i8_tc(const TcGemmArgs& a, cudaStream_t st) {
+  static bool set = false;
+  const size_t smem = (size_t)STAGES * STAGE;
+  if (!set) {
+    cudaFuncSetAttribute(gemm_i8_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    set = true;
+  }
+  dim3 grid((unsigned)(a.N / (128 * NGRP)), (unsigned)((a.M + BM - 1) / BM));
+  gemm_i8_tc_kernel<<<grid, 256, smem, st>>>(a);
+  count_launch();
+}
+
+int64_t tc_plane_bytes(int64_t M, int64_t K) { return (M + 127) / 128 * 128 * K; }
+
+}  // namespace sp

@@ -1,0 +1,28 @@
+// Prefill / replay (n_new > 1) tensor-core interfaces.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace sp {
+
+struct TcGemmArgs {
+  const void* w;            // int8 weights, core-matrix layout (common.cuh)
+  const float* wscale;      // per output channel
+  int64_t N, K;
+  const uint8_t* planes;    // activation digit planes d0 | d1 (core-matrix layout, M padded to 128)
+  int64_t plane_stride;     // bytes between d0 and d1
+  const int* exps;          // per-row exponents e_m (|x| < 2^e)
+  int64_t M;
+  float* y;
+  int64_t ldy;
+  const float* res;         // EPI_RESID (may alias y)
+  int epi;
+};
+
+int64_t tc_plane_bytes(int64_t M, int64_t K);
+void launch_digitize(const float* x, int64_t ldx, int64_t M, int64_t K, int norm, const float* g,
+                     const float* b, uint8_t* planes, int64_t plane_stride, int* exps,
+                     cudaStream_t st);
+void launch_gemm_i8_tc(const TcGemmArgs& a, cudaStream_t st);
+
+}  // namespace sp

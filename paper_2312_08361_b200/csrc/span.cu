@@ -12,6 +12,7 @@
 #include "common.cuh"
 #include "decode.cuh"
 #include "kernels.cuh"
+#include "prefill.cuh"
 
 namespace {
 thread_local std::string g_err;
@@ -89,6 +90,11 @@ struct sp_span {
   float* attn_part = nullptr;
   int* attn_cnt = nullptr;
   bool gains_one = true;   // LN/RMS gains are 1 at init (SP/model.py:192-195), never mutated
+  // tcgen05 prefill path
+  int64_t tc_cap_rows = 0;
+  uint8_t* planes = nullptr;
+  int* exps = nullptr;
+  bool use_tc_prefill = true;
   int64_t attn_ws_floats = 0;
   float* attn_ws = nullptr;
   std::mutex mu;
@@ -179,6 +185,22 @@ int ensure_decode(sp_span* s, int64_t rows) {
   SP_CUDA_TRY(cudaMemset(s->attn_cnt, 0, cap * s->kvh * sizeof(int)));
   s->dec_cap_rows = cap;
   return SP_OK;
+}
+
+int ensure_tc(sp_span* s, int64_t rows) {
+  if (rows <= s->tc_cap_rows) return SP_OK;
+  cudaFree(s->planes); cudaFree(s->exps);
+  const int64_t Mp = (rows + 127) / 128 * 128;
+  const int64_t K = std::max<int64_t>(s->d, s->F);
+  SP_CUDA_TRY(cudaMalloc(&s->planes, 2 * Mp * K));
+  SP_CUDA_TRY(cudaMalloc(&s->exps, Mp * sizeof(int)));
+  s->tc_cap_rows = Mp;
+  return SP_OK;
+}
+
+bool tc_ok(const sp_span* s) {
+  return s->cfg.weight_dtype == kI8 && s->n_qkv % 256 == 0 && s->d % 256 == 0 &&
+         s->n_up % 256 == 0 && s->d % 128 == 0 && s->F % 128 == 0;
 }
 
 int ensure_attn_ws(sp_span* s, int width) {
@@ -396,10 +418,79 @@ int run_span_decode_tc(sp_span* s, sp_kv* kv, int b0, int b1, float* y, int widt
   return SP_OK;
 }
 
+// prefill / replay (n_new > 1) with int8 weights: tcgen05 GEMMs on activation
+// digit planes (gemm_tc.cu), SIMT attention
+int run_span_prefill_tc(sp_span* s, sp_kv* kv, int b0, int b1, float* y, float* record,
+                        int width, int n_new, cudaStream_t st) {
+  const int64_t R = (int64_t)width * n_new;
+  int rc = ensure_scratch(s, R);
+  if (rc) return rc;
+  rc = ensure_attn_ws(s, width);
+  if (rc) return rc;
+  rc = ensure_tc(s, R);
+  if (rc) return rc;
+  const int fam = s->cfg.family;
+  const int norm = fam == kLlama ? 1 : 2;
+  const int64_t d = s->d, F = s->F;
+  const int64_t Mp = (R + 127) / 128 * 128;
+  const double kv_elt = s->cfg.kv_dtype == kKVBF16 ? 2.0 : 4.0;
+  AttnArgs at{};
+  at.family = fam; at.kv_dtype = s->cfg.kv_dtype;
+  at.width = width; at.n_new = n_new; at.t0 = kv->length;
+  at.H = s->H; at.kvh = s->kvh; at.hd = s->hd;
+  at.qkv = s->qkvb; at.ldqkv = s->n_qkv;
+  at.page_table = kv->d_table; at.max_pages = s->max_pages;
+  at.rope_cos = s->rope_cos; at.rope_sin = s->rope_sin; at.alibi = s->alibi;
+  at.ctx = s->ctx; at.workspace = s->attn_ws;
+  auto gemm = [&](void* w, float* sc, int64_t N, int64_t K, float* out, int64_t ldy,
+                  const float* res, int epi) {
+    ProfScope ps(s, PC_GEMM, (double)N * K + 4.0 * N + 2.0 * Mp * K + 4.0 * R * ldy,
+                 2.0 * R * N * K, st);
+    TcGemmArgs g{};
+    g.w = w; g.wscale = sc; g.N = N; g.K = K; g.planes = s->planes; g.plane_stride = Mp * K;
+    g.exps = s->exps; g.M = R; g.y = out; g.ldy = ldy; g.res = res; g.epi = epi;
+    launch_gemm_i8_tc(g, st);
+  };
+  auto digit = [&](const float* x, int64_t K, int nm, const float* gg, const float* bb) {
+    ProfScope ps(s, PC_OTHER, 4.0 * R * K + 2.0 * Mp * K, 0, st);
+    launch_digitize(x, K, R, K, nm, gg, bb, s->planes, Mp * K, s->exps, st);
+  };
+  for (int b = b0 - s->start; b < b1 - s->start; ++b) {
+    BlockW& W = s->blocks[b];
+    at.kv_pool = s->pool + (int64_t)b * s->block_stride;
+    if (record)
+      SP_CUDA_TRY(cudaMemcpyAsync(record + (int64_t)(b - (b0 - s->start)) * R * d, y,
+                                  R * d * sizeof(float), cudaMemcpyDeviceToDevice, st));
+    digit(y, d, norm, W.ln1_g, W.ln1_b);
+    gemm(W.qkv, W.s_qkv, s->n_qkv, d, s->qkvb, s->n_qkv, nullptr, EPI_STORE);
+    {
+      ProfScope ps(s, PC_OTHER, 4.0 * R * s->n_qkv + (double)R * 2 * s->kv * kv_elt, 0, st);
+      launch_rope_append(at, st);
+    }
+    {
+      const double pairs = (double)width * ((double)n_new * kv->length +
+                                            (double)n_new * (n_new + 1) / 2);
+      ProfScope ps(s, PC_ATTN_PRE, (double)width * (kv->length + n_new) * 2 * s->kv * kv_elt,
+                   4.0 * pairs * s->H * s->hd, st);
+      launch_attention_prefill(at, st);
+    }
+    digit(s->ctx, d, 0, nullptr, nullptr);
+    gemm(W.o, W.s_o, d, d, y, d, y, EPI_RESID);
+    digit(y, d, norm, W.ln2_g, W.ln2_b);
+    gemm(W.up, W.s_up, s->n_up, d, s->mlp, F, nullptr, fam == kLlama ? EPI_SWIGLU : EPI_GELU);
+    digit(s->mlp, F, 0, nullptr, nullptr);
+    gemm(W.down, W.s_down, d, F, y, d, y, EPI_RESID);
+  }
+  SP_CHECK_LAUNCH();
+  return SP_OK;
+}
+
 int run_span(sp_span* s, sp_kv* kv, int b0, int b1, float* y, float* record, int width,
              int n_new, cudaStream_t st) {
   if (n_new == 1 && s->cfg.weight_dtype != kF32 && !record)
     return run_span_decode_tc(s, kv, b0, b1, y, width, st);
+  if (n_new > 1 && tc_ok(s) && s->use_tc_prefill)
+    return run_span_prefill_tc(s, kv, b0, b1, y, record, width, n_new, st);
   const int64_t R = (int64_t)width * n_new;
   const bool decode = (n_new == 1);
   const int wd = s->cfg.weight_dtype;
@@ -626,6 +717,7 @@ int sp_span_destroy(sp_span* s) {
   cudaFree(s->mlp_raw); cudaFree(s->gemv_ws); cudaFree(s->gemv_cnt); cudaFree(s->attn_ws);
   cudaFree(s->st_norm1); cudaFree(s->st_ctx); cudaFree(s->st_norm2); cudaFree(s->st_mlp);
   cudaFree(s->ws2); cudaFree(s->cnt2); cudaFree(s->attn_part); cudaFree(s->attn_cnt);
+  cudaFree(s->planes); cudaFree(s->exps);
   for (auto& r : s->prof_recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : s->ev_pool) cudaEventDestroy(e);
   delete s;
@@ -786,6 +878,13 @@ int sp_span_forward_stateless(sp_span* s, int32_t b0, int32_t b1, const float* x
   }
   sp_kv_destroy(kv);
   return rc;
+}
+
+int sp_span_set_option(sp_span* s, int32_t option, int32_t value) {
+  if (!s) SP_FAIL(SP_ERR_ARG, "null span");
+  if (option == 0) s->use_tc_prefill = value != 0;
+  else SP_FAIL(SP_ERR_ARG, "unknown option");
+  return SP_OK;
 }
 
 int sp_span_set_profiling(sp_span* s, int32_t enable) {

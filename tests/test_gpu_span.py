@@ -213,3 +213,28 @@ def test_engine_blocks_params_hash_matches_reference(golden_toy):
     arrs = eng.blocks[0].arrays()
     assert np.array_equal(arrs[0], golden_toy["default__w_wq_0"])
     assert np.array_equal(arrs[5], golden_toy["default__w_w2_0"])
+
+
+def test_tc_prefill_matches_simt_and_is_batch_invariant():
+    """tcgen05 int8 prefill GEMM (2 activation digit planes, exact int32
+    accumulate) vs the exact-f32 SIMT GEMM on the same weights, and the
+    micro-batch invariance of T/test_server.py:247-255 on the tensor-core path."""
+    import ctypes
+    cfg = SMALL["llama_int8"]
+    from paper_2312_08361_b200 import _lib
+    from paper_2312_08361_b200.engine import DeviceSpan, B200ServerEngine
+    span_tc = DeviceSpan(cfg, 0, cfg.n_blocks)
+    span_ref = DeviceSpan(cfg, 0, cfg.n_blocks)
+    _lib.check(span_ref.lib.sp_span_set_option(span_ref.handle, 0, 0))
+    e_tc, e_ref = B200ServerEngine(cfg, span=span_tc), B200ServerEngine(cfg, span=span_ref)
+    rng = np.random.default_rng(21)
+    x = rng.standard_normal((3 * 150, cfg.hidden_dim)).astype(np.float32)
+    a = e_tc.forward(0, cfg.n_blocks, _blob(x), 3, 150, 10**9, None).array()
+    b = e_ref.forward(0, cfg.n_blocks, _blob(x), 3, 150, 10**9, None).array()
+    rel = np.abs(a - b).max() / np.abs(b).max()
+    assert rel < 2e-3, rel
+    split = e_tc.forward(0, cfg.n_blocks, _blob(x), 3, 150, 150, None).array()
+    assert np.array_equal(a, split)
+    runner = om.SpanRunner(cfg, 0, cfg.n_blocks, width=3)
+    want = runner.step(x.reshape(3, 150, -1)).reshape(-1, cfg.hidden_dim)
+    assert np.abs(a - want).max() <= 2e-2 * np.abs(want).max()
