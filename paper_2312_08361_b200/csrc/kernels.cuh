@@ -82,6 +82,8 @@ void launch_rope_append(const AttnArgs& a, cudaStream_t st);
 int64_t attn_workspace_floats(int width, int H, int hd, int max_seq);
 void launch_attention_decode(const AttnArgs& a, cudaStream_t st);
 void launch_attention_prefill(const AttnArgs& a, cudaStream_t st);
+// tensor-core flash prefill (bf16 KV, hd 64/128); false if the shape is unsupported
+bool launch_attention_prefill_mma(const AttnArgs& a, cudaStream_t st);
 
 // KV page copy (copy-on-write of a shared tail page): all blocks of the span
 void launch_page_copy(void* pool, int64_t block_stride_bytes, int n_blocks,

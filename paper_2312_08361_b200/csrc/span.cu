@@ -472,7 +472,7 @@ int run_span_prefill_tc(sp_span* s, sp_kv* kv, int b0, int b1, float* y, float* 
                                             (double)n_new * (n_new + 1) / 2);
       ProfScope ps(s, PC_ATTN_PRE, (double)width * (kv->length + n_new) * 2 * s->kv * kv_elt,
                    4.0 * pairs * s->H * s->hd, st);
-      launch_attention_prefill(at, st);
+      if (!launch_attention_prefill_mma(at, st)) launch_attention_prefill(at, st);
     }
     digit(s->ctx, d, 0, nullptr, nullptr);
     gemm(W.o, W.s_o, d, d, y, d, y, EPI_RESID);
@@ -534,7 +534,7 @@ int run_span(sp_span* s, sp_kv* kv, int b0, int b1, float* y, float* record, int
       ProfScope ps(s, decode ? PC_ATTN_DEC : PC_ATTN_PRE, kvbytes + 8.0 * R * d,
                    4.0 * pairs * s->H * s->hd, st);
       if (decode) launch_attention_decode(at, st);
-      else launch_attention_prefill(at, st);
+      else if (!launch_attention_prefill_mma(at, st)) launch_attention_prefill(at, st);
     }
     linear(s, wd, W.o, W.s_o, d, d, s->ctx, y, d, y, EPI_RESID, R, decode, st);
     {
