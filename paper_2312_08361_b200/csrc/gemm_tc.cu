@@ -113,8 +113,10 @@ __global__ void __launch_bounds__(256, 1) gemm_i8_tc_kernel(TcGemmArgs a) {
   __shared__ uint32_t tmem_base;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int ng0 = blockIdx.x * NGRP;         // first weight group of this tile
-  const int mt = blockIdx.y;                 // token tile (128 rows)
+  // token tiles vary fastest: the CTAs resident together share one weight
+  // tile, so each weight byte leaves DRAM once and the re-reads hit L2
+  const int ng0 = blockIdx.y * NGRP;         // first weight group of this tile
+  const int mt = blockIdx.x;                 // token tile (128 rows)
   const int64_t KT = a.K >> 5;               // 32-byte units along K
   const int KB = (int)(KT / KU);             // stages along K
 
@@ -330,7 +332,7 @@ void launch_gemm_i8_tc(const TcGemmArgs& a, cudaStream_t st) {
                          (int)smem);
     set = true;
   }
-  dim3 grid((unsigned)(a.N / (128 * NGRP)), (unsigned)((a.M + BM - 1) / BM));
+  dim3 grid((unsigned)((a.M + BM - 1) / BM), (unsigned)(a.N / (128 * NGRP)));
   gemm_i8_tc_kernel<<<grid, 256, smem, st>>>(a);
   count_launch();
 }
