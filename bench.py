@@ -228,6 +228,8 @@ def run_b200(args) -> None:
     t_gen = time.perf_counter() - t_gen
     eng = B200ServerEngine(cfg, span=span)
     lib = _lib.load()
+    if os.environ.get("SP_PDL") == "0":       # A/B switch: programmatic dependent launch off
+        _lib.check(lib.sp_span_set_option(span.handle, 1, 0))
     d = cfg.hidden_dim
     stream = torch.cuda.current_stream(dev)
 

@@ -67,18 +67,28 @@ __device__ void merge_tail(const AttnDecArgs& a, int G, int slot, int kh, int ch
     hL[g] = L;
   }
   __syncthreads();
-  const int64_t pstride = (int64_t)G * (HD + 2);
-  float* part = a.part + ((int64_t)(slot * a.kvh + kh) * a.max_pages + chunk) * pstride;
-  for (int i = threadIdx.x; i < G * HD; i += NTH) {
-    const int g = i / HD, dd = i % HD;
-    float O = 0.f;
+  // partials: O [(slot, kv head, chunk)][G][HD] (16-byte aligned rows), then
+  // the (max, sum) pairs [(slot, kv head, chunk)][G][2] after all O rows
+  const int64_t sk = (int64_t)slot * a.kvh + kh;
+  const int GH = G * HD;
+  float* partO = a.part + (sk * a.max_pages + chunk) * GH;
+  float* stats = a.part + (int64_t)a.width * a.H * a.max_pages * HD;
+  for (int i = threadIdx.x * 4; i < GH; i += NTH * 4) {
+    const int g = i / HD;
+    float4 O = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-    for (int w = 0; w < 4; ++w) O = fmaf(wo[(w * G + g) * HD + dd], wf[w][g], O);
-    part[g * (HD + 2) + dd] = O;
+    for (int w = 0; w < 4; ++w) {
+      const float4 v = *reinterpret_cast<const float4*>(wo + w * GH + i);
+      const float f = wf[w][g];
+      O.x = fmaf(v.x, f, O.x); O.y = fmaf(v.y, f, O.y);
+      O.z = fmaf(v.z, f, O.z); O.w = fmaf(v.w, f, O.w);
+    }
+    __stcg(reinterpret_cast<float4*>(partO + i), O);
   }
   if (threadIdx.x < G) {
-    part[threadIdx.x * (HD + 2) + HD] = hM[threadIdx.x];
-    part[threadIdx.x * (HD + 2) + HD + 1] = hL[threadIdx.x];
+    float* st = stats + ((sk * a.max_pages + chunk) * G + threadIdx.x) * 2;
+    __stcg(st, hM[threadIdx.x]);
+    __stcg(st + 1, hL[threadIdx.x]);
   }
 
   // ---- last CTA of this (slot, kv head): merge chunks in ascending order ----
@@ -95,11 +105,10 @@ __device__ void merge_tail(const AttnDecArgs& a, int G, int slot, int kh, int ch
   } else {
     __syncthreads();
   }
-  const float* pall = a.part + (int64_t)(slot * a.kvh + kh) * a.max_pages * pstride;
+  const float* sall = stats + sk * a.max_pages * G * 2;
   for (int e = threadIdx.x; e < nchunk * G; e += NTH) {
-    const int c = e / G, g = e % G;
-    pm[c * GMAX + g] = __ldcg(pall + c * pstride + g * (HD + 2) + HD);
-    pl[c * GMAX + g] = __ldcg(pall + c * pstride + g * (HD + 2) + HD + 1);
+    pm[(e / G) * GMAX + e % G] = __ldcg(sall + 2 * e);
+    pl[(e / G) * GMAX + e % G] = __ldcg(sall + 2 * e + 1);
   }
   __syncthreads();
   // per head: global max, then per-chunk factor f_c = exp(m_c - M) (in pm), 1/L
@@ -116,22 +125,30 @@ __device__ void merge_tail(const AttnDecArgs& a, int G, int slot, int kh, int ch
     hL[g] = L;
   }
   __syncthreads();
+  // every float4 of every chunk is requested before the first is used: the
+  // merge costs one L2 round trip per 8 chunks, not one per element
+  const float* oall = a.part + sk * a.max_pages * GH;
   float* outh = wo;
-  for (int i = threadIdx.x; i < G * HD; i += NTH) {
-    const int g = i / HD, dd = i % HD;
-    float O = 0.f;
+  for (int i = threadIdx.x * 4; i < GH; i += NTH * 4) {
+    const int g = i / HD;
+    float4 O = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int c0 = 0; c0 < nchunk; c0 += 8) {
-      float wv[8];
+      float4 wv[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u)
-        wv[u] = (c0 + u < nchunk) ? __ldcg(pall + (c0 + u) * pstride + g * (HD + 2) + dd) : 0.f;
+        wv[u] = (c0 + u < nchunk) ? __ldcg(reinterpret_cast<const float4*>(oall + (int64_t)(c0 + u) * GH + i))
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (c0 + u < nchunk) O = fmaf(wv[u], pm[(c0 + u) * GMAX + g], O);
+      for (int u = 0; u < 8; ++u) {
+        const float f = (c0 + u < nchunk) ? pm[(c0 + u) * GMAX + g] : 0.f;
+        O.x = fmaf(wv[u].x, f, O.x); O.y = fmaf(wv[u].y, f, O.y);
+        O.z = fmaf(wv[u].z, f, O.z); O.w = fmaf(wv[u].w, f, O.w);
+      }
     }
-    const float c = O / hL[g];
-    outh[i] = c;
-    a.ctx[(int64_t)slot * a.H * HD + (kh * G + g) * HD + dd] = c;
+    const float inv = hL[g];
+    const float4 c = make_float4(O.x / inv, O.y / inv, O.z / inv, O.w / inv);
+    *reinterpret_cast<float4*>(outh + i) = c;
+    *reinterpret_cast<float4*>(a.ctx + (int64_t)slot * a.H * HD + kh * GH + i) = c;
   }
   if (threadIdx.x == 0 && nchunk > 1) a.counters[slot * a.kvh + kh] = 0;
   __syncthreads();
@@ -379,7 +396,28 @@ __global__ void __launch_bounds__(NTH) attn_dec_mma_kernel(AttnDecArgs a) {
   const float* cs = a.rope_cos ? a.rope_cos + (int64_t)a.t0 * half : nullptr;
   const float* sn = a.rope_sin ? a.rope_sin + (int64_t)a.t0 * half : nullptr;
 
-  // ---- q (RoPE) -> bf16 hi/lo, [head][dim]; unused heads zero.  All loads
+  // ---- 1. stage this warp's 32 K/V rows first (cp.async, zero-fill past T):
+  // the loads do not depend on q, so their latency overlaps everything below.
+  // Row t0 is read stale here and patched in smem after the append ----
+  const int p0 = chunk * CHUNK + warp * 32;
+  const int nv = max(0, min(32, T - p0));
+  {
+    const int page = a.page_table[slot * a.max_pages + min(p0, T - 1) / kPageTokens];
+    const __nv_bfloat16* kbase = page_ptr<__nv_bfloat16>(a.kv_pool, page, 0, a.kvh, kh, HD) + (p0 % kPageTokens) * HD;
+    const __nv_bfloat16* vbase = page_ptr<__nv_bfloat16>(a.kv_pool, page, 1, a.kvh, kh, HD) + (p0 % kPageTokens) * HD;
+    constexpr int CPR = HD / 8;                   // 16-byte chunks per row
+    for (int c = lane; c < 32 * CPR; c += 32) {
+      const int j = c / CPR, e = (c % CPR) * 8;
+      const bool ok = j < nv;
+      cp_async16(&Kt[warp * 32 + j][e], kbase + (ok ? j : 0) * HD + e, ok);
+      cp_async16(&Vt[warp * 32 + j][e], vbase + (ok ? j : 0) * HD + e, ok);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  pdl_trigger();
+  pdl_wait();        // q / k_new / v_new come from the QKV GEMV just before
+
+  // ---- 2. q (RoPE) -> bf16 hi/lo, [head][dim]; unused heads zero.  All loads
   // of the thread are issued before any arithmetic (one latency, not eight) ----
   {
     constexpr int PER = 8 * HD / NTH;
@@ -387,7 +425,7 @@ __global__ void __launch_bounds__(NTH) attn_dec_mma_kernel(AttnDecArgs a) {
 #pragma unroll
     for (int u = 0; u < PER; ++u) {
       const int i = threadIdx.x + u * NTH, g = i / HD, dd = i % HD, j = dd % half;
-      const float* q = qrow + (kh * min(G - 1, g) + 0) * 0 + (kh * G + min(g, G - 1)) * HD;
+      const float* q = qrow + (kh * G + min(g, G - 1)) * HD;
       x1[u] = q[j];
       x2[u] = q[j + half];
       c[u] = cs ? cs[j] : 1.f;
@@ -409,35 +447,37 @@ __global__ void __launch_bounds__(NTH) attn_dec_mma_kernel(AttnDecArgs a) {
       ql[g][dd] = __float2bfloat16_rn(v - __bfloat162float(h));
     }
   }
-  // ---- append the new position ----
-  if (a.t0 / CHUNK == chunk) {
+  // ---- 3. append the new position (KVCache.append, SP/model.py:163-167) ----
+  const bool appender = (a.t0 / CHUNK == chunk);
+  __nv_bfloat16 knew[HD / NTH > 0 ? HD / NTH : 1], vnew[HD / NTH > 0 ? HD / NTH : 1];
+  if (appender) {
     const int page = a.page_table[slot * a.max_pages + a.t0 / kPageTokens];
     __nv_bfloat16* kp = page_ptr<__nv_bfloat16>(a.kv_pool, page, 0, a.kvh, kh, HD) + (a.t0 % kPageTokens) * HD;
     __nv_bfloat16* vp = page_ptr<__nv_bfloat16>(a.kv_pool, page, 1, a.kvh, kh, HD) + (a.t0 % kPageTokens) * HD;
     const float* kn = qrow + a.H * HD + kh * HD;
     const float* vn = qrow + a.H * HD + a.kvh * HD + kh * HD;
-    for (int dd = threadIdx.x; dd < HD; dd += NTH) {
-      kp[dd] = __float2bfloat16_rn((a.family == kLlama) ? rope_val(kn, dd, half, cs, sn) : kn[dd]);
-      vp[dd] = __float2bfloat16_rn(vn[dd]);
+#pragma unroll
+    for (int u = 0; u * NTH < HD; ++u) {
+      const int dd = threadIdx.x + u * NTH;
+      if (dd < HD) {
+        knew[u] = __float2bfloat16_rn((a.family == kLlama) ? rope_val(kn, dd, half, cs, sn) : kn[dd]);
+        vnew[u] = __float2bfloat16_rn(vn[dd]);
+        kp[dd] = knew[u];
+        vp[dd] = vnew[u];
+      }
     }
   }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncthreads();
-
-  // ---- stage this warp's 32 K/V rows (cp.async, zero-fill past T) ----
-  const int p0 = chunk * CHUNK + warp * 32;
-  const int nv = max(0, min(32, T - p0));
-  const int page = a.page_table[slot * a.max_pages + min(p0, T - 1) / kPageTokens];
-  const __nv_bfloat16* kbase = page_ptr<__nv_bfloat16>(a.kv_pool, page, 0, a.kvh, kh, HD) + (p0 % kPageTokens) * HD;
-  const __nv_bfloat16* vbase = page_ptr<__nv_bfloat16>(a.kv_pool, page, 1, a.kvh, kh, HD) + (p0 % kPageTokens) * HD;
-  constexpr int CPR = HD / 8;                     // 16-byte chunks per row
-  for (int c = lane; c < 32 * CPR; c += 32) {
-    const int j = c / CPR, e = (c % CPR) * 8;
-    const bool ok = j < nv;
-    cp_async16(&Kt[warp * 32 + j][e], kbase + (ok ? j : 0) * HD + e, ok);
-    cp_async16(&Vt[warp * 32 + j][e], vbase + (ok ? j : 0) * HD + e, ok);
+  if (appender) {
+    const int r = a.t0 - chunk * CHUNK;
+#pragma unroll
+    for (int u = 0; u * NTH < HD; ++u) {
+      const int dd = threadIdx.x + u * NTH;
+      if (dd < HD) { Kt[r][dd] = knew[u]; Vt[r][dd] = vnew[u]; }
+    }
+    __syncthreads();
   }
-  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
-  __syncwarp();
 
   // ---- S[32 x 8] = K . q^T ----
   float sacc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
@@ -546,7 +586,7 @@ void launch_mma(const AttnDecArgs& a, cudaStream_t st) {
                          (int)smem);
     set = smem;
   }
-  attn_dec_mma_kernel<HD><<<grid, NTH, smem, st>>>(a);
+  launch_pdl(attn_dec_mma_kernel<HD>, grid, dim3(NTH), smem, st, a);
   count_launch();
 }
 

@@ -82,6 +82,34 @@ __host__ __device__ __forceinline__ int64_t cm_offset(int64_t n, int64_t kb, int
 // host-side count of kernels launched by this library (bench `gpu_launches`)
 void count_launch();
 
+// ---- programmatic dependent launch (decode chain) ----------------------------
+// A kernel launched with launch_pdl() may start while the previous kernel in
+// the stream is still running: everything before pdl_wait() must touch only
+// data no earlier kernel of the chain writes (weights, old KV rows, page
+// tables); pdl_wait() returns once the previous grid has completed and its
+// memory is visible.  pdl_trigger() lets the next grid be scheduled early.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+extern bool g_pdl;   // sp_span_set_option(.., 1, ..): decode kernels use PDL (default on)
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 }  // namespace sp
 
 #define SP_CUDA_TRY(expr)                                       \

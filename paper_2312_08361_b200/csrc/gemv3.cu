@@ -147,6 +147,26 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
     for (int st = 0; st < STAGES; ++st) mbar_init(&ws_->bar[st], 1);
     mbar_fence_init();
   }
+  __syncwarp();
+  constexpr int XB = KTILE * 4;
+  const uint8_t* wbase = reinterpret_cast<const uint8_t*>(a.w);
+  const uint64_t policy = evict_first_policy();
+  uint64_t policy_x;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(policy_x));
+  const int nunits = u1 > u0 ? (int)(u1 - u0) : 0;
+  const int npre = nunits < STAGES ? nunits : STAGES;
+  // ---- before the dependency: the weights of the first STAGES units (no
+  // kernel writes weights), so their DRAM latency overlaps the previous
+  // kernel's tail; each stage's barrier also expects its activation bytes ----
+  if (lane == 0)
+    for (int i = 0; i < npre; ++i) {
+      const int64_t u = u0 + i;
+      mbar_expect_tx(&ws_->bar[i], UNIT_BYTES + Rn * XB);
+      tma_load_1d(ring + i * STAGE_BYTES, wbase + ((u / KT) * KT + u % KT) * UNIT_BYTES,
+                  UNIT_BYTES, &ws_->bar[i], policy);
+    }
+  pdl_trigger();
+  pdl_wait();
   // ---- per-row parameters from the producer's partial stats ----
   // CTA-wide: 256 threads load the P_in x Rn partials with several loads in
   // flight each, then a fixed-order tree (warp shuffles, then warps in order)
@@ -237,17 +257,12 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
   const int t4 = lane & 3;
 
   // ---- TMA producer (lane 0) ----
-  const uint8_t* wbase = reinterpret_cast<const uint8_t*>(a.w);
-  const uint64_t policy = evict_first_policy();
-  uint64_t policy_x;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(policy_x));
   // producer state (lane 0): next unit to issue as (group, k-tile, ring stage)
-  const int nunits = (int)(u1 - u0);
-  int p_grp = (int)(u0 / KT), p_kt = (int)(u0 % KT), p_st = 0, p_left = nunits;
+  int p_grp = (int)((u0 + npre) / KT), p_kt = (int)((u0 + npre) % KT);
+  int p_st = npre % STAGES, p_left = nunits - npre;
   auto issue_next = [&]() {
     // the unit's weights and, alongside, each batch row's activation chunk:
     // both arrive on the same mbarrier (no separate activation-load latency)
-    constexpr int XB = KTILE * 4;
     mbar_expect_tx(&ws_->bar[p_st], UNIT_BYTES + Rn * XB);
     uint8_t* dstg = ring + p_st * STAGE_BYTES;
     tma_load_1d(dstg, wbase + ((int64_t)p_grp * KT + p_kt) * UNIT_BYTES, UNIT_BYTES,
@@ -261,7 +276,12 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
   };
   __syncwarp();
   if (lane == 0)
-    for (int i = 0; i < STAGES && p_left > 0; ++i) issue_next();
+    for (int i = 0; i < npre; ++i) {     // activation chunks of the prefetched units
+      const int64_t kt = (u0 + i) % KT;
+      for (int r = 0; r < Rn; ++r)
+        tma_load_1d(ring + i * STAGE_BYTES + UNIT_BYTES + r * XSLOT,
+                    a.x + (int64_t)(r0 + r) * a.ldx + kt * KTILE, XB, &ws_->bar[i], policy_x);
+    }
 
   // ---- activation side: read from the stage (arrived with the weights) ----
   XVec xc[NT][2], gc[NT][2];
@@ -461,8 +481,8 @@ void launch_cfg(const GemvArgs& a, int r0, int rn, cudaStream_t st) {
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     set = true;
   }
-  gemv3_kernel<WT, NT, NORMT, HASG><<<grid, NW * 32, smem, st>>>(a, r0, rn, a.R, units,
-                                                                   (int64_t)grid * NW);
+  launch_pdl(gemv3_kernel<WT, NT, NORMT, HASG>, dim3(grid), dim3(NW * 32), smem, st, a, r0, rn,
+             a.R, units, (int64_t)grid * NW);
   count_launch();
 }
 

@@ -35,6 +35,7 @@ void sp_set_error(const char* file, int line, const char* msg) {
 namespace sp {
 static std::atomic<int64_t> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+bool g_pdl = true;
 }  // namespace sp
 
 using namespace sp;
@@ -883,6 +884,7 @@ int sp_span_forward_stateless(sp_span* s, int32_t b0, int32_t b1, const float* x
 int sp_span_set_option(sp_span* s, int32_t option, int32_t value) {
   if (!s) SP_FAIL(SP_ERR_ARG, "null span");
   if (option == 0) s->use_tc_prefill = value != 0;
+  else if (option == 1) g_pdl = value != 0;
   else SP_FAIL(SP_ERR_ARG, "unknown option");
   return SP_OK;
 }
