@@ -15,7 +15,10 @@
 //     ascending order (deterministic) and writes ctx plus the per-head
 //     partial statistics the O-projection GEMV folds in.
 // Bytes per launch: K+V of the visible positions (2*T*kvh*hd*elt) + q/ctx.
+#include <cstdio>
+#include <cstdlib>
 #include <type_traits>
+#include <vector>
 
 #include "common.cuh"
 #include "decode.cuh"
@@ -28,6 +31,14 @@ namespace {
 constexpr int NTH = 128;
 constexpr int CHUNK = 128;          // positions per CTA (two pages)
 constexpr int GMAX = 16;            // max query heads per kv head
+
+__device__ __forceinline__ void trace_mark(const AttnDecArgs& a, int ph) {
+  if (a.trace && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    a.trace[(blockIdx.y * gridDim.x + blockIdx.x) * 12 + ph] = t;
+  }
+}
 
 template <typename KT>
 __device__ __forceinline__ KT* page_ptr(void* pool, int page, int kvsel, int kvh, int h, int hd) {
@@ -101,55 +112,94 @@ __device__ void merge_tail(const AttnDecArgs& a, int G, int slot, int kh, int ch
       *last_flag = (old == nchunk - 1);
     }
     __syncthreads();
+    trace_mark(a, 4);
     if (!*last_flag) return;
   } else {
     __syncthreads();
   }
   const float* sall = stats + sk * a.max_pages * G * 2;
-  for (int e = threadIdx.x; e < nchunk * G; e += NTH) {
-    pm[(e / G) * GMAX + e % G] = __ldcg(sall + 2 * e);
-    pl[(e / G) * GMAX + e % G] = __ldcg(sall + 2 * e + 1);
-  }
-  __syncthreads();
-  // per head: global max, then per-chunk factor f_c = exp(m_c - M) (in pm), 1/L
-  if (threadIdx.x < G) {
-    const int g = threadIdx.x;
-    float M = -INFINITY;
-    for (int c = 0; c < nchunk; ++c) M = fmaxf(M, pm[c * GMAX + g]);
-    float L = 0.f;
-    for (int c = 0; c < nchunk; ++c) {
-      const float f = expf(pm[c * GMAX + g] - M);
-      pm[c * GMAX + g] = f;
-      L = fmaf(pl[c * GMAX + g], f, L);
-    }
-    hL[g] = L;
-  }
-  __syncthreads();
-  // every float4 of every chunk is requested before the first is used: the
-  // merge costs one L2 round trip per 8 chunks, not one per element
   const float* oall = a.part + sk * a.max_pages * GH;
-  float* outh = wo;
-  for (int i = threadIdx.x * 4; i < GH; i += NTH * 4) {
-    const int g = i / HD;
-    float4 O = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int c0 = 0; c0 < nchunk; c0 += 8) {
-      float4 wv[8];
+  // every load below is issued before its first use: the merge costs one L2
+  // round trip for the (max, sum) pairs and one per 8 chunks of O
+  {
+    float2 mv[4];
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
-        wv[u] = (c0 + u < nchunk) ? __ldcg(reinterpret_cast<const float4*>(oall + (int64_t)(c0 + u) * GH + i))
-                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int u = 0; u < 4; ++u) {
+      const int e = threadIdx.x + u * NTH;
+      mv[u] = e < nchunk * G ? __ldcg(reinterpret_cast<const float2*>(sall) + e)
+                             : make_float2(0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = threadIdx.x + u * NTH;
+      if (e < nchunk * G) { pm[(e / G) * GMAX + e % G] = mv[u].x; pl[(e / G) * GMAX + e % G] = mv[u].y; }
+    }
+    for (int e = threadIdx.x + 4 * NTH; e < nchunk * G; e += NTH) {
+      pm[(e / G) * GMAX + e % G] = __ldcg(sall + 2 * e);
+      pl[(e / G) * GMAX + e % G] = __ldcg(sall + 2 * e + 1);
+    }
+  }
+  __syncthreads();
+  // per head (one warp each): global max M, chunk factors f_c = exp(m_c - M)
+  // (stored over pm) and L = sum_c l_c f_c, by a fixed shuffle tree
+  {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int g = warp; g < G; g += NTH / 32) {
+      float m = -INFINITY;
+      for (int c = lane; c < nchunk; c += 32) m = fmaxf(m, pm[c * GMAX + g]);
+      const float M = warp_max(m);
+      float L = 0.f;
+      for (int c = lane; c < nchunk; c += 32) {
+        const float f = expf(pm[c * GMAX + g] - M);
+        pm[c * GMAX + g] = f;
+        L = fmaf(pl[c * GMAX + g], f, L);
+      }
+      L = warp_sum(L);
+      if (lane == 0) hL[g] = L;
+    }
+  }
+  __syncthreads();
+  trace_mark(a, 5);
+  float* outh = wo;
+  for (int ib = threadIdx.x * 4; ib < GH; ib += 2 * NTH * 4) {
+    const int i1 = ib + NTH * 4;
+    const bool has1 = i1 < GH;
+    float4 O0 = make_float4(0.f, 0.f, 0.f, 0.f), O1 = O0;
+    for (int c0 = 0; c0 < nchunk; c0 += 8) {
+      float4 w0[8], w1[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const float f = (c0 + u < nchunk) ? pm[(c0 + u) * GMAX + g] : 0.f;
-        O.x = fmaf(wv[u].x, f, O.x); O.y = fmaf(wv[u].y, f, O.y);
-        O.z = fmaf(wv[u].z, f, O.z); O.w = fmaf(wv[u].w, f, O.w);
+        const bool ok = c0 + u < nchunk;
+        const float4* src = reinterpret_cast<const float4*>(oall + (int64_t)(c0 + u) * GH);
+        w0[u] = ok ? __ldcg(src + ib / 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+        w1[u] = (ok && has1) ? __ldcg(src + i1 / 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const bool ok = c0 + u < nchunk;
+        const float f0 = ok ? pm[(c0 + u) * GMAX + ib / HD] : 0.f;
+        const float f1 = (ok && has1) ? pm[(c0 + u) * GMAX + i1 / HD] : 0.f;
+        O0.x = fmaf(w0[u].x, f0, O0.x); O0.y = fmaf(w0[u].y, f0, O0.y);
+        O0.z = fmaf(w0[u].z, f0, O0.z); O0.w = fmaf(w0[u].w, f0, O0.w);
+        O1.x = fmaf(w1[u].x, f1, O1.x); O1.y = fmaf(w1[u].y, f1, O1.y);
+        O1.z = fmaf(w1[u].z, f1, O1.z); O1.w = fmaf(w1[u].w, f1, O1.w);
       }
     }
-    const float inv = hL[g];
-    const float4 c = make_float4(O.x / inv, O.y / inv, O.z / inv, O.w / inv);
-    *reinterpret_cast<float4*>(outh + i) = c;
-    *reinterpret_cast<float4*>(a.ctx + (int64_t)slot * a.H * HD + kh * GH + i) = c;
+    float* ctx = a.ctx + (int64_t)slot * a.H * HD + kh * GH;
+    {
+      const float L = hL[ib / HD];
+      const float4 c = make_float4(O0.x / L, O0.y / L, O0.z / L, O0.w / L);
+      *reinterpret_cast<float4*>(outh + ib) = c;
+      *reinterpret_cast<float4*>(ctx + ib) = c;
+    }
+    if (has1) {
+      const float L = hL[i1 / HD];
+      const float4 c = make_float4(O1.x / L, O1.y / L, O1.z / L, O1.w / L);
+      *reinterpret_cast<float4*>(outh + i1) = c;
+      *reinterpret_cast<float4*>(ctx + i1) = c;
+    }
   }
+  trace_mark(a, 6);
   if (threadIdx.x == 0 && nchunk > 1) a.counters[slot * a.kvh + kh] = 0;
   __syncthreads();
   if (a.st_out) {
@@ -414,8 +464,10 @@ __global__ void __launch_bounds__(NTH) attn_dec_mma_kernel(AttnDecArgs a) {
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
+  trace_mark(a, 0);
   pdl_trigger();
   pdl_wait();        // q / k_new / v_new come from the QKV GEMV just before
+  trace_mark(a, 1);
 
   // ---- 2. q (RoPE) -> bf16 hi/lo, [head][dim]; unused heads zero.  All loads
   // of the thread are issued before any arithmetic (one latency, not eight) ----
@@ -469,6 +521,7 @@ __global__ void __launch_bounds__(NTH) attn_dec_mma_kernel(AttnDecArgs a) {
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncthreads();
+  trace_mark(a, 2);
   if (appender) {
     const int r = a.t0 - chunk * CHUNK;
 #pragma unroll
@@ -495,6 +548,7 @@ __global__ void __launch_bounds__(NTH) attn_dec_mma_kernel(AttnDecArgs a) {
       mma_bf16_16816(sacc[mt], af[0], af[1], af[2], af[3], bl0, bl1);
     }
   }
+  trace_mark(a, 8);
   // ---- softmax per head over the warp's 32 positions ----
   // lane holds S[pos mt*16 + g8 (+8)][head 2*t4 + {0,1}]
   const float rs = sqrtf((float)HD);
@@ -544,6 +598,7 @@ __global__ void __launch_bounds__(NTH) attn_dec_mma_kernel(AttnDecArgs a) {
   }
   __syncwarp();
 
+  trace_mark(a, 9);
   // ---- O^T[HD x 8] = V^T . P ----
   const int jrow = (lane & 7) + ((lane >> 4) << 3);      // ldmatrix.trans source row (pos)
   const int dcol = ((lane >> 3) & 1) * 8;                // +8 dims for matrices 1 and 3
@@ -569,8 +624,11 @@ __global__ void __launch_bounds__(NTH) attn_dec_mma_kernel(AttnDecArgs a) {
       if (head < G) wo[(warp * G + head) * HD + dim] = oacc[j];
     }
   }
+  trace_mark(a, 10);
   __syncthreads();
+  trace_mark(a, 3);
   merge_tail<HD>(a, G, slot, kh, chunk, nchunk, T, wm, wl, wo, pmv, plv, &last_flag);
+  trace_mark(a, 7);
 }
 
 template <int HD>
@@ -586,8 +644,33 @@ void launch_mma(const AttnDecArgs& a, cudaStream_t st) {
                          (int)smem);
     set = smem;
   }
-  launch_pdl(attn_dec_mma_kernel<HD>, grid, dim3(NTH), smem, st, a);
+  static int trace_call = getenv("SP_ATTN_TRACE") ? atoi(getenv("SP_ATTN_TRACE")) : -1;
+  static int ncall = 0;
+  static unsigned long long* tbuf = nullptr;
+  AttnDecArgs b = a;
+  const bool tr = trace_call >= 0 && ncall++ == trace_call;
+  const size_t tn = (size_t)grid.x * grid.y * 12;
+  if (tr) {
+    cudaMalloc(&tbuf, tn * 8);
+    cudaMemsetAsync(tbuf, 0, tn * 8, st);
+    b.trace = tbuf;
+  }
+  launch_pdl(attn_dec_mma_kernel<HD>, grid, dim3(NTH), smem, st, b);
   count_launch();
+  if (tr) {
+    std::vector<unsigned long long> h(tn);
+    cudaMemcpyAsync(h.data(), tbuf, tn * 8, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    unsigned long long t0 = ~0ull;
+    for (size_t i = 0; i < tn; i += 12) if (h[i] && h[i] < t0) t0 = h[i];
+    for (size_t i = 0; i < tn; i += 12) {
+      fprintf(stderr, "cta %3zu:", i / 12);
+      for (int p = 0; p < 11; ++p)
+        fprintf(stderr, " %7.2f", h[i + p] ? (double)(h[i + p] - t0) / 1e3 : -1.0);
+      fprintf(stderr, "\n");
+    }
+    cudaFree(tbuf);
+  }
 }
 
 template <int HD, typename KT, int GT>

@@ -37,6 +37,9 @@ struct GemvArgs {
   const float* g_next;    // gains for st_out.amax (null -> 1)
   long long* ws;          // split-K int64 accumulators [R][N] (int8) / f32 partials (bf16)
   int* counters;          // split-K arrival counters per row group (zero at rest)
+  unsigned long long* trace;   // debug (SP_GEMV_TRACE): per-warp phase timestamps, or null
+  int pre_stages;         // ring stages prefetched before griddepcontrol.wait (set by the launcher)
+  int l2_prefetch;        // further units of the warp's slice prefetched into L2 before the wait
 };
 
 int64_t gemv3_ws_bytes(int64_t N, int Rmax);
@@ -62,9 +65,10 @@ struct AttnDecArgs {
   int max_pages;
   const float* rope_cos, *rope_sin, *alibi;
   float* ctx;                    // [width][H*hd]
-  float* part;                   // [width][kvh][max_pages][G][hd+2]
+  float* part;                   // O [width*kvh][max_pages][G][hd], then (max,sum) pairs
   int* counters;                 // [width*kvh] (zero at rest)
   RowStat* st_out;               // [H][width] partial stats of ctx (P = H)
+  unsigned long long* trace;     // debug (SP_ATTN_TRACE): per-CTA phase timestamps, or null
 };
 
 void launch_attn_decode_fused(const AttnDecArgs& a, cudaStream_t st);

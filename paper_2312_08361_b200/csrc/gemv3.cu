@@ -25,7 +25,10 @@
 // and g are applied while building the B fragments, rstd in the epilogue.
 // The last warp to finish a group writes the group's outputs (+ residual /
 // SwiGLU / GELU epilogue) and the same partial stats for the next consumer.
+#include <cstdio>
+#include <cstdlib>
 #include <type_traits>
+#include <vector>
 
 #include "common.cuh"
 #include "decode.cuh"
@@ -120,6 +123,20 @@ __device__ __forceinline__ uint32_t digits4(int q0, int q1, int q2, int q3, int 
   return __byte_perm(lo, hi, sel_hi);
 }
 
+// debug trace: per warp [start, after pdl_wait, after prologue, first stage, mainloop end, exit]
+__device__ __forceinline__ void gtrace(const GemvArgs& a, int ph) {
+  if (a.trace && (threadIdx.x & 31) == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    a.trace[((int64_t)blockIdx.x * NW + (threadIdx.x >> 5)) * 8 + ph] = t;
+    if (ph == 0) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+      a.trace[((int64_t)blockIdx.x * NW + (threadIdx.x >> 5)) * 8 + 6] = smid;
+    }
+  }
+}
+
 struct WarpSmem {
   float mu[RMAX], dscale[RMAX];
   double yscale[RMAX];
@@ -143,6 +160,7 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
   const int64_t u0 = gw * units / warps_total, u1 = (gw + 1) * units / warps_total;
   const int64_t KT = a.K / KTILE;
 
+  gtrace(a, 0);
   if (lane == 0) {
     for (int st = 0; st < STAGES; ++st) mbar_init(&ws_->bar[st], 1);
     mbar_fence_init();
@@ -154,7 +172,7 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
   uint64_t policy_x;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(policy_x));
   const int nunits = u1 > u0 ? (int)(u1 - u0) : 0;
-  const int npre = nunits < STAGES ? nunits : STAGES;
+  const int npre = nunits < a.pre_stages ? nunits : a.pre_stages;
   // ---- before the dependency: the weights of the first STAGES units (no
   // kernel writes weights), so their DRAM latency overlaps the previous
   // kernel's tail; each stage's barrier also expects its activation bytes ----
@@ -165,8 +183,18 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
       tma_load_1d(ring + i * STAGE_BYTES, wbase + ((u / KT) * KT + u % KT) * UNIT_BYTES,
                   UNIT_BYTES, &ws_->bar[i], policy);
     }
+  // ...and the next l2_prefetch units of the slice into L2 (one bulk prefetch;
+  // the slice is contiguous), so the start of the stream after the wait hits
+  // L2 while the previous kernel's tail leaves DRAM bandwidth unused
+  if (lane == 0 && nunits > npre && a.l2_prefetch > 0) {
+    const int np = (nunits - npre) < a.l2_prefetch ? (nunits - npre) : a.l2_prefetch;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(wbase + (u0 + npre) * UNIT_BYTES),
+                 "r"((uint32_t)np * UNIT_BYTES)
+                 : "memory");
+  }
   pdl_trigger();
   pdl_wait();
+  gtrace(a, 1);
   // ---- per-row parameters from the producer's partial stats ----
   // CTA-wide: 256 threads load the P_in x Rn partials with several loads in
   // flight each, then a fixed-order tree (warp shuffles, then warps in order)
@@ -193,6 +221,14 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
           S[r] += t[j].sum; Q[r] += t[j].sumsq; M[r] = fmaxf(M[r], t[j].amax);
         }
       }
+    }
+  if (lane == 0)
+    for (int i = 0; i < npre; ++i) {     // activation chunks of the prefetched units
+      // (issued right behind the stats loads, ahead of their reduction)
+      const int64_t kt = (u0 + i) % KT;
+      for (int r = 0; r < Rn; ++r)
+        tma_load_1d(ring + i * STAGE_BYTES + UNIT_BYTES + r * XSLOT,
+                    a.x + (int64_t)(r0 + r) * a.ldx + kt * KTILE, XB, &ws_->bar[i], policy_x);
     }
 #pragma unroll
     for (int r = 0; r < RMAX; ++r) {
@@ -228,6 +264,7 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
     }
     __syncthreads();
   }
+  gtrace(a, 2);
   if (u0 >= u1) return;
   if (lane < RMAX) {
     ws_->mu[lane] = prm_mu[lane];
@@ -274,14 +311,9 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
     if (++p_st == STAGES) p_st = 0;
     --p_left;
   };
+  if (lane == 0)                          // stages not prefetched before the dependency
+    for (int i = npre; i < STAGES && p_left > 0; ++i) issue_next();
   __syncwarp();
-  if (lane == 0)
-    for (int i = 0; i < npre; ++i) {     // activation chunks of the prefetched units
-      const int64_t kt = (u0 + i) % KT;
-      for (int r = 0; r < Rn; ++r)
-        tma_load_1d(ring + i * STAGE_BYTES + UNIT_BYTES + r * XSLOT,
-                    a.x + (int64_t)(r0 + r) * a.ldx + kt * KTILE, XB, &ws_->bar[i], policy_x);
-    }
 
   // ---- activation side: read from the stage (arrived with the weights) ----
   XVec xc[NT][2], gc[NT][2];
@@ -301,6 +333,7 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
 
   for (int i = 0; i < nunits; ++i) {
     mbar_wait(&ws_->bar[c_st], c_ph);
+    if (i == 0) gtrace(a, 3);
     const uint8_t* stage = ring + c_st * STAGE_BYTES;
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
@@ -373,6 +406,7 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
     const int nkt = c_kt + 1 - seg_kt0;
     const bool grp_end = (c_kt + 1 == KT) || (i + 1 == nunits);
     if (++c_kt == KT) { c_kt = 0; ++c_grp; seg_kt0 = 0; }
+    if (i + 1 == nunits) gtrace(a, 4);
     if (!grp_end) continue;
     // combine this segment's digit/hi-lo columns per (row, batch row) in registers
     unsigned long long* acc64 = reinterpret_cast<unsigned long long*>(a.ws);
@@ -429,34 +463,52 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
     if (!last) continue;
 
     // ---- epilogue for the group (128 channels x Rn rows), last warp only ----
-    const int nout = (a.epi == EPI_SWIGLU) ? 64 : 128;
+    // every load of the lane (4 accumulators, their scales, residuals, next
+    // gains) is issued before the first is used: one round trip, not four
+    const bool swiglu = (a.epi == EPI_SWIGLU);
+    const int nj = swiglu ? 2 : 4;         // outputs per lane (64 or 128 per group)
     for (int r = 0; r < Rn; ++r) {
       unsigned long long* accr = acc64 + (int64_t)(r0 + r) * a.N + grp * 128;
       const double ys = ws_->yscale[r];
+      const int64_t yrow = (int64_t)(r0 + r) * a.ldy;
+      long long D[4];
+      float wsc[4], rv[4], gn[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int row = lane + 32 * j;
+        D[j] = (long long)atomicExch(accr + row, 0ull);
+        wsc[j] = (WT == kI8) ? __ldg(a.wscale + grp * 128 + row) : 1.f;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int64_t col = swiglu ? grp * 64 + lane + 32 * j : grp * 128 + lane + 32 * j;
+        rv[j] = (j < nj && a.epi == EPI_RESID) ? a.res[yrow + col] : 0.f;
+        gn[j] = (j < nj && a.g_next) ? __ldg(a.g_next + col) : 1.f;
+      }
+      auto val_of = [&](int k) {
+        if (WT == kI8) return (float)((double)D[k] * ys * (double)wsc[k]);
+        return (float)((double)D[k] * ys);
+      };
       float S = 0.f, Q = 0.f, M = 0.f;
-      for (int o = lane; o < nout; o += 32) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (j >= nj) break;
         float val;
         int64_t col;
-        auto fetch = [&](int row) {
-          const long long D = (long long)atomicExch(accr + row, 0ull);
-          if (WT == kI8) return (float)((double)D * ys * (double)a.wscale[grp * 128 + row]);
-          return (float)((double)D * ys);
-        };
-        if (a.epi == EPI_SWIGLU) {
+        if (swiglu) {
           // group = [gate 64 rows | up 64 rows] of outputs grp*64 + o
-          const float gt = fetch(o), up = fetch(64 + o);
-          val = silu_f(gt) * up;
-          col = grp * 64 + o;
+          val = silu_f(val_of(j)) * val_of(j + 2);
+          col = grp * 64 + lane + 32 * j;
         } else {
-          col = grp * 128 + o;
-          val = fetch(o);
-          if (a.epi == EPI_RESID) val += a.res[(int64_t)(r0 + r) * a.ldy + col];
+          col = grp * 128 + lane + 32 * j;
+          val = val_of(j);
+          if (a.epi == EPI_RESID) val += rv[j];
           else if (a.epi == EPI_GELU) val = gelu_f(val);
         }
-        a.y[(int64_t)(r0 + r) * a.ldy + col] = val;
+        a.y[yrow + col] = val;
         S += val;
         Q = fmaf(val, val, Q);
-        M = fmaxf(M, fabsf(val * (a.g_next ? a.g_next[col] : 1.f)));
+        M = fmaxf(M, fabsf(val * gn[j]));
       }
       if (a.st_out) {
         S = warp_sum(S); Q = warp_sum(Q); M = warp_max(M);
@@ -465,6 +517,7 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
     }
     __syncwarp();
   }
+  gtrace(a, 5);
 }
 
 int g_num_sms = 0;
@@ -481,9 +534,40 @@ void launch_cfg(const GemvArgs& a, int r0, int rn, cudaStream_t st) {
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     set = true;
   }
-  launch_pdl(gemv3_kernel<WT, NT, NORMT, HASG>, dim3(grid), dim3(NW * 32), smem, st, a, r0, rn,
+  static int trace_call = getenv("SP_GEMV_TRACE") ? atoi(getenv("SP_GEMV_TRACE")) : -1;
+  static int ncall = 0;   // per instantiation
+  GemvArgs b = a;
+  static int pre = getenv("SP_GEMV_PRE") ? atoi(getenv("SP_GEMV_PRE")) : STAGES;
+  static int l2pf = getenv("SP_GEMV_L2PF") ? atoi(getenv("SP_GEMV_L2PF")) : 0;  // measured: hurts
+  b.pre_stages = pre;
+  b.l2_prefetch = l2pf;
+  const bool tr = trace_call >= 0 && ncall++ == trace_call;
+  const size_t tn = (size_t)grid * NW * 8;
+  unsigned long long* tbuf = nullptr;
+  if (tr) {
+    cudaMalloc(&tbuf, tn * 8);
+    cudaMemsetAsync(tbuf, 0, tn * 8, st);
+    b.trace = tbuf;
+  }
+  launch_pdl(gemv3_kernel<WT, NT, NORMT, HASG>, dim3(grid), dim3(NW * 32), smem, st, b, r0, rn,
              a.R, units, (int64_t)grid * NW);
   count_launch();
+  if (tr) {
+    std::vector<unsigned long long> h(tn);
+    cudaMemcpyAsync(h.data(), tbuf, tn * 8, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    unsigned long long t0 = ~0ull;
+    for (size_t i = 0; i < tn; i += 8) if (h[i] && h[i] < t0) t0 = h[i];
+    fprintf(stderr, "gemv N=%lld K=%lld\n", (long long)a.N, (long long)a.K);
+    for (size_t i = 0; i < tn; i += 8) {
+      fprintf(stderr, "w %4zu:", i / 8);
+      for (int p = 0; p < 6; ++p)
+        fprintf(stderr, " %7.2f", h[i + p] ? (double)(h[i + p] - t0) / 1e3 : -1.0);
+      fprintf(stderr, " %llu", h[i + 6]);
+      fprintf(stderr, "\n");
+    }
+    cudaFree(tbuf);
+  }
 }
 
 template <int WT, int NT>

@@ -1,9 +1,9 @@
 #!/bin/bash
 # A/B of the decode chain with and without programmatic dependent launch
 set -o pipefail
-python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+timeout -s KILL 300 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
 for pdl in 1 0 1; do
-  SP_PDL=$pdl python bench.py --blocks ${BLOCKS:-8} --prefill 2048 --steps 10 --no-cpu > gpurun_out/ab_$pdl.log 2>&1 || { tail -5 gpurun_out/ab_$pdl.log; exit 1; }
+  SP_PDL=$pdl timeout -s KILL 300 python bench.py --blocks ${BLOCKS:-8} --prefill 2048 --steps 10 --no-cpu > gpurun_out/ab_$pdl.log 2>&1 || { tail -5 gpurun_out/ab_$pdl.log; exit 1; }
   python - "$pdl" <<'PY'
 import json, sys
 d = json.loads(open(f"gpurun_out/ab_{sys.argv[1]}.log").read().strip().splitlines()[-1])

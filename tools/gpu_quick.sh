@@ -1,8 +1,8 @@
 #!/bin/bash
 # quick GPU iteration: tests, small bench, optional ncu of decode kernels
 set -o pipefail
-python -m pytest tests -m gpu -x -q 2>&1 | tail -3
-python bench.py --blocks 8 --prefill 256 --steps 5 --no-cpu > gpurun_out/plain.log 2>&1 || { tail -20 gpurun_out/plain.log; exit 1; }
+timeout -s KILL 300 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
+timeout -s KILL 300 python bench.py --blocks 8 --prefill 256 --steps 5 --no-cpu > gpurun_out/plain.log 2>&1 || { tail -20 gpurun_out/plain.log; exit 1; }
 python - <<'PY'
 import json
 d = json.loads(open("gpurun_out/plain.log").read().strip().splitlines()[-1])
