@@ -230,6 +230,8 @@ def run_b200(args) -> None:
     lib = _lib.load()
     if os.environ.get("SP_PDL") == "0":       # A/B switch: programmatic dependent launch off
         _lib.check(lib.sp_span_set_option(span.handle, 1, 0))
+    if os.environ.get("SP_TC_PAIR") == "0":   # A/B switch: single-CTA tcgen05 prefill GEMM
+        _lib.check(lib.sp_span_set_option(span.handle, 2, 0))
     d = cfg.hidden_dim
     stream = torch.cuda.current_stream(dev)
 
@@ -250,8 +252,14 @@ def run_b200(args) -> None:
     sessions = max(1, world)       # sessions in flight (one per pipeline stage)
 
     # ---- prefill (2048 tokens per session), timed on the device ----
-    caches = [eng.make_caches(start, end, 1) for _ in range(sessions)]
     x_pre = torch.randn(args.prefill, d, device=dev, generator=g)
+    # untimed warm-up prefill on a throw-away cache: first-call scratch
+    # allocations and kernel attribute setup stay out of the timed region
+    warm = eng.make_caches(start, end, 1)
+    eng.run_cached(start, end, warm, HiddenBlob.from_device(x_pre), 1, args.prefill, False)
+    torch.cuda.synchronize()
+    del warm
+    caches = [eng.make_caches(start, end, 1) for _ in range(sessions)]
     prof(True)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:

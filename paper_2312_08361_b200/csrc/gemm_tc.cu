@@ -10,7 +10,8 @@
 // * int8 weights are consumed as stored (no dequantisation pass): the MMA is
 //   tcgen05.mma.cta_group::1.kind::i8, M = 128 tokens x N = 128 channels x
 //   K = 32, both operands K-major SWIZZLE_NONE (LBO = 2048 B along K, SBO = 128 B
-//   per 8 rows).  One CTA owns a 128 x 256 output tile = 2 planes x 2 weight
+//   per 8 rows).  The CTA-pair kernel below (cta_group::2, M = 256, N = 256) is
+//   the default; this one is the reference it is checked against bit for bit.  One CTA owns a 128 x 256 output tile = 2 planes x 2 weight
 //   groups = 4 int32 accumulators = all 512 TMEM columns.
 // * Accumulation is exact (int32 per plane, int64 when the planes combine), so
 //   every output row is independent of M and of its tile position — the
@@ -18,6 +19,8 @@
 // * Warp roles: warp 0 = TMA producer (one lane), warp 1 = MMA issuer (one
 //   lane), warp 2 = TMEM allocator, warps 4..7 = epilogue (tcgen05.ld, scale,
 //   residual / GELU / SwiGLU, store).  3-stage smem ring of 64 KB stages.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.cuh"
 #include "prefill.cuh"
@@ -246,6 +249,218 @@ __global__ void __launch_bounds__(256, 1) gemm_i8_tc_kernel(TcGemmArgs a) {
                  : "memory");
 }
 
+// ---- CTA-pair variant (cta_group::2) ------------------------------------------
+// A cluster of two CTAs on one TPC computes a 256-token x 256-channel tile:
+// CTA r stages its own 128 tokens (both digit planes) and weight group ng0 + r;
+// the leader issues tcgen05.mma.cta_group::2 (M = 256, N = 256), which reads
+// A and B halves from both CTAs' shared memory and writes each CTA's TMEM
+// rows.  Per SM and K unit this moves 12 KB from L2 instead of 16 KB for the
+// same MMA work — the single-CTA kernel is bound by L2->SM throughput, not by
+// the tensor pipe.  The peer's stage arrivals are relayed to the leader with
+// a cluster-scope mbarrier arrive; MMA completion is multicast to both CTAs.
+constexpr int STAGES2 = 4;
+constexpr int A2_BYTES = 2 * KU * UNIT;   // two digit planes, 128 tokens
+constexpr int B2_BYTES = KU * UNIT;       // one 128-channel weight group
+constexpr int STAGE2 = A2_BYTES + B2_BYTES;
+constexpr uint32_t kIdescI8x2 = (2u << 4) | (1u << 7) | (1u << 10) | ((256u >> 3) << 17) |
+                                ((256u >> 4) << 24);
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" :::
+                   "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mma_i8_x2(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(kIdescI8x2), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit_x2(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+    gemm_i8_tc2_kernel(TcGemmArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ __align__(8) uint64_t full[STAGES2], peer_full[STAGES2], empty[STAGES2], tmem_full;
+  __shared__ uint32_t tmem_base;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int mt = blockIdx.x >> 1;            // 256-token tile of the pair (token tiles fastest)
+  const int ng0 = blockIdx.y * 2;            // the pair's two 128-channel weight groups
+  const int64_t KT = a.K >> 5;
+  const int KB = (int)(KT / KU);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES2; ++s) {
+      mbar_init(&full[s], 1); mbar_init(&peer_full[s], 1); mbar_init(&empty[s], 1);
+    }
+    mbar_init(&tmem_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(&tmem_base))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();      // both CTAs' barriers and TMEM exist before any cross-CTA use
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tbase = tmem_base;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer: this CTA's half of every stage ----------------
+    const uint8_t* pa0 = a.planes;
+    const uint8_t* pa1 = a.planes + a.plane_stride;
+    const uint8_t* wb = reinterpret_cast<const uint8_t*>(a.w);
+    const int64_t arow = (int64_t)mt * 2 + rank;         // this CTA's 128-token block
+    for (int kb = 0; kb < KB; ++kb) {
+      const int s = kb % STAGES2;
+      if (kb >= STAGES2) mbar_wait(&empty[s], ((kb / STAGES2) - 1) & 1);
+      uint8_t* st = smem + (size_t)s * STAGE2;
+      if (a.debug == 2) {
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[s])) : "memory");
+        continue;
+      }
+      mbar_expect_tx(&full[s], STAGE2);
+      const int64_t ua = (arow * KT + (int64_t)kb * KU) * UNIT;
+      tma_load_1d(st, pa0 + ua, KU * UNIT, &full[s]);
+      tma_load_1d(st + KU * UNIT, pa1 + ua, KU * UNIT, &full[s]);
+      const int64_t ub = ((int64_t)(ng0 + rank) * KT + (int64_t)kb * KU) * UNIT;
+      tma_load_1d(st + A2_BYTES, wb + ub, KU * UNIT, &full[s]);
+    }
+  } else if (warp == 3 && lane == 0 && rank == 1) {
+    // ---------------- relay (peer): stage landed here -> leader ----------------
+    const uint32_t pf = mapa_shared(smem_u32(&peer_full[0]), 0);
+    for (int kb = 0; kb < KB; ++kb) {
+      const int s = kb % STAGES2;
+      mbar_wait(&full[s], (kb / STAGES2) & 1);
+      mbar_arrive_remote(pf + (uint32_t)s * 8u);
+    }
+  } else if (warp == 1 && lane == 0 && rank == 0) {
+    // ---------------- MMA issuer (leader) ----------------
+    for (int kb = 0; kb < KB; ++kb) {
+      const int s = kb % STAGES2;
+      const uint32_t ph = (kb / STAGES2) & 1;
+      mbar_wait(&full[s], ph);
+      mbar_wait_cluster(&peer_full[s], ph);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint8_t* st = smem + (size_t)s * STAGE2;
+#pragma unroll
+      for (int u = 0; u < KU; ++u) {
+        if (a.debug == 1) break;
+        const uint64_t bd = umma_desc(st + A2_BYTES + u * UNIT, 2048, 128);
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+          const uint64_t ad = umma_desc(st + p * KU * UNIT + u * UNIT, 2048, 128);
+          mma_i8_x2(tbase + (uint32_t)(p * 256), ad, bd, (kb | u) ? 1u : 0u);
+        }
+      }
+      mma_commit_x2(&empty[s]);        // frees stage s in both CTAs when these MMAs finish
+    }
+    mma_commit_x2(&tmem_full);
+  }
+  {
+    // ---------------- epilogue: this CTA's 128 tokens x 256 channels ----------------
+    // all 8 warps, once their pipeline roles are done: warp w reads TMEM lane
+    // quarter w % 4 (the lanes a warp may access) and weight group w / 4
+    __syncwarp();                      // role lanes rejoin: tcgen05.ld is warp-aligned
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const int64_t m = ((int64_t)mt * 2 + rank) * 128 + row;
+    mbar_wait(&tmem_full, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const bool valid = m < a.M;
+    const double ys = valid ? ldexp(1.0, a.exps[m] - 14) : 0.0;
+    const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
+    {
+      const int j = warp >> 2;
+      const int64_t n0 = (int64_t)(ng0 + j) * 128;
+      if (a.epi == EPI_SWIGLU) {
+        for (int c0 = 0; c0 < 64; c0 += 32) {
+          int g0[32], g1[32], u0[32], u1[32];
+          tmem_ld32(tbase + lane_addr + (uint32_t)(0 * 256 + j * 128 + c0), g0);
+          tmem_ld32(tbase + lane_addr + (uint32_t)(1 * 256 + j * 128 + c0), g1);
+          tmem_ld32(tbase + lane_addr + (uint32_t)(0 * 256 + j * 128 + 64 + c0), u0);
+          tmem_ld32(tbase + lane_addr + (uint32_t)(1 * 256 + j * 128 + 64 + c0), u1);
+          if (!valid) continue;
+          float* out = a.y + m * a.ldy + (ng0 + j) * 64 + c0;
+#pragma unroll
+          for (int c = 0; c < 32; c += 4) {
+            float o4[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int cc = c + e;
+              const double gd = (double)((long long)g0[cc] * 256 + g1[cc]) * ys *
+                                (double)a.wscale[n0 + c0 + cc];
+              const double ud = (double)((long long)u0[cc] * 256 + u1[cc]) * ys *
+                                (double)a.wscale[n0 + 64 + c0 + cc];
+              o4[e] = silu_f((float)gd) * (float)ud;
+            }
+            *reinterpret_cast<float4*>(out + c) = make_float4(o4[0], o4[1], o4[2], o4[3]);
+          }
+        }
+      } else {
+        for (int c0 = 0; c0 < 128; c0 += 32) {
+          int v0[32], v1[32];
+          tmem_ld32(tbase + lane_addr + (uint32_t)(0 * 256 + j * 128 + c0), v0);
+          tmem_ld32(tbase + lane_addr + (uint32_t)(1 * 256 + j * 128 + c0), v1);
+          if (!valid) continue;
+          float* out = a.y + m * a.ldy + n0 + c0;
+          const float* res = a.res ? a.res + m * a.ldy + n0 + c0 : nullptr;
+#pragma unroll
+          for (int c = 0; c < 32; c += 4) {
+            float o4[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int cc = c + e;
+              float v = (float)((double)((long long)v0[cc] * 256 + v1[cc]) * ys *
+                                (double)a.wscale[n0 + c0 + cc]);
+              if (a.epi == EPI_RESID) v += res[cc];
+              else if (a.epi == EPI_GELU) v = gelu_f(v);
+              o4[e] = v;
+            }
+            *reinterpret_cast<float4*>(out + c) = make_float4(o4[0], o4[1], o4[2], o4[3]);
+          }
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();      // the leader's MMAs wrote the peer's TMEM: free it only now
+  if (warp == 2)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tbase)
+                 : "memory");
+}
+
 // ---- activation digit planes: one CTA per (padded) row -----------------------
 // norm: 0 none, 1 RMSNorm, 2 LayerNorm (gains g, bias b; eps 1e-5)
 __global__ void __launch_bounds__(256) digitize_kernel(const float* __restrict__ x, int64_t ldx,
@@ -315,16 +530,34 @@ __global__ void __launch_bounds__(256) digitize_kernel(const float* __restrict__
 
 }  // namespace
 
+bool g_tc_pair = true;
+
 void launch_digitize(const float* x, int64_t ldx, int64_t M, int64_t K, int norm, const float* g,
                      const float* b, uint8_t* planes, int64_t plane_stride, int* exps,
                      cudaStream_t st) {
-  const int64_t Mp = (M + 127) / 128 * 128;
+  const int64_t Mp = tc_rows(M);
   digitize_kernel<<<(unsigned)Mp, 256, 0, st>>>(x, ldx, M, K, norm, g, b, planes, plane_stride,
                                                 exps);
   count_launch();
 }
 
 void launch_gemm_i8_tc(const TcGemmArgs& a, cudaStream_t st) {
+  if (g_tc_pair) {
+    static bool set2 = false;
+    const size_t smem2 = (size_t)STAGES2 * STAGE2;
+    if (!set2) {
+      cudaFuncSetAttribute(gemm_i8_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem2);
+      set2 = true;
+    }
+    dim3 grid2((unsigned)(2 * ((a.M + 255) / 256)), (unsigned)(a.N / 256));
+    static int dbg = getenv("SP_TC_DEBUG") ? atoi(getenv("SP_TC_DEBUG")) : 0;
+    TcGemmArgs b = a;
+    b.debug = dbg;
+    gemm_i8_tc2_kernel<<<grid2, 256, smem2, st>>>(b);
+    count_launch();
+    return;
+  }
   static bool set = false;
   const size_t smem = (size_t)STAGES * STAGE;
   if (!set) {
@@ -337,6 +570,6 @@ void launch_gemm_i8_tc(const TcGemmArgs& a, cudaStream_t st) {
   count_launch();
 }
 
-int64_t tc_plane_bytes(int64_t M, int64_t K) { return (M + 127) / 128 * 128 * K; }
+int64_t tc_plane_bytes(int64_t M, int64_t K) { return tc_rows(M) * K; }
 
 }  // namespace sp

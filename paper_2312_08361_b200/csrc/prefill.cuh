@@ -9,7 +9,7 @@ struct TcGemmArgs {
   const void* w;            // int8 weights, core-matrix layout (common.cuh)
   const float* wscale;      // per output channel
   int64_t N, K;
-  const uint8_t* planes;    // activation digit planes d0 | d1 (core-matrix layout, M padded to 128)
+  const uint8_t* planes;    // activation digit planes d0 | d1 (core-matrix layout, M padded to 256)
   int64_t plane_stride;     // bytes between d0 and d1
   const int* exps;          // per-row exponents e_m (|x| < 2^e)
   int64_t M;
@@ -17,9 +17,13 @@ struct TcGemmArgs {
   int64_t ldy;
   const float* res;         // EPI_RESID (may alias y)
   int epi;
+  int debug;                // (tools) 1: skip the MMAs, 2: skip the TMA loads — timing only
 };
 
+// token rows of the digit planes: padded to the 256-token CTA-pair tile
+inline int64_t tc_rows(int64_t M) { return (M + 255) / 256 * 256; }
 int64_t tc_plane_bytes(int64_t M, int64_t K);
+extern bool g_tc_pair;    // sp_span_set_option(.., 2, ..): CTA-pair tcgen05 GEMM (default on)
 void launch_digitize(const float* x, int64_t ldx, int64_t M, int64_t K, int norm, const float* g,
                      const float* b, uint8_t* planes, int64_t plane_stride, int* exps,
                      cudaStream_t st);

@@ -191,7 +191,7 @@ int ensure_decode(sp_span* s, int64_t rows) {
 int ensure_tc(sp_span* s, int64_t rows) {
   if (rows <= s->tc_cap_rows) return SP_OK;
   cudaFree(s->planes); cudaFree(s->exps);
-  const int64_t Mp = (rows + 127) / 128 * 128;
+  const int64_t Mp = tc_rows(rows);       // the CTA-pair GEMM tiles 256 tokens
   const int64_t K = std::max<int64_t>(s->d, s->F);
   SP_CUDA_TRY(cudaMalloc(&s->planes, 2 * Mp * K));
   SP_CUDA_TRY(cudaMalloc(&s->exps, Mp * sizeof(int)));
@@ -433,7 +433,7 @@ int run_span_prefill_tc(sp_span* s, sp_kv* kv, int b0, int b1, float* y, float* 
   const int fam = s->cfg.family;
   const int norm = fam == kLlama ? 1 : 2;
   const int64_t d = s->d, F = s->F;
-  const int64_t Mp = (R + 127) / 128 * 128;
+  const int64_t Mp = tc_rows(R);
   const double kv_elt = s->cfg.kv_dtype == kKVBF16 ? 2.0 : 4.0;
   AttnArgs at{};
   at.family = fam; at.kv_dtype = s->cfg.kv_dtype;
@@ -885,6 +885,7 @@ int sp_span_set_option(sp_span* s, int32_t option, int32_t value) {
   if (!s) SP_FAIL(SP_ERR_ARG, "null span");
   if (option == 0) s->use_tc_prefill = value != 0;
   else if (option == 1) g_pdl = value != 0;
+  else if (option == 2) g_tc_pair = value != 0;
   else SP_FAIL(SP_ERR_ARG, "unknown option");
   return SP_OK;
 }

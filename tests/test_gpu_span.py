@@ -238,3 +238,25 @@ def test_tc_prefill_matches_simt_and_is_batch_invariant():
     runner = om.SpanRunner(cfg, 0, cfg.n_blocks, width=3)
     want = runner.step(x.reshape(3, 150, -1)).reshape(-1, cfg.hidden_dim)
     assert np.abs(a - want).max() <= 2e-2 * np.abs(want).max()
+
+
+@pytest.mark.gpu
+def test_tc_pair_gemm_equals_single_cta():
+    """The CTA-pair tcgen05 GEMM (cta_group::2, M = 256) and the single-CTA one
+    accumulate the same exact integers: outputs must be bit-identical, also for
+    token counts that are not a multiple of the 256-token pair tile."""
+    cfg = SMALL["llama_int8"]
+    from paper_2312_08361_b200 import _lib
+    from paper_2312_08361_b200.engine import DeviceSpan, B200ServerEngine
+    span = DeviceSpan(cfg, 0, cfg.n_blocks)
+    eng = B200ServerEngine(cfg, span=span)
+    rng = np.random.default_rng(5)
+    for batch, tokens in ((1, 300), (2, 129), (1, 512)):
+        x = rng.standard_normal((batch * tokens, cfg.hidden_dim)).astype(np.float32)
+        _lib.check(span.lib.sp_span_set_option(span.handle, 2, 1))
+        pair = eng.forward(0, cfg.n_blocks, _blob(x), batch, tokens, 10**9, None).array()
+        _lib.check(span.lib.sp_span_set_option(span.handle, 2, 0))
+        single = eng.forward(0, cfg.n_blocks, _blob(x), batch, tokens, 10**9, None).array()
+        _lib.check(span.lib.sp_span_set_option(span.handle, 2, 1))
+        assert np.array_equal(pair, single), (batch, tokens, float(np.abs(pair - single).max()),
+                                              float(np.abs(single).max()))
