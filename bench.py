@@ -163,6 +163,12 @@ def run_reference(args) -> None:
     if rank != 0:
         return
     from paper_2312_08361_b200.config import llama2_70b
+    # torchrun exports OMP_NUM_THREADS=1; the reference arm uses every host core
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(limits=os.cpu_count())
+    except Exception:
+        pass
     cfg = llama2_70b()
     context = args.prefill
     # each step = one oracle block decode at `context` (bounded sample); the
