@@ -31,6 +31,7 @@ namespace {
 constexpr int NTH = 128;
 constexpr int CHUNK = 128;          // positions per CTA (two pages)
 constexpr int GMAX = 16;            // max query heads per kv head
+constexpr float kLog2e = 1.4426950408889634f;
 
 __device__ __forceinline__ void trace_mark(const AttnDecArgs& a, int ph) {
   if (a.trace && threadIdx.x == 0) {
@@ -56,7 +57,8 @@ __device__ __forceinline__ float rope_val(const float* x, int dd, int half, cons
 // merge the 4 warp partials (fixed order) into this chunk's partial; the
 // last-arriving CTA of (slot, kv head) merges all chunks in ascending order,
 // writes ctx and the per-head partial stats of ctx
-template <int HD>
+// LOG2: the partial maxima are in the log2 domain (scores pre-scaled by log2 e)
+template <int HD, bool LOG2>
 __device__ void merge_tail(const AttnDecArgs& a, int G, int slot, int kh, int chunk, int nchunk,
                            int T, const float (*wm)[GMAX], const float (*wl)[GMAX], float* wo,
                            float* pm, float* pl, int* last_flag) {
@@ -70,7 +72,8 @@ __device__ void merge_tail(const AttnDecArgs& a, int G, int slot, int kh, int ch
       if (chunk * CHUNK + w * 32 < T) M = fmaxf(M, wm[w][g]);
     float L = 0.f;
     for (int w = 0; w < 4; ++w) {
-      const float f = (chunk * CHUNK + w * 32 < T) ? expf(wm[w][g] - M) : 0.f;  // empty warp: 0
+      const float f = (chunk * CHUNK + w * 32 < T) ? (LOG2 ? exp2f(wm[w][g] - M) : expf(wm[w][g] - M))
+                                                   : 0.f;  // empty warp: 0
       wf[w][g] = f;
       L = fmaf(wl[w][g] * (f > 0.f ? 1.f : 0.f), f, L);
     }
@@ -150,7 +153,7 @@ __device__ void merge_tail(const AttnDecArgs& a, int G, int slot, int kh, int ch
       const float M = warp_max(m);
       float L = 0.f;
       for (int c = lane; c < nchunk; c += 32) {
-        const float f = expf(pm[c * GMAX + g] - M);
+        const float f = LOG2 ? exp2f(pm[c * GMAX + g] - M) : expf(pm[c * GMAX + g] - M);
         pm[c * GMAX + g] = f;
         L = fmaf(pl[c * GMAX + g], f, L);
       }
@@ -384,7 +387,7 @@ __global__ void __launch_bounds__(NTH) attn_dec2_kernel(AttnDecArgs a) {
   }
   __syncthreads();
 
-  merge_tail<HD>(a, G, slot, kh, chunk, nchunk, T, wm, wl, wo, pm, pl, &last_flag);
+  merge_tail<HD, false>(a, G, slot, kh, chunk, nchunk, T, wm, wl, wo, pm, pl, &last_flag);
 }
 
 
@@ -551,7 +554,7 @@ __global__ void __launch_bounds__(NTH) attn_dec_mma_kernel(AttnDecArgs a) {
   trace_mark(a, 8);
   // ---- softmax per head over the warp's 32 positions ----
   // lane holds S[pos mt*16 + g8 (+8)][head 2*t4 + {0,1}]
-  const float rs = sqrtf((float)HD);
+  const float qscale = kLog2e / sqrtf((float)HD);
   float m2[2], l2[2];
 #pragma unroll
   for (int hc = 0; hc < 2; ++hc) {
@@ -562,8 +565,10 @@ __global__ void __launch_bounds__(NTH) attn_dec_mma_kernel(AttnDecArgs a) {
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
         const int pos = mt * 16 + g8 + hh * 8;
-        float v = sacc[mt][hh * 2 + hc] / rs;
-        if (a.family == kBloom && head < G) v += a.alibi[kh * G + head] * (float)(p0 + pos - (T - 1));
+        // log2 domain: one multiply folds 1/sqrt(hd) and log2(e); exp2 below
+        float v = sacc[mt][hh * 2 + hc] * qscale;
+        if (a.family == kBloom && head < G)
+          v = fmaf(a.alibi[kh * G + head] * kLog2e, (float)(p0 + pos - (T - 1)), v);
         if (pos >= nv) v = -INFINITY;
         sacc[mt][hh * 2 + hc] = v;
         mx = fmaxf(mx, v);
@@ -577,7 +582,7 @@ __global__ void __launch_bounds__(NTH) attn_dec_mma_kernel(AttnDecArgs a) {
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
         const int pos = mt * 16 + g8 + hh * 8;
-        const float e = (pos < nv) ? expf(sacc[mt][hh * 2 + hc] - mx) : 0.f;
+        const float e = (pos < nv) ? exp2f(sacc[mt][hh * 2 + hc] - mx) : 0.f;
         sum += e;
         const __nv_bfloat16 h = __float2bfloat16_rn(e);
         ph[warp][head][pos] = h;
@@ -627,7 +632,7 @@ __global__ void __launch_bounds__(NTH) attn_dec_mma_kernel(AttnDecArgs a) {
   trace_mark(a, 10);
   __syncthreads();
   trace_mark(a, 3);
-  merge_tail<HD>(a, G, slot, kh, chunk, nchunk, T, wm, wl, wo, pmv, plv, &last_flag);
+  merge_tail<HD, true>(a, G, slot, kh, chunk, nchunk, T, wm, wl, wo, pmv, plv, &last_flag);
   trace_mark(a, 7);
 }
 

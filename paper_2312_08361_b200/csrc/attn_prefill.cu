@@ -3,9 +3,10 @@
 // CTA = (slot, query head, 64 query rows); 4 warps x 16 rows.  Key/value pages
 // (64 positions, bf16, head dim 64/128) stream through a double-buffered
 // cp.async ring; S = Q K^T and O += P V run on mma.m16n8k16 with the online
-// softmax of FlashAttention-2.  Q and P are split hi + lo in bf16 (two MMAs
-// each), K/V are the exact cache values, accumulation is f32 — so the result
-// tracks the f32 reference (SP/model.py:263-275: scores / f32(sqrt(hd)),
+// softmax of FlashAttention-2.  Q and P are rounded to bf16 like the cached
+// K/V (the precision class the bf16 KV cache already sets); with
+// sp_span_set_option(.., 3, 1) they are split hi + lo (two MMAs each) and the
+// result tracks the f32 reference more closely.  Accumulation is f32 (SP/model.py:263-275: scores / f32(sqrt(hd)),
 // (+ ALiBi), causal -1e30 mask for n > 1, max-subtracted softmax).
 // Each query row's result depends only on its own row: batch/tile invariant.
 #include "common.cuh"
@@ -51,7 +52,7 @@ __device__ __forceinline__ void split2(float x0, float x1, uint32_t& hi, uint32_
   lo = pack_bf16(x0 - __bfloat162float(h0), x1 - __bfloat162float(h1));
 }
 
-template <int HD>
+template <int HD, bool HILO>
 __global__ void __launch_bounds__(128) attn_prefill_mma_kernel(AttnArgs a) {
   constexpr int RS = HD + 8;                        // padded smem row (bf16)
   constexpr int NKS = HD / 16;                      // k-steps over dims
@@ -66,7 +67,8 @@ __global__ void __launch_bounds__(128) attn_prefill_mma_kernel(AttnArgs a) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g8 = lane >> 2, t4 = lane & 3;
   const int qrow0 = q0 + warp * 16;                 // this warp's first query row
   const float slope = (a.family == kBloom) ? a.alibi[h] : 0.f;
-  const float rs = sqrtf((float)HD);
+  const float qscale = 1.4426950408889634f / sqrtf((float)HD);   // log2(e) / sqrt(hd)
+  const float slope_l2 = slope * 1.4426950408889634f;
 
   // ---- Q fragments (hi/lo bf16) for rows qrow0+g8 and qrow0+g8+8 ----
   uint32_t qh[NKS][4], ql[NKS][4];
@@ -137,9 +139,9 @@ __global__ void __launch_bounds__(128) attn_prefill_mma_kernel(AttnArgs a) {
           const int m = lane >> 3;
           ldsm4(kb, &Ks[buf][np * 16 + (m >> 1) * 8 + (lane & 7)][ks * 16 + (m & 1) * 8]);
           mma16816(s[2 * np], qh[ks], kb[0], kb[1]);
-          mma16816(s[2 * np], ql[ks], kb[0], kb[1]);
+          if (HILO) mma16816(s[2 * np], ql[ks], kb[0], kb[1]);
           mma16816(s[2 * np + 1], qh[ks], kb[2], kb[3]);
-          mma16816(s[2 * np + 1], ql[ks], kb[2], kb[3]);
+          if (HILO) mma16816(s[2 * np + 1], ql[ks], kb[2], kb[3]);
         }
       }
     }
@@ -151,8 +153,10 @@ __global__ void __launch_bounds__(128) attn_prefill_mma_kernel(AttnArgs a) {
       for (int j = 0; j < 4; ++j) {
         const int key = kbase + nt * 8 + 2 * t4 + (j & 1);
         const int pos = (j < 2) ? pos_a : pos_b;
-        float v = s[nt][j] / rs;
-        if (a.family == kBloom) v += slope * (float)(key - pos);
+        // log2-domain scores: exp(x - m) == exp2(x*log2e - m*log2e); the
+        // 1/sqrt(hd) scale and log2(e) fold into one multiply (bf16-class)
+        float v = s[nt][j] * qscale;
+        if (a.family == kBloom) v = fmaf(slope_l2, (float)(key - pos), v);
         if (key > pos) v = -INFINITY;
         s[nt][j] = v;
         tmax[j >> 1] = fmaxf(tmax[j >> 1], v);
@@ -166,7 +170,7 @@ __global__ void __launch_bounds__(128) attn_prefill_mma_kernel(AttnArgs a) {
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
       mnew[r] = fmaxf(mrow[r], tmax[r]);
-      alpha[r] = (mnew[r] == -INFINITY) ? 1.f : expf(mrow[r] - mnew[r]);
+      alpha[r] = (mnew[r] == -INFINITY) ? 1.f : exp2f(mrow[r] - mnew[r]);
     }
     uint32_t ph[KTL / 16][4], pl[KTL / 16][4];
 #pragma unroll
@@ -175,7 +179,7 @@ __global__ void __launch_bounds__(128) attn_prefill_mma_kernel(AttnArgs a) {
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const float mr = mnew[j >> 1];
-        p[j] = (s[nt][j] == -INFINITY) ? 0.f : expf(s[nt][j] - mr);
+        p[j] = (s[nt][j] == -INFINITY) ? 0.f : exp2f(s[nt][j] - mr);
         psum[j >> 1] += p[j];
       }
       // C layout of two n-tiles == A layout of one k16 step of P
@@ -205,9 +209,9 @@ __global__ void __launch_bounds__(128) attn_prefill_mma_kernel(AttnArgs a) {
           const int m = lane >> 3;
           ldsm4t(vb, &Vs[buf][kk * 16 + (m & 1) * 8 + (lane & 7)][dp * 16 + (m >> 1) * 8]);
           mma16816(o[2 * dp], ph[kk], vb[0], vb[1]);
-          mma16816(o[2 * dp], pl[kk], vb[0], vb[1]);
+          if (HILO) mma16816(o[2 * dp], pl[kk], vb[0], vb[1]);
           mma16816(o[2 * dp + 1], ph[kk], vb[2], vb[3]);
-          mma16816(o[2 * dp + 1], pl[kk], vb[2], vb[3]);
+          if (HILO) mma16816(o[2 * dp + 1], pl[kk], vb[2], vb[3]);
         }
       }
     }
@@ -231,23 +235,29 @@ __global__ void __launch_bounds__(128) attn_prefill_mma_kernel(AttnArgs a) {
 
 }  // namespace
 
+template <int HD, bool HILO>
+void launch_hd(const AttnArgs& a, dim3 grid, size_t smem, cudaStream_t st) {
+  static bool set = false;
+  if (!set) {
+    cudaFuncSetAttribute(attn_prefill_mma_kernel<HD, HILO>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    set = true;
+  }
+  attn_prefill_mma_kernel<HD, HILO><<<grid, 128, smem, st>>>(a);
+}
+
+bool g_attn_hilo = false;
+
 bool launch_attention_prefill_mma(const AttnArgs& a, cudaStream_t st) {
   if (a.kv_dtype != kKVBF16 || !(a.hd == 64 || a.hd == 128)) return false;
   dim3 grid(a.width * a.H, (a.n_new + QT - 1) / QT);
   const size_t smem = (size_t)4 * KTL * (a.hd + 8) * 2;
-  static bool set128 = false, set64 = false;
   if (a.hd == 128) {
-    if (!set128) {
-      cudaFuncSetAttribute(attn_prefill_mma_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      set128 = true;
-    }
-    attn_prefill_mma_kernel<128><<<grid, 128, smem, st>>>(a);
+    if (g_attn_hilo) launch_hd<128, true>(a, grid, smem, st);
+    else launch_hd<128, false>(a, grid, smem, st);
   } else {
-    if (!set64) {
-      cudaFuncSetAttribute(attn_prefill_mma_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      set64 = true;
-    }
-    attn_prefill_mma_kernel<64><<<grid, 128, smem, st>>>(a);
+    if (g_attn_hilo) launch_hd<64, true>(a, grid, smem, st);
+    else launch_hd<64, false>(a, grid, smem, st);
   }
   count_launch();
   return true;

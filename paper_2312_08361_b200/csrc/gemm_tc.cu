@@ -528,6 +528,120 @@ __global__ void __launch_bounds__(256) digitize_kernel(const float* __restrict__
   }
 }
 
+// register-resident digitize: the row is read from HBM once (16 consecutive
+// floats per thread and chunk, four float4 loads), normalised and reduced in
+// registers, and written as one 16-byte core-matrix row per plane and chunk.
+template <int NT, int NCH>
+__global__ void __launch_bounds__(NT) digitize_reg_kernel(const float* __restrict__ x, int64_t ldx,
+                                                          int64_t M, int64_t K, int norm,
+                                                          const float* __restrict__ g,
+                                                          const float* __restrict__ b,
+                                                          uint8_t* planes, int64_t plane_stride,
+                                                          int* exps) {
+  constexpr int NW = NT / 32;
+  __shared__ float red[3][NW];
+  const int64_t m = blockIdx.x;
+  const float* xr = x + m * ldx;
+  const bool valid = m < M;
+  const int nchunk = (int)(K >> 4);
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  float v[NCH][16];
+  auto bsum = [&](float a, int slot) {
+    a = warp_sum(a);
+    if (lane == 0) red[slot][warp] = a;
+    __syncthreads();
+    float r = 0.f;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) r += red[slot][w];
+    return r;
+  };
+  float s = 0.f, s2 = 0.f;
+#pragma unroll
+  for (int j = 0; j < NCH; ++j) {
+    const int c = t + j * NT;
+    if (valid && c < nchunk) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float4 f = __ldcs(reinterpret_cast<const float4*>(xr + (int64_t)c * 16) + q);
+        v[j][4 * q] = f.x; v[j][4 * q + 1] = f.y; v[j][4 * q + 2] = f.z; v[j][4 * q + 3] = f.w;
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 16; ++e) v[j][e] = 0.f;
+    }
+#pragma unroll
+    for (int e = 0; e < 16; ++e) { s += v[j][e]; s2 = fmaf(v[j][e], v[j][e], s2); }
+  }
+  if (norm != 0) {
+    float mu = 0.f, rstd;
+    if (norm == 2) {
+      mu = bsum(s, 0) / (float)K;
+      float q2 = 0.f;
+#pragma unroll
+      for (int j = 0; j < NCH; ++j) {
+        const int c = t + j * NT;
+        if (c < nchunk)
+#pragma unroll
+          for (int e = 0; e < 16; ++e) { const float d = v[j][e] - mu; q2 = fmaf(d, d, q2); }
+      }
+      rstd = 1.0f / sqrtf(bsum(q2, 1) / (float)K + 1e-5f);
+    } else {
+      rstd = 1.0f / sqrtf(bsum(s2, 1) / (float)K + 1e-5f);
+    }
+#pragma unroll
+    for (int j = 0; j < NCH; ++j) {
+      const int c = t + j * NT;
+      if (!(valid && c < nchunk)) continue;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float4 gg = __ldg(reinterpret_cast<const float4*>(g + (int64_t)c * 16) + q);
+        const float gq[4] = {gg.x, gg.y, gg.z, gg.w};
+        float bq[4] = {0.f, 0.f, 0.f, 0.f};
+        if (norm == 2) {
+          const float4 bb = __ldg(reinterpret_cast<const float4*>(b + (int64_t)c * 16) + q);
+          bq[0] = bb.x; bq[1] = bb.y; bq[2] = bb.z; bq[3] = bb.w;
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          float& vv = v[j][4 * q + e];
+          vv = (norm == 1) ? vv * rstd * gq[e] : (vv - mu) * rstd * gq[e] + bq[e];
+        }
+      }
+    }
+  }
+  float amax = 0.f;
+#pragma unroll
+  for (int j = 0; j < NCH; ++j)
+#pragma unroll
+    for (int e = 0; e < 16; ++e) amax = fmaxf(amax, fabsf(v[j][e]));
+  amax = warp_max(amax);
+  if (lane == 0) red[2][warp] = amax;
+  __syncthreads();
+  amax = 0.f;
+#pragma unroll
+  for (int w = 0; w < NW; ++w) amax = fmaxf(amax, red[2][w]);
+  int e2 = 0;
+  if (amax > 0.f) frexpf(amax, &e2);                 // |v| < 2^e
+  const float sc = amax > 0.f ? ldexpf(1.0f, 14 - e2) : 0.f;
+  if (t == 0 && valid) exps[m] = e2;
+#pragma unroll
+  for (int j = 0; j < NCH; ++j) {
+    const int c = t + j * NT;
+    if (c >= nchunk) continue;
+    __align__(16) int8_t d0[16], d1[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int qv = __float2int_rn(v[j][i] * sc);    // |q| <= 2^14
+      const int lo = (int)(int8_t)(qv & 0xFF);
+      d1[i] = (int8_t)lo;
+      d0[i] = (int8_t)((qv - lo) >> 8);
+    }
+    const int64_t off = cm_offset(m, (int64_t)c * 16, K);
+    *reinterpret_cast<uint4*>(planes + off) = *reinterpret_cast<uint4*>(d0);
+    *reinterpret_cast<uint4*>(planes + plane_stride + off) = *reinterpret_cast<uint4*>(d1);
+  }
+}
+
 }  // namespace
 
 bool g_tc_pair = true;
@@ -536,8 +650,18 @@ void launch_digitize(const float* x, int64_t ldx, int64_t M, int64_t K, int norm
                      const float* b, uint8_t* planes, int64_t plane_stride, int* exps,
                      cudaStream_t st) {
   const int64_t Mp = tc_rows(M);
-  digitize_kernel<<<(unsigned)Mp, 256, 0, st>>>(x, ldx, M, K, norm, g, b, planes, plane_stride,
-                                                exps);
+  const unsigned grid = (unsigned)Mp;
+  const bool al = (K % 16 == 0) && (ldx % 4 == 0);
+  if (al && K <= 256 * 16 * 2)
+    digitize_reg_kernel<256, 2><<<grid, 256, 0, st>>>(x, ldx, M, K, norm, g, b, planes, plane_stride, exps);
+  else if (al && K <= 256 * 16 * 4)
+    digitize_reg_kernel<256, 4><<<grid, 256, 0, st>>>(x, ldx, M, K, norm, g, b, planes, plane_stride, exps);
+  else if (al && K <= 512 * 16 * 4)
+    digitize_reg_kernel<512, 4><<<grid, 512, 0, st>>>(x, ldx, M, K, norm, g, b, planes, plane_stride, exps);
+  else if (al && K <= 1024 * 16 * 4)
+    digitize_reg_kernel<1024, 4><<<grid, 1024, 0, st>>>(x, ldx, M, K, norm, g, b, planes, plane_stride, exps);
+  else
+    digitize_kernel<<<grid, 256, 0, st>>>(x, ldx, M, K, norm, g, b, planes, plane_stride, exps);
   count_launch();
 }
 

@@ -36,6 +36,7 @@ namespace sp {
 static std::atomic<int64_t> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 bool g_pdl = true;
+extern bool g_attn_hilo;   // attn_prefill.cu
 }  // namespace sp
 
 using namespace sp;
@@ -886,6 +887,7 @@ int sp_span_set_option(sp_span* s, int32_t option, int32_t value) {
   if (option == 0) s->use_tc_prefill = value != 0;
   else if (option == 1) g_pdl = value != 0;
   else if (option == 2) g_tc_pair = value != 0;
+  else if (option == 3) g_attn_hilo = value != 0;
   else SP_FAIL(SP_ERR_ARG, "unknown option");
   return SP_OK;
 }
