@@ -389,6 +389,15 @@ def run_b200(args) -> None:
                              f"70B-shape block at context {args.prefill}, median of 3, scaled "
                              f"to {n_blocks} blocks"}
         peak = peaks["hbm_gbs"]
+        # DRAM traffic per GEMV launch (dram__bytes_read.sum + dram__bytes_write.sum)
+        # from the committed ncu --set full capture of one block's 4 GEMVs
+        traffic, traffic_src = None, None
+        try:
+            tj = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                             "profiles", "gemv_traffic.json")))
+            traffic, traffic_src = tj["dram_bytes_per_launch"], tj["source"]
+        except Exception:
+            pass
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
@@ -404,7 +413,8 @@ def run_b200(args) -> None:
                        "span_per_gpu": [start, end], "prefill_tokens": args.prefill,
                        "l2": "inputs larger than L2 (68.5 GB weights)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None,
+                         "frac": achieved / peak, "traffic": traffic,
+                         "traffic_src": traffic_src,
                          "kernel": "gemv3_kernel<int8> (decode QKV/O/gate-up/down GEMVs, "
                                    "norm folded in)",
                          "peak_src": peaks["_src"], "launches": gemv_launches,
