@@ -467,6 +467,22 @@ __global__ void __launch_bounds__(NTH) attn_dec_mma_kernel(AttnDecArgs a) {
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
+  // L2 prefetch of the next kernel's weights: this CTA's share, in 64 KB
+  // bulk prefetches (cp.async.bulk.prefetch.L2) issued by one thread
+  if (a.l2_prefetch && threadIdx.x == 32) {
+    const int64_t nct = (int64_t)gridDim.x * gridDim.y;
+    const int64_t cta = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
+    const int64_t per = ((a.l2_prefetch_bytes + nct - 1) / nct + 15) / 16 * 16;
+    const int64_t b0 = cta * per;
+    const int64_t b1 = b0 + per < a.l2_prefetch_bytes ? b0 + per : a.l2_prefetch_bytes;
+    const char* base = reinterpret_cast<const char*>(a.l2_prefetch);
+    for (int64_t o = b0; o < b1; o += 65536) {
+      const int64_t n = b1 - o < 65536 ? b1 - o : 65536;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + o),
+                   "r"((uint32_t)n)
+                   : "memory");
+    }
+  }
   trace_mark(a, 0);
   pdl_trigger();
   pdl_wait();        // q / k_new / v_new come from the QKV GEMV just before

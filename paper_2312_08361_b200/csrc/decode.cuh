@@ -69,6 +69,8 @@ struct AttnDecArgs {
   int* counters;                 // [width*kvh] (zero at rest)
   RowStat* st_out;               // [H][width] partial stats of ctx (P = H)
   unsigned long long* trace;     // debug (SP_ATTN_TRACE): per-CTA phase timestamps, or null
+  const void* l2_prefetch;       // next kernel's weights to pull into L2 (or null)
+  int64_t l2_prefetch_bytes;
 };
 
 void launch_attn_decode_fused(const AttnDecArgs& a, cudaStream_t st);

@@ -22,7 +22,7 @@ from . import _lib
 class SpanPipeline:
     def __init__(self, engine, start: int, end: int, caches: list, rank: int, world: int, d: int,
                  device: torch.device, seed: int = 7):
-        self.eng, self.lib = engine, engine.lib
+        self.eng, self.lib = engine, getattr(engine, "lib", None)
         self.start, self.end = start, end
         self.caches = caches
         self.rank, self.world, self.d = rank, world, d
@@ -42,12 +42,16 @@ class SpanPipeline:
         if world == 1:
             self.y.copy_(self.init_rows[0])
 
-    def _forward(self, session: int, x_ptr: int, codes_ptr: int, scales_ptr: int,
-                 quantize_out: bool) -> None:
+    def _forward(self, session: int, x, coded_input: bool, quantize_out: bool) -> None:
+        """One span pass of `session` (1 row): input `x` (f32 rows) or, when
+        `coded_input`, the received int8 codes + scales; writes `self.y` and,
+        when `quantize_out`, `self.out_codes` / `self.out_scales`."""
         st = torch.cuda.current_stream(self.dev).cuda_stream
         _lib.check(self.lib.sp_span_forward(
-            self.eng.span.handle, self.caches[session].handle, self.start, self.end, x_ptr,
-            codes_ptr, scales_ptr, self.y.data_ptr(),
+            self.eng.span.handle, self.caches[session].handle, self.start, self.end,
+            0 if coded_input else x.data_ptr(),
+            self.in_codes.data_ptr() if coded_input else 0,
+            self.in_scales.data_ptr() if coded_input else 0, self.y.data_ptr(),
             self.out_codes.data_ptr() if quantize_out else 0,
             self.out_scales.data_ptr() if quantize_out else 0, 1, 1, st))
 
@@ -55,7 +59,7 @@ class SpanPipeline:
         k, r, N = self.k, self.rank, self.world
         if N == 1:
             # autoregressive feedback: the span output is the next input (in place)
-            self._forward(0, self.y.data_ptr(), 0, 0, False)
+            self._forward(0, self.y, False, False)
             self.k += 1
             return
         import torch.distributed as dist
@@ -65,10 +69,9 @@ class SpanPipeline:
         if active:
             if r == 0:
                 x = self.init_rows[s] if k < N else self.ring_in
-                self._forward(s, x.data_ptr(), 0, 0, True)
+                self._forward(s, x, False, True)
             else:
-                self._forward(s, 0, self.in_codes.data_ptr(), self.in_scales.data_ptr(),
-                              not last)
+                self._forward(s, None, True, not last)
         ops = []
         if active:
             if last:
