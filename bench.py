@@ -292,7 +292,9 @@ def run_b200(args) -> None:
     # ---- decode: W warm-up + K timed steps ----
     from paper_2312_08361_b200.pipeline import SpanPipeline
     pipe = SpanPipeline(eng, start, end, caches, rank, world, d, dev)
-    for _ in range(args.warmup):
+    # W warm-up ticks, plus N more for N > 1: the last-to-first ring edge is
+    # first used at tick N - 1, and NCCL sets up a p2p connection on first use
+    for _ in range(args.warmup + (world if world > 1 else 0)):
         pipe.step()
     torch.cuda.synchronize()
     if world > 1:
