@@ -19,7 +19,9 @@
 // * Warp roles: warp 0 = TMA producer (one lane), warp 1 = MMA issuer (one
 //   lane), warp 2 = TMEM allocator, warps 4..7 = epilogue (tcgen05.ld, scale,
 //   residual / GELU / SwiGLU, store).  3-stage smem ring of 64 KB stages.
+#include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -305,6 +307,14 @@ __device__ __forceinline__ void mma_commit_x2(uint64_t* bar) {
       : "memory");
 }
 
+__device__ __forceinline__ void tc_trace(const TcGemmArgs& a, int ph) {
+  if (a.trace) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    a.trace[((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * 4 + ph] = t;
+  }
+}
+
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     gemm_i8_tc2_kernel(TcGemmArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -312,6 +322,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   __shared__ uint32_t tmem_base;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) tc_trace(a, 0);
   const uint32_t rank = cluster_rank();
   const int mt = blockIdx.x >> 1;            // 256-token tile of the pair (token tiles fastest)
   const int ng0 = blockIdx.y * 2;            // the pair's two 128-channel weight groups
@@ -398,6 +409,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     const int64_t m = ((int64_t)mt * 2 + rank) * 128 + row;
     mbar_wait(&tmem_full, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (threadIdx.x == 128) tc_trace(a, 1);
     const bool valid = m < a.M;
     const double ys = valid ? ldexp(1.0, a.exps[m] - 14) : 0.0;
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
@@ -454,8 +466,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       }
     }
   }
+  if (threadIdx.x == 128) tc_trace(a, 2);
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   cluster_sync_all();      // the leader's MMAs wrote the peer's TMEM: free it only now
+  if (threadIdx.x == 0) tc_trace(a, 3);
   if (warp == 2)
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tbase)
                  : "memory");
@@ -676,9 +690,29 @@ void launch_gemm_i8_tc(const TcGemmArgs& a, cudaStream_t st) {
     }
     dim3 grid2((unsigned)(2 * ((a.M + 255) / 256)), (unsigned)(a.N / 256));
     static int dbg = getenv("SP_TC_DEBUG") ? atoi(getenv("SP_TC_DEBUG")) : 0;
+    static int trc = getenv("SP_TC_TRACE") ? atoi(getenv("SP_TC_TRACE")) : -1;
+    static int ncall = 0;
     TcGemmArgs b = a;
     b.debug = dbg;
+    const bool tr = trc >= 0 && ncall++ == trc;
+    const size_t tn = (size_t)grid2.x * grid2.y * 4;
+    if (tr) {
+      cudaMalloc(&b.trace, tn * 8);
+      cudaMemsetAsync(b.trace, 0, tn * 8, st);
+    }
     gemm_i8_tc2_kernel<<<grid2, 256, smem2, st>>>(b);
+    if (tr) {
+      std::vector<unsigned long long> h(tn);
+      cudaMemcpyAsync(h.data(), b.trace, tn * 8, cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      unsigned long long t0 = ~0ull;
+      for (size_t i = 0; i < tn; i += 4) if (h[i] && h[i] < t0) t0 = h[i];
+      fprintf(stderr, "tcgemm M=%lld N=%lld K=%lld\n", (long long)a.M, (long long)a.N, (long long)a.K);
+      for (size_t i = 0; i < tn; i += 4)
+        fprintf(stderr, "c %zu %.2f %.2f %.2f %.2f\n", i / 4, (h[i] - t0) / 1e3, (h[i + 1] - t0) / 1e3,
+                (h[i + 2] - t0) / 1e3, (h[i + 3] - t0) / 1e3);
+      cudaFree(b.trace);
+    }
     count_launch();
     return;
   }

@@ -18,6 +18,7 @@ struct TcGemmArgs {
   const float* res;         // EPI_RESID (may alias y)
   int epi;
   int debug;                // (tools) 1: skip the MMAs, 2: skip the TMA loads — timing only
+  unsigned long long* trace;  // (tools, SP_TC_TRACE) per-CTA globaltimer phases, or null
 };
 
 // token rows of the digit planes: padded to the 256-token CTA-pair tile
