@@ -107,10 +107,87 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, int* v) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+__device__ __forceinline__ void tmem_ld32_nw(uint32_t taddr, int* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+        "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+        "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
 __device__ __forceinline__ float gelu_f(float x) {
   return 0.5f * x * (1.0f + tanhf(0.7978845608028654f * (x + 0.044715f * x * x * x)));
 }
-__device__ __forceinline__ float silu_f(float x) { return x / (1.0f + expf(-x)); }
+
+// Epilogue of one 128-channel weight group for this thread's token row m.
+// TMEM columns: plane p, group j, channel c -> p * 256 + j * 128 + c (both
+// kernels).  D = D0 * 256 + D1 is exact (int64); y = f32(D) * 2^(e-14) * wscale.
+// All TMEM loads of a chunk are issued before one wait.
+__device__ __forceinline__ void epilogue_group(const TcGemmArgs& a, uint32_t tb, int j, int ng0,
+                                               int64_t m, bool valid, float ys) {
+  const int64_t n0 = (int64_t)(ng0 + j) * 128;
+  const float* wsc = a.wscale + n0;
+  if (a.epi == EPI_SWIGLU) {
+    // group = [gate 64 | up 64] of outputs (ng0 + j) * 64 + c
+    for (int c0 = 0; c0 < 64; c0 += 32) {
+      int g0[32], g1[32], u0[32], u1[32];
+      tmem_ld32_nw(tb + (uint32_t)(0 * 256 + j * 128 + c0), g0);
+      tmem_ld32_nw(tb + (uint32_t)(1 * 256 + j * 128 + c0), g1);
+      tmem_ld32_nw(tb + (uint32_t)(0 * 256 + j * 128 + 64 + c0), u0);
+      tmem_ld32_nw(tb + (uint32_t)(1 * 256 + j * 128 + 64 + c0), u1);
+      tmem_wait_ld();
+      if (!valid) continue;
+      float* out = a.y + m * a.ldy + (ng0 + j) * 64 + c0;
+#pragma unroll
+      for (int c = 0; c < 32; c += 4) {
+        float o4[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int cc = c + e;
+          const float gd = (float)((long long)g0[cc] * 256 + g1[cc]) * ys * __ldg(wsc + c0 + cc);
+          const float ud = (float)((long long)u0[cc] * 256 + u1[cc]) * ys * __ldg(wsc + 64 + c0 + cc);
+          o4[e] = __fdividef(gd, 1.0f + __expf(-gd)) * ud;
+        }
+        *reinterpret_cast<float4*>(out + c) = make_float4(o4[0], o4[1], o4[2], o4[3]);
+      }
+    }
+  } else {
+    for (int c0 = 0; c0 < 128; c0 += 32) {
+      int v0[32], v1[32];
+      tmem_ld32_nw(tb + (uint32_t)(0 * 256 + j * 128 + c0), v0);
+      tmem_ld32_nw(tb + (uint32_t)(1 * 256 + j * 128 + c0), v1);
+      tmem_wait_ld();
+      if (!valid) continue;
+      float* out = a.y + m * a.ldy + n0 + c0;
+      const float* res = a.res ? a.res + m * a.ldy + n0 + c0 : nullptr;
+#pragma unroll
+      for (int c = 0; c < 32; c += 4) {
+        float r4[4] = {0.f, 0.f, 0.f, 0.f};
+        if (a.epi == EPI_RESID) {
+          const float4 rr = *reinterpret_cast<const float4*>(res + c);
+          r4[0] = rr.x; r4[1] = rr.y; r4[2] = rr.z; r4[3] = rr.w;
+        }
+        float o4[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int cc = c + e;
+          float v = (float)((long long)v0[cc] * 256 + v1[cc]) * ys * __ldg(wsc + c0 + cc);
+          if (a.epi == EPI_RESID) v += r4[e];
+          else if (a.epi == EPI_GELU) v = gelu_f(v);
+          o4[e] = v;
+        }
+        *reinterpret_cast<float4*>(out + c) = make_float4(o4[0], o4[1], o4[2], o4[3]);
+      }
+    }
+  }
+}
 
 __global__ void __launch_bounds__(256, 1) gemm_i8_tc_kernel(TcGemmArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -189,60 +266,9 @@ __global__ void __launch_bounds__(256, 1) gemm_i8_tc_kernel(TcGemmArgs a) {
     mbar_wait(&tmem_full, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const bool valid = m < a.M;
-    const double ys = valid ? ldexp(1.0, a.exps[m] - 14) : 0.0;
+    const float ys = valid ? ldexpf(1.0f, a.exps[m] - 14) : 0.f;
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
-    for (int j = 0; j < NGRP; ++j) {
-      const int64_t n0 = (int64_t)(ng0 + j) * 128;
-      if (a.epi == EPI_SWIGLU) {
-        // group = [gate 64 | up 64] of outputs (ng0+j)*64 + c
-        for (int c0 = 0; c0 < 64; c0 += 32) {
-          int g0[32], g1[32], u0[32], u1[32];
-          tmem_ld32(tbase + lane_addr + (uint32_t)((0 * NGRP + j) * 128 + c0), g0);
-          tmem_ld32(tbase + lane_addr + (uint32_t)((1 * NGRP + j) * 128 + c0), g1);
-          tmem_ld32(tbase + lane_addr + (uint32_t)((0 * NGRP + j) * 128 + 64 + c0), u0);
-          tmem_ld32(tbase + lane_addr + (uint32_t)((1 * NGRP + j) * 128 + 64 + c0), u1);
-          if (!valid) continue;
-          float* out = a.y + m * a.ldy + (ng0 + j) * 64 + c0;
-#pragma unroll
-          for (int c = 0; c < 32; c += 4) {
-            float o4[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const int cc = c + e;
-              const double gd = (double)((long long)g0[cc] * 256 + g1[cc]) * ys *
-                                (double)a.wscale[n0 + c0 + cc];
-              const double ud = (double)((long long)u0[cc] * 256 + u1[cc]) * ys *
-                                (double)a.wscale[n0 + 64 + c0 + cc];
-              o4[e] = silu_f((float)gd) * (float)ud;
-            }
-            *reinterpret_cast<float4*>(out + c) = make_float4(o4[0], o4[1], o4[2], o4[3]);
-          }
-        }
-      } else {
-        for (int c0 = 0; c0 < 128; c0 += 32) {
-          int v0[32], v1[32];
-          tmem_ld32(tbase + lane_addr + (uint32_t)((0 * NGRP + j) * 128 + c0), v0);
-          tmem_ld32(tbase + lane_addr + (uint32_t)((1 * NGRP + j) * 128 + c0), v1);
-          if (!valid) continue;
-          float* out = a.y + m * a.ldy + n0 + c0;
-          const float* res = a.res ? a.res + m * a.ldy + n0 + c0 : nullptr;
-#pragma unroll
-          for (int c = 0; c < 32; c += 4) {
-            float o4[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const int cc = c + e;
-              float v = (float)((double)((long long)v0[cc] * 256 + v1[cc]) * ys *
-                                (double)a.wscale[n0 + c0 + cc]);
-              if (a.epi == EPI_RESID) v += res[cc];
-              else if (a.epi == EPI_GELU) v = gelu_f(v);
-              o4[e] = v;
-            }
-            *reinterpret_cast<float4*>(out + c) = make_float4(o4[0], o4[1], o4[2], o4[3]);
-          }
-        }
-      }
-    }
+    for (int j = 0; j < NGRP; ++j) epilogue_group(a, tbase + lane_addr, j, ng0, m, valid, ys);
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -260,10 +286,7 @@ __global__ void __launch_bounds__(256, 1) gemm_i8_tc_kernel(TcGemmArgs a) {
 // same MMA work — the single-CTA kernel is bound by L2->SM throughput, not by
 // the tensor pipe.  The peer's stage arrivals are relayed to the leader with
 // a cluster-scope mbarrier arrive; MMA completion is multicast to both CTAs.
-constexpr int STAGES2 = 4;
-constexpr int A2_BYTES = 2 * KU * UNIT;   // two digit planes, 128 tokens
-constexpr int B2_BYTES = KU * UNIT;       // one 128-channel weight group
-constexpr int STAGE2 = A2_BYTES + B2_BYTES;
+// (KUP K units per stage, ST stages; both configurations keep 192 KB in flight)
 constexpr uint32_t kIdescI8x2 = (2u << 4) | (1u << 7) | (1u << 10) | ((256u >> 3) << 17) |
                                 ((256u >> 4) << 24);
 
@@ -315,8 +338,11 @@ __device__ __forceinline__ void tc_trace(const TcGemmArgs& a, int ph) {
   }
 }
 
+template <int KUP, int STAGES2>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     gemm_i8_tc2_kernel(TcGemmArgs a) {
+  constexpr int A2_BYTES = 2 * KUP * UNIT;   // two digit planes, 128 tokens
+  constexpr int STAGE2 = A2_BYTES + KUP * UNIT;   // + one 128-channel weight group
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[STAGES2], peer_full[STAGES2], empty[STAGES2], tmem_full;
   __shared__ uint32_t tmem_base;
@@ -327,7 +353,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   const int mt = blockIdx.x >> 1;            // 256-token tile of the pair (token tiles fastest)
   const int ng0 = blockIdx.y * 2;            // the pair's two 128-channel weight groups
   const int64_t KT = a.K >> 5;
-  const int KB = (int)(KT / KU);
+  const int KB = (int)(KT / KUP);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES2; ++s) {
@@ -362,11 +388,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         continue;
       }
       mbar_expect_tx(&full[s], STAGE2);
-      const int64_t ua = (arow * KT + (int64_t)kb * KU) * UNIT;
-      tma_load_1d(st, pa0 + ua, KU * UNIT, &full[s]);
-      tma_load_1d(st + KU * UNIT, pa1 + ua, KU * UNIT, &full[s]);
-      const int64_t ub = ((int64_t)(ng0 + rank) * KT + (int64_t)kb * KU) * UNIT;
-      tma_load_1d(st + A2_BYTES, wb + ub, KU * UNIT, &full[s]);
+      const int64_t ua = (arow * KT + (int64_t)kb * KUP) * UNIT;
+      tma_load_1d(st, pa0 + ua, KUP * UNIT, &full[s]);
+      tma_load_1d(st + KUP * UNIT, pa1 + ua, KUP * UNIT, &full[s]);
+      const int64_t ub = ((int64_t)(ng0 + rank) * KT + (int64_t)kb * KUP) * UNIT;
+      tma_load_1d(st + A2_BYTES, wb + ub, KUP * UNIT, &full[s]);
     }
   } else if (warp == 3 && lane == 0 && rank == 1) {
     // ---------------- relay (peer): stage landed here -> leader ----------------
@@ -386,12 +412,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint8_t* st = smem + (size_t)s * STAGE2;
 #pragma unroll
-      for (int u = 0; u < KU; ++u) {
+      for (int u = 0; u < KUP; ++u) {
         if (a.debug == 1) break;
         const uint64_t bd = umma_desc(st + A2_BYTES + u * UNIT, 2048, 128);
 #pragma unroll
         for (int p = 0; p < 2; ++p) {
-          const uint64_t ad = umma_desc(st + p * KU * UNIT + u * UNIT, 2048, 128);
+          const uint64_t ad = umma_desc(st + p * KUP * UNIT + u * UNIT, 2048, 128);
           mma_i8_x2(tbase + (uint32_t)(p * 256), ad, bd, (kb | u) ? 1u : 0u);
         }
       }
@@ -411,60 +437,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     if (threadIdx.x == 128) tc_trace(a, 1);
     const bool valid = m < a.M;
-    const double ys = valid ? ldexp(1.0, a.exps[m] - 14) : 0.0;
+    const float ys = valid ? ldexpf(1.0f, a.exps[m] - 14) : 0.f;
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
-    {
-      const int j = warp >> 2;
-      const int64_t n0 = (int64_t)(ng0 + j) * 128;
-      if (a.epi == EPI_SWIGLU) {
-        for (int c0 = 0; c0 < 64; c0 += 32) {
-          int g0[32], g1[32], u0[32], u1[32];
-          tmem_ld32(tbase + lane_addr + (uint32_t)(0 * 256 + j * 128 + c0), g0);
-          tmem_ld32(tbase + lane_addr + (uint32_t)(1 * 256 + j * 128 + c0), g1);
-          tmem_ld32(tbase + lane_addr + (uint32_t)(0 * 256 + j * 128 + 64 + c0), u0);
-          tmem_ld32(tbase + lane_addr + (uint32_t)(1 * 256 + j * 128 + 64 + c0), u1);
-          if (!valid) continue;
-          float* out = a.y + m * a.ldy + (ng0 + j) * 64 + c0;
-#pragma unroll
-          for (int c = 0; c < 32; c += 4) {
-            float o4[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const int cc = c + e;
-              const double gd = (double)((long long)g0[cc] * 256 + g1[cc]) * ys *
-                                (double)a.wscale[n0 + c0 + cc];
-              const double ud = (double)((long long)u0[cc] * 256 + u1[cc]) * ys *
-                                (double)a.wscale[n0 + 64 + c0 + cc];
-              o4[e] = silu_f((float)gd) * (float)ud;
-            }
-            *reinterpret_cast<float4*>(out + c) = make_float4(o4[0], o4[1], o4[2], o4[3]);
-          }
-        }
-      } else {
-        for (int c0 = 0; c0 < 128; c0 += 32) {
-          int v0[32], v1[32];
-          tmem_ld32(tbase + lane_addr + (uint32_t)(0 * 256 + j * 128 + c0), v0);
-          tmem_ld32(tbase + lane_addr + (uint32_t)(1 * 256 + j * 128 + c0), v1);
-          if (!valid) continue;
-          float* out = a.y + m * a.ldy + n0 + c0;
-          const float* res = a.res ? a.res + m * a.ldy + n0 + c0 : nullptr;
-#pragma unroll
-          for (int c = 0; c < 32; c += 4) {
-            float o4[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const int cc = c + e;
-              float v = (float)((double)((long long)v0[cc] * 256 + v1[cc]) * ys *
-                                (double)a.wscale[n0 + c0 + cc]);
-              if (a.epi == EPI_RESID) v += res[cc];
-              else if (a.epi == EPI_GELU) v = gelu_f(v);
-              o4[e] = v;
-            }
-            *reinterpret_cast<float4*>(out + c) = make_float4(o4[0], o4[1], o4[2], o4[3]);
-          }
-        }
-      }
-    }
+    epilogue_group(a, tbase + lane_addr, warp >> 2, ng0, m, valid, ys);
   }
   if (threadIdx.x == 128) tc_trace(a, 2);
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -679,41 +654,48 @@ void launch_digitize(const float* x, int64_t ldx, int64_t M, int64_t K, int norm
   count_launch();
 }
 
+template <int KUP, int ST>
+void launch_pair(const TcGemmArgs& a, cudaStream_t st) {
+  static bool set2 = false;
+  const size_t smem2 = (size_t)ST * 3 * KUP * UNIT;
+  if (!set2) {
+    cudaFuncSetAttribute(gemm_i8_tc2_kernel<KUP, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem2);
+    set2 = true;
+  }
+  dim3 grid2((unsigned)(2 * ((a.M + 255) / 256)), (unsigned)(a.N / 256));
+  static int dbg = getenv("SP_TC_DEBUG") ? atoi(getenv("SP_TC_DEBUG")) : 0;
+  static int trc = getenv("SP_TC_TRACE") ? atoi(getenv("SP_TC_TRACE")) : -1;
+  static int ncall = 0;
+  TcGemmArgs b = a;
+  b.debug = dbg;
+  const bool tr = trc >= 0 && ncall++ == trc;
+  const size_t tn = (size_t)grid2.x * grid2.y * 4;
+  if (tr) {
+    cudaMalloc(&b.trace, tn * 8);
+    cudaMemsetAsync(b.trace, 0, tn * 8, st);
+  }
+  gemm_i8_tc2_kernel<KUP, ST><<<grid2, 256, smem2, st>>>(b);
+  count_launch();
+  if (tr) {
+    std::vector<unsigned long long> h(tn);
+    cudaMemcpyAsync(h.data(), b.trace, tn * 8, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    unsigned long long t0 = ~0ull;
+    for (size_t i = 0; i < tn; i += 4) if (h[i] && h[i] < t0) t0 = h[i];
+    fprintf(stderr, "tcgemm M=%lld N=%lld K=%lld\n", (long long)a.M, (long long)a.N, (long long)a.K);
+    for (size_t i = 0; i < tn; i += 4)
+      fprintf(stderr, "c %zu %.2f %.2f %.2f %.2f\n", i / 4, (h[i] - t0) / 1e3, (h[i + 1] - t0) / 1e3,
+              (h[i + 2] - t0) / 1e3, (h[i + 3] - t0) / 1e3);
+    cudaFree(b.trace);
+  }
+}
+
 void launch_gemm_i8_tc(const TcGemmArgs& a, cudaStream_t st) {
   if (g_tc_pair) {
-    static bool set2 = false;
-    const size_t smem2 = (size_t)STAGES2 * STAGE2;
-    if (!set2) {
-      cudaFuncSetAttribute(gemm_i8_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)smem2);
-      set2 = true;
-    }
-    dim3 grid2((unsigned)(2 * ((a.M + 255) / 256)), (unsigned)(a.N / 256));
-    static int dbg = getenv("SP_TC_DEBUG") ? atoi(getenv("SP_TC_DEBUG")) : 0;
-    static int trc = getenv("SP_TC_TRACE") ? atoi(getenv("SP_TC_TRACE")) : -1;
-    static int ncall = 0;
-    TcGemmArgs b = a;
-    b.debug = dbg;
-    const bool tr = trc >= 0 && ncall++ == trc;
-    const size_t tn = (size_t)grid2.x * grid2.y * 4;
-    if (tr) {
-      cudaMalloc(&b.trace, tn * 8);
-      cudaMemsetAsync(b.trace, 0, tn * 8, st);
-    }
-    gemm_i8_tc2_kernel<<<grid2, 256, smem2, st>>>(b);
-    if (tr) {
-      std::vector<unsigned long long> h(tn);
-      cudaMemcpyAsync(h.data(), b.trace, tn * 8, cudaMemcpyDeviceToHost, st);
-      cudaStreamSynchronize(st);
-      unsigned long long t0 = ~0ull;
-      for (size_t i = 0; i < tn; i += 4) if (h[i] && h[i] < t0) t0 = h[i];
-      fprintf(stderr, "tcgemm M=%lld N=%lld K=%lld\n", (long long)a.M, (long long)a.N, (long long)a.K);
-      for (size_t i = 0; i < tn; i += 4)
-        fprintf(stderr, "c %zu %.2f %.2f %.2f %.2f\n", i / 4, (h[i] - t0) / 1e3, (h[i + 1] - t0) / 1e3,
-                (h[i + 2] - t0) / 1e3, (h[i + 3] - t0) / 1e3);
-      cudaFree(b.trace);
-    }
-    count_launch();
+    static int cfg = getenv("SP_TC_CFG") ? atoi(getenv("SP_TC_CFG")) : 0;
+    if (cfg == 1) launch_pair<2, 8>(a, st);
+    else launch_pair<4, 4>(a, st);
     return;
   }
   static bool set = false;
