@@ -87,3 +87,38 @@ def test_dropin_inside_reference_block_server():
     finally:
         swarmpipe.swarm.RealServerEngine = orig
         swarmpipe.server.RealServerEngine = orig
+
+
+@pytest.mark.skipif(_reference_importable() is None, reason="reference package not installed")
+def test_dropin_beam_search_matches_reference_oracle():
+    """§8f item 2, T/test_beam.py:21-44 with the GPU engine inside the reference's
+    own swarm: k = 4 beams (reorder = page-table permutation with copy-on-write
+    tails) give the local beam oracle's hypotheses and scores, also through a
+    crashed server, and k = 1 degenerates to greedy."""
+    sys.path.insert(0, _reference_importable())
+    import swarmpipe.server
+    import swarmpipe.swarm
+    from swarmpipe.model import ModelConfig, reference_beam, reference_generate
+    from paper_2312_08361_b200.engine import B200ServerEngine
+    orig = swarmpipe.swarm.RealServerEngine
+    swarmpipe.swarm.RealServerEngine = B200ServerEngine
+    swarmpipe.server.RealServerEngine = B200ServerEngine
+    try:
+        cfg = ModelConfig(seed=1)
+        swarm = swarmpipe.swarm.build_sim_swarm(cfg, seed=0)
+        assert swarm.client().beam_generate([4, 2], 16, k=1).tokens == \
+            reference_generate(cfg, [4, 2], 16)
+        want = reference_beam(cfg, [4, 2], 24, k=4)
+        res = swarmpipe.swarm.build_sim_swarm(cfg, seed=0).client().beam_generate([4, 2], 24, k=4)
+        assert [h for h, _ in res.beams] == [h for h, _ in want]
+        for (_, sa), (_, sb) in zip(res.beams, want):
+            assert sa == pytest.approx(sb, abs=1e-4)
+        want = reference_beam(cfg, [4, 2], 16, k=4)
+        swarm = swarmpipe.swarm.build_sim_swarm(
+            cfg, seed=0, server_overrides={"s2a": {"crash_after_messages": 10}})
+        res = swarm.client().beam_generate([4, 2], 16, k=4)
+        assert [h for h, _ in res.beams] == [h for h, _ in want]
+        assert res.counters.recoveries >= 1
+    finally:
+        swarmpipe.swarm.RealServerEngine = orig
+        swarmpipe.server.RealServerEngine = orig
