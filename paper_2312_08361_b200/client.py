@@ -314,21 +314,24 @@ class SwarmClient:
 
 
 def build_swarm(engine_factory, config, n_stages: int, replicas: int,
-                crash: dict | None = None, transport=None):
+                crash: dict | None = None, transport=None, engine_for=None):
     """A one-process swarm like `build_sim_swarm` (SP/swarm.py:52-94):
     ``replicas`` servers per stage_intervals span, ids s{stage}{a,b,..}, with
-    optional crash injection {server_id: crash_after_messages}."""
+    optional crash injection {server_id: crash_after_messages}.
+    ``engine_for(server_id, stage, replica)`` gives a server its own engine
+    (e.g. one GPU per server); otherwise all share ``engine_factory()``."""
     from .balancer import stage_intervals
     from .server import BlockServer, ServerCfg
     from .transport import LocalTransport
     net = transport or LocalTransport()
     servers, routes = {}, []
-    eng = engine_factory()
+    eng = engine_factory() if engine_for is None else None
     for si, (a, b) in enumerate(stage_intervals(config.n_blocks, n_stages)):
         for r in range(replicas):
             sid = f"s{si}{chr(ord('a') + r)}"
+            e = eng if engine_for is None else engine_for(sid, si, r)
             srv = BlockServer(ServerCfg(sid, b - a, a,
-                                        crash_after_messages=(crash or {}).get(sid)), eng, net)
+                                        crash_after_messages=(crash or {}).get(sid)), e, net)
             servers[sid] = srv
             net.register(sid, srv)
             routes.append(ServerRoute(sid, a, b))

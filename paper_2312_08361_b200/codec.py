@@ -33,13 +33,15 @@ def quantize_device(x: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
     n = x.numel()
     codes = torch.empty(n, dtype=torch.int8, device=x.device)
     scales = torch.empty((n + BLOCK_SIZE - 1) // BLOCK_SIZE, dtype=torch.float32, device=x.device)
-    _lib.check(_lib.load().sp_quantize_blockwise(x.data_ptr(), codes.data_ptr(),
-                                                 scales.data_ptr(), n, _stream(x)))
+    with torch.cuda.device(x.device):      # the kernel runs where the data lives
+        _lib.check(_lib.load().sp_quantize_blockwise(x.data_ptr(), codes.data_ptr(),
+                                                     scales.data_ptr(), n, _stream(x)))
     return codes, scales
 
 
 def dequantize_device(codes: torch.Tensor, scales: torch.Tensor, n: int) -> torch.Tensor:
     out = torch.empty(n, dtype=torch.float32, device=codes.device)
-    _lib.check(_lib.load().sp_dequantize_blockwise(codes.data_ptr(), scales.data_ptr(),
-                                                   out.data_ptr(), n, _stream(codes)))
+    with torch.cuda.device(codes.device):
+        _lib.check(_lib.load().sp_dequantize_blockwise(codes.data_ptr(), scales.data_ptr(),
+                                                       out.data_ptr(), n, _stream(codes)))
     return out

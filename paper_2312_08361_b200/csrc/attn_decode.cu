@@ -659,11 +659,12 @@ void launch_mma(const AttnDecArgs& a, cudaStream_t st) {
   const int G = a.H / a.kvh;
   const size_t smem = (size_t)2 * 4 * 32 * (HD + 8) * 2 +
                       (size_t)(4 * G * HD + 2 * a.max_pages * GMAX) * sizeof(float);
-  static size_t set = 0;
-  if (smem > set) {
+  static size_t set[kMaxDevices] = {};
+  const int dv = current_device();
+  if (smem > set[dv]) {
     cudaFuncSetAttribute(attn_dec_mma_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
-    set = smem;
+    set[dv] = smem;
   }
   static int trace_call = getenv("SP_ATTN_TRACE") ? atoi(getenv("SP_ATTN_TRACE")) : -1;
   static int ncall = 0;
@@ -700,11 +701,12 @@ void launch_g(const AttnDecArgs& a, cudaStream_t st) {
   dim3 grid(a.width * a.kvh, (T + CHUNK - 1) / CHUNK);
   const int G = a.H / a.kvh;
   const size_t smem = (size_t)(4 * G * HD + 2 * a.max_pages * GMAX) * sizeof(float);
-  static size_t set = 0;
-  if (smem > set) {
+  static size_t set[kMaxDevices] = {};
+  const int dv = current_device();
+  if (smem > set[dv]) {
     cudaFuncSetAttribute(attn_dec2_kernel<HD, KT, GT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
-    set = smem;
+    set[dv] = smem;
   }
   attn_dec2_kernel<HD, KT, GT><<<grid, NTH, smem, st>>>(a);
   count_launch();

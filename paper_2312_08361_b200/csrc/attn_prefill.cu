@@ -237,11 +237,12 @@ __global__ void __launch_bounds__(128) attn_prefill_mma_kernel(AttnArgs a) {
 
 template <int HD, bool HILO>
 void launch_hd(const AttnArgs& a, dim3 grid, size_t smem, cudaStream_t st) {
-  static bool set = false;
-  if (!set) {
+  static bool set[kMaxDevices] = {};
+  const int dv = current_device();
+  if (!set[dv]) {
     cudaFuncSetAttribute(attn_prefill_mma_kernel<HD, HILO>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    set = true;
+    set[dv] = true;
   }
   attn_prefill_mma_kernel<HD, HILO><<<grid, 128, smem, st>>>(a);
 }

@@ -82,6 +82,15 @@ __host__ __device__ __forceinline__ int64_t cm_offset(int64_t n, int64_t kb, int
 // host-side count of kernels launched by this library (bench `gpu_launches`)
 void count_launch();
 
+// kernel attributes (max dynamic smem) are per device: launchers remember
+// them per device index
+constexpr int kMaxDevices = 64;
+inline int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d < kMaxDevices ? d : kMaxDevices - 1;
+}
+
 // ---- programmatic dependent launch (decode chain) ----------------------------
 // A kernel launched with launch_pdl() may start while the previous kernel in
 // the stream is still running: everything before pdl_wait() must touch only

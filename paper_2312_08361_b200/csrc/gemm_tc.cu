@@ -656,12 +656,13 @@ void launch_digitize(const float* x, int64_t ldx, int64_t M, int64_t K, int norm
 
 template <int KUP, int ST>
 void launch_pair(const TcGemmArgs& a, cudaStream_t st) {
-  static bool set2 = false;
+  static bool set2[kMaxDevices] = {};
+  const int dv = current_device();
   const size_t smem2 = (size_t)ST * 3 * KUP * UNIT;
-  if (!set2) {
+  if (!set2[dv]) {
     cudaFuncSetAttribute(gemm_i8_tc2_kernel<KUP, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem2);
-    set2 = true;
+    set2[dv] = true;
   }
   dim3 grid2((unsigned)(2 * ((a.M + 255) / 256)), (unsigned)(a.N / 256));
   static int dbg = getenv("SP_TC_DEBUG") ? atoi(getenv("SP_TC_DEBUG")) : 0;
@@ -698,12 +699,13 @@ void launch_gemm_i8_tc(const TcGemmArgs& a, cudaStream_t st) {
     else launch_pair<4, 4>(a, st);
     return;
   }
-  static bool set = false;
+  static bool set[kMaxDevices] = {};
+  const int dv = current_device();
   const size_t smem = (size_t)STAGES * STAGE;
-  if (!set) {
+  if (!set[dv]) {
     cudaFuncSetAttribute(gemm_i8_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
-    set = true;
+    set[dv] = true;
   }
   dim3 grid((unsigned)((a.M + BM - 1) / BM), (unsigned)(a.N / (128 * NGRP)));
   gemm_i8_tc_kernel<<<grid, 256, smem, st>>>(a);

@@ -520,7 +520,8 @@ void launch_wt(const GemvArgs& a, int ks, int r0, int rn, int Rs, cudaStream_t s
   const int nt = cols <= 8 ? 1 : (cols <= 16 ? 2 : 3);
   const size_t red_bytes = (size_t)NW * RT * nt * 32 * 16;
   const size_t smem = red_bytes > RING_BYTES ? red_bytes : RING_BYTES;
-  static bool attr_set[3] = {false, false, false};
+  static bool attr_set_all[kMaxDevices][3] = {};
+  bool* attr_set = attr_set_all[current_device()];
   if (nt == 1) {
     if (!attr_set[0]) {
       cudaFuncSetAttribute(gemv2_kernel<WT, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

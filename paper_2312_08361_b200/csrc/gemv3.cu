@@ -528,11 +528,12 @@ void launch_cfg(const GemvArgs& a, int r0, int rn, cudaStream_t st) {
   const int64_t units = (a.N / 128) * (a.K / KTILE);
   const int grid = g_num_sms * CTAS_PER_SM;
   const size_t smem = (size_t)NW * STAGES * stage_bytes(NT) + (size_t)NW * sizeof(WarpSmem) + 128;
-  static bool set = false;
-  if (!set) {
+  static bool set[kMaxDevices] = {};
+  const int dv = current_device();
+  if (!set[dv]) {
     cudaFuncSetAttribute(gemv3_kernel<WT, NT, NORMT, HASG>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    set = true;
+    set[dv] = true;
   }
   static int trace_call = getenv("SP_GEMV_TRACE") ? atoi(getenv("SP_GEMV_TRACE")) : -1;
   static int ncall = 0;   // per instantiation

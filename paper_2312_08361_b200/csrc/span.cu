@@ -42,6 +42,20 @@ bool g_attn_l2pf = false;  // option 4 (measured: slower, off)
 
 using namespace sp;
 
+// the span's device is current for the duration of a call; the caller's
+// device is restored on return (spans on several GPUs in one process)
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) == cudaSuccess && prev != dev) cudaSetDevice(dev);
+    else prev = -1;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+
 namespace {
 
 constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ull;
@@ -782,7 +796,7 @@ int sp_kv_destroy(sp_kv* kv) {
     for (auto& pg : kv->pages)
       for (int p : pg) release_page(s, p);
   }
-  cudaSetDevice(s->device);
+  DeviceGuard dg(s->device);
   cudaFree(kv->d_table);
   delete kv;
   return SP_OK;
@@ -807,7 +821,7 @@ int sp_kv_reorder(sp_kv* kv, const int32_t* parents0, int32_t new_width, void* s
     for (int p : pg) release_page(s, p);
   kv->pages.swap(np);
   kv->width = new_width;
-  SP_CUDA_TRY(cudaSetDevice(s->device));
+  DeviceGuard dg(s->device);
   return upload_table(kv, (cudaStream_t)stream);
 }
 
@@ -839,6 +853,7 @@ static int forward_impl(sp_span* s, sp_kv* kv, int32_t b0, int32_t b1, const flo
                         int8_t* y_codes, float* y_scales, int32_t width, int32_t n_new,
                         void* stream) {
   if (!s || !kv || !y) SP_FAIL(SP_ERR_ARG, "null argument");
+  DeviceGuard dg(s->device);
   if (!(s->start <= b0 && b0 < b1 && b1 <= s->end)) SP_FAIL(SP_ERR_ARG, "blocks outside span");
   if (width != kv->width) SP_FAIL(SP_ERR_STATE, "width mismatch");
   if (n_new < 1) SP_FAIL(SP_ERR_ARG, "n_new must be >= 1");

@@ -230,11 +230,15 @@ class B200ServerEngine:
         d = self.config.hidden_dim
         if getattr(blob, "synthetic", False):
             raise ProtocolError("synthetic blob carries no data")
+        # device payloads produced on another GPU (the previous span's server)
+        # move peer to peer over NVLink; same-device payloads are used in place
+        here = self.device if isinstance(self.device, torch.device) else torch.device(
+            "cuda", self.device)
         if getattr(blob, "dev_codes", None) is not None:
-            c, s = blob.dev_codes, blob.dev_scales
+            c, s = blob.dev_codes.to(here), blob.dev_scales.to(here)
             return 0, c.data_ptr(), s.data_ptr(), (c, s)
         if getattr(blob, "dev", None) is not None:
-            x = blob.dev
+            x = blob.dev.to(here)
             return x.data_ptr(), 0, 0, (x,)
         q = blob.quant
         if q is not None:
