@@ -1,6 +1,6 @@
 // Prefill / replay attention (n_new > 1) on tensor cores, flash-style.
 //
-// CTA = (slot, query head, 64 query rows); 4 warps x 16 rows.  Key/value pages
+// CTA = (slot, query head, 128 query rows); 8 warps x 16 rows share each K/V tile.  Key/value pages
 // (64 positions, bf16, head dim 64/128) stream through a double-buffered
 // cp.async ring; S = Q K^T and O += P V run on mma.m16n8k16 with the online
 // softmax of FlashAttention-2.  Q and P are rounded to bf16 like the cached
@@ -9,6 +9,8 @@
 // result tracks the f32 reference more closely.  Accumulation is f32 (SP/model.py:263-275: scores / f32(sqrt(hd)),
 // (+ ALiBi), causal -1e30 mask for n > 1, max-subtracted softmax).
 // Each query row's result depends only on its own row: batch/tile invariant.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -16,7 +18,6 @@ namespace sp {
 
 namespace {
 
-constexpr int QT = 64;            // query rows per CTA
 constexpr int KTL = 64;           // keys per tile (one page)
 
 __device__ __forceinline__ void mma16816(float* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
@@ -52,8 +53,9 @@ __device__ __forceinline__ void split2(float x0, float x1, uint32_t& hi, uint32_
   lo = pack_bf16(x0 - __bfloat162float(h0), x1 - __bfloat162float(h1));
 }
 
-template <int HD, bool HILO>
-__global__ void __launch_bounds__(128) attn_prefill_mma_kernel(AttnArgs a) {
+template <int HD, bool HILO, int NWARP>
+__global__ void __launch_bounds__(NWARP * 32) attn_prefill_mma_kernel(AttnArgs a) {
+  constexpr int QT = 16 * NWARP;                    // query rows per CTA (share each K/V tile)
   constexpr int RS = HD + 8;                        // padded smem row (bf16)
   constexpr int NKS = HD / 16;                      // k-steps over dims
   extern __shared__ __align__(16) uint8_t dsm_[];
@@ -63,7 +65,8 @@ __global__ void __launch_bounds__(128) attn_prefill_mma_kernel(AttnArgs a) {
 
   const int G = a.H / a.kvh;
   const int slot = blockIdx.x / a.H, h = blockIdx.x % a.H, kh = h / G;
-  const int q0 = blockIdx.y * QT;
+  // the heaviest (latest) query tiles launch first: causal work grows with q0
+  const int q0 = (gridDim.y - 1 - blockIdx.y) * QT;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g8 = lane >> 2, t4 = lane & 3;
   const int qrow0 = q0 + warp * 16;                 // this warp's first query row
   const float slope = (a.family == kBloom) ? a.alibi[h] : 0.f;
@@ -107,7 +110,7 @@ __global__ void __launch_bounds__(128) attn_prefill_mma_kernel(AttnArgs a) {
     const __nv_bfloat16* vp = reinterpret_cast<const __nv_bfloat16*>(a.kv_pool) +
                               (((int64_t)page * 2 + 1) * a.kvh + kh) * kPageTokens * HD;
     constexpr int CPR = HD / 8;                     // 16-byte chunks per row
-    for (int c = threadIdx.x; c < KTL * CPR; c += 128) {
+    for (int c = threadIdx.x; c < KTL * CPR; c += NWARP * 32) {
       const int j = c / CPR, e = (c % CPR) * 8;
       cp16(&Ks[buf][j][e], kp + j * HD + e);
       cp16(&Vs[buf][j][e], vp + j * HD + e);
@@ -235,30 +238,37 @@ __global__ void __launch_bounds__(128) attn_prefill_mma_kernel(AttnArgs a) {
 
 }  // namespace
 
-template <int HD, bool HILO>
-void launch_hd(const AttnArgs& a, dim3 grid, size_t smem, cudaStream_t st) {
+template <int HD, bool HILO, int NW>
+void launch_hd(const AttnArgs& a, size_t smem, cudaStream_t st) {
   static bool set[kMaxDevices] = {};
   const int dv = current_device();
   if (!set[dv]) {
-    cudaFuncSetAttribute(attn_prefill_mma_kernel<HD, HILO>,
+    cudaFuncSetAttribute(attn_prefill_mma_kernel<HD, HILO, NW>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     set[dv] = true;
   }
-  attn_prefill_mma_kernel<HD, HILO><<<grid, 128, smem, st>>>(a);
+  dim3 grid(a.width * a.H, (a.n_new + 16 * NW - 1) / (16 * NW));
+  attn_prefill_mma_kernel<HD, HILO, NW><<<grid, NW * 32, smem, st>>>(a);
 }
 
 bool g_attn_hilo = false;
 
+template <int HD, bool HILO>
+void launch_nw(const AttnArgs& a, size_t smem, cudaStream_t st) {
+  static int nw = getenv("SP_ATTN_PF_WARPS") ? atoi(getenv("SP_ATTN_PF_WARPS")) : 4;
+  if (nw == 8) launch_hd<HD, HILO, 8>(a, smem, st);
+  else launch_hd<HD, HILO, 4>(a, smem, st);
+}
+
 bool launch_attention_prefill_mma(const AttnArgs& a, cudaStream_t st) {
   if (a.kv_dtype != kKVBF16 || !(a.hd == 64 || a.hd == 128)) return false;
-  dim3 grid(a.width * a.H, (a.n_new + QT - 1) / QT);
   const size_t smem = (size_t)4 * KTL * (a.hd + 8) * 2;
   if (a.hd == 128) {
-    if (g_attn_hilo) launch_hd<128, true>(a, grid, smem, st);
-    else launch_hd<128, false>(a, grid, smem, st);
+    if (g_attn_hilo) launch_nw<128, true>(a, smem, st);
+    else launch_nw<128, false>(a, smem, st);
   } else {
-    if (g_attn_hilo) launch_hd<64, true>(a, grid, smem, st);
-    else launch_hd<64, false>(a, grid, smem, st);
+    if (g_attn_hilo) launch_nw<64, true>(a, smem, st);
+    else launch_nw<64, false>(a, smem, st);
   }
   count_launch();
   return true;
