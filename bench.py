@@ -364,8 +364,8 @@ def run_b200(args) -> None:
         eng.run_cached(start, end, c_e2e, HiddenBlob.from_array(
             np.random.default_rng(0).standard_normal((args.prefill, d)).astype(np.float32)), 1,
             args.prefill, False)
-        rows = np.random.default_rng(1).standard_normal((args.steps + args.warmup, 1, d)).astype(
-            np.float32)
+        rows = torch.from_numpy(np.random.default_rng(1).standard_normal(
+            (args.steps + args.warmup, 1, d)).astype(np.float32)).pin_memory().numpy()
         for i in range(args.warmup):
             eng.run_cached(start, end, c_e2e, HiddenBlob.from_array(rows[i]), 1, 1, False).array()
         torch.cuda.synchronize()
@@ -377,6 +377,29 @@ def run_b200(args) -> None:
         e2e = {"value": args.steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 4 * d,
                "d2h_bytes_per_step": 4 * d}
         del c_e2e
+    else:
+        # N > 1: every rank's span call goes through B200ServerEngine.run_cached;
+        # rank 0 uploads its session's input row from pinned host memory, the
+        # last rank reads its output row back to the host, every tick
+        host_rows = torch.randn(sessions, 1, d, generator=torch.Generator().manual_seed(3)
+                                ).pin_memory().numpy()
+        for _ in range(args.warmup):
+            pipe.step_api(host_rows)
+        torch.cuda.synchronize()
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            pipe.step_api(host_rows)
+        torch.cuda.synchronize()
+        dist.barrier()
+        e2e_t = torch.tensor([time.perf_counter() - t0], device=dev)
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+        e2e_s = float(e2e_t.item())
+        e2e = {"value": args.steps * sessions / max(1, world) / e2e_s, "unit": UNIT,
+               "h2d_bytes_per_step": 4 * d, "d2h_bytes_per_step": 4 * d,
+               "note": "per tick: rank 0 H2D of one input row, last rank D2H of one output "
+                       "row; wall clock max over ranks"}
 
     # ---- roofline of the dominant kernel (decode GEMV) ----
     achieved = wbytes.value / (gemv_ms / 1e3) / 1e9

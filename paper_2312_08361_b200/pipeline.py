@@ -88,6 +88,44 @@ class SpanPipeline:
                 w.wait()
         self.k += 1
 
+    def step_api(self, host_rows) -> None:
+        """One tick through the public engine API (`run_cached`): rank 0 takes its
+        session's input row from host memory (H2D inside the call), the last rank
+        reads its result to the host (D2H); the span-to-span wire is the same
+        int8 codes + scales over NCCL.  (`bench.py` e2e at N > 1.)"""
+        from .blob import HiddenBlob
+        k, r, N = self.k, self.rank, self.world
+        active = k >= r
+        s = (k - r) % N
+        last = r == N - 1
+        if active:
+            if r == 0:
+                blob = HiddenBlob.from_array(host_rows[s])
+            else:
+                blob = HiddenBlob(1, self.d, dev_codes=self.in_codes, dev_scales=self.in_scales)
+            out = self.eng.run_cached(self.start, self.end, self.caches[s], blob, 1, 1,
+                                      not last)
+            if last:
+                self.host_out = out.array()               # the step's result on the host
+                self.y.copy_(out.dev)
+            else:
+                self.out_codes.copy_(out.dev_codes)
+                self.out_scales.copy_(out.dev_scales)
+        import torch.distributed as dist
+        ops = []
+        if active:
+            ops.append(dist.P2POp(dist.isend, self.y if last else self.out_wire,
+                                  0 if last else r + 1))
+        if r == 0:
+            if k >= N - 1:
+                ops.append(dist.P2POp(dist.irecv, self.ring_in, N - 1))
+        elif k >= r - 1:
+            ops.append(dist.P2POp(dist.irecv, self.in_wire, r - 1))
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+        self.k += 1
+
     @property
     def wire_bytes_per_token(self) -> int:
         return int(self.out_wire.numel())
