@@ -260,3 +260,34 @@ def test_tc_pair_gemm_equals_single_cta():
         _lib.check(span.lib.sp_span_set_option(span.handle, 2, 1))
         assert np.array_equal(pair, single), (batch, tokens, float(np.abs(pair - single).max()),
                                               float(np.abs(single).max()))
+
+
+@pytest.mark.parametrize("name", ["llama_int8", "bloom_int8", "llama_bf16"])
+def test_extended_families_greedy_tokens_match_oracle(name):
+    """BASELINE north star: identical greedy tokens to the CPU oracle and
+    max-abs logits diff <= 1e-2 — prompt through the prefill path (tcgen05 for
+    int8), then 24 decode steps (tensor-core GEMV + fused attention), GPU head."""
+    from paper_2312_08361_b200.head import ClientHead
+    cfg = SMALL[name]
+    eng = _engine(cfg)
+    head = ClientHead(cfg)
+    emb = om.init_embedding(cfg)
+    runner = om.SpanRunner(cfg, 0, cfg.n_blocks)
+    c = eng.make_caches(0, cfg.n_blocks, 1)
+    toks_gpu, toks_cpu = [3, 1, 4], [3, 1, 4]
+    xg = head.embed_array(toks_gpu)
+    xc = emb[toks_cpu]
+    assert np.array_equal(xg, xc)
+    worst = 0.0
+    for _ in range(24):
+        yg = eng.run_cached(0, cfg.n_blocks, c, _blob(xg), 1, xg.shape[0], False).array()
+        yc = runner.step(xc[None])[0]
+        lg, lc = om.logits_for(emb, yg[-1]), om.logits_for(emb, yc[-1])
+        worst = max(worst, float(np.abs(lg - lc).max()))
+        tg, tc = head.pick(yg), om.greedy_pick(lc)
+        toks_gpu.append(tg)
+        toks_cpu.append(tc)
+        xg = head.embed_array([tg])
+        xc = emb[[tc]]
+    assert toks_gpu == toks_cpu
+    assert worst <= 1e-2, worst

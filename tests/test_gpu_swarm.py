@@ -122,3 +122,42 @@ def test_dropin_beam_search_matches_reference_oracle():
     finally:
         swarmpipe.swarm.RealServerEngine = orig
         swarmpipe.server.RealServerEngine = orig
+
+
+@pytest.mark.parametrize("quantized", [False, True])
+def test_llama_int8_failover_greedy_tokens_match_oracle(quantized):
+    """BASELINE north star on the 70B kernel family (int8 weights, GQA, RoPE,
+    SwiGLU, bf16 KV): 2 stages x 2 replicas, a stage-1 server crashes
+    mid-generation, the client replays its cached inputs onto the replica —
+    greedy tokens equal the CPU oracle's (reference_generate restated)."""
+    from oracle import model as om
+    from paper_2312_08361_b200.client import SwarmClient, build_swarm
+    from paper_2312_08361_b200.config import SpanConfig
+    from paper_2312_08361_b200.engine import B200ServerEngine
+    from paper_2312_08361_b200.head import ClientHead
+    cfg = SpanConfig(n_blocks=4, hidden_dim=512, n_heads=4, n_kv_heads=2, ffn_dim=1024,
+                     vocab_size=64, max_seq_len=512, family="llama", weight_dtype="int8",
+                     kv_dtype="bf16", seed=5)
+    eng = B200ServerEngine(cfg)
+    net, servers, routes = build_swarm(lambda: eng, cfg, 2, 2, crash={"s1a": 9})
+    res = SwarmClient("client1", cfg, net, routes, ClientHead(cfg)).generate(
+        [3, 1, 4], 24, quantized=quantized)
+    assert res.counters.recoveries >= 1 and res.counters.restore_events
+    if not quantized:
+        assert res.tokens == om.reference_generate(cfg, [3, 1, 4], 24)
+    else:
+        # stage boundary coded: the oracle applies the same codec round trip
+        from oracle import codec as oc
+        emb = om.init_embedding(cfg)
+        r0, r1 = om.SpanRunner(cfg, 0, 2), om.SpanRunner(cfg, 2, 4)
+        toks = [3, 1, 4]
+        x = emb[toks]
+        for _ in range(24):
+            h = r0.step(x[None])[0]
+            codes, scales = oc.quantize(h)
+            h = oc.dequantize(codes, scales, h.shape)
+            y = r1.step(h[None])[0]
+            t = om.greedy_pick(om.logits_for(emb, y[-1]))
+            toks.append(t)
+            x = emb[[t]]
+        assert res.tokens == toks
