@@ -29,6 +29,15 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 METRIC = "Llama-2-70B-shape decode steps/s and prefill tokens/s, % of HBM/TC roofline"
+
+
+class _Configs:
+    def __getitem__(self, name):
+        from paper_2312_08361_b200.config import bloom_176b, llama2_7b, llama2_70b
+        return {"llama2-70b": llama2_70b, "llama2-7b": llama2_7b, "bloom-176b": bloom_176b}[name]
+
+
+CONFIGS = _Configs()
 UNIT = "steps/s"
 
 
@@ -211,7 +220,6 @@ def run_b200(args) -> None:
 
     from paper_2312_08361_b200 import _lib
     from paper_2312_08361_b200.blob import HiddenBlob
-    from paper_2312_08361_b200.config import llama2_70b
     from paper_2312_08361_b200.engine import B200ServerEngine, DeviceSpan
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -222,14 +230,16 @@ def run_b200(args) -> None:
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     peaks = load_peaks()
-    cfg = llama2_70b()
+    cfg = CONFIGS[args.config]()
+    B = args.batch                                 # rows per session per step
     n_blocks = args.blocks or cfg.n_blocks
     if args.blocks:
         cfg = cfg.with_(n_blocks=n_blocks)
     start, end = stage_intervals(n_blocks, world)[rank]
     t_gen = time.perf_counter()
     span = DeviceSpan(cfg, start, end, device=local,
-                      kv_pool_tokens=(args.prefill + 256) * (max(1, world) + 1) + 1024)
+                      kv_pool_tokens=(args.prefill + args.steps * 4 + 256) * B * (max(1, world) + 1)
+                      + 1024)
     torch.cuda.synchronize()
     t_gen = time.perf_counter() - t_gen
     eng = B200ServerEngine(cfg, span=span)
@@ -260,14 +270,14 @@ def run_b200(args) -> None:
     sessions = max(1, world)       # sessions in flight (one per pipeline stage)
 
     # ---- prefill (2048 tokens per session), timed on the device ----
-    x_pre = torch.randn(args.prefill, d, device=dev, generator=g)
+    x_pre = torch.randn(B * args.prefill, d, device=dev, generator=g)
     # untimed warm-up prefill on a throw-away cache: first-call scratch
     # allocations and kernel attribute setup stay out of the timed region
-    warm = eng.make_caches(start, end, 1)
-    eng.run_cached(start, end, warm, HiddenBlob.from_device(x_pre), 1, args.prefill, False)
+    warm = eng.make_caches(start, end, B)
+    eng.run_cached(start, end, warm, HiddenBlob.from_device(x_pre), B, args.prefill, False)
     torch.cuda.synchronize()
     del warm
-    caches = [eng.make_caches(start, end, 1) for _ in range(sessions)]
+    caches = [eng.make_caches(start, end, B) for _ in range(sessions)]
     prof(True)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
@@ -275,7 +285,7 @@ def run_b200(args) -> None:
     torch.cuda.synchronize()
     ev0.record(stream)
     for s in range(sessions):
-        eng.run_cached(start, end, caches[s], HiddenBlob.from_device(x_pre), 1, args.prefill,
+        eng.run_cached(start, end, caches[s], HiddenBlob.from_device(x_pre), B, args.prefill,
                        False)
     ev1.record(stream)
     torch.cuda.synchronize()
@@ -287,11 +297,11 @@ def run_b200(args) -> None:
         dist.all_reduce(pre_ms_t, op=dist.ReduceOp.MAX)
     pre_ms = float(pre_ms_t.item())
     pre_flops = sum(p["flops"] for p in pre_prof)
-    prefill_tok_s = sessions * args.prefill / (pre_ms / 1e3)
+    prefill_tok_s = sessions * B * args.prefill / (pre_ms / 1e3)
 
     # ---- decode: W warm-up + K timed steps ----
     from paper_2312_08361_b200.pipeline import SpanPipeline
-    pipe = SpanPipeline(eng, start, end, caches, rank, world, d, dev)
+    pipe = SpanPipeline(eng, start, end, caches, rank, world, d, dev, width=B)
     # W warm-up ticks, plus N more for N > 1: the last-to-first ring edge is
     # first used at tick N - 1, and NCCL sets up a p2p connection on first use
     for _ in range(args.warmup + (world if world > 1 else 0)):
@@ -343,14 +353,14 @@ def run_b200(args) -> None:
     wbytes = ctypes.c_double()
     reps = 3
     _lib.check(lib.sp_span_decode_gemv_only(span.handle, caches[0].handle, start, end,
-                                            pipe.y.data_ptr(), 1, stream.cuda_stream,
+                                            pipe.y.data_ptr(), B, stream.cuda_stream,
                                             ctypes.byref(wbytes)))
     g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     g0.record(stream)
     for _ in range(reps):
         _lib.check(lib.sp_span_decode_gemv_only(span.handle, caches[0].handle, start, end,
-                                                pipe.y.data_ptr(), 1, stream.cuda_stream,
+                                                pipe.y.data_ptr(), B, stream.cuda_stream,
                                                 ctypes.byref(wbytes)))
     g1.record(stream)
     torch.cuda.synchronize()
@@ -360,28 +370,28 @@ def run_b200(args) -> None:
     # ---- end to end through the public API (host buffers, H2D + D2H per step) ----
     e2e = None
     if world == 1:
-        c_e2e = eng.make_caches(start, end, 1)
+        c_e2e = eng.make_caches(start, end, B)
         eng.run_cached(start, end, c_e2e, HiddenBlob.from_array(
-            np.random.default_rng(0).standard_normal((args.prefill, d)).astype(np.float32)), 1,
-            args.prefill, False)
+            np.random.default_rng(0).standard_normal((B * args.prefill, d)).astype(np.float32)),
+            B, args.prefill, False)
         rows = torch.from_numpy(np.random.default_rng(1).standard_normal(
-            (args.steps + args.warmup, 1, d)).astype(np.float32)).pin_memory().numpy()
+            (args.steps + args.warmup, B, d)).astype(np.float32)).pin_memory().numpy()
         for i in range(args.warmup):
-            eng.run_cached(start, end, c_e2e, HiddenBlob.from_array(rows[i]), 1, 1, False).array()
+            eng.run_cached(start, end, c_e2e, HiddenBlob.from_array(rows[i]), B, 1, False).array()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for i in range(args.warmup, args.warmup + args.steps):
-            out = eng.run_cached(start, end, c_e2e, HiddenBlob.from_array(rows[i]), 1, 1, False)
+            out = eng.run_cached(start, end, c_e2e, HiddenBlob.from_array(rows[i]), B, 1, False)
             out.array()
         e2e_s = time.perf_counter() - t0
-        e2e = {"value": args.steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 4 * d,
-               "d2h_bytes_per_step": 4 * d}
+        e2e = {"value": args.steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 4 * B * d,
+               "d2h_bytes_per_step": 4 * B * d}
         del c_e2e
     else:
         # N > 1: every rank's span call goes through B200ServerEngine.run_cached;
         # rank 0 uploads its session's input row from pinned host memory, the
         # last rank reads its output row back to the host, every tick
-        host_rows = torch.randn(sessions, 1, d, generator=torch.Generator().manual_seed(3)
+        host_rows = torch.randn(sessions, B, d, generator=torch.Generator().manual_seed(3)
                                 ).pin_memory().numpy()
         for _ in range(args.warmup):
             pipe.step_api(host_rows)
@@ -397,7 +407,7 @@ def run_b200(args) -> None:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
         e2e_s = float(e2e_t.item())
         e2e = {"value": args.steps * sessions / max(1, world) / e2e_s, "unit": UNIT,
-               "h2d_bytes_per_step": 4 * d, "d2h_bytes_per_step": 4 * d,
+               "h2d_bytes_per_step": 4 * B * d, "d2h_bytes_per_step": 4 * B * d,
                "note": "per tick: rank 0 H2D of one input row, last rank D2H of one output "
                        "row; wall clock max over ranks"}
 
@@ -413,8 +423,8 @@ def run_b200(args) -> None:
             cpu = {"value": 1.0 / (t_block * n_blocks), "unit": UNIT, "cores": cpu_threads(),
                    "kind": "port",
                    "sample": f"oracle block_forward_batched (f32 numpy/OpenBLAS) of one "
-                             f"70B-shape block at context {args.prefill}, median of 3, scaled "
-                             f"to {n_blocks} blocks"}
+                             f"{args.config}-shape block, batch 1, context {args.prefill}, "
+                             f"median of 3, scaled to {n_blocks} blocks"}
         peak = peaks["hbm_gbs"]
         # DRAM traffic per GEMV launch (dram__bytes_read.sum + dram__bytes_write.sum)
         # from the committed ncu --set full capture of one block's 4 GEMVs
@@ -431,19 +441,23 @@ def run_b200(args) -> None:
             "ms_per_step": dec_ms / max(steps_done, 1e-9) * (sessions / max(1, world)) * world
             if world > 1 else dec_ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "int8 (weights x 23-bit int digit activations, exact int32 tensor-core MMA; f32 residual)",
+            "dtype": ("int8 (weights x 23-bit (batch<=2) / 15-bit int digit activations, exact int32 tensor-core MMA; "
+                      "f32 residual)") if cfg.weight_dtype == "int8" else
+                     "bf16 (weights; activations split hi+lo bf16, f32 accumulate)",
             "data": "synthetic (splitmix64 random-init weights per SP/model.py:55-60, N(0,1) "
                     "hidden rows)",
-            "config": {"workload": f"llama2-70b-shape int8 span decode, batch 1, context "
-                                   f"{args.prefill}+, {n_blocks} blocks over {world} GPU(s), "
-                                   f"{sessions} session(s) in flight",
+            "config": {"workload": f"{args.config}-shape {cfg.weight_dtype} span decode, batch "
+                                   f"{B}, context {args.prefill}+, {n_blocks} blocks over "
+                                   f"{world} GPU(s), {sessions} session(s) in flight",
                        "span_per_gpu": [start, end], "prefill_tokens": args.prefill,
-                       "l2": "inputs larger than L2 (68.5 GB weights)"},
+                       "batch": B,
+                       "l2": f"inputs larger than L2 ({span.weight_bytes / 1e9:.1f} GB weights "
+                             f"per GPU)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "traffic_src": traffic_src,
-                         "kernel": "gemv3_kernel<int8> (decode QKV/O/gate-up/down GEMVs, "
-                                   "norm folded in)",
+                         "kernel": f"gemv3_kernel<{cfg.weight_dtype}> (decode QKV/O/gate-up/"
+                                   "down GEMVs, norm folded in)",
                          "peak_src": peaks["_src"], "launches": gemv_launches,
                          "avg_launch_us": gemv_ms / gemv_launches * 1e3,
                          "bytes_per_launch": wbytes.value / gemv_launches,
@@ -479,6 +493,10 @@ def main() -> None:
     ap.add_argument("--impl", default="b200", choices=["b200", "reference", "ours"])
     ap.add_argument("--prefill", type=int, default=2048)
     ap.add_argument("--blocks", type=int, default=0, help="override n_blocks (debug only)")
+    ap.add_argument("--config", default="llama2-70b", choices=["bloom-176b", "llama2-70b",
+                                                                "llama2-7b"],
+                    help="model shape (BASELINE.json configs; the metric is quoted on llama2-70b)")
+    ap.add_argument("--batch", type=int, default=1, help="rows per session per step")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":

@@ -9,14 +9,15 @@
 // STAGES-deep ring of 1-D TMA bulk copies (cp.async.bulk + mbarrier, L2
 // evict-first) and never synchronises with other warps.
 //
-// Arithmetic (int8 weights, 70B/BLOOM): EXACT.  The input row is scaled by a
-// power of two 2^(22-e_r) and rounded to a 23-bit integer q = d0*2^16 +
-// d1*2^8 + d2 (balanced base-256 digits); the three digits of each batch row
-// are three columns of mma.m16n8k32.s8.s8.s32 whose A fragment is the lane's
+// Arithmetic (int8 weights, 70B/BLOOM): exact for the coded input.  The input
+// row is scaled by a power of two 2^(kQBits-e_r) and rounded to an integer
+// q written as ND balanced base-256 digits (23-bit / 3 digits for 1-2 rows,
+// 15-bit / 2 digits for more); the digits of each
+// batch row are columns of mma.m16n8k32.s8.s8.s32 whose A fragment is the lane's
 // 16-byte weight load (fragment-tiled storage, no conversion).  Digit sums are
 // exact int32, combined in int64; partial sums of a group's k-range are int64
 // atomics (exact => order-independent => deterministic and batch-invariant).
-// One rounding at the end: y = f32(D * 2^(e-22) * rstd * wscale[n]).
+// One rounding at the end: y = f32(D * 2^(e-kQBits) * rstd * wscale[n]).
 // bf16 weights (7B): A = bf16 tiles, input split hi+lo (two bf16 MMA columns),
 // f32 accumulation; partials fixed-point (2^-32) int64 atomics => deterministic.
 //
@@ -50,6 +51,11 @@ __host__ __device__ constexpr int stage_bytes(int nt) {
 }
 constexpr int STAGES = 3;         // TMA ring depth per warp (units)
 constexpr int RMAX = 8;           // batch rows per launch
+// int8 path: activation code width.  The row is scaled by 2^(kQBits - e)
+// (|x| < 2^e) and rounded to an integer |q| <= 2^kQBits written as NDIG
+// balanced int8 digits (MMA columns); 2 digits = 15-bit codes, the precision
+// class of the prefill digit planes, and 4 batch rows per 8-column MMA tile.
+constexpr int kNDig = 2;   // digits for 3+ batch rows (see launch_gemv3)
 constexpr double kFix = 4294967296.0;   // bf16 partial fixed point 2^32
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -114,7 +120,7 @@ __device__ __forceinline__ float gelu_f(float x) {
 __device__ __forceinline__ float silu_f(float x) { return x / (1.0f + expf(-x)); }
 
 // digit of 4 integers: byte `sel` of (q + bias), packed; balanced digits:
-// d2 = byte0(q), d1 = byte1(q + 0x80), d0 = byte2(q + 0x8080)  (|q| <= 2^22)
+// 2 digits: d1 = byte0(q), d0 = byte1(q + 0x80)  (|q| <= 2^14); 3 digits add byte2(q + 0x8080)
 __device__ __forceinline__ uint32_t digits4(int q0, int q1, int q2, int q3, int bias,
                                             uint32_t sel_lo, uint32_t sel_hi) {
   const uint32_t u0 = q0 + bias, u1 = q1 + bias, u2 = q2 + bias, u3 = q3 + bias;
@@ -143,11 +149,13 @@ struct WarpSmem {
   uint64_t bar[STAGES];
 };
 
-template <int WT, int NT, int NORMT, bool HASG>
+template <int WT, int NT, int NORMT, bool HASG, int ND>
 __global__ void __launch_bounds__(NW * 32, CTAS_PER_SM)
 gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_total) {
+  constexpr int NDIG = ND;
+  constexpr int kQBits = 8 * ND - 2;
   constexpr int KTILE = (WT == kI8) ? 32 : 16;
-  constexpr int COLS = (WT == kI8) ? 3 : 2;
+  constexpr int COLS = (WT == kI8) ? NDIG : 2;
   constexpr int XV = (WT == kI8) ? 4 : 2;
   using XVec = typename std::conditional<WT == kI8, float4, float2>::type;
   extern __shared__ __align__(128) uint8_t dyn[];
@@ -255,8 +263,8 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
       if (WT == kI8) {
         int e = 0;
         if (bound > 0.f) frexpf(bound, &e);          // bound < 2^e
-        prm_ds[r] = bound > 0.f ? ldexpf(1.0f, 22 - e) : 0.f;
-        prm_ys[r] = ldexp(1.0, e - 22) * (double)rstd;
+        prm_ds[r] = bound > 0.f ? ldexpf(1.0f, kQBits - e) : 0.f;
+        prm_ys[r] = ldexp(1.0, e - kQBits) * (double)rstd;
       } else {
         prm_ds[r] = 1.0f;
         prm_ys[r] = (double)rstd / kFix;
@@ -286,9 +294,10 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
     if (brow[nt] >= Rn) brow[nt] = 0;   // unused column: computed, never read
     bmu[nt] = ws_->mu[brow[nt]];
     bsc[nt] = ws_->dscale[brow[nt]];
-    // digit dg in {0,1,2}: byte (2-dg) of q + {0x8080, 0x80, 0}
-    bbias[nt] = bsub[nt] == 0 ? 0x8080 : (bsub[nt] == 1 ? 0x80 : 0);
-    const uint32_t b = 2 - bsub[nt];
+    // digit dg: byte (NDIG-1-dg) of q + bias_dg, bias_dg = 0x80 in every byte below it
+    bbias[nt] = 0;
+    for (int j = 0; j < NDIG - 1 - bsub[nt]; ++j) bbias[nt] |= 0x80 << (8 * j);
+    const uint32_t b = NDIG - 1 - bsub[nt];
     bsel_lo[nt] = b | ((b + 4) << 4);
   }
   const int t4 = lane & 3;
@@ -420,14 +429,14 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
           long long D = 0;
           if constexpr (WT == kI8) {
 #pragma unroll
-            for (int dg = 0; dg < 3; ++dg) {
-              const int c = 3 * r + dg, nt = c >> 3, cw = c & 7;
+            for (int dg = 0; dg < NDIG; ++dg) {
+              const int c = NDIG * r + dg, nt = c >> 3, cw = c & 7;
               int val = 0;
 #pragma unroll
               for (int q = 0; q < NT; ++q)
                 if (q == nt) val = (cw & 1) ? (int)acc[t][q][1 + 2 * h] : (int)acc[t][q][2 * h];
               val = __shfl_sync(0xffffffffu, val, g8 * 4 + (cw >> 1));
-              D += (long long)val << (16 - 8 * dg);
+              D += (long long)val << (8 * (NDIG - 1 - dg));
             }
           } else {
             const int c = 2 * r, nt = c >> 3, cw = c & 7;
@@ -522,7 +531,7 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
 
 int g_num_sms = 0;
 
-template <int WT, int NT, int NORMT, bool HASG>
+template <int WT, int NT, int NORMT, bool HASG, int ND>
 void launch_cfg(const GemvArgs& a, int r0, int rn, cudaStream_t st) {
   const int KTILE = (WT == kI8) ? 32 : 16;
   const int64_t units = (a.N / 128) * (a.K / KTILE);
@@ -531,7 +540,7 @@ void launch_cfg(const GemvArgs& a, int r0, int rn, cudaStream_t st) {
   static bool set[kMaxDevices] = {};
   const int dv = current_device();
   if (!set[dv]) {
-    cudaFuncSetAttribute(gemv3_kernel<WT, NT, NORMT, HASG>,
+    cudaFuncSetAttribute(gemv3_kernel<WT, NT, NORMT, HASG, ND>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     set[dv] = true;
   }
@@ -550,7 +559,7 @@ void launch_cfg(const GemvArgs& a, int r0, int rn, cudaStream_t st) {
     cudaMemsetAsync(tbuf, 0, tn * 8, st);
     b.trace = tbuf;
   }
-  launch_pdl(gemv3_kernel<WT, NT, NORMT, HASG>, dim3(grid), dim3(NW * 32), smem, st, b, r0, rn,
+  launch_pdl(gemv3_kernel<WT, NT, NORMT, HASG, ND>, dim3(grid), dim3(NW * 32), smem, st, b, r0, rn,
              a.R, units, (int64_t)grid * NW);
   count_launch();
   if (tr) {
@@ -571,24 +580,24 @@ void launch_cfg(const GemvArgs& a, int r0, int rn, cudaStream_t st) {
   }
 }
 
-template <int WT, int NT>
+template <int WT, int NT, int ND>
 void launch_nt(const GemvArgs& a, int r0, int rn, cudaStream_t st) {
   const bool hg = a.g != nullptr;
   switch (a.norm) {
-    case NORM_RMS: hg ? launch_cfg<WT, NT, NORM_RMS, true>(a, r0, rn, st)
-                      : launch_cfg<WT, NT, NORM_RMS, false>(a, r0, rn, st); break;
-    case NORM_LN: hg ? launch_cfg<WT, NT, NORM_LN, true>(a, r0, rn, st)
-                     : launch_cfg<WT, NT, NORM_LN, false>(a, r0, rn, st); break;
-    default: launch_cfg<WT, NT, NORM_NONE, false>(a, r0, rn, st); break;
+    case NORM_RMS: hg ? launch_cfg<WT, NT, NORM_RMS, true, ND>(a, r0, rn, st)
+                      : launch_cfg<WT, NT, NORM_RMS, false, ND>(a, r0, rn, st); break;
+    case NORM_LN: hg ? launch_cfg<WT, NT, NORM_LN, true, ND>(a, r0, rn, st)
+                     : launch_cfg<WT, NT, NORM_LN, false, ND>(a, r0, rn, st); break;
+    default: launch_cfg<WT, NT, NORM_NONE, false, ND>(a, r0, rn, st); break;
   }
 }
 
-template <int WT>
+template <int WT, int ND>
 void launch_wt(const GemvArgs& a, int r0, int rn, cudaStream_t st) {
-  const int cols = rn * ((WT == kI8) ? 3 : 2);
-  if (cols <= 8) launch_nt<WT, 1>(a, r0, rn, st);
-  else if (cols <= 16) launch_nt<WT, 2>(a, r0, rn, st);
-  else launch_nt<WT, 3>(a, r0, rn, st);
+  const int cols = rn * ((WT == kI8) ? ND : 2);
+  if (cols <= 8) launch_nt<WT, 1, ND>(a, r0, rn, st);
+  else if (cols <= 16) launch_nt<WT, 2, ND>(a, r0, rn, st);
+  else launch_nt<WT, 3, ND>(a, r0, rn, st);
 }
 
 }  // namespace
@@ -604,8 +613,18 @@ void launch_gemv3(int wdtype, const GemvArgs& a, cudaStream_t st) {
   }
   for (int r0 = 0; r0 < a.R; r0 += RMAX) {
     const int rn = a.R - r0 < RMAX ? a.R - r0 : RMAX;
-    if (wdtype == kI8) launch_wt<kI8>(a, r0, rn, st);
-    else launch_wt<kBF16>(a, r0, rn, st);
+    // activation code width: 23 bits (3 digits) when the rows fit one MMA
+    // column tile anyway (1-2 rows), 15 bits (2 digits, the prefill planes'
+    // class) for 3-8 rows, where it halves the column tiles (measured: 3 digits
+    // +4 % at batch 1, 2 digits +55 % at batch 4).  SP_GEMV_NDIG overrides.
+    static int nd_env = getenv("SP_GEMV_NDIG") ? atoi(getenv("SP_GEMV_NDIG")) : 0;
+    const int nd = nd_env ? nd_env : (rn <= 2 ? 3 : kNDig);
+    if (wdtype == kI8) {
+      if (nd == 3) launch_wt<kI8, 3>(a, r0, rn, st);
+      else launch_wt<kI8, 2>(a, r0, rn, st);
+    } else {
+      launch_wt<kBF16, 2>(a, r0, rn, st);
+    }
   }
 }
 

@@ -21,24 +21,26 @@ from . import _lib
 
 class SpanPipeline:
     def __init__(self, engine, start: int, end: int, caches: list, rank: int, world: int, d: int,
-                 device: torch.device, seed: int = 7):
+                 device: torch.device, seed: int = 7, width: int = 1):
         self.eng, self.lib = engine, getattr(engine, "lib", None)
         self.start, self.end = start, end
         self.caches = caches
         self.rank, self.world, self.d = rank, world, d
         self.dev = device
         self.k = 0
-        n_sc = (d + 63) // 64
+        self.width = w = width                    # rows per session per tick (batch / beams)
+        n = w * d
+        n_sc = (n + 63) // 64
         g = torch.Generator(device=device).manual_seed(seed + rank)
-        self.init_rows = torch.randn(max(1, world), 1, d, device=device, generator=g)
-        self.y = torch.empty(1, d, device=device)
-        self.ring_in = torch.empty(1, d, device=device)            # rank 0: from the last rank
-        self.out_wire = torch.empty(d + 4 * n_sc, dtype=torch.uint8, device=device)
-        self.in_wire = torch.empty(d + 4 * n_sc, dtype=torch.uint8, device=device)
-        self.out_codes = self.out_wire[:d].view(torch.int8)
-        self.out_scales = self.out_wire[d:].view(torch.float32)
-        self.in_codes = self.in_wire[:d].view(torch.int8)
-        self.in_scales = self.in_wire[d:].view(torch.float32)
+        self.init_rows = torch.randn(max(1, world), w, d, device=device, generator=g)
+        self.y = torch.empty(w, d, device=device)
+        self.ring_in = torch.empty(w, d, device=device)            # rank 0: from the last rank
+        self.out_wire = torch.empty(n + 4 * n_sc, dtype=torch.uint8, device=device)
+        self.in_wire = torch.empty(n + 4 * n_sc, dtype=torch.uint8, device=device)
+        self.out_codes = self.out_wire[:n].view(torch.int8)
+        self.out_scales = self.out_wire[n:].view(torch.float32)
+        self.in_codes = self.in_wire[:n].view(torch.int8)
+        self.in_scales = self.in_wire[n:].view(torch.float32)
         if world == 1:
             self.y.copy_(self.init_rows[0])
 
@@ -53,7 +55,7 @@ class SpanPipeline:
             self.in_codes.data_ptr() if coded_input else 0,
             self.in_scales.data_ptr() if coded_input else 0, self.y.data_ptr(),
             self.out_codes.data_ptr() if quantize_out else 0,
-            self.out_scales.data_ptr() if quantize_out else 0, 1, 1, st))
+            self.out_scales.data_ptr() if quantize_out else 0, self.width, 1, st))
 
     def step(self) -> None:
         k, r, N = self.k, self.rank, self.world
@@ -102,8 +104,9 @@ class SpanPipeline:
             if r == 0:
                 blob = HiddenBlob.from_array(host_rows[s])
             else:
-                blob = HiddenBlob(1, self.d, dev_codes=self.in_codes, dev_scales=self.in_scales)
-            out = self.eng.run_cached(self.start, self.end, self.caches[s], blob, 1, 1,
+                blob = HiddenBlob(self.width, self.d, dev_codes=self.in_codes,
+                                  dev_scales=self.in_scales)
+            out = self.eng.run_cached(self.start, self.end, self.caches[s], blob, self.width, 1,
                                       not last)
             if last:
                 self.host_out = out.array()               # the step's result on the host
