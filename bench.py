@@ -430,6 +430,8 @@ def run_b200(args) -> None:
         # from the committed ncu --set full capture of one block's 4 GEMVs
         traffic, traffic_src = None, None
         try:
+            if args.config != "llama2-70b" or args.batch != 1:
+                raise ValueError("the committed capture is of the 70B batch-1 GEMVs")
             tj = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)),
                                              "profiles", "gemv_traffic.json")))
             traffic, traffic_src = tj["dram_bytes_per_launch"], tj["source"]
