@@ -26,6 +26,8 @@
 
 namespace sp {
 
+extern int g_attn_nsub;   // sp_span_set_option(.., 5, n): forced sub-chunks per CTA (0 = auto)
+
 namespace {
 
 constexpr int NTH = 128;
@@ -61,7 +63,7 @@ __device__ __forceinline__ float rope_val(const float* x, int dd, int half, cons
 template <int HD, bool LOG2>
 __device__ void merge_tail(const AttnDecArgs& a, int G, int slot, int kh, int chunk, int nchunk,
                            int T, const float (*wm)[GMAX], const float (*wl)[GMAX], float* wo,
-                           float* pm, float* pl, int* last_flag) {
+                           float* pm, float* pl, int* last_flag, int CH = CHUNK) {
   __shared__ float wf[4][GMAX];        // per (warp, head) rescale factors
   __shared__ float hM[GMAX], hL[GMAX];
   // ---- merge the 4 warps (fixed order) -> chunk partial ----
@@ -69,10 +71,10 @@ __device__ void merge_tail(const AttnDecArgs& a, int G, int slot, int kh, int ch
     const int g = threadIdx.x;
     float M = -INFINITY;
     for (int w = 0; w < 4; ++w)
-      if (chunk * CHUNK + w * 32 < T) M = fmaxf(M, wm[w][g]);
+      if (chunk * CH + w * 32 < T) M = fmaxf(M, wm[w][g]);
     float L = 0.f;
     for (int w = 0; w < 4; ++w) {
-      const float f = (chunk * CHUNK + w * 32 < T) ? (LOG2 ? exp2f(wm[w][g] - M) : expf(wm[w][g] - M))
+      const float f = (chunk * CH + w * 32 < T) ? (LOG2 ? exp2f(wm[w][g] - M) : expf(wm[w][g] - M))
                                                    : 0.f;  // empty warp: 0
       wf[w][g] = f;
       L = fmaf(wl[w][g] * (f > 0.f ? 1.f : 0.f), f, L);
@@ -431,17 +433,24 @@ __global__ void __launch_bounds__(NTH) attn_dec_mma_kernel(AttnDecArgs a) {
   extern __shared__ __align__(16) float dsm[];
   const int G = a.H / a.kvh;
   typedef __nv_bfloat16 Row[RS];
-  Row* Kt = reinterpret_cast<Row*>(dsm);          // [4*32][RS]
-  Row* Vt = Kt + 4 * 32;                          // [4*32][RS]
-  float* wo = reinterpret_cast<float*>(Vt + 4 * 32);   // [4][G][HD]
+  // K/V of a 128-position sub-chunk, double-buffered: [2][4*32][RS] each.  A
+  // CTA streams a.nsub sub-chunks (MHA shapes: many kv heads, few positions per
+  // CTA otherwise) with a running online softmax per warp
+  Row* Kbuf = reinterpret_cast<Row*>(dsm);
+  Row* Vbuf = Kbuf + 2 * 4 * 32;
+  float* wo = reinterpret_cast<float*>(Vbuf + 2 * 4 * 32);   // [4][G][HD]
   float* pmv = wo + 4 * G * HD;
   float* plv = pmv + a.max_pages * GMAX;
 
   const int slot = blockIdx.x / a.kvh, kh = blockIdx.x % a.kvh;
   const int chunk = blockIdx.y;
   const int T = a.t0 + 1;
-  const int nchunk = (T + CHUNK - 1) / CHUNK;
+  const int nsub = a.nsub > 0 ? a.nsub : 1;
+  const int CH = CHUNK * nsub;                    // positions per CTA
+  const int nchunk = (T + CH - 1) / CH;
   if (chunk >= nchunk) return;
+  const int base = chunk * CH;
+  const int nsub_here = min(nsub, (T - base + CHUNK - 1) / CHUNK);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g8 = lane >> 2, t4 = lane & 3;
   const int half = HD / 2;
@@ -449,24 +458,28 @@ __global__ void __launch_bounds__(NTH) attn_dec_mma_kernel(AttnDecArgs a) {
   const float* cs = a.rope_cos ? a.rope_cos + (int64_t)a.t0 * half : nullptr;
   const float* sn = a.rope_sin ? a.rope_sin + (int64_t)a.t0 * half : nullptr;
 
-  // ---- 1. stage this warp's 32 K/V rows first (cp.async, zero-fill past T):
-  // the loads do not depend on q, so their latency overlaps everything below.
-  // Row t0 is read stale here and patched in smem after the append ----
-  const int p0 = chunk * CHUNK + warp * 32;
-  const int nv = max(0, min(32, T - p0));
-  {
-    const int page = a.page_table[slot * a.max_pages + min(p0, T - 1) / kPageTokens];
-    const __nv_bfloat16* kbase = page_ptr<__nv_bfloat16>(a.kv_pool, page, 0, a.kvh, kh, HD) + (p0 % kPageTokens) * HD;
-    const __nv_bfloat16* vbase = page_ptr<__nv_bfloat16>(a.kv_pool, page, 1, a.kvh, kh, HD) + (p0 % kPageTokens) * HD;
-    constexpr int CPR = HD / 8;                   // 16-byte chunks per row
+  // ---- 1. stage this warp's 32 K/V rows of sub-chunk j (cp.async, zero-fill
+  // past T) into buffer j & 1; sub-chunk 0 is issued first of all: the loads do
+  // not depend on q, so their latency overlaps everything below.  Row t0 is
+  // read stale and patched in smem after the append ----
+  constexpr int CPR = HD / 8;                     // 16-byte chunks per row
+  auto stage = [&](int j) {
+    const int q0 = base + j * CHUNK + warp * 32;
+    const int nvj = max(0, min(32, T - q0));
+    const int page = a.page_table[slot * a.max_pages + min(q0, T - 1) / kPageTokens];
+    const __nv_bfloat16* kbase = page_ptr<__nv_bfloat16>(a.kv_pool, page, 0, a.kvh, kh, HD) + (q0 % kPageTokens) * HD;
+    const __nv_bfloat16* vbase = page_ptr<__nv_bfloat16>(a.kv_pool, page, 1, a.kvh, kh, HD) + (q0 % kPageTokens) * HD;
+    Row* Kt = Kbuf + (j & 1) * 128;
+    Row* Vt = Vbuf + (j & 1) * 128;
     for (int c = lane; c < 32 * CPR; c += 32) {
-      const int j = c / CPR, e = (c % CPR) * 8;
-      const bool ok = j < nv;
-      cp_async16(&Kt[warp * 32 + j][e], kbase + (ok ? j : 0) * HD + e, ok);
-      cp_async16(&Vt[warp * 32 + j][e], vbase + (ok ? j : 0) * HD + e, ok);
+      const int r = c / CPR, e = (c % CPR) * 8;
+      const bool ok = r < nvj;
+      cp_async16(&Kt[warp * 32 + r][e], kbase + (ok ? r : 0) * HD + e, ok);
+      cp_async16(&Vt[warp * 32 + r][e], vbase + (ok ? r : 0) * HD + e, ok);
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
-  }
+  };
+  stage(0);
   // L2 prefetch of the next kernel's weights: this CTA's share, in 64 KB
   // bulk prefetches (cp.async.bulk.prefetch.L2) issued by one thread
   if (a.l2_prefetch && threadIdx.x == 32) {
@@ -519,7 +532,8 @@ __global__ void __launch_bounds__(NTH) attn_dec_mma_kernel(AttnDecArgs a) {
     }
   }
   // ---- 3. append the new position (KVCache.append, SP/model.py:163-167) ----
-  const bool appender = (a.t0 / CHUNK == chunk);
+  const bool appender = (a.t0 / CH == chunk);
+  const int app_sub = (a.t0 - base) / CHUNK;       // the appender's sub-chunk holding t0
   __nv_bfloat16 knew[HD / NTH > 0 ? HD / NTH : 1], vnew[HD / NTH > 0 ? HD / NTH : 1];
   if (appender) {
     const int page = a.page_table[slot * a.max_pages + a.t0 / kPageTokens];
@@ -538,77 +552,118 @@ __global__ void __launch_bounds__(NTH) attn_dec_mma_kernel(AttnDecArgs a) {
       }
     }
   }
-  asm volatile("cp.async.wait_group 0;" ::: "memory");
-  __syncthreads();
-  trace_mark(a, 2);
-  if (appender) {
-    const int r = a.t0 - chunk * CHUNK;
+  const float qscale = kLog2e / sqrtf((float)HD);
+  const int jrow = (lane & 7) + ((lane >> 4) << 3);      // ldmatrix.trans source row (pos)
+  const int dcol = ((lane >> 3) & 1) * 8;                // +8 dims for matrices 1 and 3
+  float m2[2] = {-INFINITY, -INFINITY}, l2[2] = {0.f, 0.f};
+  float oacc[HD / 16][4];
 #pragma unroll
-    for (int u = 0; u * NTH < HD; ++u) {
-      const int dd = threadIdx.x + u * NTH;
-      if (dd < HD) { Kt[r][dd] = knew[u]; Vt[r][dd] = vnew[u]; }
+  for (int mt = 0; mt < HD / 16; ++mt) oacc[mt][0] = oacc[mt][1] = oacc[mt][2] = oacc[mt][3] = 0.f;
+
+  for (int js = 0; js < nsub_here; ++js) {
+    if (js + 1 < nsub_here) {
+      stage(js + 1);                              // next sub-chunk streams under this one
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
     __syncthreads();
-  }
-
-  // ---- S[32 x 8] = K . q^T ----
-  float sacc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+    if (js == 0) trace_mark(a, 2);
+    Row* Kt = Kbuf + (js & 1) * 128;
+    Row* Vt = Vbuf + (js & 1) * 128;
+    if (appender && js == app_sub) {
+      const int r = a.t0 - base - js * CHUNK;
 #pragma unroll
-  for (int ks = 0; ks < HD / 16; ++ks) {
-    const uint32_t bh0 = *reinterpret_cast<const uint32_t*>(&qh[g8][ks * 16 + 2 * t4]);
-    const uint32_t bh1 = *reinterpret_cast<const uint32_t*>(&qh[g8][ks * 16 + 2 * t4 + 8]);
-    const uint32_t bl0 = *reinterpret_cast<const uint32_t*>(&ql[g8][ks * 16 + 2 * t4]);
-    const uint32_t bl1 = *reinterpret_cast<const uint32_t*>(&ql[g8][ks * 16 + 2 * t4 + 8]);
-#pragma unroll
-    for (int mt = 0; mt < 2; ++mt) {
-      uint32_t af[4];
-      ldsm_x4(af, &Kt[warp * 32 + mt * 16 + (lane & 15)][ks * 16 + (lane >> 4) * 8]);
-      mma_bf16_16816(sacc[mt], af[0], af[1], af[2], af[3], bh0, bh1);
-      mma_bf16_16816(sacc[mt], af[0], af[1], af[2], af[3], bl0, bl1);
+      for (int u = 0; u * NTH < HD; ++u) {
+        const int dd = threadIdx.x + u * NTH;
+        if (dd < HD) { Kt[r][dd] = knew[u]; Vt[r][dd] = vnew[u]; }
+      }
+      __syncthreads();
     }
-  }
-  trace_mark(a, 8);
-  // ---- softmax per head over the warp's 32 positions ----
-  // lane holds S[pos mt*16 + g8 (+8)][head 2*t4 + {0,1}]
-  const float qscale = kLog2e / sqrtf((float)HD);
-  float m2[2], l2[2];
+    const int p0 = base + js * CHUNK + warp * 32;
+    const int nv = max(0, min(32, T - p0));
+
+    // ---- S[32 x 8] = K . q^T ----
+    float sacc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
 #pragma unroll
-  for (int hc = 0; hc < 2; ++hc) {
-    const int head = 2 * t4 + hc;
-    float mx = -INFINITY;
+    for (int ks = 0; ks < HD / 16; ++ks) {
+      const uint32_t bh0 = *reinterpret_cast<const uint32_t*>(&qh[g8][ks * 16 + 2 * t4]);
+      const uint32_t bh1 = *reinterpret_cast<const uint32_t*>(&qh[g8][ks * 16 + 2 * t4 + 8]);
+      const uint32_t bl0 = *reinterpret_cast<const uint32_t*>(&ql[g8][ks * 16 + 2 * t4]);
+      const uint32_t bl1 = *reinterpret_cast<const uint32_t*>(&ql[g8][ks * 16 + 2 * t4 + 8]);
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        const int pos = mt * 16 + g8 + hh * 8;
-        // log2 domain: one multiply folds 1/sqrt(hd) and log2(e); exp2 below
-        float v = sacc[mt][hh * 2 + hc] * qscale;
-        if (a.family == kBloom && head < G)
-          v = fmaf(a.alibi[kh * G + head] * kLog2e, (float)(p0 + pos - (T - 1)), v);
-        if (pos >= nv) v = -INFINITY;
-        sacc[mt][hh * 2 + hc] = v;
-        mx = fmaxf(mx, v);
+      for (int mt = 0; mt < 2; ++mt) {
+        uint32_t af[4];
+        ldsm_x4(af, &Kt[warp * 32 + mt * 16 + (lane & 15)][ks * 16 + (lane >> 4) * 8]);
+        mma_bf16_16816(sacc[mt], af[0], af[1], af[2], af[3], bh0, bh1);
+        mma_bf16_16816(sacc[mt], af[0], af[1], af[2], af[3], bl0, bl1);
       }
-    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
-    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
-    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
-    float sum = 0.f;
+    }
+    if (js == 0) trace_mark(a, 8);
+    // ---- online softmax per head over the warp's 32 positions ----
+    // lane holds S[pos mt*16 + g8 (+8)][head 2*t4 + {0,1}]
+    float alpha[2];
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
+    for (int hc = 0; hc < 2; ++hc) {
+      const int head = 2 * t4 + hc;
+      float mx = -INFINITY;
 #pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        const int pos = mt * 16 + g8 + hh * 8;
-        const float e = (pos < nv) ? exp2f(sacc[mt][hh * 2 + hc] - mx) : 0.f;
-        sum += e;
-        const __nv_bfloat16 h = __float2bfloat16_rn(e);
-        ph[warp][head][pos] = h;
-        pl_[warp][head][pos] = __float2bfloat16_rn(e - __bfloat162float(h));
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const int pos = mt * 16 + g8 + hh * 8;
+          // log2 domain: one multiply folds 1/sqrt(hd) and log2(e); exp2 below
+          float v = sacc[mt][hh * 2 + hc] * qscale;
+          if (a.family == kBloom && head < G)
+            v = fmaf(a.alibi[kh * G + head] * kLog2e, (float)(p0 + pos - (T - 1)), v);
+          if (pos >= nv) v = -INFINITY;
+          sacc[mt][hh * 2 + hc] = v;
+          mx = fmaxf(mx, v);
+        }
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+      const float mnew = fmaxf(m2[hc], mx);
+      alpha[hc] = (m2[hc] == -INFINITY) ? 0.f : exp2f(m2[hc] - mnew);
+      float sum = 0.f;
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const int pos = mt * 16 + g8 + hh * 8;
+          const float e = (pos < nv) ? exp2f(sacc[mt][hh * 2 + hc] - mnew) : 0.f;
+          sum += e;
+          const __nv_bfloat16 h = __float2bfloat16_rn(e);
+          ph[warp][head][pos] = h;
+          pl_[warp][head][pos] = __float2bfloat16_rn(e - __bfloat162float(h));
+        }
+      sum += __shfl_xor_sync(0xffffffffu, sum, 4);
+      sum += __shfl_xor_sync(0xffffffffu, sum, 8);
+      sum += __shfl_xor_sync(0xffffffffu, sum, 16);
+      m2[hc] = mnew;
+      l2[hc] = l2[hc] * alpha[hc] + sum;
+    }
+    __syncwarp();
+    if (js == 0) trace_mark(a, 9);
+    // ---- O^T[HD x 8] = alpha * O^T + V^T . P ----
+#pragma unroll
+    for (int mt = 0; mt < HD / 16; ++mt) {
+      // oacc columns: head 2*t4 + (j & 1)
+      oacc[mt][0] *= alpha[0]; oacc[mt][1] *= alpha[1];
+      oacc[mt][2] *= alpha[0]; oacc[mt][3] *= alpha[1];
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks) {
+        uint32_t af[4];
+        ldsm_x4_t(af, &Vt[warp * 32 + ks * 16 + jrow][mt * 16 + dcol]);
+        const uint32_t bh0 = *reinterpret_cast<const uint32_t*>(&ph[warp][g8][ks * 16 + 2 * t4]);
+        const uint32_t bh1 = *reinterpret_cast<const uint32_t*>(&ph[warp][g8][ks * 16 + 2 * t4 + 8]);
+        const uint32_t bl0 = *reinterpret_cast<const uint32_t*>(&pl_[warp][g8][ks * 16 + 2 * t4]);
+        const uint32_t bl1 = *reinterpret_cast<const uint32_t*>(&pl_[warp][g8][ks * 16 + 2 * t4 + 8]);
+        mma_bf16_16816(oacc[mt], af[0], af[1], af[2], af[3], bh0, bh1);
+        mma_bf16_16816(oacc[mt], af[0], af[1], af[2], af[3], bl0, bl1);
       }
-    sum += __shfl_xor_sync(0xffffffffu, sum, 4);
-    sum += __shfl_xor_sync(0xffffffffu, sum, 8);
-    sum += __shfl_xor_sync(0xffffffffu, sum, 16);
-    m2[hc] = mx;
-    l2[hc] = sum;
+    }
+    __syncthreads();                              // buffer js & 1 is refilled next
   }
   if (g8 == 0) {
 #pragma unroll
@@ -617,47 +672,37 @@ __global__ void __launch_bounds__(NTH) attn_dec_mma_kernel(AttnDecArgs a) {
       if (head < G) { wm[warp][head] = m2[hc]; wl[warp][head] = l2[hc]; }
     }
   }
-  __syncwarp();
-
-  trace_mark(a, 9);
-  // ---- O^T[HD x 8] = V^T . P ----
-  const int jrow = (lane & 7) + ((lane >> 4) << 3);      // ldmatrix.trans source row (pos)
-  const int dcol = ((lane >> 3) & 1) * 8;                // +8 dims for matrices 1 and 3
+  // oacc: O^T[dim mt*16 + g8 (+8)][head 2*t4 + {0,1}]
 #pragma unroll
-  for (int mt = 0; mt < HD / 16; ++mt) {
-    float oacc[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-    for (int ks = 0; ks < 2; ++ks) {
-      uint32_t af[4];
-      ldsm_x4_t(af, &Vt[warp * 32 + ks * 16 + jrow][mt * 16 + dcol]);
-      const uint32_t bh0 = *reinterpret_cast<const uint32_t*>(&ph[warp][g8][ks * 16 + 2 * t4]);
-      const uint32_t bh1 = *reinterpret_cast<const uint32_t*>(&ph[warp][g8][ks * 16 + 2 * t4 + 8]);
-      const uint32_t bl0 = *reinterpret_cast<const uint32_t*>(&pl_[warp][g8][ks * 16 + 2 * t4]);
-      const uint32_t bl1 = *reinterpret_cast<const uint32_t*>(&pl_[warp][g8][ks * 16 + 2 * t4 + 8]);
-      mma_bf16_16816(oacc, af[0], af[1], af[2], af[3], bh0, bh1);
-      mma_bf16_16816(oacc, af[0], af[1], af[2], af[3], bl0, bl1);
-    }
-    // oacc: O^T[dim mt*16 + g8 (+8)][head 2*t4 + {0,1}]
+  for (int mt = 0; mt < HD / 16; ++mt)
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int head = 2 * t4 + (j & 1);
       const int dim = mt * 16 + g8 + ((j >> 1) << 3);
-      if (head < G) wo[(warp * G + head) * HD + dim] = oacc[j];
+      if (head < G) wo[(warp * G + head) * HD + dim] = oacc[mt][j];
     }
-  }
   trace_mark(a, 10);
   __syncthreads();
   trace_mark(a, 3);
-  merge_tail<HD, true>(a, G, slot, kh, chunk, nchunk, T, wm, wl, wo, pmv, plv, &last_flag);
+  merge_tail<HD, true>(a, G, slot, kh, chunk, nchunk, T, wm, wl, wo, pmv, plv, &last_flag, CH);
   trace_mark(a, 7);
 }
 
 template <int HD>
-void launch_mma(const AttnDecArgs& a, cudaStream_t st) {
+void launch_mma(const AttnDecArgs& a_in, cudaStream_t st) {
+  AttnDecArgs a = a_in;
   const int T = a.t0 + 1;
-  dim3 grid(a.width * a.kvh, (T + CHUNK - 1) / CHUNK);
+  // sub-chunks per CTA: one (136 CTAs for 70B GQA at 2 K positions) unless the
+  // grid would exceed ~2 CTAs per SM (MHA: 112 kv heads x 17 chunks for BLOOM)
+  const int64_t n128 = (int64_t)a.width * a.kvh * ((T + CHUNK - 1) / CHUNK);
+  static int num_sms = 0;
+  if (!num_sms) cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, current_device());
+  int nsub = g_attn_nsub > 0 ? g_attn_nsub : (int)((n128 + 2 * num_sms - 1) / (2 * num_sms));
+  nsub = nsub < 1 ? 1 : (nsub > 32 ? 32 : nsub);
+  a.nsub = nsub;
+  dim3 grid(a.width * a.kvh, (T + CHUNK * nsub - 1) / (CHUNK * nsub));
   const int G = a.H / a.kvh;
-  const size_t smem = (size_t)2 * 4 * 32 * (HD + 8) * 2 +
+  const size_t smem = (size_t)2 * 2 * 4 * 32 * (HD + 8) * 2 +
                       (size_t)(4 * G * HD + 2 * a.max_pages * GMAX) * sizeof(float);
   static size_t set[kMaxDevices] = {};
   const int dv = current_device();
@@ -733,6 +778,8 @@ void dispatch(const AttnDecArgs& a, cudaStream_t st) {
 }
 
 }  // namespace
+
+int g_attn_nsub = 0;
 
 int64_t attn_dec_part_floats(int width, int H, int hd, int max_pages) {
   return (int64_t)width * H * max_pages * (hd + 2);

@@ -69,6 +69,7 @@ struct AttnDecArgs {
   int* counters;                 // [width*kvh] (zero at rest)
   RowStat* st_out;               // [H][width] partial stats of ctx (P = H)
   unsigned long long* trace;     // debug (SP_ATTN_TRACE): per-CTA phase timestamps, or null
+  int nsub;                      // 128-position sub-chunks streamed per CTA (MMA kernel; 0 = 1)
   const void* l2_prefetch;       // next kernel's weights to pull into L2 (or null)
   int64_t l2_prefetch_bytes;
 };

@@ -638,8 +638,9 @@ bool g_tc_pair = true;
 void launch_digitize(const float* x, int64_t ldx, int64_t M, int64_t K, int norm, const float* g,
                      const float* b, uint8_t* planes, int64_t plane_stride, int* exps,
                      cudaStream_t st) {
-  const int64_t Mp = tc_rows(M);
-  const unsigned grid = (unsigned)Mp;
+  // padding rows of the planes are never written: a tile's rows are
+  // independent in the MMA and the GEMM epilogue drops rows >= M
+  const unsigned grid = (unsigned)M;
   const bool al = (K % 16 == 0) && (ldx % 4 == 0);
   if (al && K <= 256 * 16 * 2)
     digitize_reg_kernel<256, 2><<<grid, 256, 0, st>>>(x, ldx, M, K, norm, g, b, planes, plane_stride, exps);
@@ -693,7 +694,9 @@ void launch_pair(const TcGemmArgs& a, cudaStream_t st) {
 }
 
 void launch_gemm_i8_tc(const TcGemmArgs& a, cudaStream_t st) {
-  if (g_tc_pair) {
+  // up to 128 tokens (wide decode, short prompts): one 128-token tile per CTA
+  // does half the padded MMA work of a 256-token pair tile
+  if (g_tc_pair && a.M > 128) {
     static int cfg = getenv("SP_TC_CFG") ? atoi(getenv("SP_TC_CFG")) : 0;
     if (cfg == 1) launch_pair<2, 8>(a, st);
     else launch_pair<4, 4>(a, st);

@@ -38,6 +38,7 @@ void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 bool g_pdl = true;
 extern bool g_attn_hilo;   // attn_prefill.cu
 bool g_attn_l2pf = false;  // option 4 (measured: slower, off)
+extern int g_attn_nsub;    // attn_decode.cu, option 5
 }  // namespace sp
 
 using namespace sp;
@@ -506,8 +507,70 @@ int run_span_prefill_tc(sp_span* s, sp_kv* kv, int b0, int b1, float* y, float* 
   return SP_OK;
 }
 
+// Wide decode (n_new == 1, width >= kWideDecode rows, int8): the linears run
+// on the tcgen05 GEMM (one pass over the weights for all rows, 15-bit digit
+// planes) instead of the GEMV, whose per-unit digit/MMA work makes it
+// latency-bound beyond a few rows; attention stays the fused decode kernel.
+constexpr int kWideDecode = 8;
+
+int run_span_decode_wide(sp_span* s, sp_kv* kv, int b0, int b1, float* y, int width,
+                         cudaStream_t st) {
+  const int64_t R = width;
+  int rc = ensure_scratch(s, R);
+  if (rc) return rc;
+  rc = ensure_decode(s, R);
+  if (rc) return rc;
+  rc = ensure_tc(s, R);
+  if (rc) return rc;
+  const int fam = s->cfg.family;
+  const int norm = fam == kLlama ? 1 : 2;
+  const int64_t d = s->d, F = s->F;
+  const int64_t Mp = tc_rows(R);
+  const double kv_elt = s->cfg.kv_dtype == kKVBF16 ? 2.0 : 4.0;
+  AttnDecArgs at{};
+  at.family = fam; at.kv_dtype = s->cfg.kv_dtype; at.width = width; at.t0 = kv->length;
+  at.H = s->H; at.kvh = s->kvh; at.hd = s->hd; at.qkv = s->qkvb; at.ldqkv = s->n_qkv;
+  at.page_table = kv->d_table; at.max_pages = s->max_pages;
+  at.rope_cos = s->rope_cos; at.rope_sin = s->rope_sin; at.alibi = s->alibi;
+  at.ctx = s->ctx; at.part = s->attn_part; at.counters = s->attn_cnt; at.st_out = nullptr;
+  auto gemm = [&](void* w, float* sc, int64_t N, int64_t K, float* out, int64_t ldy,
+                  const float* res, int epi) {
+    ProfScope ps(s, PC_GEMV, (double)N * K + 4.0 * N + 2.0 * Mp * K + 4.0 * R * ldy,
+                 2.0 * R * N * K, st);
+    TcGemmArgs g{};
+    g.w = w; g.wscale = sc; g.N = N; g.K = K; g.planes = s->planes; g.plane_stride = Mp * K;
+    g.exps = s->exps; g.M = R; g.y = out; g.ldy = ldy; g.res = res; g.epi = epi;
+    launch_gemm_i8_tc(g, st);
+  };
+  auto digit = [&](const float* x, int64_t K, int nm, const float* gg, const float* bb) {
+    ProfScope ps(s, PC_OTHER, 4.0 * R * K + 2.0 * Mp * K, 0, st);
+    launch_digitize(x, K, R, K, nm, gg, bb, s->planes, Mp * K, s->exps, st);
+  };
+  for (int b = b0 - s->start; b < b1 - s->start; ++b) {
+    BlockW& W = s->blocks[b];
+    digit(y, d, norm, W.ln1_g, W.ln1_b);
+    gemm(W.qkv, W.s_qkv, s->n_qkv, d, s->qkvb, s->n_qkv, nullptr, EPI_STORE);
+    at.kv_pool = s->pool + (int64_t)b * s->block_stride;
+    {
+      ProfScope ps(s, PC_ATTN_DEC, (double)width * (kv->length + 1) * 2 * s->kv * kv_elt,
+                   4.0 * width * (kv->length + 1) * s->H * s->hd, st);
+      launch_attn_decode_fused(at, st);
+    }
+    digit(s->ctx, d, 0, nullptr, nullptr);
+    gemm(W.o, W.s_o, d, d, y, d, y, EPI_RESID);
+    digit(y, d, norm, W.ln2_g, W.ln2_b);
+    gemm(W.up, W.s_up, s->n_up, d, s->mlp, F, nullptr, fam == kLlama ? EPI_SWIGLU : EPI_GELU);
+    digit(s->mlp, F, 0, nullptr, nullptr);
+    gemm(W.down, W.s_down, d, F, y, d, y, EPI_RESID);
+  }
+  SP_CHECK_LAUNCH();
+  return SP_OK;
+}
+
 int run_span(sp_span* s, sp_kv* kv, int b0, int b1, float* y, float* record, int width,
              int n_new, cudaStream_t st) {
+  if (n_new == 1 && width >= kWideDecode && tc_ok(s) && s->use_tc_prefill && !record)
+    return run_span_decode_wide(s, kv, b0, b1, y, width, st);
   if (n_new == 1 && s->cfg.weight_dtype != kF32 && !record)
     return run_span_decode_tc(s, kv, b0, b1, y, width, st);
   if (n_new > 1 && tc_ok(s) && s->use_tc_prefill)
@@ -909,6 +972,7 @@ int sp_span_set_option(sp_span* s, int32_t option, int32_t value) {
   else if (option == 2) g_tc_pair = value != 0;
   else if (option == 3) g_attn_hilo = value != 0;
   else if (option == 4) g_attn_l2pf = value != 0;
+  else if (option == 5) g_attn_nsub = value;
   else SP_FAIL(SP_ERR_ARG, "unknown option");
   return SP_OK;
 }

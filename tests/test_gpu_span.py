@@ -291,3 +291,48 @@ def test_extended_families_greedy_tokens_match_oracle(name):
         xc = emb[[tc]]
     assert toks_gpu == toks_cpu
     assert worst <= 1e-2, worst
+
+
+@pytest.mark.parametrize("name,width", [("llama_int8", 8), ("bloom_int8", 16)])
+def test_wide_decode_vs_oracle(name, width):
+    """Decode with >= 8 rows per step runs its linears on the tcgen05 GEMM
+    (one pass over the weights for all rows) and attention on the fused decode
+    kernel; every row vs the oracle at the decode tolerance."""
+    cfg = SMALL[name]
+    eng = _engine(cfg)
+    rng = np.random.default_rng(13)
+    d = cfg.hidden_dim
+    x = rng.standard_normal((width, 40 + 4, d)).astype(np.float32)
+    runner = om.SpanRunner(cfg, 0, cfg.n_blocks, width=width)
+    c = eng.make_caches(0, cfg.n_blocks, width)
+    eng.run_cached(0, cfg.n_blocks, c, _blob(x[:, :40].reshape(-1, d)), width, 40, False)
+    runner.step(x[:, :40])
+    for i in range(40, 44):
+        g = eng.run_cached(0, cfg.n_blocks, c, _blob(x[:, i]), width, 1, False).array()
+        w = runner.step(x[:, i:i + 1])[:, 0]
+        s = np.abs(w).max()
+        assert np.abs(g - w).max() <= 2e-3 * s, (i, np.abs(g - w).max() / s)
+    assert eng.cache_length(c) == 44
+
+
+@pytest.mark.parametrize("name", ["bloom_int8", "llama_int8"])
+def test_decode_attention_streamed_subchunks(name):
+    """Decode attention streaming several 128-position sub-chunks per CTA with
+    a running online softmax (the MHA/BLOOM launch shape) equals the one-sub-
+    chunk-per-CTA launch to f32 rounding, across page and chunk boundaries."""
+    from paper_2312_08361_b200 import _lib
+    cfg = SMALL[name]
+    rng = np.random.default_rng(17)
+    d = cfg.hidden_dim
+    x = rng.standard_normal((2, 300 + 5, d)).astype(np.float32)
+    outs = []
+    for nsub in (1, 3):
+        eng = _engine(cfg)
+        _lib.check(eng.lib.sp_span_set_option(eng.span.handle, 5, nsub))
+        c = eng.make_caches(0, cfg.n_blocks, 2)
+        eng.run_cached(0, cfg.n_blocks, c, _blob(x[:, :300].reshape(-1, d)), 2, 300, False)
+        outs.append([eng.run_cached(0, cfg.n_blocks, c, _blob(x[:, i]), 2, 1, False).array()
+                     for i in range(300, 305)])
+        _lib.check(eng.lib.sp_span_set_option(eng.span.handle, 5, 0))
+    for a, b in zip(*outs):
+        assert np.abs(a - b).max() <= 1e-5 * np.abs(b).max()
