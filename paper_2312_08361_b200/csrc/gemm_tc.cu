@@ -189,6 +189,52 @@ __device__ __forceinline__ void epilogue_group(const TcGemmArgs& a, uint32_t tb,
   }
 }
 
+// split-K, phase 1: this CTA's exact partial D = D0 * 256 + D1 of one weight
+// group for row m, added into the int64 workspace (order-independent => the
+// result is deterministic)
+__device__ __forceinline__ void partial_group(const TcGemmArgs& a, uint32_t tb, int j, int ng0,
+                                              int64_t m, bool valid) {
+  unsigned long long* ws = reinterpret_cast<unsigned long long*>(a.ws) + m * a.N +
+                           (int64_t)(ng0 + j) * 128;
+  for (int c0 = 0; c0 < 128; c0 += 32) {
+    int v0[32], v1[32];
+    tmem_ld32_nw(tb + (uint32_t)(0 * 256 + j * 128 + c0), v0);
+    tmem_ld32_nw(tb + (uint32_t)(1 * 256 + j * 128 + c0), v1);
+    tmem_wait_ld();
+    if (!valid) continue;
+#pragma unroll
+    for (int c = 0; c < 32; ++c)
+      atomicAdd(ws + c0 + c, (unsigned long long)((long long)v0[c] * 256 + v1[c]));
+  }
+}
+
+// split-K, phase 2 (last CTA of the tile): the epilogue of epilogue_group on
+// the summed workspace, which is zeroed for the next use
+__device__ __forceinline__ void finish_group(const TcGemmArgs& a, int j, int ng0, int64_t m,
+                                             float ys) {
+  unsigned long long* ws = reinterpret_cast<unsigned long long*>(a.ws) + m * a.N;
+  const int64_t n0 = (int64_t)(ng0 + j) * 128;
+  const float* wsc = a.wscale + n0;
+  auto D = [&](int c) { return (float)(long long)atomicExch(ws + n0 + c, 0ull); };
+  if (a.epi == EPI_SWIGLU) {
+    float* out = a.y + m * a.ldy + (ng0 + j) * 64;
+    for (int c = 0; c < 64; ++c) {
+      const float gd = D(c) * ys * __ldg(wsc + c);
+      const float ud = D(64 + c) * ys * __ldg(wsc + 64 + c);
+      out[c] = __fdividef(gd, 1.0f + __expf(-gd)) * ud;
+    }
+  } else {
+    float* out = a.y + m * a.ldy + n0;
+    const float* res = a.res ? a.res + m * a.ldy + n0 : nullptr;
+    for (int c = 0; c < 128; ++c) {
+      float v = D(c) * ys * __ldg(wsc + c);
+      if (a.epi == EPI_RESID) v += res[c];
+      else if (a.epi == EPI_GELU) v = gelu_f(v);
+      out[c] = v;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256, 1) gemm_i8_tc_kernel(TcGemmArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], tmem_full;
@@ -200,7 +246,11 @@ __global__ void __launch_bounds__(256, 1) gemm_i8_tc_kernel(TcGemmArgs a) {
   const int ng0 = blockIdx.y * NGRP;         // first weight group of this tile
   const int mt = blockIdx.x;                 // token tile (128 rows)
   const int64_t KT = a.K >> 5;               // 32-byte units along K
-  const int KB = (int)(KT / KU);             // stages along K
+  const int KBT = (int)(KT / KU);            // stages along K
+  const int S = a.ksplit > 1 ? a.ksplit : 1; // K split (blockIdx.z = part)
+  const int kb0 = (int)((int64_t)blockIdx.z * KBT / S), kb1 = (int)((int64_t)(blockIdx.z + 1) * KBT / S);
+  const int KB = kb1 - kb0;                  // stages of this CTA
+  __shared__ int last_cta;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
@@ -228,11 +278,11 @@ __global__ void __launch_bounds__(256, 1) gemm_i8_tc_kernel(TcGemmArgs a) {
       if (kb >= STAGES) mbar_wait(&empty[s], ((kb / STAGES) - 1) & 1);
       uint8_t* st = smem + (size_t)s * STAGE;
       mbar_expect_tx(&full[s], STAGE);
-      const int64_t ua = ((int64_t)mt * KT + (int64_t)kb * KU) * UNIT;
+      const int64_t ua = ((int64_t)mt * KT + (int64_t)(kb0 + kb) * KU) * UNIT;
       tma_load_1d(st, pa0 + ua, KU * UNIT, &full[s]);
       tma_load_1d(st + KU * UNIT, pa1 + ua, KU * UNIT, &full[s]);
       for (int j = 0; j < NGRP; ++j) {
-        const int64_t ub = ((int64_t)(ng0 + j) * KT + (int64_t)kb * KU) * UNIT;
+        const int64_t ub = ((int64_t)(ng0 + j) * KT + (int64_t)(kb0 + kb) * KU) * UNIT;
         tma_load_1d(st + A_BYTES + j * KU * UNIT, wb + ub, KU * UNIT, &full[s]);
       }
     }
@@ -266,9 +316,32 @@ __global__ void __launch_bounds__(256, 1) gemm_i8_tc_kernel(TcGemmArgs a) {
     mbar_wait(&tmem_full, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const bool valid = m < a.M;
-    const float ys = valid ? ldexpf(1.0f, a.exps[m] - 14) : 0.f;
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
-    for (int j = 0; j < NGRP; ++j) epilogue_group(a, tbase + lane_addr, j, ng0, m, valid, ys);
+    if (S == 1) {
+      const float ys = valid ? ldexpf(1.0f, a.exps[m] - 14) : 0.f;
+      for (int j = 0; j < NGRP; ++j) epilogue_group(a, tbase + lane_addr, j, ng0, m, valid, ys);
+    } else {
+      for (int j = 0; j < NGRP; ++j) partial_group(a, tbase + lane_addr, j, ng0, m, valid);
+      __threadfence();
+    }
+  }
+  if (S > 1) {
+    // split-K: the last CTA of this output tile applies the epilogue
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int* cnt = a.counters + (int64_t)mt * gridDim.y + blockIdx.y;
+      const int old = atomicAdd(cnt, 1);
+      last_cta = (old == S - 1);
+      if (last_cta) { __threadfence(); *cnt = 0; }
+    }
+    __syncthreads();
+    if (last_cta && warp >= 4) {
+      const int64_t m = (int64_t)mt * BM + (warp - 4) * 32 + lane;
+      if (m < a.M) {
+        const float ys = ldexpf(1.0f, a.exps[m] - 14);
+        for (int j = 0; j < NGRP; ++j) finish_group(a, j, ng0, m, ys);
+      }
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -710,8 +783,18 @@ void launch_gemm_i8_tc(const TcGemmArgs& a, cudaStream_t st) {
                          (int)smem);
     set[dv] = true;
   }
-  dim3 grid((unsigned)((a.M + BM - 1) / BM), (unsigned)(a.N / (128 * NGRP)));
-  gemm_i8_tc_kernel<<<grid, 256, smem, st>>>(a);
+  TcGemmArgs b = a;
+  const int tiles = (int)(((a.M + BM - 1) / BM) * (a.N / (128 * NGRP)));
+  const int kbt = (int)(a.K / 32 / KU);
+  int S = 1;
+  if (a.ws && a.counters && tiles < 148) {     // few-token GEMM: fill the SMs along K
+    S = (148 + tiles / 2) / tiles;
+    if (S > kbt / 4) S = kbt / 4;
+    if (S < 1) S = 1;
+  }
+  b.ksplit = S;
+  dim3 grid((unsigned)((a.M + BM - 1) / BM), (unsigned)(a.N / (128 * NGRP)), (unsigned)S);
+  gemm_i8_tc_kernel<<<grid, 256, smem, st>>>(b);
   count_launch();
 }
 

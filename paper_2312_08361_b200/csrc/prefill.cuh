@@ -19,6 +19,11 @@ struct TcGemmArgs {
   int epi;
   int debug;                // (tools) 1: skip the MMAs, 2: skip the TMA loads — timing only
   unsigned long long* trace;  // (tools, SP_TC_TRACE) per-CTA globaltimer phases, or null
+  // split-K (few-token GEMMs, single-CTA kernel): int64 partials [M][N] and one
+  // arrival counter per output tile, both zero at rest; null = no split
+  long long* ws;
+  int* counters;
+  int ksplit;               // set by the launcher
 };
 
 // token rows of the digit planes: padded to the 256-token CTA-pair tile

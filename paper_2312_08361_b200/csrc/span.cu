@@ -540,6 +540,7 @@ int run_span_decode_wide(sp_span* s, sp_kv* kv, int b0, int b1, float* y, int wi
     TcGemmArgs g{};
     g.w = w; g.wscale = sc; g.N = N; g.K = K; g.planes = s->planes; g.plane_stride = Mp * K;
     g.exps = s->exps; g.M = R; g.y = out; g.ldy = ldy; g.res = res; g.epi = epi;
+    g.ws = s->ws2; g.counters = s->cnt2;      // split-K workspace (the GEMV's, zero at rest)
     launch_gemm_i8_tc(g, st);
   };
   auto digit = [&](const float* x, int64_t K, int nm, const float* gg, const float* bb) {
