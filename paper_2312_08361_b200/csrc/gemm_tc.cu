@@ -208,29 +208,33 @@ __device__ __forceinline__ void partial_group(const TcGemmArgs& a, uint32_t tb, 
   }
 }
 
-// split-K, phase 2 (last CTA of the tile): the epilogue of epilogue_group on
-// the summed workspace, which is zeroed for the next use
-__device__ __forceinline__ void finish_group(const TcGemmArgs& a, int j, int ng0, int64_t m,
-                                             float ys) {
-  unsigned long long* ws = reinterpret_cast<unsigned long long*>(a.ws) + m * a.N;
-  const int64_t n0 = (int64_t)(ng0 + j) * 128;
-  const float* wsc = a.wscale + n0;
-  auto D = [&](int c) { return (float)(long long)atomicExch(ws + n0 + c, 0ull); };
-  if (a.epi == EPI_SWIGLU) {
-    float* out = a.y + m * a.ldy + (ng0 + j) * 64;
-    for (int c = 0; c < 64; ++c) {
-      const float gd = D(c) * ys * __ldg(wsc + c);
-      const float ud = D(64 + c) * ys * __ldg(wsc + 64 + c);
-      out[c] = __fdividef(gd, 1.0f + __expf(-gd)) * ud;
-    }
-  } else {
-    float* out = a.y + m * a.ldy + n0;
-    const float* res = a.res ? a.res + m * a.ldy + n0 : nullptr;
-    for (int c = 0; c < 128; ++c) {
-      float v = D(c) * ys * __ldg(wsc + c);
-      if (a.epi == EPI_RESID) v += res[c];
+// split-K, phase 2 (last CTA of the tile, all 256 threads, consecutive threads
+// on consecutive outputs): the epilogue of epilogue_group on the summed
+// workspace, which is zeroed for the next use.  Plain L2 loads: every partial
+// was fenced before its CTA's arrival on the tile counter.
+__device__ __forceinline__ void finish_tile(const TcGemmArgs& a, int mt, int ng0) {
+  const int rows = (int)min((int64_t)BM, a.M - (int64_t)mt * BM);
+  const bool swiglu = a.epi == EPI_SWIGLU;
+  const int outs = swiglu ? 64 : 128;                // outputs per weight group
+  long long* ws = a.ws;
+  for (int i = threadIdx.x; i < rows * NGRP * outs; i += blockDim.x) {
+    const int r = i / (NGRP * outs), rem = i % (NGRP * outs), j = rem / outs, c = rem % outs;
+    const int64_t m = (int64_t)mt * BM + r;
+    const float ys = ldexpf(1.0f, a.exps[m] - 14);
+    const int64_t n0 = (int64_t)(ng0 + j) * 128;
+    long long* wr = ws + m * a.N + n0;
+    if (swiglu) {
+      const float gd = (float)__ldcg(wr + c) * ys * __ldg(a.wscale + n0 + c);
+      const float ud = (float)__ldcg(wr + 64 + c) * ys * __ldg(a.wscale + n0 + 64 + c);
+      wr[c] = 0;
+      wr[64 + c] = 0;
+      a.y[m * a.ldy + (ng0 + j) * 64 + c] = __fdividef(gd, 1.0f + __expf(-gd)) * ud;
+    } else {
+      float v = (float)__ldcg(wr + c) * ys * __ldg(a.wscale + n0 + c);
+      wr[c] = 0;
+      if (a.epi == EPI_RESID) v += a.res[m * a.ldy + n0 + c];
       else if (a.epi == EPI_GELU) v = gelu_f(v);
-      out[c] = v;
+      a.y[m * a.ldy + n0 + c] = v;
     }
   }
 }
@@ -335,13 +339,7 @@ __global__ void __launch_bounds__(256, 1) gemm_i8_tc_kernel(TcGemmArgs a) {
       if (last_cta) { __threadfence(); *cnt = 0; }
     }
     __syncthreads();
-    if (last_cta && warp >= 4) {
-      const int64_t m = (int64_t)mt * BM + (warp - 4) * 32 + lane;
-      if (m < a.M) {
-        const float ys = ldexpf(1.0f, a.exps[m] - 14);
-        for (int j = 0; j < NGRP; ++j) finish_group(a, j, ng0, m, ys);
-      }
-    }
+    if (last_cta) finish_tile(a, mt, ng0);
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
