@@ -83,6 +83,15 @@ __device__ __forceinline__ uint64_t umma_desc(const void* smem, uint32_t lbo, ui
 constexpr uint32_t kIdescI8 = (2u << 4) | (1u << 7) | (1u << 10) | ((128u >> 3) << 17) |
                               ((128u >> 4) << 24);
 
+// bf16 operands, f32 accumulation (kind::f16; c_format F32, a/b_format BF16)
+constexpr uint32_t kIdescBF16 = (1u << 4) | (1u << 7) | (1u << 10) | ((128u >> 3) << 17) |
+                                ((128u >> 4) << 24);
+__device__ __forceinline__ void mma_bf16_tc(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(kIdescBF16), "r"(acc));
+}
 __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t acc) {
   asm volatile(
       "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
@@ -133,7 +142,12 @@ __device__ __forceinline__ float gelu_f(float x) {
 __device__ __forceinline__ void epilogue_group(const TcGemmArgs& a, uint32_t tb, int j, int ng0,
                                                int64_t m, bool valid, float ys) {
   const int64_t n0 = (int64_t)(ng0 + j) * 128;
-  const float* wsc = a.wscale + n0;
+  const float* wsc = a.wscale ? a.wscale + n0 : nullptr;
+  // int8: D = D0 * 256 + D1 exact in int64; bf16: hi + lo f32 accumulators
+  const bool bf = a.bf16 != 0;
+  auto comb = [bf](int x0, int x1) {
+    return bf ? __int_as_float(x0) + __int_as_float(x1) : (float)((long long)x0 * 256 + x1);
+  };
   if (a.epi == EPI_SWIGLU) {
     // group = [gate 64 | up 64] of outputs (ng0 + j) * 64 + c
     for (int c0 = 0; c0 < 64; c0 += 32) {
@@ -151,8 +165,8 @@ __device__ __forceinline__ void epilogue_group(const TcGemmArgs& a, uint32_t tb,
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const int cc = c + e;
-          const float gd = (float)((long long)g0[cc] * 256 + g1[cc]) * ys * __ldg(wsc + c0 + cc);
-          const float ud = (float)((long long)u0[cc] * 256 + u1[cc]) * ys * __ldg(wsc + 64 + c0 + cc);
+          const float gd = comb(g0[cc], g1[cc]) * ys * (wsc ? __ldg(wsc + c0 + cc) : 1.f);
+          const float ud = comb(u0[cc], u1[cc]) * ys * (wsc ? __ldg(wsc + 64 + c0 + cc) : 1.f);
           o4[e] = __fdividef(gd, 1.0f + __expf(-gd)) * ud;
         }
         *reinterpret_cast<float4*>(out + c) = make_float4(o4[0], o4[1], o4[2], o4[3]);
@@ -178,7 +192,7 @@ __device__ __forceinline__ void epilogue_group(const TcGemmArgs& a, uint32_t tb,
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const int cc = c + e;
-          float v = (float)((long long)v0[cc] * 256 + v1[cc]) * ys * __ldg(wsc + c0 + cc);
+          float v = comb(v0[cc], v1[cc]) * ys * (wsc ? __ldg(wsc + c0 + cc) : 1.f);
           if (a.epi == EPI_RESID) v += r4[e];
           else if (a.epi == EPI_GELU) v = gelu_f(v);
           o4[e] = v;
@@ -239,6 +253,7 @@ __device__ __forceinline__ void finish_tile(const TcGemmArgs& a, int mt, int ng0
   }
 }
 
+template <bool BF>
 __global__ void __launch_bounds__(256, 1) gemm_i8_tc_kernel(TcGemmArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], tmem_full;
@@ -305,7 +320,8 @@ __global__ void __launch_bounds__(256, 1) gemm_i8_tc_kernel(TcGemmArgs a) {
 #pragma unroll
           for (int j = 0; j < NGRP; ++j) {
             const uint64_t bd = umma_desc(st + A_BYTES + j * KU * UNIT + u * UNIT, 2048, 128);
-            mma_i8(tbase + (uint32_t)((p * NGRP + j) * 128), ad, bd, (kb | u) ? 1u : 0u);
+            if (BF) mma_bf16_tc(tbase + (uint32_t)((p * NGRP + j) * 128), ad, bd, (kb | u) ? 1u : 0u);
+            else mma_i8(tbase + (uint32_t)((p * NGRP + j) * 128), ad, bd, (kb | u) ? 1u : 0u);
           }
         }
       }
@@ -322,7 +338,7 @@ __global__ void __launch_bounds__(256, 1) gemm_i8_tc_kernel(TcGemmArgs a) {
     const bool valid = m < a.M;
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
     if (S == 1) {
-      const float ys = valid ? ldexpf(1.0f, a.exps[m] - 14) : 0.f;
+      const float ys = (valid && !BF) ? ldexpf(1.0f, a.exps[m] - 14) : 1.f;
       for (int j = 0; j < NGRP; ++j) epilogue_group(a, tbase + lane_addr, j, ng0, m, valid, ys);
     } else {
       for (int j = 0; j < NGRP; ++j) partial_group(a, tbase + lane_addr, j, ng0, m, valid);
@@ -387,6 +403,14 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
       "r"(parity)
       : "memory");
 }
+constexpr uint32_t kIdescBF16x2 = (1u << 4) | (1u << 7) | (1u << 10) | ((256u >> 3) << 17) |
+                                  ((256u >> 4) << 24);
+__device__ __forceinline__ void mma_bf16_x2(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(kIdescBF16x2), "r"(acc));
+}
 __device__ __forceinline__ void mma_i8_x2(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t acc) {
   asm volatile(
       "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
@@ -409,7 +433,7 @@ __device__ __forceinline__ void tc_trace(const TcGemmArgs& a, int ph) {
   }
 }
 
-template <int KUP, int STAGES2>
+template <int KUP, int STAGES2, bool BF>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     gemm_i8_tc2_kernel(TcGemmArgs a) {
   constexpr int A2_BYTES = 2 * KUP * UNIT;   // two digit planes, 128 tokens
@@ -489,7 +513,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
 #pragma unroll
         for (int p = 0; p < 2; ++p) {
           const uint64_t ad = umma_desc(st + p * KUP * UNIT + u * UNIT, 2048, 128);
-          mma_i8_x2(tbase + (uint32_t)(p * 256), ad, bd, (kb | u) ? 1u : 0u);
+          if (BF) mma_bf16_x2(tbase + (uint32_t)(p * 256), ad, bd, (kb | u) ? 1u : 0u);
+          else mma_i8_x2(tbase + (uint32_t)(p * 256), ad, bd, (kb | u) ? 1u : 0u);
         }
       }
       mma_commit_x2(&empty[s]);        // frees stage s in both CTAs when these MMAs finish
@@ -508,7 +533,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     if (threadIdx.x == 128) tc_trace(a, 1);
     const bool valid = m < a.M;
-    const float ys = valid ? ldexpf(1.0f, a.exps[m] - 14) : 0.f;
+    const float ys = (valid && !BF) ? ldexpf(1.0f, a.exps[m] - 14) : 1.f;
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
     epilogue_group(a, tbase + lane_addr, warp >> 2, ng0, m, valid, ys);
   }
@@ -702,6 +727,88 @@ __global__ void __launch_bounds__(NT) digitize_reg_kernel(const float* __restric
   }
 }
 
+// bf16 operands for the tcgen05 GEMM (bf16 weights, Llama-2-7B): the
+// (normalised) row as hi = bf16(x) and lo = bf16(x - hi) planes in the same
+// core-matrix layout (16-byte rows = 8 elements); no exponent
+template <int NT, int NCH>
+__global__ void __launch_bounds__(NT) digitize_bf16_kernel(const float* __restrict__ x, int64_t ldx,
+                                                           int64_t M, int64_t K, int norm,
+                                                           const float* __restrict__ g,
+                                                           const float* __restrict__ b,
+                                                           uint8_t* planes, int64_t plane_stride) {
+  constexpr int NW = NT / 32;
+  __shared__ float red[2][NW];
+  const int64_t m = blockIdx.x;
+  const float* xr = x + m * ldx;
+  const int nchunk = (int)(K >> 3);               // 8 elements per 16-byte core-matrix row
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  float v[NCH][8];
+  auto bsum = [&](float a, int slot) {
+    a = warp_sum(a);
+    if (lane == 0) red[slot][warp] = a;
+    __syncthreads();
+    float r = 0.f;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) r += red[slot][w];
+    return r;
+  };
+  float s = 0.f, s2 = 0.f;
+#pragma unroll
+  for (int j = 0; j < NCH; ++j) {
+    const int c = t + j * NT;
+    if (c < nchunk) {
+      const float4 f0 = __ldcs(reinterpret_cast<const float4*>(xr + (int64_t)c * 8));
+      const float4 f1 = __ldcs(reinterpret_cast<const float4*>(xr + (int64_t)c * 8) + 1);
+      v[j][0] = f0.x; v[j][1] = f0.y; v[j][2] = f0.z; v[j][3] = f0.w;
+      v[j][4] = f1.x; v[j][5] = f1.y; v[j][6] = f1.z; v[j][7] = f1.w;
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) v[j][e] = 0.f;
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) { s += v[j][e]; s2 = fmaf(v[j][e], v[j][e], s2); }
+  }
+  if (norm != 0) {
+    float mu = 0.f, rstd;
+    if (norm == 2) {
+      mu = bsum(s, 0) / (float)K;
+      float q2 = 0.f;
+#pragma unroll
+      for (int j = 0; j < NCH; ++j)
+        if (t + j * NT < nchunk)
+#pragma unroll
+          for (int e = 0; e < 8; ++e) { const float dd = v[j][e] - mu; q2 = fmaf(dd, dd, q2); }
+      rstd = 1.0f / sqrtf(bsum(q2, 1) / (float)K + 1e-5f);
+    } else {
+      rstd = 1.0f / sqrtf(bsum(s2, 1) / (float)K + 1e-5f);
+    }
+#pragma unroll
+    for (int j = 0; j < NCH; ++j) {
+      const int c = t + j * NT;
+      if (c >= nchunk) continue;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int64_t k = (int64_t)c * 8 + e;
+        v[j][e] = (norm == 1) ? v[j][e] * rstd * g[k] : (v[j][e] - mu) * rstd * g[k] + b[k];
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < NCH; ++j) {
+    const int c = t + j * NT;
+    if (c >= nchunk) continue;
+    __align__(16) __nv_bfloat16 hi[8], lo[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      hi[e] = __float2bfloat16_rn(v[j][e]);
+      lo[e] = __float2bfloat16_rn(v[j][e] - __bfloat162float(hi[e]));
+    }
+    const int64_t off = cm_offset(m, (int64_t)c * 16, 2 * K);
+    *reinterpret_cast<uint4*>(planes + off) = *reinterpret_cast<uint4*>(hi);
+    *reinterpret_cast<uint4*>(planes + plane_stride + off) = *reinterpret_cast<uint4*>(lo);
+  }
+}
+
 }  // namespace
 
 bool g_tc_pair = true;
@@ -726,13 +833,13 @@ void launch_digitize(const float* x, int64_t ldx, int64_t M, int64_t K, int norm
   count_launch();
 }
 
-template <int KUP, int ST>
+template <int KUP, int ST, bool BF>
 void launch_pair(const TcGemmArgs& a, cudaStream_t st) {
   static bool set2[kMaxDevices] = {};
   const int dv = current_device();
   const size_t smem2 = (size_t)ST * 3 * KUP * UNIT;
   if (!set2[dv]) {
-    cudaFuncSetAttribute(gemm_i8_tc2_kernel<KUP, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(gemm_i8_tc2_kernel<KUP, ST, BF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem2);
     set2[dv] = true;
   }
@@ -748,7 +855,7 @@ void launch_pair(const TcGemmArgs& a, cudaStream_t st) {
     cudaMalloc(&b.trace, tn * 8);
     cudaMemsetAsync(b.trace, 0, tn * 8, st);
   }
-  gemm_i8_tc2_kernel<KUP, ST><<<grid2, 256, smem2, st>>>(b);
+  gemm_i8_tc2_kernel<KUP, ST, BF><<<grid2, 256, smem2, st>>>(b);
   count_launch();
   if (tr) {
     std::vector<unsigned long long> h(tn);
@@ -769,33 +876,50 @@ void launch_gemm_i8_tc(const TcGemmArgs& a, cudaStream_t st) {
   // does half the padded MMA work of a 256-token pair tile
   if (g_tc_pair && a.M > 128) {
     static int cfg = getenv("SP_TC_CFG") ? atoi(getenv("SP_TC_CFG")) : 0;
-    if (cfg == 1) launch_pair<2, 8>(a, st);
-    else launch_pair<4, 4>(a, st);
+    if (a.bf16) launch_pair<4, 4, true>(a, st);
+    else if (cfg == 1) launch_pair<2, 8, false>(a, st);
+    else launch_pair<4, 4, false>(a, st);
     return;
   }
-  static bool set[kMaxDevices] = {};
+  static bool set[kMaxDevices][2] = {};
   const int dv = current_device();
   const size_t smem = (size_t)STAGES * STAGE;
-  if (!set[dv]) {
-    cudaFuncSetAttribute(gemm_i8_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    set[dv] = true;
+  if (!set[dv][a.bf16 ? 1 : 0]) {
+    if (a.bf16)
+      cudaFuncSetAttribute(gemm_i8_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem);
+    else
+      cudaFuncSetAttribute(gemm_i8_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem);
+    set[dv][a.bf16 ? 1 : 0] = true;
   }
   TcGemmArgs b = a;
   const int tiles = (int)(((a.M + BM - 1) / BM) * (a.N / (128 * NGRP)));
   const int kbt = (int)(a.K / 32 / KU);
   int S = 1;
-  if (a.ws && a.counters && tiles < 148) {     // few-token GEMM: fill the SMs along K
+  if (a.ws && a.counters && tiles < 148 && !a.bf16) {   // few-token GEMM: fill the SMs along K
     S = (148 + tiles / 2) / tiles;
     if (S > kbt / 4) S = kbt / 4;
     if (S < 1) S = 1;
   }
   b.ksplit = S;
   dim3 grid((unsigned)((a.M + BM - 1) / BM), (unsigned)(a.N / (128 * NGRP)), (unsigned)S);
-  gemm_i8_tc_kernel<<<grid, 256, smem, st>>>(b);
+  if (a.bf16) gemm_i8_tc_kernel<true><<<grid, 256, smem, st>>>(b);
+  else gemm_i8_tc_kernel<false><<<grid, 256, smem, st>>>(b);
   count_launch();
 }
 
 int64_t tc_plane_bytes(int64_t M, int64_t K) { return tc_rows(M) * K; }
+
+void launch_digitize_bf16(const float* x, int64_t ldx, int64_t M, int64_t K, int norm,
+                          const float* g, const float* b, uint8_t* planes, int64_t plane_stride,
+                          cudaStream_t st) {
+  const unsigned grid = (unsigned)M;
+  if (K <= 256 * 8 * 4)
+    digitize_bf16_kernel<256, 4><<<grid, 256, 0, st>>>(x, ldx, M, K, norm, g, b, planes, plane_stride);
+  else
+    digitize_bf16_kernel<512, 4><<<grid, 512, 0, st>>>(x, ldx, M, K, norm, g, b, planes, plane_stride);
+  count_launch();
+}
 
 }  // namespace sp

@@ -24,6 +24,7 @@ struct TcGemmArgs {
   long long* ws;
   int* counters;
   int ksplit;               // set by the launcher
+  int bf16;                 // bf16 weights and hi/lo bf16 planes (K counted in bytes)
 };
 
 // token rows of the digit planes: padded to the 256-token CTA-pair tile
@@ -34,5 +35,9 @@ void launch_digitize(const float* x, int64_t ldx, int64_t M, int64_t K, int norm
                      const float* b, uint8_t* planes, int64_t plane_stride, int* exps,
                      cudaStream_t st);
 void launch_gemm_i8_tc(const TcGemmArgs& a, cudaStream_t st);
+// bf16 operand planes (hi, lo) for bf16 weights; K <= 16384
+void launch_digitize_bf16(const float* x, int64_t ldx, int64_t M, int64_t K, int norm,
+                          const float* g, const float* b, uint8_t* planes, int64_t plane_stride,
+                          cudaStream_t st);
 
 }  // namespace sp

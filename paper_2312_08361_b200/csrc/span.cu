@@ -209,7 +209,7 @@ int ensure_tc(sp_span* s, int64_t rows) {
   if (rows <= s->tc_cap_rows) return SP_OK;
   cudaFree(s->planes); cudaFree(s->exps);
   const int64_t Mp = tc_rows(rows);       // the CTA-pair GEMM tiles 256 tokens
-  const int64_t K = std::max<int64_t>(s->d, s->F);
+  const int64_t K = std::max<int64_t>(s->d, s->F) * (s->cfg.weight_dtype == kBF16 ? 2 : 1);
   SP_CUDA_TRY(cudaMalloc(&s->planes, 2 * Mp * K));
   SP_CUDA_TRY(cudaMalloc(&s->exps, Mp * sizeof(int)));
   s->tc_cap_rows = Mp;
@@ -217,8 +217,12 @@ int ensure_tc(sp_span* s, int64_t rows) {
 }
 
 bool tc_ok(const sp_span* s) {
-  return s->cfg.weight_dtype == kI8 && s->n_qkv % 256 == 0 && s->d % 256 == 0 &&
-         s->n_up % 256 == 0 && s->d % 128 == 0 && s->F % 128 == 0;
+  const int wd = s->cfg.weight_dtype;
+  // int8: K multiple of 128 elements (4 x 32-byte units per stage); bf16: 64
+  const int64_t kq = wd == kI8 ? 128 : 64;
+  return (wd == kI8 || wd == kBF16) && s->n_qkv % 256 == 0 && s->d % 256 == 0 &&
+         s->n_up % 256 == 0 && s->d % kq == 0 && s->F % kq == 0 &&
+         (wd == kI8 || std::max(s->d, s->F) <= 16384);
 }
 
 int ensure_attn_ws(sp_span* s, int width) {
@@ -453,6 +457,8 @@ int run_span_prefill_tc(sp_span* s, sp_kv* kv, int b0, int b1, float* y, float* 
   if (rc) return rc;
   const int fam = s->cfg.family;
   const int norm = fam == kLlama ? 1 : 2;
+  const bool bf = s->cfg.weight_dtype == kBF16;
+  const int64_t eb = bf ? 2 : 1;
   const int64_t d = s->d, F = s->F;
   const int64_t Mp = tc_rows(R);
   const double kv_elt = s->cfg.kv_dtype == kKVBF16 ? 2.0 : 4.0;
@@ -469,13 +475,17 @@ int run_span_prefill_tc(sp_span* s, sp_kv* kv, int b0, int b1, float* y, float* 
     ProfScope ps(s, PC_GEMM, (double)N * K + 4.0 * N + 2.0 * Mp * K + 4.0 * R * ldy,
                  2.0 * R * N * K, st);
     TcGemmArgs g{};
-    g.w = w; g.wscale = sc; g.N = N; g.K = K; g.planes = s->planes; g.plane_stride = Mp * K;
+    const int64_t Kb = K * eb;                     // K in bytes (32-byte units)
+    g.w = w; g.wscale = bf ? nullptr : sc; g.N = N; g.K = Kb; g.planes = s->planes;
+    g.plane_stride = Mp * Kb;
     g.exps = s->exps; g.M = R; g.y = out; g.ldy = ldy; g.res = res; g.epi = epi;
+    g.bf16 = bf ? 1 : 0;
     launch_gemm_i8_tc(g, st);
   };
   auto digit = [&](const float* x, int64_t K, int nm, const float* gg, const float* bb) {
-    ProfScope ps(s, PC_OTHER, 4.0 * R * K + 2.0 * Mp * K, 0, st);
-    launch_digitize(x, K, R, K, nm, gg, bb, s->planes, Mp * K, s->exps, st);
+    ProfScope ps(s, PC_OTHER, 4.0 * R * K + 2.0 * Mp * K * eb, 0, st);
+    if (bf) launch_digitize_bf16(x, K, R, K, nm, gg, bb, s->planes, Mp * K * eb, st);
+    else launch_digitize(x, K, R, K, nm, gg, bb, s->planes, Mp * K, s->exps, st);
   };
   for (int b = b0 - s->start; b < b1 - s->start; ++b) {
     BlockW& W = s->blocks[b];
@@ -524,6 +534,8 @@ int run_span_decode_wide(sp_span* s, sp_kv* kv, int b0, int b1, float* y, int wi
   if (rc) return rc;
   const int fam = s->cfg.family;
   const int norm = fam == kLlama ? 1 : 2;
+  const bool bf = false;                          // int8 only (split-K is integer)
+  const int64_t eb = 1;
   const int64_t d = s->d, F = s->F;
   const int64_t Mp = tc_rows(R);
   const double kv_elt = s->cfg.kv_dtype == kKVBF16 ? 2.0 : 4.0;
@@ -544,8 +556,9 @@ int run_span_decode_wide(sp_span* s, sp_kv* kv, int b0, int b1, float* y, int wi
     launch_gemm_i8_tc(g, st);
   };
   auto digit = [&](const float* x, int64_t K, int nm, const float* gg, const float* bb) {
-    ProfScope ps(s, PC_OTHER, 4.0 * R * K + 2.0 * Mp * K, 0, st);
-    launch_digitize(x, K, R, K, nm, gg, bb, s->planes, Mp * K, s->exps, st);
+    ProfScope ps(s, PC_OTHER, 4.0 * R * K + 2.0 * Mp * K * eb, 0, st);
+    if (bf) launch_digitize_bf16(x, K, R, K, nm, gg, bb, s->planes, Mp * K * eb, st);
+    else launch_digitize(x, K, R, K, nm, gg, bb, s->planes, Mp * K, s->exps, st);
   };
   for (int b = b0 - s->start; b < b1 - s->start; ++b) {
     BlockW& W = s->blocks[b];
@@ -570,7 +583,8 @@ int run_span_decode_wide(sp_span* s, sp_kv* kv, int b0, int b1, float* y, int wi
 
 int run_span(sp_span* s, sp_kv* kv, int b0, int b1, float* y, float* record, int width,
              int n_new, cudaStream_t st) {
-  if (n_new == 1 && width >= kWideDecode && tc_ok(s) && s->use_tc_prefill && !record)
+  if (n_new == 1 && width >= kWideDecode && tc_ok(s) && s->cfg.weight_dtype == kI8 &&
+      s->use_tc_prefill && !record)
     return run_span_decode_wide(s, kv, b0, b1, y, width, st);
   if (n_new == 1 && s->cfg.weight_dtype != kF32 && !record)
     return run_span_decode_tc(s, kv, b0, b1, y, width, st);

@@ -336,3 +336,24 @@ def test_decode_attention_streamed_subchunks(name):
         _lib.check(eng.lib.sp_span_set_option(eng.span.handle, 5, 0))
     for a, b in zip(*outs):
         assert np.abs(a - b).max() <= 1e-5 * np.abs(b).max()
+
+
+def test_bf16_tc_prefill_matches_simt():
+    """bf16 weights (Llama-2-7B family) on the tcgen05 GEMM (kind::f16, hi/lo
+    bf16 activation planes, f32 accumulation) vs the exact-f32 SIMT GEMM, and
+    the micro-batch invariance of T/test_server.py:247-255."""
+    from paper_2312_08361_b200 import _lib
+    from paper_2312_08361_b200.engine import DeviceSpan, B200ServerEngine
+    cfg = SMALL["llama_bf16"]
+    span_tc = DeviceSpan(cfg, 0, cfg.n_blocks)
+    span_ref = DeviceSpan(cfg, 0, cfg.n_blocks)
+    _lib.check(span_ref.lib.sp_span_set_option(span_ref.handle, 0, 0))
+    e_tc, e_ref = B200ServerEngine(cfg, span=span_tc), B200ServerEngine(cfg, span=span_ref)
+    rng = np.random.default_rng(23)
+    x = rng.standard_normal((2 * 150, cfg.hidden_dim)).astype(np.float32)
+    a = e_tc.forward(0, cfg.n_blocks, _blob(x), 2, 150, 10**9, None).array()
+    b = e_ref.forward(0, cfg.n_blocks, _blob(x), 2, 150, 10**9, None).array()
+    rel = np.abs(a - b).max() / np.abs(b).max()
+    assert rel < 2e-3, rel
+    split = e_tc.forward(0, cfg.n_blocks, _blob(x), 2, 150, 150, None).array()
+    assert np.array_equal(a, split)
