@@ -436,9 +436,12 @@ __global__ void __launch_bounds__(NTH) attn_dec_mma_kernel(AttnDecArgs a) {
   // K/V of a 128-position sub-chunk, double-buffered: [2][4*32][RS] each.  A
   // CTA streams a.nsub sub-chunks (MHA shapes: many kv heads, few positions per
   // CTA otherwise) with a running online softmax per warp
+  // (one buffer when a CTA has a single sub-chunk: 70 KB instead of 139 KB, so
+  // the next GEMV's CTA fits beside it and prefetches its weights)
+  const int nbuf = a.nsub > 1 ? 2 : 1;
   Row* Kbuf = reinterpret_cast<Row*>(dsm);
-  Row* Vbuf = Kbuf + 2 * 4 * 32;
-  float* wo = reinterpret_cast<float*>(Vbuf + 2 * 4 * 32);   // [4][G][HD]
+  Row* Vbuf = Kbuf + nbuf * 4 * 32;
+  float* wo = reinterpret_cast<float*>(Vbuf + nbuf * 4 * 32);   // [4][G][HD]
   float* pmv = wo + 4 * G * HD;
   float* plv = pmv + a.max_pages * GMAX;
 
@@ -469,8 +472,8 @@ __global__ void __launch_bounds__(NTH) attn_dec_mma_kernel(AttnDecArgs a) {
     const int page = a.page_table[slot * a.max_pages + min(q0, T - 1) / kPageTokens];
     const __nv_bfloat16* kbase = page_ptr<__nv_bfloat16>(a.kv_pool, page, 0, a.kvh, kh, HD) + (q0 % kPageTokens) * HD;
     const __nv_bfloat16* vbase = page_ptr<__nv_bfloat16>(a.kv_pool, page, 1, a.kvh, kh, HD) + (q0 % kPageTokens) * HD;
-    Row* Kt = Kbuf + (j & 1) * 128;
-    Row* Vt = Vbuf + (j & 1) * 128;
+    Row* Kt = Kbuf + (j % nbuf) * 128;
+    Row* Vt = Vbuf + (j % nbuf) * 128;
     for (int c = lane; c < 32 * CPR; c += 32) {
       const int r = c / CPR, e = (c % CPR) * 8;
       const bool ok = r < nvj;
@@ -569,8 +572,8 @@ __global__ void __launch_bounds__(NTH) attn_dec_mma_kernel(AttnDecArgs a) {
     }
     __syncthreads();
     if (js == 0) trace_mark(a, 2);
-    Row* Kt = Kbuf + (js & 1) * 128;
-    Row* Vt = Vbuf + (js & 1) * 128;
+    Row* Kt = Kbuf + (js % nbuf) * 128;
+    Row* Vt = Vbuf + (js % nbuf) * 128;
     if (appender && js == app_sub) {
       const int r = a.t0 - base - js * CHUNK;
 #pragma unroll
@@ -702,7 +705,7 @@ void launch_mma(const AttnDecArgs& a_in, cudaStream_t st) {
   a.nsub = nsub;
   dim3 grid(a.width * a.kvh, (T + CHUNK * nsub - 1) / (CHUNK * nsub));
   const int G = a.H / a.kvh;
-  const size_t smem = (size_t)2 * 2 * 4 * 32 * (HD + 8) * 2 +
+  const size_t smem = (size_t)(nsub > 1 ? 2 : 1) * 2 * 4 * 32 * (HD + 8) * 2 +
                       (size_t)(4 * G * HD + 2 * a.max_pages * GMAX) * sizeof(float);
   static size_t set[kMaxDevices] = {};
   const int dv = current_device();
