@@ -238,8 +238,10 @@ def run_b200(args) -> None:
     start, end = stage_intervals(n_blocks, world)[rank]
     t_gen = time.perf_counter()
     span = DeviceSpan(cfg, start, end, device=local,
-                      kv_pool_tokens=(args.prefill + args.steps * 4 + 256) * B * (max(1, world) + 1)
-                      + 1024)
+                      # sessions in flight (+1 for the N=1 e2e session; the warm-up
+                      # prefill's cache is freed before the sessions are created)
+                      kv_pool_tokens=(args.prefill + args.steps * 4 + 256) * B
+                      * (max(1, world) + (1 if world == 1 else 0)) + 1024)
     torch.cuda.synchronize()
     t_gen = time.perf_counter() - t_gen
     eng = B200ServerEngine(cfg, span=span)
