@@ -149,7 +149,7 @@ struct WarpSmem {
   uint64_t bar[STAGES];
 };
 
-template <int WT, int NT, int NORMT, bool HASG, int ND>
+template <int WT, int NT, int NORMT, bool HASG, int ND, int RM>
 __global__ void __launch_bounds__(NW * 32, CTAS_PER_SM)
 gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_total) {
   constexpr int NDIG = ND;
@@ -206,17 +206,17 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
   // ---- per-row parameters from the producer's partial stats ----
   // CTA-wide: 256 threads load the P_in x Rn partials with several loads in
   // flight each, then a fixed-order tree (warp shuffles, then warps in order)
-  __shared__ float red_s[NW][RMAX][3];
-  __shared__ float prm_mu[RMAX], prm_ds[RMAX];
-  __shared__ double prm_ys[RMAX];
+  __shared__ float red_s[NW][RM][3];
+  __shared__ float prm_mu[RM], prm_ds[RM];
+  __shared__ double prm_ys[RM];
   {
-    float S[RMAX], Q[RMAX], M[RMAX];
+    float S[RM], Q[RM], M[RM];
 #pragma unroll
-    for (int r = 0; r < RMAX; ++r) { S[r] = 0.f; Q[r] = 0.f; M[r] = 0.f; }
+    for (int r = 0; r < RM; ++r) { S[r] = 0.f; Q[r] = 0.f; M[r] = 0.f; }
     constexpr int PU = 4;
     for (int p0 = threadIdx.x; p0 < a.P_in; p0 += PU * NW * 32) {
 #pragma unroll
-      for (int r = 0; r < RMAX; ++r) {
+      for (int r = 0; r < RM; ++r) {
         if (r >= Rn) break;
         RowStat t[PU];
 #pragma unroll
@@ -234,12 +234,12 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
     for (int i = 0; i < npre; ++i) {     // activation chunks of the prefetched units
       // (issued right behind the stats loads, ahead of their reduction)
       const int64_t kt = (u0 + i) % KT;
-      for (int r = 0; r < Rn; ++r)
+      for (int r = 0; r < (RM == 1 ? 1 : Rn); ++r)
         tma_load_1d(ring + i * STAGE_BYTES + UNIT_BYTES + r * XSLOT,
                     a.x + (int64_t)(r0 + r) * a.ldx + kt * KTILE, XB, &ws_->bar[i], policy_x);
     }
 #pragma unroll
-    for (int r = 0; r < RMAX; ++r) {
+    for (int r = 0; r < RM; ++r) {
       const float vs = warp_sum(S[r]), vq = warp_sum(Q[r]), vm = warp_max(M[r]);
       if (lane == 0) { red_s[warp][r][0] = vs; red_s[warp][r][1] = vq; red_s[warp][r][2] = vm; }
     }
@@ -274,7 +274,7 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
   }
   gtrace(a, 2);
   if (u0 >= u1) return;
-  if (lane < RMAX) {
+  if (lane < RM) {
     ws_->mu[lane] = prm_mu[lane];
     ws_->dscale[lane] = prm_ds[lane];
     ws_->yscale[lane] = prm_ys[lane];
@@ -313,7 +313,7 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
     uint8_t* dstg = ring + p_st * STAGE_BYTES;
     tma_load_1d(dstg, wbase + ((int64_t)p_grp * KT + p_kt) * UNIT_BYTES, UNIT_BYTES,
                 &ws_->bar[p_st], policy);
-    for (int r = 0; r < Rn; ++r)
+    for (int r = 0; r < (RM == 1 ? 1 : Rn); ++r)
       tma_load_1d(dstg + UNIT_BYTES + r * XSLOT, a.x + (int64_t)(r0 + r) * a.ldx + p_kt * KTILE,
                   XB, &ws_->bar[p_st], policy_x);
     if (++p_kt == KT) { p_kt = 0; ++p_grp; }
@@ -425,7 +425,7 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int64_t n = grp * 128 + t * 16 + g8 + h * 8;
-        for (int r = 0; r < Rn; ++r) {
+        for (int r = 0; r < (RM == 1 ? 1 : Rn); ++r) {
           long long D = 0;
           if constexpr (WT == kI8) {
 #pragma unroll
@@ -476,7 +476,7 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
     // gains) is issued before the first is used: one round trip, not four
     const bool swiglu = (a.epi == EPI_SWIGLU);
     const int nj = swiglu ? 2 : 4;         // outputs per lane (64 or 128 per group)
-    for (int r = 0; r < Rn; ++r) {
+    for (int r = 0; r < (RM == 1 ? 1 : Rn); ++r) {
       unsigned long long* accr = acc64 + (int64_t)(r0 + r) * a.N + grp * 128;
       const double ys = ws_->yscale[r];
       const int64_t yrow = (int64_t)(r0 + r) * a.ldy;
@@ -531,7 +531,7 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
 
 int g_num_sms = 0;
 
-template <int WT, int NT, int NORMT, bool HASG, int ND>
+template <int WT, int NT, int NORMT, bool HASG, int ND, int RM>
 void launch_cfg(const GemvArgs& a, int r0, int rn, cudaStream_t st) {
   const int KTILE = (WT == kI8) ? 32 : 16;
   const int64_t units = (a.N / 128) * (a.K / KTILE);
@@ -540,7 +540,7 @@ void launch_cfg(const GemvArgs& a, int r0, int rn, cudaStream_t st) {
   static bool set[kMaxDevices] = {};
   const int dv = current_device();
   if (!set[dv]) {
-    cudaFuncSetAttribute(gemv3_kernel<WT, NT, NORMT, HASG, ND>,
+    cudaFuncSetAttribute(gemv3_kernel<WT, NT, NORMT, HASG, ND, RM>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     set[dv] = true;
   }
@@ -559,7 +559,7 @@ void launch_cfg(const GemvArgs& a, int r0, int rn, cudaStream_t st) {
     cudaMemsetAsync(tbuf, 0, tn * 8, st);
     b.trace = tbuf;
   }
-  launch_pdl(gemv3_kernel<WT, NT, NORMT, HASG, ND>, dim3(grid), dim3(NW * 32), smem, st, b, r0, rn,
+  launch_pdl(gemv3_kernel<WT, NT, NORMT, HASG, ND, RM>, dim3(grid), dim3(NW * 32), smem, st, b, r0, rn,
              a.R, units, (int64_t)grid * NW);
   count_launch();
   if (tr) {
@@ -580,16 +580,24 @@ void launch_cfg(const GemvArgs& a, int r0, int rn, cudaStream_t st) {
   }
 }
 
-template <int WT, int NT, int ND>
-void launch_nt(const GemvArgs& a, int r0, int rn, cudaStream_t st) {
+template <int WT, int NT, int ND, int RM>
+void launch_nt2(const GemvArgs& a, int r0, int rn, cudaStream_t st) {
   const bool hg = a.g != nullptr;
   switch (a.norm) {
-    case NORM_RMS: hg ? launch_cfg<WT, NT, NORM_RMS, true, ND>(a, r0, rn, st)
-                      : launch_cfg<WT, NT, NORM_RMS, false, ND>(a, r0, rn, st); break;
-    case NORM_LN: hg ? launch_cfg<WT, NT, NORM_LN, true, ND>(a, r0, rn, st)
-                     : launch_cfg<WT, NT, NORM_LN, false, ND>(a, r0, rn, st); break;
-    default: launch_cfg<WT, NT, NORM_NONE, false, ND>(a, r0, rn, st); break;
+    case NORM_RMS: hg ? launch_cfg<WT, NT, NORM_RMS, true, ND, RM>(a, r0, rn, st)
+                      : launch_cfg<WT, NT, NORM_RMS, false, ND, RM>(a, r0, rn, st); break;
+    case NORM_LN: hg ? launch_cfg<WT, NT, NORM_LN, true, ND, RM>(a, r0, rn, st)
+                     : launch_cfg<WT, NT, NORM_LN, false, ND, RM>(a, r0, rn, st); break;
+    default: launch_cfg<WT, NT, NORM_NONE, false, ND, RM>(a, r0, rn, st); break;
   }
+}
+
+// one-row launches get their own instantiation (RM = 1): the per-row loops of
+// the prologue, flush and epilogue collapse, and the kernel is a third smaller
+template <int WT, int NT, int ND>
+void launch_nt(const GemvArgs& a, int r0, int rn, cudaStream_t st) {
+  if (NT == 1 && rn == 1) launch_nt2<WT, NT, ND, 1>(a, r0, rn, st);
+  else launch_nt2<WT, NT, ND, RMAX>(a, r0, rn, st);
 }
 
 template <int WT, int ND>
