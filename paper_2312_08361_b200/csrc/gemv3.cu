@@ -149,7 +149,7 @@ struct WarpSmem {
   uint64_t bar[STAGES];
 };
 
-template <int WT, int NT, int NORMT, bool HASG, int ND, int RM>
+template <int WT, int NT, int NORMT, bool HASG, int ND, int RM, int EP>
 __global__ void __launch_bounds__(NW * 32, CTAS_PER_SM)
 gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_total) {
   constexpr int NDIG = ND;
@@ -231,9 +231,9 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
       }
     }
   if (lane == 0)
-    for (int i = 0; i < npre; ++i) {     // activation chunks of the prefetched units
+    for (int i = 0, kt0 = (int)(u0 % KT); i < npre; ++i) {   // x chunks of the prefetched units
       // (issued right behind the stats loads, ahead of their reduction)
-      const int64_t kt = (u0 + i) % KT;
+      const int64_t kt = kt0 + i < KT ? kt0 + i : kt0 + i - KT;
       for (int r = 0; r < (RM == 1 ? 1 : Rn); ++r)
         tma_load_1d(ring + i * STAGE_BYTES + UNIT_BYTES + r * XSLOT,
                     a.x + (int64_t)(r0 + r) * a.ldx + kt * KTILE, XB, &ws_->bar[i], policy_x);
@@ -474,7 +474,10 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
     // ---- epilogue for the group (128 channels x Rn rows), last warp only ----
     // every load of the lane (4 accumulators, their scales, residuals, next
     // gains) is issued before the first is used: one round trip, not four
-    const bool swiglu = (a.epi == EPI_SWIGLU);
+    // EP >= 0: the epilogue type is a template constant (single-row kernels:
+    // the unused variants' code is not emitted)
+    const int epi = EP >= 0 ? EP : a.epi;
+    const bool swiglu = (epi == EPI_SWIGLU);
     const int nj = swiglu ? 2 : 4;         // outputs per lane (64 or 128 per group)
     for (int r = 0; r < (RM == 1 ? 1 : Rn); ++r) {
       unsigned long long* accr = acc64 + (int64_t)(r0 + r) * a.N + grp * 128;
@@ -491,7 +494,7 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int64_t col = swiglu ? grp * 64 + lane + 32 * j : grp * 128 + lane + 32 * j;
-        rv[j] = (j < nj && a.epi == EPI_RESID) ? a.res[yrow + col] : 0.f;
+        rv[j] = (j < nj && epi == EPI_RESID) ? a.res[yrow + col] : 0.f;
         gn[j] = (j < nj && a.g_next) ? __ldg(a.g_next + col) : 1.f;
       }
       auto val_of = [&](int k) {
@@ -511,8 +514,8 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
         } else {
           col = grp * 128 + lane + 32 * j;
           val = val_of(j);
-          if (a.epi == EPI_RESID) val += rv[j];
-          else if (a.epi == EPI_GELU) val = gelu_f(val);
+          if (epi == EPI_RESID) val += rv[j];
+          else if (epi == EPI_GELU) val = gelu_f(val);
         }
         a.y[yrow + col] = val;
         S += val;
@@ -531,7 +534,7 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
 
 int g_num_sms = 0;
 
-template <int WT, int NT, int NORMT, bool HASG, int ND, int RM>
+template <int WT, int NT, int NORMT, bool HASG, int ND, int RM, int EP>
 void launch_cfg(const GemvArgs& a, int r0, int rn, cudaStream_t st) {
   const int KTILE = (WT == kI8) ? 32 : 16;
   const int64_t units = (a.N / 128) * (a.K / KTILE);
@@ -540,7 +543,7 @@ void launch_cfg(const GemvArgs& a, int r0, int rn, cudaStream_t st) {
   static bool set[kMaxDevices] = {};
   const int dv = current_device();
   if (!set[dv]) {
-    cudaFuncSetAttribute(gemv3_kernel<WT, NT, NORMT, HASG, ND, RM>,
+    cudaFuncSetAttribute(gemv3_kernel<WT, NT, NORMT, HASG, ND, RM, EP>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     set[dv] = true;
   }
@@ -559,7 +562,7 @@ void launch_cfg(const GemvArgs& a, int r0, int rn, cudaStream_t st) {
     cudaMemsetAsync(tbuf, 0, tn * 8, st);
     b.trace = tbuf;
   }
-  launch_pdl(gemv3_kernel<WT, NT, NORMT, HASG, ND, RM>, dim3(grid), dim3(NW * 32), smem, st, b, r0, rn,
+  launch_pdl(gemv3_kernel<WT, NT, NORMT, HASG, ND, RM, EP>, dim3(grid), dim3(NW * 32), smem, st, b, r0, rn,
              a.R, units, (int64_t)grid * NW);
   count_launch();
   if (tr) {
@@ -580,15 +583,48 @@ void launch_cfg(const GemvArgs& a, int r0, int rn, cudaStream_t st) {
   }
 }
 
-template <int WT, int NT, int ND, int RM>
-void launch_nt2(const GemvArgs& a, int r0, int rn, cudaStream_t st) {
+template <int WT, int NT, int ND, int RM, int EP>
+void launch_norm(const GemvArgs& a, int r0, int rn, cudaStream_t st) {
   const bool hg = a.g != nullptr;
   switch (a.norm) {
-    case NORM_RMS: hg ? launch_cfg<WT, NT, NORM_RMS, true, ND, RM>(a, r0, rn, st)
-                      : launch_cfg<WT, NT, NORM_RMS, false, ND, RM>(a, r0, rn, st); break;
-    case NORM_LN: hg ? launch_cfg<WT, NT, NORM_LN, true, ND, RM>(a, r0, rn, st)
-                     : launch_cfg<WT, NT, NORM_LN, false, ND, RM>(a, r0, rn, st); break;
-    default: launch_cfg<WT, NT, NORM_NONE, false, ND, RM>(a, r0, rn, st); break;
+    case NORM_RMS: hg ? launch_cfg<WT, NT, NORM_RMS, true, ND, RM, EP>(a, r0, rn, st)
+                      : launch_cfg<WT, NT, NORM_RMS, false, ND, RM, EP>(a, r0, rn, st); break;
+    case NORM_LN: hg ? launch_cfg<WT, NT, NORM_LN, true, ND, RM, EP>(a, r0, rn, st)
+                     : launch_cfg<WT, NT, NORM_LN, false, ND, RM, EP>(a, r0, rn, st); break;
+    default: launch_cfg<WT, NT, NORM_NONE, false, ND, RM, EP>(a, r0, rn, st); break;
+  }
+}
+
+template <int WT, int NT, int ND, int RM>
+void launch_nt2(const GemvArgs& a, int r0, int rn, cudaStream_t st) {
+  if constexpr (RM != 1) {
+    launch_norm<WT, NT, ND, RM, -1>(a, r0, rn, st);
+  } else {
+    // single-row kernels: one instantiation per (pre-norm, epilogue) pair the
+    // span uses — normed input -> STORE / SWIGLU / GELU, raw input -> RESID
+    const bool hg = a.g != nullptr;
+    if ((a.norm == NORM_NONE) != (a.epi == EPI_RESID)) {   // other pairs: generic kernel
+      launch_norm<WT, NT, ND, RMAX, -1>(a, r0, rn, st);
+      return;
+    }
+    if (a.norm == NORM_NONE) {
+      launch_cfg<WT, NT, NORM_NONE, false, ND, RM, EPI_RESID>(a, r0, rn, st);
+      return;
+    }
+    auto pick = [&](auto ep) {
+      constexpr int E = decltype(ep)::value;
+      if (a.norm == NORM_RMS)
+        hg ? launch_cfg<WT, NT, NORM_RMS, true, ND, RM, E>(a, r0, rn, st)
+           : launch_cfg<WT, NT, NORM_RMS, false, ND, RM, E>(a, r0, rn, st);
+      else
+        hg ? launch_cfg<WT, NT, NORM_LN, true, ND, RM, E>(a, r0, rn, st)
+           : launch_cfg<WT, NT, NORM_LN, false, ND, RM, E>(a, r0, rn, st);
+    };
+    switch (a.epi) {
+      case EPI_STORE: pick(std::integral_constant<int, EPI_STORE>{}); break;
+      case EPI_SWIGLU: pick(std::integral_constant<int, EPI_SWIGLU>{}); break;
+      default: pick(std::integral_constant<int, EPI_GELU>{}); break;
+    }
   }
 }
 
