@@ -17,6 +17,11 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-Xptxas", "-v"]
+# developer builds with per-warp / per-CTA globaltimer tracing compiled in
+# (SP_GEMV_TRACE, SP_ATTN_TRACE, SP_TC_TRACE); off by default: the tracing
+# code would otherwise sit in the hot kernels' instruction footprint
+if os.environ.get("SP_BUILD_TRACE") == "1":
+    FLAGS = FLAGS + ["-DSP_DEV_TRACE=1"]
 
 
 def sources() -> list[str]:

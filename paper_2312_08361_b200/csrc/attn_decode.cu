@@ -36,7 +36,7 @@ constexpr int GMAX = 16;            // max query heads per kv head
 constexpr float kLog2e = 1.4426950408889634f;
 
 __device__ __forceinline__ void trace_mark(const AttnDecArgs& a, int ph) {
-  if (a.trace && threadIdx.x == 0) {
+  if (SP_DEV_TRACE && a.trace && threadIdx.x == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     a.trace[(blockIdx.y * gridDim.x + blockIdx.x) * 12 + ph] = t;
@@ -60,10 +60,11 @@ __device__ __forceinline__ float rope_val(const float* x, int dd, int half, cons
 // last-arriving CTA of (slot, kv head) merges all chunks in ascending order,
 // writes ctx and the per-head partial stats of ctx
 // LOG2: the partial maxima are in the log2 domain (scores pre-scaled by log2 e)
-template <int HD, bool LOG2>
-__device__ void merge_tail(const AttnDecArgs& a, int G, int slot, int kh, int chunk, int nchunk,
+template <int HD, bool LOG2, int GT = 0>
+__device__ void merge_tail(const AttnDecArgs& a, int G_rt, int slot, int kh, int chunk, int nchunk,
                            int T, const float (*wm)[GMAX], const float (*wl)[GMAX], float* wo,
                            float* pm, float* pl, int* last_flag, int CH = CHUNK) {
+  const int G = GT ? GT : G_rt;            // compile-time group size where known
   __shared__ float wf[4][GMAX];        // per (warp, head) rescale factors
   __shared__ float hM[GMAX], hL[GMAX];
   // ---- merge the 4 warps (fixed order) -> chunk partial ----
@@ -423,7 +424,7 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src, bool vali
                "l"(src), "r"(valid ? 16 : 0));
 }
 
-template <int HD>
+template <int HD, int GT>
 __global__ void __launch_bounds__(NTH) attn_dec_mma_kernel(AttnDecArgs a) {
   constexpr int RS = HD + 8;                      // padded smem row (bf16), breaks ldmatrix conflicts
   __shared__ __align__(16) __nv_bfloat16 qh[8][RS], ql[8][RS];      // [head][dim]
@@ -431,7 +432,7 @@ __global__ void __launch_bounds__(NTH) attn_dec_mma_kernel(AttnDecArgs a) {
   __shared__ float wm[4][GMAX], wl[4][GMAX];
   __shared__ int last_flag;
   extern __shared__ __align__(16) float dsm[];
-  const int G = a.H / a.kvh;
+  const int G = GT ? GT : a.H / a.kvh;   // query heads per kv head (compile-time when known)
   typedef __nv_bfloat16 Row[RS];
   // K/V of a 128-position sub-chunk, double-buffered: [2][4*32][RS] each.  A
   // CTA streams a.nsub sub-chunks (MHA shapes: many kv heads, few positions per
@@ -483,22 +484,6 @@ __global__ void __launch_bounds__(NTH) attn_dec_mma_kernel(AttnDecArgs a) {
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
   stage(0);
-  // L2 prefetch of the next kernel's weights: this CTA's share, in 64 KB
-  // bulk prefetches (cp.async.bulk.prefetch.L2) issued by one thread
-  if (a.l2_prefetch && threadIdx.x == 32) {
-    const int64_t nct = (int64_t)gridDim.x * gridDim.y;
-    const int64_t cta = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
-    const int64_t per = ((a.l2_prefetch_bytes + nct - 1) / nct + 15) / 16 * 16;
-    const int64_t b0 = cta * per;
-    const int64_t b1 = b0 + per < a.l2_prefetch_bytes ? b0 + per : a.l2_prefetch_bytes;
-    const char* base = reinterpret_cast<const char*>(a.l2_prefetch);
-    for (int64_t o = b0; o < b1; o += 65536) {
-      const int64_t n = b1 - o < 65536 ? b1 - o : 65536;
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + o),
-                   "r"((uint32_t)n)
-                   : "memory");
-    }
-  }
   trace_mark(a, 0);
   pdl_trigger();
   pdl_wait();        // q / k_new / v_new come from the QKV GEMV just before
@@ -687,11 +672,11 @@ __global__ void __launch_bounds__(NTH) attn_dec_mma_kernel(AttnDecArgs a) {
   trace_mark(a, 10);
   __syncthreads();
   trace_mark(a, 3);
-  merge_tail<HD, true>(a, G, slot, kh, chunk, nchunk, T, wm, wl, wo, pmv, plv, &last_flag, CH);
+  merge_tail<HD, true, GT>(a, G, slot, kh, chunk, nchunk, T, wm, wl, wo, pmv, plv, &last_flag, CH);
   trace_mark(a, 7);
 }
 
-template <int HD>
+template <int HD, int GT>
 void launch_mma(const AttnDecArgs& a_in, cudaStream_t st) {
   AttnDecArgs a = a_in;
   const int T = a.t0 + 1;
@@ -710,7 +695,7 @@ void launch_mma(const AttnDecArgs& a_in, cudaStream_t st) {
   static size_t set[kMaxDevices] = {};
   const int dv = current_device();
   if (smem > set[dv]) {
-    cudaFuncSetAttribute(attn_dec_mma_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(attn_dec_mma_kernel<HD, GT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
     set[dv] = smem;
   }
@@ -725,7 +710,7 @@ void launch_mma(const AttnDecArgs& a_in, cudaStream_t st) {
     cudaMemsetAsync(tbuf, 0, tn * 8, st);
     b.trace = tbuf;
   }
-  launch_pdl(attn_dec_mma_kernel<HD>, grid, dim3(NTH), smem, st, b);
+  launch_pdl(attn_dec_mma_kernel<HD, GT>, grid, dim3(NTH), smem, st, b);
   count_launch();
   if (tr) {
     std::vector<unsigned long long> h(tn);
@@ -791,8 +776,18 @@ int64_t attn_dec_part_floats(int width, int H, int hd, int max_pages) {
 void launch_attn_decode_fused(const AttnDecArgs& a, cudaStream_t st) {
   const int G = a.H / a.kvh;
   if (a.kv_dtype == kKVBF16 && G <= 8 && (a.hd == 64 || a.hd == 128)) {
-    if (a.hd == 128) launch_mma<128>(a, st);
-    else launch_mma<64>(a, st);
+    // group size as a template constant for the shapes we serve (70B: 8,
+    // MHA/BLOOM: 1); others keep it at run time
+    auto go = [&](auto hdc) {
+      constexpr int HDv = decltype(hdc)::value;
+      switch (G) {
+        case 8: launch_mma<HDv, 8>(a, st); break;
+        case 1: launch_mma<HDv, 1>(a, st); break;
+        default: launch_mma<HDv, 0>(a, st); break;
+      }
+    };
+    if (a.hd == 128) go(std::integral_constant<int, 128>{});
+    else go(std::integral_constant<int, 64>{});
     return;
   }
   if (a.kv_dtype == kKVBF16) dispatch<__nv_bfloat16>(a, st);

@@ -79,6 +79,11 @@ __host__ __device__ __forceinline__ int64_t cm_offset(int64_t n, int64_t kb, int
   return ((g * (Kbytes >> 5) + kt) * 2 + kc) * 2048 + r8 * 128 + rr * 16 + b;
 }
 
+// device-side phase tracing (tools): compiled in only with -DSP_DEV_TRACE=1
+#ifndef SP_DEV_TRACE
+#define SP_DEV_TRACE 0
+#endif
+
 // host-side count of kernels launched by this library (bench `gpu_launches`)
 void count_launch();
 

@@ -39,7 +39,6 @@ struct GemvArgs {
   int* counters;          // split-K arrival counters per row group (zero at rest)
   unsigned long long* trace;   // debug (SP_GEMV_TRACE): per-warp phase timestamps, or null
   int pre_stages;         // ring stages prefetched before griddepcontrol.wait (set by the launcher)
-  int l2_prefetch;        // further units of the warp's slice prefetched into L2 before the wait
 };
 
 int64_t gemv3_ws_bytes(int64_t N, int Rmax);
@@ -70,8 +69,6 @@ struct AttnDecArgs {
   RowStat* st_out;               // [H][width] partial stats of ctx (P = H)
   unsigned long long* trace;     // debug (SP_ATTN_TRACE): per-CTA phase timestamps, or null
   int nsub;                      // 128-position sub-chunks streamed per CTA (MMA kernel; 0 = 1)
-  const void* l2_prefetch;       // next kernel's weights to pull into L2 (or null)
-  int64_t l2_prefetch_bytes;
 };
 
 void launch_attn_decode_fused(const AttnDecArgs& a, cudaStream_t st);

@@ -426,7 +426,7 @@ __device__ __forceinline__ void mma_commit_x2(uint64_t* bar) {
 }
 
 __device__ __forceinline__ void tc_trace(const TcGemmArgs& a, int ph) {
-  if (a.trace) {
+  if (SP_DEV_TRACE && a.trace) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     a.trace[((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * 4 + ph] = t;

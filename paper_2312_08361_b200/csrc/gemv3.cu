@@ -131,7 +131,7 @@ __device__ __forceinline__ uint32_t digits4(int q0, int q1, int q2, int q3, int 
 
 // debug trace: per warp [start, after pdl_wait, after prologue, first stage, mainloop end, exit]
 __device__ __forceinline__ void gtrace(const GemvArgs& a, int ph) {
-  if (a.trace && (threadIdx.x & 31) == 0) {
+  if (SP_DEV_TRACE && a.trace && (threadIdx.x & 31) == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     a.trace[((int64_t)blockIdx.x * NW + (threadIdx.x >> 5)) * 8 + ph] = t;
@@ -191,15 +191,6 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
       tma_load_1d(ring + i * STAGE_BYTES, wbase + ((u / KT) * KT + u % KT) * UNIT_BYTES,
                   UNIT_BYTES, &ws_->bar[i], policy);
     }
-  // ...and the next l2_prefetch units of the slice into L2 (one bulk prefetch;
-  // the slice is contiguous), so the start of the stream after the wait hits
-  // L2 while the previous kernel's tail leaves DRAM bandwidth unused
-  if (lane == 0 && nunits > npre && a.l2_prefetch > 0) {
-    const int np = (nunits - npre) < a.l2_prefetch ? (nunits - npre) : a.l2_prefetch;
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(wbase + (u0 + npre) * UNIT_BYTES),
-                 "r"((uint32_t)np * UNIT_BYTES)
-                 : "memory");
-  }
   pdl_trigger();
   pdl_wait();
   gtrace(a, 1);
@@ -551,9 +542,7 @@ void launch_cfg(const GemvArgs& a, int r0, int rn, cudaStream_t st) {
   static int ncall = 0;   // per instantiation
   GemvArgs b = a;
   static int pre = getenv("SP_GEMV_PRE") ? atoi(getenv("SP_GEMV_PRE")) : STAGES;
-  static int l2pf = getenv("SP_GEMV_L2PF") ? atoi(getenv("SP_GEMV_L2PF")) : 0;  // measured: hurts
   b.pre_stages = pre;
-  b.l2_prefetch = l2pf;
   const bool tr = trace_call >= 0 && ncall++ == trace_call;
   const size_t tn = (size_t)grid * NW * 8;
   unsigned long long* tbuf = nullptr;

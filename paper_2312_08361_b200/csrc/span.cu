@@ -37,7 +37,6 @@ static std::atomic<int64_t> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 bool g_pdl = true;
 extern bool g_attn_hilo;   // attn_prefill.cu
-bool g_attn_l2pf = false;  // option 4 (measured: slower, off)
 extern int g_attn_nsub;    // attn_decode.cu, option 5
 }  // namespace sp
 
@@ -404,10 +403,6 @@ int run_span_decode_tc(sp_span* s, sp_kv* kv, int b0, int b1, float* y, int widt
       const double kvb = (double)width * (kv->length + 1) * 2 * s->kv * kv_elt;
       ProfScope ps(s, PC_ATTN_DEC, kvb + 4.0 * R * (s->n_qkv + d),
                    4.0 * width * (kv->length + 1) * s->H * s->hd, st);
-      // the O projection's weights are pulled into L2 by the attention CTAs
-      // while attention is latency-bound and HBM idle (read once, evict-first)
-      at.l2_prefetch = g_attn_l2pf ? W.o : nullptr;
-      at.l2_prefetch_bytes = (int64_t)d * d * elt_bytes(wd);
       launch_attn_decode_fused(at, st);
     }
     // 3) x += ctx @ Wo      (stats for norm2)
@@ -986,7 +981,6 @@ int sp_span_set_option(sp_span* s, int32_t option, int32_t value) {
   else if (option == 1) g_pdl = value != 0;
   else if (option == 2) g_tc_pair = value != 0;
   else if (option == 3) g_attn_hilo = value != 0;
-  else if (option == 4) g_attn_l2pf = value != 0;
   else if (option == 5) g_attn_nsub = value;
   else SP_FAIL(SP_ERR_ARG, "unknown option");
   return SP_OK;
