@@ -16,8 +16,8 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-OUT = os.path.join(ROOT, "gpurun_out")
-PROF = os.path.join(ROOT, "profiles")
+OUT = os.environ.get("NCU_OUT", os.path.join(ROOT, "gpurun_out"))
+PROF = os.environ.get("NCU_PROF", os.path.join(ROOT, "profiles"))
 
 KEYS = [
     ("gpu__time_duration.sum", "duration"),

@@ -27,3 +27,9 @@ $T ncu --set full --clock-control none --import-source on -k regex:"gemm_i8_tc2"
     -o gpurun_out/${TAG}_pair_gemm python bench.py --no-cpu --blocks 1 --steps 2 > gpurun_out/ncu_pg.log 2>&1; echo "pair gemm rc=$?"
 $T ncu --set full --clock-control none --import-source on -k regex:"attn_prefill|digitize_reg" -s 5 -c 2 \
     -o gpurun_out/${TAG}_prefill python bench.py --no-cpu --blocks 1 --steps 2 > gpurun_out/ncu_prefill.log 2>&1; echo "prefill rc=$?"
+# summaries written next to the reports (gpurun_out/ travels back; the raw
+# .ncu-rep files are dropped unless KEEP_REPS=1 — together they exceed 64 MiB)
+mkdir -p gpurun_out/prof_${TAG}
+cp gpurun_out/${TAG}_launches.csv gpurun_out/${TAG}_prefill_launches.csv gpurun_out/prof_${TAG}/ 2>/dev/null
+NCU_PROF=gpurun_out/prof_${TAG} python tools/ncu_summary.py ${TAG}
+[ "$KEEP_REPS" == "1" ] || rm -f gpurun_out/${TAG}_*.ncu-rep
