@@ -38,7 +38,6 @@ struct GemvArgs {
   long long* ws;          // split-K int64 accumulators [R][N] (int8) / f32 partials (bf16)
   int* counters;          // split-K arrival counters per row group (zero at rest)
   unsigned long long* trace;   // debug (SP_GEMV_TRACE): per-warp phase timestamps, or null
-  int pre_stages;         // ring stages prefetched before griddepcontrol.wait (set by the launcher)
 };
 
 int64_t gemv3_ws_bytes(int64_t N, int Rmax);

@@ -165,8 +165,19 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
   WarpSmem* ws_ = reinterpret_cast<WarpSmem*>(dyn + (size_t)NW * STAGES * STAGE_BYTES) + warp;
 
   const int64_t gw = (int64_t)blockIdx.x * NW + warp;
-  const int64_t u0 = gw * units / warps_total, u1 = (gw + 1) * units / warps_total;
-  const int64_t KT = a.K / KTILE;
+  // unit indices fit 32 bits (units = N/128 * K/KTILE < 2^31); the slice
+  // bounds floor(gw * units / W) use one double division with an exact
+  // integer fix-up instead of two 64-bit divisions (code size: see DESIGN)
+  const int W32 = (int)warps_total, U32 = (int)units;
+  auto slice_bound = [&](int w) {
+    const long long num = (long long)w * U32;
+    int q = (int)((double)num / (double)W32);
+    if ((long long)q * W32 > num) --q;
+    else if ((long long)(q + 1) * W32 <= num) ++q;
+    return q;
+  };
+  const int u0 = slice_bound((int)gw), u1 = slice_bound((int)gw + 1);
+  const int KT = (int)(a.K / KTILE);
 
   gtrace(a, 0);
   if (lane == 0) {
@@ -180,15 +191,15 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
   uint64_t policy_x;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(policy_x));
   const int nunits = u1 > u0 ? (int)(u1 - u0) : 0;
-  const int npre = nunits < a.pre_stages ? nunits : a.pre_stages;
+  const int npre = nunits < STAGES ? nunits : STAGES;   // the whole ring before the wait
   // ---- before the dependency: the weights of the first STAGES units (no
   // kernel writes weights), so their DRAM latency overlaps the previous
   // kernel's tail; each stage's barrier also expects its activation bytes ----
   if (lane == 0)
     for (int i = 0; i < npre; ++i) {
-      const int64_t u = u0 + i;
+      const int64_t u = (int64_t)u0 + i;
       mbar_expect_tx(&ws_->bar[i], UNIT_BYTES + Rn * XB);
-      tma_load_1d(ring + i * STAGE_BYTES, wbase + ((u / KT) * KT + u % KT) * UNIT_BYTES,
+      tma_load_1d(ring + i * STAGE_BYTES, wbase + u * UNIT_BYTES,
                   UNIT_BYTES, &ws_->bar[i], policy);
     }
   pdl_trigger();
@@ -204,7 +215,7 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
     float S[RM], Q[RM], M[RM];
 #pragma unroll
     for (int r = 0; r < RM; ++r) { S[r] = 0.f; Q[r] = 0.f; M[r] = 0.f; }
-    constexpr int PU = 4;
+    constexpr int PU = RM == 1 ? 2 : 4;   // P_in <= 2 * 256 for one row
     for (int p0 = threadIdx.x; p0 < a.P_in; p0 += PU * NW * 32) {
 #pragma unroll
       for (int r = 0; r < RM; ++r) {
@@ -222,7 +233,7 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
       }
     }
   if (lane == 0)
-    for (int i = 0, kt0 = (int)(u0 % KT); i < npre; ++i) {   // x chunks of the prefetched units
+    for (int i = 0, kt0 = u0 % KT; i < npre; ++i) {   // x chunks of the prefetched units
       // (issued right behind the stats loads, ahead of their reduction)
       const int64_t kt = kt0 + i < KT ? kt0 + i : kt0 + i - KT;
       for (int r = 0; r < (RM == 1 ? 1 : Rn); ++r)
@@ -295,7 +306,7 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
 
   // ---- TMA producer (lane 0) ----
   // producer state (lane 0): next unit to issue as (group, k-tile, ring stage)
-  int p_grp = (int)((u0 + npre) / KT), p_kt = (int)((u0 + npre) % KT);
+  int p_grp = (u0 + npre) / KT, p_kt = (u0 + npre) % KT;
   int p_st = npre % STAGES, p_left = nunits - npre;
   auto issue_next = [&]() {
     // the unit's weights and, alongside, each batch row's activation chunk:
@@ -311,14 +322,12 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
     if (++p_st == STAGES) p_st = 0;
     --p_left;
   };
-  if (lane == 0)                          // stages not prefetched before the dependency
-    for (int i = npre; i < STAGES && p_left > 0; ++i) issue_next();
   __syncwarp();
 
   // ---- activation side: read from the stage (arrived with the weights) ----
   XVec xc[NT][2], gc[NT][2];
   constexpr int KOFF = (WT == kI8) ? 16 : 8;
-  int c_grp = (int)(u0 / KT), c_kt = (int)(u0 % KT), c_st = 0;
+  int c_grp = u0 / KT, c_kt = u0 % KT, c_st = 0;
   uint32_t c_ph = 0;
 
   using AccT = typename std::conditional<WT == kI8, int, float>::type;
@@ -541,8 +550,6 @@ void launch_cfg(const GemvArgs& a, int r0, int rn, cudaStream_t st) {
   static int trace_call = getenv("SP_GEMV_TRACE") ? atoi(getenv("SP_GEMV_TRACE")) : -1;
   static int ncall = 0;   // per instantiation
   GemvArgs b = a;
-  static int pre = getenv("SP_GEMV_PRE") ? atoi(getenv("SP_GEMV_PRE")) : STAGES;
-  b.pre_stages = pre;
   const bool tr = trace_call >= 0 && ncall++ == trace_call;
   const size_t tn = (size_t)grid * NW * 8;
   unsigned long long* tbuf = nullptr;
