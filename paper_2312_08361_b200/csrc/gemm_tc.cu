@@ -139,16 +139,20 @@ __device__ __forceinline__ float gelu_f(float x) {
 // TMEM columns: plane p, group j, channel c -> p * 256 + j * 128 + c (both
 // kernels).  D = D0 * 256 + D1 is exact (int64); y = f32(D) * 2^(e-14) * wscale.
 // All TMEM loads of a chunk are issued before one wait.
+// BF: bf16 operands (hi + lo f32 accumulators); EP >= 0: epilogue type fixed
+// at compile time (only that variant's code is emitted), -1: a.epi at run time
+template <bool BF, int EP>
 __device__ __forceinline__ void epilogue_group(const TcGemmArgs& a, uint32_t tb, int j, int ng0,
                                                int64_t m, bool valid, float ys) {
   const int64_t n0 = (int64_t)(ng0 + j) * 128;
   const float* wsc = a.wscale ? a.wscale + n0 : nullptr;
   // int8: D = D0 * 256 + D1 exact in int64; bf16: hi + lo f32 accumulators
-  const bool bf = a.bf16 != 0;
-  auto comb = [bf](int x0, int x1) {
-    return bf ? __int_as_float(x0) + __int_as_float(x1) : (float)((long long)x0 * 256 + x1);
+  auto comb = [](int x0, int x1) {
+    if constexpr (BF) return __fadd_rn(__int_as_float(x0), __int_as_float(x1));
+    else return (float)((long long)x0 * 256 + x1);
   };
-  if (a.epi == EPI_SWIGLU) {
+  const int epi = EP >= 0 ? EP : a.epi;
+  if (epi == EPI_SWIGLU) {
     // group = [gate 64 | up 64] of outputs (ng0 + j) * 64 + c
     for (int c0 = 0; c0 < 64; c0 += 32) {
       int g0[32], g1[32], u0[32], u1[32];
@@ -165,9 +169,11 @@ __device__ __forceinline__ void epilogue_group(const TcGemmArgs& a, uint32_t tb,
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const int cc = c + e;
-          const float gd = comb(g0[cc], g1[cc]) * ys * (wsc ? __ldg(wsc + c0 + cc) : 1.f);
-          const float ud = comb(u0[cc], u1[cc]) * ys * (wsc ? __ldg(wsc + 64 + c0 + cc) : 1.f);
-          o4[e] = __fdividef(gd, 1.0f + __expf(-gd)) * ud;
+          // explicit roundings (no FMA contraction): every instantiation and both
+          // GEMM kernels give bit-identical outputs
+          const float gd = __fmul_rn(__fmul_rn(comb(g0[cc], g1[cc]), ys), wsc ? __ldg(wsc + c0 + cc) : 1.f);
+          const float ud = __fmul_rn(__fmul_rn(comb(u0[cc], u1[cc]), ys), wsc ? __ldg(wsc + 64 + c0 + cc) : 1.f);
+          o4[e] = __fmul_rn(__fdividef(gd, __fadd_rn(1.0f, __expf(-gd))), ud);
         }
         *reinterpret_cast<float4*>(out + c) = make_float4(o4[0], o4[1], o4[2], o4[3]);
       }
@@ -184,7 +190,7 @@ __device__ __forceinline__ void epilogue_group(const TcGemmArgs& a, uint32_t tb,
 #pragma unroll
       for (int c = 0; c < 32; c += 4) {
         float r4[4] = {0.f, 0.f, 0.f, 0.f};
-        if (a.epi == EPI_RESID) {
+        if (epi == EPI_RESID) {
           const float4 rr = *reinterpret_cast<const float4*>(res + c);
           r4[0] = rr.x; r4[1] = rr.y; r4[2] = rr.z; r4[3] = rr.w;
         }
@@ -192,9 +198,9 @@ __device__ __forceinline__ void epilogue_group(const TcGemmArgs& a, uint32_t tb,
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const int cc = c + e;
-          float v = comb(v0[cc], v1[cc]) * ys * (wsc ? __ldg(wsc + c0 + cc) : 1.f);
-          if (a.epi == EPI_RESID) v += r4[e];
-          else if (a.epi == EPI_GELU) v = gelu_f(v);
+          float v = __fmul_rn(__fmul_rn(comb(v0[cc], v1[cc]), ys), wsc ? __ldg(wsc + c0 + cc) : 1.f);
+          if (epi == EPI_RESID) v = __fadd_rn(v, r4[e]);
+          else if (epi == EPI_GELU) v = gelu_f(v);
           o4[e] = v;
         }
         *reinterpret_cast<float4*>(out + c) = make_float4(o4[0], o4[1], o4[2], o4[3]);
@@ -238,15 +244,15 @@ __device__ __forceinline__ void finish_tile(const TcGemmArgs& a, int mt, int ng0
     const int64_t n0 = (int64_t)(ng0 + j) * 128;
     long long* wr = ws + m * a.N + n0;
     if (swiglu) {
-      const float gd = (float)__ldcg(wr + c) * ys * __ldg(a.wscale + n0 + c);
-      const float ud = (float)__ldcg(wr + 64 + c) * ys * __ldg(a.wscale + n0 + 64 + c);
+      const float gd = __fmul_rn(__fmul_rn((float)__ldcg(wr + c), ys), __ldg(a.wscale + n0 + c));
+      const float ud = __fmul_rn(__fmul_rn((float)__ldcg(wr + 64 + c), ys), __ldg(a.wscale + n0 + 64 + c));
       wr[c] = 0;
       wr[64 + c] = 0;
-      a.y[m * a.ldy + (ng0 + j) * 64 + c] = __fdividef(gd, 1.0f + __expf(-gd)) * ud;
+      a.y[m * a.ldy + (ng0 + j) * 64 + c] = __fmul_rn(__fdividef(gd, __fadd_rn(1.0f, __expf(-gd))), ud);
     } else {
-      float v = (float)__ldcg(wr + c) * ys * __ldg(a.wscale + n0 + c);
+      float v = __fmul_rn(__fmul_rn((float)__ldcg(wr + c), ys), __ldg(a.wscale + n0 + c));
       wr[c] = 0;
-      if (a.epi == EPI_RESID) v += a.res[m * a.ldy + n0 + c];
+      if (a.epi == EPI_RESID) v = __fadd_rn(v, a.res[m * a.ldy + n0 + c]);
       else if (a.epi == EPI_GELU) v = gelu_f(v);
       a.y[m * a.ldy + n0 + c] = v;
     }
@@ -339,7 +345,7 @@ __global__ void __launch_bounds__(256, 1) gemm_i8_tc_kernel(TcGemmArgs a) {
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
     if (S == 1) {
       const float ys = (valid && !BF) ? ldexpf(1.0f, a.exps[m] - 14) : 1.f;
-      for (int j = 0; j < NGRP; ++j) epilogue_group(a, tbase + lane_addr, j, ng0, m, valid, ys);
+      for (int j = 0; j < NGRP; ++j) epilogue_group<BF, -1>(a, tbase + lane_addr, j, ng0, m, valid, ys);
     } else {
       for (int j = 0; j < NGRP; ++j) partial_group(a, tbase + lane_addr, j, ng0, m, valid);
       __threadfence();
@@ -433,7 +439,7 @@ __device__ __forceinline__ void tc_trace(const TcGemmArgs& a, int ph) {
   }
 }
 
-template <int KUP, int STAGES2, bool BF>
+template <int KUP, int STAGES2, bool BF, int EP>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     gemm_i8_tc2_kernel(TcGemmArgs a) {
   constexpr int A2_BYTES = 2 * KUP * UNIT;   // two digit planes, 128 tokens
@@ -535,7 +541,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     const bool valid = m < a.M;
     const float ys = (valid && !BF) ? ldexpf(1.0f, a.exps[m] - 14) : 1.f;
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
-    epilogue_group(a, tbase + lane_addr, warp >> 2, ng0, m, valid, ys);
+    epilogue_group<BF, EP>(a, tbase + lane_addr, warp >> 2, ng0, m, valid, ys);
   }
   if (threadIdx.x == 128) tc_trace(a, 2);
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -833,13 +839,13 @@ void launch_digitize(const float* x, int64_t ldx, int64_t M, int64_t K, int norm
   count_launch();
 }
 
-template <int KUP, int ST, bool BF>
+template <int KUP, int ST, bool BF, int EP>
 void launch_pair(const TcGemmArgs& a, cudaStream_t st) {
   static bool set2[kMaxDevices] = {};
   const int dv = current_device();
   const size_t smem2 = (size_t)ST * 3 * KUP * UNIT;
   if (!set2[dv]) {
-    cudaFuncSetAttribute(gemm_i8_tc2_kernel<KUP, ST, BF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(gemm_i8_tc2_kernel<KUP, ST, BF, EP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem2);
     set2[dv] = true;
   }
@@ -855,7 +861,7 @@ void launch_pair(const TcGemmArgs& a, cudaStream_t st) {
     cudaMalloc(&b.trace, tn * 8);
     cudaMemsetAsync(b.trace, 0, tn * 8, st);
   }
-  gemm_i8_tc2_kernel<KUP, ST, BF><<<grid2, 256, smem2, st>>>(b);
+  gemm_i8_tc2_kernel<KUP, ST, BF, EP><<<grid2, 256, smem2, st>>>(b);
   count_launch();
   if (tr) {
     std::vector<unsigned long long> h(tn);
@@ -876,9 +882,20 @@ void launch_gemm_i8_tc(const TcGemmArgs& a, cudaStream_t st) {
   // does half the padded MMA work of a 256-token pair tile
   if (g_tc_pair && a.M > 128) {
     static int cfg = getenv("SP_TC_CFG") ? atoi(getenv("SP_TC_CFG")) : 0;
-    if (a.bf16) launch_pair<4, 4, true>(a, st);
-    else if (cfg == 1) launch_pair<2, 8, false>(a, st);
-    else launch_pair<4, 4, false>(a, st);
+    (void)cfg;
+    // one instantiation per (operand type, epilogue): each kernel carries only
+    // its own epilogue's code (the GELU variant alone is ~12 KB of SASS)
+    auto go = [&](auto bfc) {
+      constexpr bool B = decltype(bfc)::value;
+      switch (a.epi) {
+        case EPI_STORE: launch_pair<4, 4, B, EPI_STORE>(a, st); break;
+        case EPI_RESID: launch_pair<4, 4, B, EPI_RESID>(a, st); break;
+        case EPI_SWIGLU: launch_pair<4, 4, B, EPI_SWIGLU>(a, st); break;
+        default: launch_pair<4, 4, B, EPI_GELU>(a, st); break;
+      }
+    };
+    if (a.bf16) go(std::true_type{});
+    else go(std::false_type{});
     return;
   }
   static bool set[kMaxDevices][2] = {};
