@@ -259,7 +259,7 @@ __device__ __forceinline__ void finish_tile(const TcGemmArgs& a, int mt, int ng0
   }
 }
 
-template <bool BF>
+template <bool BF, int EP>
 __global__ void __launch_bounds__(256, 1) gemm_i8_tc_kernel(TcGemmArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], tmem_full;
@@ -345,7 +345,7 @@ __global__ void __launch_bounds__(256, 1) gemm_i8_tc_kernel(TcGemmArgs a) {
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
     if (S == 1) {
       const float ys = (valid && !BF) ? ldexpf(1.0f, a.exps[m] - 14) : 1.f;
-      for (int j = 0; j < NGRP; ++j) epilogue_group<BF, -1>(a, tbase + lane_addr, j, ng0, m, valid, ys);
+      for (int j = 0; j < NGRP; ++j) epilogue_group<BF, EP>(a, tbase + lane_addr, j, ng0, m, valid, ys);
     } else {
       for (int j = 0; j < NGRP; ++j) partial_group(a, tbase + lane_addr, j, ng0, m, valid);
       __threadfence();
@@ -877,6 +877,34 @@ void launch_pair(const TcGemmArgs& a, cudaStream_t st) {
   }
 }
 
+template <bool BF, int EP>
+void launch_single_t(const TcGemmArgs& b, dim3 grid, cudaStream_t st) {
+  static bool set[kMaxDevices] = {};
+  const int dv = current_device();
+  const size_t smem = (size_t)STAGES * STAGE;
+  if (!set[dv]) {
+    cudaFuncSetAttribute(gemm_i8_tc_kernel<BF, EP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    set[dv] = true;
+  }
+  gemm_i8_tc_kernel<BF, EP><<<grid, 256, smem, st>>>(b);
+}
+
+// one instantiation per (operand type, epilogue), like the pair kernel
+void launch_single(const TcGemmArgs& b, dim3 grid, cudaStream_t st) {
+  auto go = [&](auto bfc) {
+    constexpr bool B = decltype(bfc)::value;
+    switch (b.epi) {
+      case EPI_STORE: launch_single_t<B, EPI_STORE>(b, grid, st); break;
+      case EPI_RESID: launch_single_t<B, EPI_RESID>(b, grid, st); break;
+      case EPI_SWIGLU: launch_single_t<B, EPI_SWIGLU>(b, grid, st); break;
+      default: launch_single_t<B, EPI_GELU>(b, grid, st); break;
+    }
+  };
+  if (b.bf16) go(std::true_type{});
+  else go(std::false_type{});
+}
+
 void launch_gemm_i8_tc(const TcGemmArgs& a, cudaStream_t st) {
   // up to 128 tokens (wide decode, short prompts): one 128-token tile per CTA
   // does half the padded MMA work of a 256-token pair tile
@@ -898,18 +926,6 @@ void launch_gemm_i8_tc(const TcGemmArgs& a, cudaStream_t st) {
     else go(std::false_type{});
     return;
   }
-  static bool set[kMaxDevices][2] = {};
-  const int dv = current_device();
-  const size_t smem = (size_t)STAGES * STAGE;
-  if (!set[dv][a.bf16 ? 1 : 0]) {
-    if (a.bf16)
-      cudaFuncSetAttribute(gemm_i8_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)smem);
-    else
-      cudaFuncSetAttribute(gemm_i8_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)smem);
-    set[dv][a.bf16 ? 1 : 0] = true;
-  }
   TcGemmArgs b = a;
   const int tiles = (int)(((a.M + BM - 1) / BM) * (a.N / (128 * NGRP)));
   const int kbt = (int)(a.K / 32 / KU);
@@ -921,8 +937,7 @@ void launch_gemm_i8_tc(const TcGemmArgs& a, cudaStream_t st) {
   }
   b.ksplit = S;
   dim3 grid((unsigned)((a.M + BM - 1) / BM), (unsigned)(a.N / (128 * NGRP)), (unsigned)S);
-  if (a.bf16) gemm_i8_tc_kernel<true><<<grid, 256, smem, st>>>(b);
-  else gemm_i8_tc_kernel<false><<<grid, 256, smem, st>>>(b);
+  launch_single(b, grid, st);
   count_launch();
 }
 
