@@ -75,7 +75,7 @@ __device__ void merge_tail(const AttnDecArgs& a, int G_rt, int slot, int kh, int
       if (chunk * CH + w * 32 < T) M = fmaxf(M, wm[w][g]);
     float L = 0.f;
     for (int w = 0; w < 4; ++w) {
-      const float f = (chunk * CH + w * 32 < T) ? (LOG2 ? exp2f(wm[w][g] - M) : expf(wm[w][g] - M))
+      const float f = (chunk * CH + w * 32 < T) ? (LOG2 ? ex2_approx(wm[w][g] - M) : expf(wm[w][g] - M))
                                                    : 0.f;  // empty warp: 0
       wf[w][g] = f;
       L = fmaf(wl[w][g] * (f > 0.f ? 1.f : 0.f), f, L);
@@ -156,7 +156,7 @@ __device__ void merge_tail(const AttnDecArgs& a, int G_rt, int slot, int kh, int
       const float M = warp_max(m);
       float L = 0.f;
       for (int c = lane; c < nchunk; c += 32) {
-        const float f = LOG2 ? exp2f(pm[c * GMAX + g] - M) : expf(pm[c * GMAX + g] - M);
+        const float f = LOG2 ? ex2_approx(pm[c * GMAX + g] - M) : expf(pm[c * GMAX + g] - M);
         pm[c * GMAX + g] = f;
         L = fmaf(pl[c * GMAX + g], f, L);
       }
@@ -612,14 +612,14 @@ __global__ void __launch_bounds__(NTH) attn_dec_mma_kernel(AttnDecArgs a) {
       mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
       mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
       const float mnew = fmaxf(m2[hc], mx);
-      alpha[hc] = (m2[hc] == -INFINITY) ? 0.f : exp2f(m2[hc] - mnew);
+      alpha[hc] = (m2[hc] == -INFINITY) ? 0.f : ex2_approx(m2[hc] - mnew);
       float sum = 0.f;
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
           const int pos = mt * 16 + g8 + hh * 8;
-          const float e = (pos < nv) ? exp2f(sacc[mt][hh * 2 + hc] - mnew) : 0.f;
+          const float e = (pos < nv) ? ex2_approx(sacc[mt][hh * 2 + hc] - mnew) : 0.f;
           sum += e;
           const __nv_bfloat16 h = __float2bfloat16_rn(e);
           ph[warp][head][pos] = h;

@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(NWARP * 32) attn_prefill_mma_kernel(AttnArgs a
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
       mnew[r] = fmaxf(mrow[r], tmax[r]);
-      alpha[r] = (mnew[r] == -INFINITY) ? 1.f : exp2f(mrow[r] - mnew[r]);
+      alpha[r] = (mnew[r] == -INFINITY) ? 1.f : ex2_approx(mrow[r] - mnew[r]);
     }
     uint32_t ph[KTL / 16][4], pl[KTL / 16][4];
 #pragma unroll
@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(NWARP * 32) attn_prefill_mma_kernel(AttnArgs a
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const float mr = mnew[j >> 1];
-        p[j] = (s[nt][j] == -INFINITY) ? 0.f : exp2f(s[nt][j] - mr);
+        p[j] = (s[nt][j] == -INFINITY) ? 0.f : ex2_approx(s[nt][j] - mr);
         psum[j >> 1] += p[j];
       }
       // C layout of two n-tiles == A layout of one k16 step of P
@@ -220,18 +220,19 @@ __global__ void __launch_bounds__(NWARP * 32) attn_prefill_mma_kernel(AttnArgs a
     }
     __syncthreads();
   }
-  // ---- write ctx rows ----
+  // ---- write ctx rows (one reciprocal per row, then multiplies) ----
+  const float inv0 = __frcp_rn(lrow[0]), inv1 = __frcp_rn(lrow[1]);
   const int ra = qrow0 + g8, rb = ra + 8;
 #pragma unroll
   for (int i = 0; i < HD / 8; ++i) {
     const int dim = i * 8 + 2 * t4;
     if (ra < a.n_new) {
       float* dst = a.ctx + (int64_t)(slot * a.n_new + ra) * a.H * HD + h * HD + dim;
-      *reinterpret_cast<float2*>(dst) = make_float2(o[i][0] / lrow[0], o[i][1] / lrow[0]);
+      *reinterpret_cast<float2*>(dst) = make_float2(o[i][0] * inv0, o[i][1] * inv0);
     }
     if (rb < a.n_new) {
       float* dst = a.ctx + (int64_t)(slot * a.n_new + rb) * a.H * HD + h * HD + dim;
-      *reinterpret_cast<float2*>(dst) = make_float2(o[i][2] / lrow[1], o[i][3] / lrow[1]);
+      *reinterpret_cast<float2*>(dst) = make_float2(o[i][2] * inv1, o[i][3] * inv1);
     }
   }
 }

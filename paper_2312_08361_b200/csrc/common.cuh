@@ -79,6 +79,14 @@ __host__ __device__ __forceinline__ int64_t cm_offset(int64_t n, int64_t kb, int
   return ((g * (Kbytes >> 5) + kt) * 2 + kc) * 2048 + r8 * 128 + rr * 16 + b;
 }
 
+// 2^x on the SFU (MUFU.EX2, ~2^-22 relative error): the bf16-class softmax of
+// the attention kernels; exp2f() carries a multi-instruction accurate path
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // device-side phase tracing (tools): compiled in only with -DSP_DEV_TRACE=1
 #ifndef SP_DEV_TRACE
 #define SP_DEV_TRACE 0
