@@ -43,10 +43,6 @@ struct GemvArgs {
 int64_t gemv3_ws_bytes(int64_t N, int Rmax);
 int64_t gemv3_counters(int64_t N);
 void launch_gemv3(int wdtype, const GemvArgs& a, cudaStream_t st);
-int64_t gemv2_ws_bytes(int wdtype, int64_t N, int64_t K, int Rmax);
-int64_t gemv2_counters(int64_t N);
-int gemv2_groups(int64_t N);     // producer partial count of st_out for a [N] output
-void launch_gemv2(int wdtype, const GemvArgs& a, cudaStream_t st);
 
 // statistics of the span input rows (producer for the first block's norm)
 void launch_row_stats(const float* x, int R, int64_t d, const float* g_next, RowStat* st_out,

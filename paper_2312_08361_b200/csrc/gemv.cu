@@ -1,7 +1,7 @@
 // Decode linear layers for f32 weights (the reference toy model, which is
 // computed in f32 end to end, SP/model.py:9 and SURVEY.md §0.8): warp per
 // output channel, fixed shuffle-tree reduction (deterministic, batch-invariant).
-// bf16 / int8 weights use the tensor-pipe GEMV in gemv2.cu.
+// bf16 / int8 weights use the tensor-pipe GEMV in gemv3.cu.
 #include "common.cuh"
 #include "kernels.cuh"
 
