@@ -19,6 +19,8 @@
  *                               (block_forward_batched + KVCache.append,
  *                                SP/model.py:244-280, :163-167)
  *   sp_span_forward_stateless<- RealServerEngine.forward      SP/server.py:106-125
+ *   sp_span_block_backward   <- block_backward (per block of RealServerEngine.backward)
+ *                                                      SP/model.py:320-381, SP/server.py:127-139
  *   sp_kv_reorder            <- RealServerEngine.reorder / KVCache.gather
  *                                                      SP/server.py:102-104, SP/model.py:169-175
  *   sp_kv_read               <- KVCache.keys / .values views (test access,
@@ -128,6 +130,13 @@ int sp_span_forward(sp_span* span, sp_kv* kv, int32_t block_begin, int32_t block
 int sp_span_forward_stateless(sp_span* span, int32_t block_begin, int32_t block_end,
                               const float* x, float* y, float* record, int32_t batch,
                               int32_t tokens, void* stream);
+/* prompt-tuning backward of one block: dx = (d block / d x)^T dy for `batch`
+ * sequences of `tokens` rows, recomputing the forward from the recorded block
+ * input x in float64 (SP/model.py:320-381); x, dy, dx f32 [batch*tokens][hidden]
+ * on the device.  Defined, like the reference, for the reference model family
+ * (f32 weights, LayerNorm, MHA, GELU); SP_ERR_ARG otherwise. */
+int sp_span_block_backward(sp_span* span, int32_t block, const float* x, const float* dy,
+                           float* dx, int32_t batch, int32_t tokens, void* stream);
 
 /* ---- client head (SP/model.py:388-400) -------------
  * embedding generated on the device bit-identically (role 11, block n_blocks);

@@ -341,6 +341,61 @@ class SpanRunner:
             c.gather(parents0)
 
 
+# ---------------------------------------------------------------------------
+# prompt-tuning backward (training mode: full causal sequence, no KV history)
+# ---------------------------------------------------------------------------
+
+def _ln_grad(x, g, dy):
+    """d LayerNorm / dx applied to dy (SP/model.py:303-311), float64."""
+    n = x.shape[-1]
+    xc = x - x.mean(axis=-1, keepdims=True)
+    inv = 1.0 / np.sqrt((xc * xc).mean(axis=-1, keepdims=True) + LN_EPS)
+    xhat = xc * inv
+    gy = dy * g
+    return inv * (gy - gy.sum(axis=-1, keepdims=True) / n
+                  - xhat * (gy * xhat).sum(axis=-1, keepdims=True) / n)
+
+
+def _gelu_deriv(x):
+    """d tanh-GELU / dx (SP/model.py:314-317), float64."""
+    th = np.tanh(GELU_C * (x + 0.044715 * x ** 3))
+    return 0.5 * (1.0 + th) + 0.5 * x * (1.0 - th * th) * GELU_C * (1.0 + 0.134145 * x * x)
+
+
+def block_backward(cfg, p: dict, x32: np.ndarray, dy32: np.ndarray) -> np.ndarray:
+    """Gradient of one block's output wrt its input for [B, t, d] sequences
+    (block_backward, SP/model.py:320-381): the forward is recomputed in float64
+    from the recorded input (causal attention within each sequence), then
+    back-propagated; parameters are only read.  Reference family only."""
+    f8 = lambda a: np.asarray(a, np.float64)  # noqa: E731
+    x, dy = f8(x32), f8(dy32)
+    B, t, d = x.shape
+    H = cfg.n_heads
+    hd = d // H
+    wq, wk, wv, wo, w1, w2 = (f8(p[k]) for k in ("wq", "wk", "wv", "wo", "w1", "w2"))
+    g1, b1, g2, b2 = (f8(p[k]) for k in ("ln1_g", "ln1_b", "ln2_g", "ln2_b"))
+    # forward, keeping what the backward needs
+    h = ln(x, g1, b1)
+    q, k, v = (_split_heads(h @ w, H) for w in (wq, wk, wv))
+    causal = np.triu(np.ones((t, t), bool), 1)
+    s = np.where(causal, -1e30, np.einsum("bhid,bhjd->bhij", q, k) / np.sqrt(hd))
+    e = np.exp(s - s.max(axis=-1, keepdims=True))
+    att = e / e.sum(axis=-1, keepdims=True)
+    x1 = x + _merge_heads(att @ v) @ wo
+    a = ln(x1, g2, b2) @ w1
+    # backward
+    dx1 = dy + _ln_grad(x1, g2, ((dy @ w2.T) * _gelu_deriv(a)) @ w1.T)
+    dctx = _split_heads(dx1 @ wo.T, H)
+    datt = np.einsum("bhid,bhjd->bhij", dctx, v)
+    ds = att * (datt - (datt * att).sum(axis=-1, keepdims=True))
+    ds = np.where(causal, 0.0, ds) / np.sqrt(hd)
+    dq = ds @ k
+    dk = np.einsum("bhij,bhid->bhjd", ds, q)
+    dv = np.einsum("bhij,bhid->bhjd", att, dctx)
+    dh = _merge_heads(dq) @ wq.T + _merge_heads(dk) @ wk.T + _merge_heads(dv) @ wv.T
+    return (dx1 + _ln_grad(x, g1, dh)).astype(np.float32)
+
+
 def logits_for(embedding: np.ndarray, row: np.ndarray) -> np.ndarray:
     """Tied unembedding, SP/model.py:393-395 (no final norm)."""
     return row @ embedding.T

@@ -32,7 +32,7 @@ EXPORTS = (
     "sp_span_forward", "sp_span_forward_stateless", "sp_fnv1a64",
     "sp_span_set_profiling", "sp_span_profile_read", "sp_kernel_launches",
     "sp_span_decode_gemv_only", "sp_head_create", "sp_head_destroy", "sp_head_embed",
-    "sp_head_greedy", "sp_head_read_embedding", "sp_span_set_option",
+    "sp_head_greedy", "sp_head_read_embedding", "sp_span_set_option", "sp_span_block_backward",
 )
 
 
@@ -88,6 +88,7 @@ def load() -> ctypes.CDLL:
         "sp_kv_read": (I32, [P, I32, I32, P, P]),
         "sp_span_forward": (I32, [P, P, I32, I32, P, P, P, P, P, P, I32, I32, P]),
         "sp_span_forward_stateless": (I32, [P, I32, I32, P, P, P, I32, I32, P]),
+        "sp_span_block_backward": (I32, [P, I32, P, P, P, I32, I32, P]),
         "sp_fnv1a64": (ctypes.c_uint64, [P, I64]),
         "sp_span_set_profiling": (I32, [P, I32]),
         "sp_span_profile_read": (I32, [P, I32, P, P, P, P]),

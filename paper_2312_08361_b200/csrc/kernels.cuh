@@ -92,4 +92,12 @@ void launch_page_copy(void* pool, int64_t block_stride_bytes, int n_blocks,
 void launch_kv_gather_slot(const void* pool, int kv_dtype, const int* page_table_row, int t,
                            int kvh, int hd, float* k_out, float* v_out, cudaStream_t st);
 
+// prompt-tuning backward of one toy-family block (backward.cu): float64
+// recompute + backprop, f32 in/out; 0 or -1 (scratch allocation failed)
+int block_backward_f64(const float* wqkv_t, const float* wo_t, const float* w1_t,
+                       const float* w2_t, const float* ln1_g, const float* ln1_b,
+                       const float* ln2_g, const float* ln2_b, int d, int H, int F,
+                       const float* x, const float* dy, float* dx, int batch, int tokens,
+                       cudaStream_t st);
+
 }  // namespace sp

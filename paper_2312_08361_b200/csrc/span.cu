@@ -975,6 +975,25 @@ int sp_span_forward_stateless(sp_span* s, int32_t b0, int32_t b1, const float* x
   return rc;
 }
 
+int sp_span_block_backward(sp_span* s, int32_t block, const float* x, const float* dy, float* dx,
+                           int32_t batch, int32_t tokens, void* stream) {
+  if (!s || !x || !dy || !dx) SP_FAIL(SP_ERR_ARG, "null argument");
+  if (block < s->start || block >= s->end) SP_FAIL(SP_ERR_ARG, "block outside span");
+  if (batch < 1 || tokens < 1) SP_FAIL(SP_ERR_ARG, "empty batch");
+  // the reference defines block_backward for its own family only (SP/model.py:320)
+  if (s->cfg.weight_dtype != kF32 || s->cfg.family != kToy || s->kvh != s->H)
+    SP_FAIL(SP_ERR_ARG, "backward is defined for the reference (toy) family only");
+  DeviceGuard dg(s->device);
+  BlockW& W = s->blocks[block - s->start];
+  const int d = s->d;
+  if (block_backward_f64((const float*)W.qkv, (const float*)W.o, (const float*)W.up,
+                         (const float*)W.down, W.ln1_g, W.ln1_b, W.ln2_g, W.ln2_b, d, s->H, s->F,
+                         x, dy, dx, batch, tokens, (cudaStream_t)stream))
+    SP_FAIL(SP_ERR_CUDA, "backward scratch allocation failed");
+  SP_CHECK_LAUNCH();
+  return SP_OK;
+}
+
 int sp_span_set_option(sp_span* s, int32_t option, int32_t value) {
   if (!s) SP_FAIL(SP_ERR_ARG, "null span");
   if (option == 0) s->use_tc_prefill = value != 0;

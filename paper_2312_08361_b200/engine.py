@@ -314,8 +314,34 @@ class B200ServerEngine:
 
     def backward(self, start: int, end: int, blob, batch: int, tokens: int,
                  record: list) -> HiddenBlob:
-        raise NotImplementedError(
-            "prompt-tuning backward on the GPU is the next tier (SURVEY.md §8f item 3)")
+        """`RealServerEngine.backward` (SP/server.py:127-139): the gradient wrt the
+        span input, block by block in reverse from the inputs `forward` recorded
+        (per micro-batch chunk), each block recomputed in float64 on the GPU
+        (`sp_span_block_backward`, block_backward of SP/model.py:320-381)."""
+        d = self.config.hidden_dim
+        with torch.cuda.device(self.device):
+            here = self.device if isinstance(self.device, torch.device) else torch.device(
+                "cuda", self.device)
+            if getattr(blob, "dev", None) is not None:                # our device blob
+                g = blob.dev.to(here)
+            else:                                                      # host / coded / reference blob
+                g = torch.from_numpy(np.ascontiguousarray(blob.array(), np.float32)).to(here)
+            g = g.reshape(batch, tokens, d)
+            grads = []
+            for chunk, per_block in record:
+                nb = chunk.stop - chunk.start
+                gc = g[chunk].contiguous().reshape(nb * tokens, d)
+                for offset, bi in enumerate(reversed(range(start, end))):
+                    xin = per_block[len(per_block) - 1 - offset]
+                    xin = torch.as_tensor(xin, device=here).reshape(nb * tokens, d).contiguous()
+                    out = torch.empty_like(gc)
+                    _lib.check(self.lib.sp_span_block_backward(
+                        self.span.handle, bi, xin.data_ptr(), gc.data_ptr(), out.data_ptr(), nb,
+                        tokens, _stream(self.device)))
+                    gc = out
+                grads.append(gc.reshape(nb, tokens, d))
+            out = torch.cat(grads, dim=0).reshape(batch * tokens, d)
+        return HiddenBlob.from_device(out)
 
     def blob_checksum(self, blob) -> int:
         """FNV-1a 64 over the f32 bytes (SP/server.py:141-142)."""

@@ -151,9 +151,38 @@ def assignment_vectors() -> None:
         json.dump(out, f)
 
 
+def backward_vectors() -> None:
+    """Prompt-tuning backward (SP/model.py:320-381, SP/server.py:106-139): one
+    block's input gradient, and the engine-level forward(record) + backward of a
+    span with micro-batching, from the reference's RealServerEngine."""
+    from swarmpipe.server import RealServerEngine
+    from swarmpipe.wire import HiddenBlob
+    cfg = M.ModelConfig(seed=1)
+    blocks, _ = M.init_model(cfg)
+    rng = np.random.default_rng(31)
+    arrays = {}
+    x = rng.standard_normal((2, 7, cfg.hidden_dim)).astype(np.float32)
+    dy = rng.standard_normal((2, 7, cfg.hidden_dim)).astype(np.float32)
+    arrays["block_x"], arrays["block_dy"] = x, dy
+    for b in (0, 5):
+        arrays[f"block{b}_dx"] = M.block_backward(blocks[b], M.HiddenStates(x), M.HiddenStates(dy),
+                                                  cfg.n_heads).data
+    eng = RealServerEngine(cfg, blocks)
+    batch, tokens = 3, 6
+    xs = rng.standard_normal((batch * tokens, cfg.hidden_dim)).astype(np.float32)
+    gs = rng.standard_normal((batch * tokens, cfg.hidden_dim)).astype(np.float32)
+    record: list = []
+    y = eng.forward(2, 6, HiddenBlob.from_array(xs), batch, tokens, 12, record)
+    gx = eng.backward(2, 6, HiddenBlob.from_array(gs), batch, tokens, record)
+    arrays["span_x"], arrays["span_g"] = xs, gs
+    arrays["span_y"], arrays["span_dx"] = y.array(), gx.array()
+    np.savez_compressed(os.path.join(OUT, "backward.npz"), **arrays)
+
+
 if __name__ == "__main__":
     codec_vectors()
     toy_model_vectors()
     swarm_traces()
     assignment_vectors()
+    backward_vectors()
     print("golden vectors written to", OUT)

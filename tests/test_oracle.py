@@ -128,3 +128,41 @@ def test_swarm_trace_fixture_is_self_consistent():
         assert t["tokens"] == t["oracle"]
         for (_, _, tt, nbytes) in t["restore_events"]:
             assert nbytes == tt * 64 * 4
+
+
+def test_oracle_block_backward_matches_reference_golden():
+    """oracle.block_backward restates SP/model.py:320-381 bit for bit
+    (golden vectors from the reference, tests/golden/backward.npz)."""
+    g = np.load(os.path.join(GOLDEN, "backward.npz"))
+    cfg = toy(seed=1)
+    for b in (0, 5):
+        got = om.block_backward(cfg, om.init_block(cfg, b), g["block_x"], g["block_dy"])
+        assert np.array_equal(got, g[f"block{b}_dx"])
+
+
+def test_oracle_span_forward_backward_matches_reference_golden():
+    """forward(record) with whole-sequence micro-batches then backward block by
+    block in reverse (SP/server.py:106-139), on the oracle."""
+    g = np.load(os.path.join(GOLDEN, "backward.npz"))
+    cfg = toy(seed=1)
+    d, batch, tokens = cfg.hidden_dim, 3, 6
+    x = g["span_x"].reshape(batch, tokens, d)
+    gr = g["span_g"].reshape(batch, tokens, d)
+    blocks = {b: om.init_block(cfg, b) for b in range(2, 6)}
+    tables = om.Tables(cfg)
+    per_chunk = max(1, 12 // tokens)
+    ys, dxs = [], []
+    for lo in range(0, batch, per_chunk):
+        h = x[lo:lo + per_chunk]
+        rec = []
+        for b in range(2, 6):
+            rec.append(h)
+            empty = np.zeros((h.shape[0], 0, cfg.kv_heads, cfg.head_dim), np.float32)
+            h, _, _ = om.block_forward_batched(cfg, blocks[b], h, empty, empty, tables)
+        ys.append(h)
+        gc = gr[lo:lo + per_chunk]
+        for i, b in enumerate(reversed(range(2, 6))):
+            gc = om.block_backward(cfg, blocks[b], rec[len(rec) - 1 - i], gc)
+        dxs.append(gc)
+    assert np.array_equal(np.concatenate(ys).reshape(-1, d), g["span_y"])
+    assert np.array_equal(np.concatenate(dxs).reshape(-1, d), g["span_dx"])
