@@ -301,6 +301,26 @@ def run_b200(args) -> None:
     pre_flops = sum(p["flops"] for p in pre_prof)
     prefill_tok_s = sessions * B * args.prefill / (pre_ms / 1e3)
 
+    # ---- C5 prompt-tune forward: the Table 6 shape, 32
+    # sequences x (4 prompt + 128) tokens through the span via engine.forward with
+    # the reference server's 1024-token micro-batches (SP/server.py:189-194, 216) ----
+    pt_b, pt_t = 32, 4 + 128
+    x_pt = HiddenBlob.from_device(torch.randn(pt_b * pt_t, d, device=dev, generator=g))
+    eng.forward(start, end, x_pt, pt_b, pt_t, 1024, None)              # untimed warm-up
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    eng.forward(start, end, x_pt, pt_b, pt_t, 1024, None)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    pt_ms = ev0.elapsed_time(ev1)
+    del x_pt
+    pt_flops = (end - start) * (2 * cfg.block_params() * pt_b * pt_t
+                                + pt_b * 2 * cfg.n_heads * cfg.head_dim * pt_t * pt_t)
+    pt_ms_t = torch.tensor([pt_ms], device=dev)
+    if world > 1:
+        dist.all_reduce(pt_ms_t, op=dist.ReduceOp.MAX)
+    pt_ms = float(pt_ms_t.item())
+
     # ---- decode: W warm-up + K timed steps ----
     from paper_2312_08361_b200.pipeline import SpanPipeline
     pipe = SpanPipeline(eng, start, end, caches, rank, world, d, dev, width=B)
@@ -477,6 +497,12 @@ def run_b200(args) -> None:
                         "tc_frac": pre_flops / (pre_ms / 1e3) / 1e12 / peaks["bf16_tflops"],
                         "gemm_ms": pre_prof[1]["ms"], "attn_ms": pre_prof[3]["ms"],
                         "gemm_tflops": pre_prof[1]["flops"] / max(pre_prof[1]["ms"], 1e-9) / 1e9},
+            "prompt_tune_forward": {"sequences": pt_b, "tokens_per_seq": pt_t,
+                                    "micro_batch_tokens": 1024, "ms": pt_ms,
+                                    "tokens_per_s": pt_b * pt_t / (pt_ms / 1e3),
+                                    "tflops": pt_flops / (pt_ms / 1e3) / 1e12,
+                                    "tc_frac": pt_flops / (pt_ms / 1e3) / 1e12 / peaks["bf16_tflops"],
+                                    "note": "C5: engine.forward, Table 6 shape (PAPER.md:611-628)"},
             "decode_breakdown_ms_per_tick_evented": {k: dec_prof[i]["ms"] / ticks for i, k in
                                                      enumerate(["gemv", "gemm", "attn_decode",
                                                                 "attn_prefill", "other"])},

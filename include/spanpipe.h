@@ -156,7 +156,12 @@ int sp_head_read_embedding(sp_head* head, float* dst_host);
  * flops and the number of launches, then clears the records. */
 int sp_span_set_profiling(sp_span* span, int32_t enable);
 /* options: 0 = use the tcgen05 prefill GEMM when the shape allows (default 1;
- * 0 selects the exact-f32 SIMT GEMM, used by parity tests as a cross-check) */
+ * 0 selects the exact-f32 SIMT GEMM, used by parity tests as a cross-check);
+ * 1 = programmatic dependent launch of the decode chain (default 1);
+ * 2 = CTA-pair (cta_group::2) prefill GEMM (default 1); 3 = bf16 hi/lo prefill
+ * attention (default 0); 5 = decode-attention sub-chunks per CTA (0 = auto);
+ * 6 = decode-attention cluster merge for 8 query heads per kv head
+ * (-1 = global last-CTA merge, the default; 0 = auto; 8 or 16 = cluster size) */
 int sp_span_set_option(sp_span* span, int32_t option, int32_t value);
 int sp_span_profile_read(sp_span* span, int32_t n_classes, double* ms, double* bytes,
                          double* flops, int64_t* launches);

@@ -15,6 +15,7 @@
 //     ascending order (deterministic) and writes ctx plus the per-head
 //     partial statistics the O-projection GEMV folds in.
 // Bytes per launch: K+V of the visible positions (2*T*kvh*hd*elt) + q/ctx.
+#include <cooperative_groups.h>
 #include <cstdio>
 #include <cstdlib>
 #include <type_traits>
@@ -26,6 +27,7 @@
 
 namespace sp {
 
+extern int g_attn_cluster;  // option 6: decode-attention cluster size (0 auto, -1 off, 8, 16)
 extern int g_attn_nsub;   // sp_span_set_option(.., 5, n): forced sub-chunks per CTA (0 = auto)
 
 namespace {
@@ -63,7 +65,8 @@ __device__ __forceinline__ float rope_val(const float* x, int dd, int half, cons
 template <int HD, bool LOG2, int GT = 0>
 __device__ void merge_tail(const AttnDecArgs& a, int G_rt, int slot, int kh, int chunk, int nchunk,
                            int T, const float (*wm)[GMAX], const float (*wl)[GMAX], float* wo,
-                           float* pm, float* pl, int* last_flag, int CH = CHUNK) {
+                           float* pm, float* pl, int* last_flag, int CH = CHUNK,
+                           float* stg = nullptr, int stg_cap = 0) {
   const int G = GT ? GT : G_rt;            // compile-time group size where known
   __shared__ float wf[4][GMAX];        // per (warp, head) rescale factors
   __shared__ float hM[GMAX], hL[GMAX];
@@ -125,6 +128,15 @@ __device__ void merge_tail(const AttnDecArgs& a, int G_rt, int slot, int kh, int
   }
   const float* sall = stats + sk * a.max_pages * G * 2;
   const float* oall = a.part + sk * a.max_pages * GH;
+  // when the chunk partials fit the (now idle) K/V staging buffer, one burst of
+  // cp.async pulls all of them from L2 in one round trip, under the stats merge
+  const bool staged = stg != nullptr && nchunk * GH <= stg_cap;
+  if (staged) {
+    for (int i = threadIdx.x * 4; i < nchunk * GH; i += NTH * 4)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                       (uint32_t)__cvta_generic_to_shared(stg + i)), "l"(oall + i));
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
   // every load below is issued before its first use: the merge costs one L2
   // round trip for the (max, sum) pairs and one per 8 chunks of O
   {
@@ -164,10 +176,27 @@ __device__ void merge_tail(const AttnDecArgs& a, int G_rt, int slot, int kh, int
       if (lane == 0) hL[g] = L;
     }
   }
+  if (staged) asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncthreads();
   trace_mark(a, 5);
   float* outh = wo;
-  for (int ib = threadIdx.x * 4; ib < GH; ib += 2 * NTH * 4) {
+  if (staged) {
+    float* ctx = a.ctx + (int64_t)slot * a.H * HD + kh * GH;
+    for (int i = threadIdx.x * 4; i < GH; i += NTH * 4) {
+      float4 O = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int c = 0; c < nchunk; ++c) {               // ascending chunks, like the path below
+        const float4 w = *reinterpret_cast<const float4*>(stg + c * GH + i);
+        const float f = pm[c * GMAX + i / HD];
+        O.x = fmaf(w.x, f, O.x); O.y = fmaf(w.y, f, O.y);
+        O.z = fmaf(w.z, f, O.z); O.w = fmaf(w.w, f, O.w);
+      }
+      const float L = hL[i / HD];
+      const float4 cv = make_float4(O.x / L, O.y / L, O.z / L, O.w / L);
+      *reinterpret_cast<float4*>(outh + i) = cv;
+      *reinterpret_cast<float4*>(ctx + i) = cv;
+    }
+  }
+  for (int ib = staged ? GH : threadIdx.x * 4; ib < GH; ib += 2 * NTH * 4) {
     const int i1 = ib + NTH * 4;
     const bool has1 = i1 < GH;
     float4 O0 = make_float4(0.f, 0.f, 0.f, 0.f), O1 = O0;
@@ -424,7 +453,92 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src, bool vali
                "l"(src), "r"(valid ? 16 : 0));
 }
 
-template <int HD, int GT>
+// Cluster merge (70B shape: G = 8 query heads per kv head, a cluster of CY = 8
+// or 16 CTAs per (slot, kv head) along the positions): each CTA folds its 4 warps'
+// partials into one (O[G][HD], max, sum) in shared memory; after one cluster
+// barrier CTA r merges head r from the 8 CTAs' partials over DSMEM, in fixed
+// rank order, and writes ctx and the head's row statistics.  No global partial
+// round trip, no arrival counter, no serial last-CTA merge.
+template <int HD, int CY>
+__device__ void cluster_merge(const AttnDecArgs& a, int G, int slot, int kh, bool has_rows,
+                              const float (*wm)[GMAX], const float (*wl)[GMAX], const float* wo,
+                              int T, int base) {
+  namespace cg = cooperative_groups;
+  __shared__ __align__(16) float cO[8][HD];
+  __shared__ float cM[8], cL[8], wf[4][8];
+  __shared__ float red[3][4];
+  cg::cluster_group cluster = cg::this_cluster();
+  // ---- this CTA's partial: the 4 warps merged (warps without rows: weight 0) ----
+  if (threadIdx.x < G) {
+    const int g = threadIdx.x;
+    float M = -INFINITY;
+    for (int w = 0; w < 4; ++w)
+      if (has_rows && base + w * 32 < T) M = fmaxf(M, wm[w][g]);
+    float L = 0.f;
+    for (int w = 0; w < 4; ++w) {
+      const float f = (has_rows && base + w * 32 < T && M != -INFINITY) ? ex2_approx(wm[w][g] - M) : 0.f;
+      wf[w][g] = f;
+      L = fmaf(f > 0.f ? wl[w][g] : 0.f, f, L);
+    }
+    cM[g] = M;
+    cL[g] = L;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < G * HD; i += NTH) {
+    const int g = i / HD, dd = i % HD;
+    float O = 0.f;
+#pragma unroll
+    for (int w = 0; w < 4; ++w)                  // (a warp without rows holds no finite O)
+      if (wf[w][g] != 0.f) O = fmaf(wo[(w * G + g) * HD + dd], wf[w][g], O);
+    cO[g][dd] = O;
+  }
+  cluster.sync();
+  // ---- CTA r merges head r over the 8 CTAs (DSMEM, ascending rank) ----
+  const int g = (int)cluster.block_rank();
+  if (g < G) {
+    float Mc[CY], Lc[CY];
+    float M = -INFINITY;
+#pragma unroll
+    for (int c = 0; c < CY; ++c) {
+      Mc[c] = *cluster.map_shared_rank(&cM[g], c);
+      Lc[c] = *cluster.map_shared_rank(&cL[g], c);
+      M = fmaxf(M, Mc[c]);
+    }
+    float L = 0.f, f[CY];
+#pragma unroll
+    for (int c = 0; c < CY; ++c) {
+      f[c] = Mc[c] == -INFINITY ? 0.f : ex2_approx(Mc[c] - M);
+      L = fmaf(Lc[c], f[c], L);
+    }
+    const float inv = __frcp_rn(L);
+    float S = 0.f, Q = 0.f, Mx = 0.f;
+    for (int dd = threadIdx.x; dd < HD; dd += NTH) {
+      float O = 0.f;
+#pragma unroll
+      for (int c = 0; c < CY; ++c)
+        if (f[c] != 0.f) O = fmaf(*cluster.map_shared_rank(&cO[g][dd], c), f[c], O);
+      const float v = O * inv;
+      a.ctx[(int64_t)slot * a.H * HD + (kh * G + g) * HD + dd] = v;
+      S += v;
+      Q = fmaf(v, v, Q);
+      Mx = fmaxf(Mx, fabsf(v));
+    }
+    if (a.st_out) {
+      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+      S = warp_sum(S); Q = warp_sum(Q); Mx = warp_max(Mx);
+      if (lane == 0) { red[0][warp] = S; red[1][warp] = Q; red[2][warp] = Mx; }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        float s2 = 0.f, q2 = 0.f, m2 = 0.f;
+        for (int w = 0; w < NTH / 32; ++w) { s2 += red[0][w]; q2 += red[1][w]; m2 = fmaxf(m2, red[2][w]); }
+        a.st_out[(int64_t)(kh * G + g) * a.width + slot] = RowStat{s2, q2, m2, 0.f};
+      }
+    }
+  }
+  cluster.sync();          // peers' shared memory stays valid until everyone has read it
+}
+
+template <int HD, int GT, int CL = 0>
 __global__ void __launch_bounds__(NTH) attn_dec_mma_kernel(AttnDecArgs a) {
   constexpr int RS = HD + 8;                      // padded smem row (bf16), breaks ldmatrix conflicts
   __shared__ __align__(16) __nv_bfloat16 qh[8][RS], ql[8][RS];      // [head][dim]
@@ -452,9 +566,9 @@ __global__ void __launch_bounds__(NTH) attn_dec_mma_kernel(AttnDecArgs a) {
   const int nsub = a.nsub > 0 ? a.nsub : 1;
   const int CH = CHUNK * nsub;                    // positions per CTA
   const int nchunk = (T + CH - 1) / CH;
-  if (chunk >= nchunk) return;
+  if (CL == 0 && chunk >= nchunk) return;            // (cluster mode: every CTA joins the barriers)
   const int base = chunk * CH;
-  const int nsub_here = min(nsub, (T - base + CHUNK - 1) / CHUNK);
+  const int nsub_here = base < T ? min(nsub, (T - base + CHUNK - 1) / CHUNK) : 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g8 = lane >> 2, t4 = lane & 3;
   const int half = HD / 2;
@@ -483,7 +597,7 @@ __global__ void __launch_bounds__(NTH) attn_dec_mma_kernel(AttnDecArgs a) {
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
-  stage(0);
+  if (nsub_here > 0) stage(0);
   trace_mark(a, 0);
   pdl_trigger();
   pdl_wait();        // q / k_new / v_new come from the QKV GEMV just before
@@ -672,12 +786,16 @@ __global__ void __launch_bounds__(NTH) attn_dec_mma_kernel(AttnDecArgs a) {
   trace_mark(a, 10);
   __syncthreads();
   trace_mark(a, 3);
-  merge_tail<HD, true, GT>(a, G, slot, kh, chunk, nchunk, T, wm, wl, wo, pmv, plv, &last_flag, CH);
+  if constexpr (CL > 0)
+    cluster_merge<HD, CL>(a, G, slot, kh, nsub_here > 0, wm, wl, wo, T, base);
+  else
+    merge_tail<HD, true, GT>(a, G, slot, kh, chunk, nchunk, T, wm, wl, wo, pmv, plv, &last_flag, CH,
+                             reinterpret_cast<float*>(dsm), nbuf * 2 * 4 * 32 * RS / 2);
   trace_mark(a, 7);
 }
 
-template <int HD, int GT>
-void launch_mma(const AttnDecArgs& a_in, cudaStream_t st) {
+template <int HD, int GT, int CL>
+void launch_mma_cl(const AttnDecArgs& a_in, cudaStream_t st) {
   AttnDecArgs a = a_in;
   const int T = a.t0 + 1;
   // sub-chunks per CTA: one (136 CTAs for 70B GQA at 2 K positions) unless the
@@ -686,17 +804,21 @@ void launch_mma(const AttnDecArgs& a_in, cudaStream_t st) {
   static int num_sms = 0;
   if (!num_sms) cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, current_device());
   int nsub = g_attn_nsub > 0 ? g_attn_nsub : (int)((n128 + 2 * num_sms - 1) / (2 * num_sms));
+  if (CL > 0) nsub = (T + CHUNK * CL - 1) / (CHUNK * CL);   // CL CTAs cover the positions
   nsub = nsub < 1 ? 1 : (nsub > 32 ? 32 : nsub);
   a.nsub = nsub;
-  dim3 grid(a.width * a.kvh, (T + CHUNK * nsub - 1) / (CHUNK * nsub));
+  dim3 grid(a.width * a.kvh, CL > 0 ? CL : (T + CHUNK * nsub - 1) / (CHUNK * nsub));
   const int G = a.H / a.kvh;
   const size_t smem = (size_t)(nsub > 1 ? 2 : 1) * 2 * 4 * 32 * (HD + 8) * 2 +
                       (size_t)(4 * G * HD + 2 * a.max_pages * GMAX) * sizeof(float);
   static size_t set[kMaxDevices] = {};
   const int dv = current_device();
   if (smem > set[dv]) {
-    cudaFuncSetAttribute(attn_dec_mma_kernel<HD, GT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(attn_dec_mma_kernel<HD, GT, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
+    if (CL > 8)
+      cudaFuncSetAttribute(attn_dec_mma_kernel<HD, GT, CL>,
+                           cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     set[dv] = smem;
   }
   static int trace_call = getenv("SP_ATTN_TRACE") ? atoi(getenv("SP_ATTN_TRACE")) : -1;
@@ -710,7 +832,10 @@ void launch_mma(const AttnDecArgs& a_in, cudaStream_t st) {
     cudaMemsetAsync(tbuf, 0, tn * 8, st);
     b.trace = tbuf;
   }
-  launch_pdl(attn_dec_mma_kernel<HD, GT>, grid, dim3(NTH), smem, st, b);
+  if (CL > 0)
+    launch_pdl_cluster(attn_dec_mma_kernel<HD, GT, CL>, grid, dim3(NTH), smem, st, CL, b);
+  else
+    launch_pdl(attn_dec_mma_kernel<HD, GT, CL>, grid, dim3(NTH), smem, st, b);
   count_launch();
   if (tr) {
     std::vector<unsigned long long> h(tn);
@@ -726,6 +851,26 @@ void launch_mma(const AttnDecArgs& a_in, cudaStream_t st) {
     }
     cudaFree(tbuf);
   }
+}
+
+// Cluster merge for G = 8 (70B GQA): 8 CTAs per (slot, kv head) up to 1 K
+// positions, 16 beyond (one 128-position sub-chunk each at 2 K).  Measured on
+// the 70B shape at 2 K positions: 8-CTA clusters tie the global last-CTA merge
+// (0.118 ms per 8-block tick either way), 16-CTA clusters lose (0.167 ms), so
+// the default (g_attn_cluster = -1, option 6 / SP_ATTN_CLUSTER) stays global;
+// 0 = the size rule above, 8 or 16 = forced.
+
+template <int HD, int GT>
+void launch_mma(const AttnDecArgs& a, cudaStream_t st) {
+  const int T = a.t0 + 1;
+  int cy = 0;
+  if (GT == 8 && g_attn_cluster >= 0) {
+    cy = g_attn_cluster > 0 ? g_attn_cluster : (T > 8 * CHUNK ? 16 : 8);
+    if (T > 32 * CHUNK * cy) cy = 0;
+  }
+  if (cy == 16) launch_mma_cl<HD, GT, GT == 8 ? 16 : 0>(a, st);
+  else if (cy == 8) launch_mma_cl<HD, GT, GT == 8 ? 8 : 0>(a, st);
+  else launch_mma_cl<HD, GT, 0>(a, st);
 }
 
 template <int HD, typename KT, int GT>
@@ -768,6 +913,7 @@ void dispatch(const AttnDecArgs& a, cudaStream_t st) {
 }  // namespace
 
 int g_attn_nsub = 0;
+int g_attn_cluster = getenv("SP_ATTN_CLUSTER") ? atoi(getenv("SP_ATTN_CLUSTER")) : -1;
 
 int64_t attn_dec_part_floats(int width, int H, int hd, int max_pages) {
   return (int64_t)width * H * max_pages * (hd + 2);

@@ -38,6 +38,7 @@ void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 bool g_pdl = true;
 extern bool g_attn_hilo;   // attn_prefill.cu
 extern int g_attn_nsub;    // attn_decode.cu, option 5
+extern int g_attn_cluster; // attn_decode.cu, option 6
 }  // namespace sp
 
 using namespace sp;
@@ -1001,6 +1002,7 @@ int sp_span_set_option(sp_span* s, int32_t option, int32_t value) {
   else if (option == 2) g_tc_pair = value != 0;
   else if (option == 3) g_attn_hilo = value != 0;
   else if (option == 5) g_attn_nsub = value;
+  else if (option == 6) g_attn_cluster = value;
   else SP_FAIL(SP_ERR_ARG, "unknown option");
   return SP_OK;
 }

@@ -216,6 +216,8 @@ class B200ServerEngine:
         self.device = self.span.device
         self.lib = self.span.lib
         self.blocks = _BlockList(self.span)
+        # stateless forward chunk (tokens): see device_micro_batches
+        self.stateless_tokens = min(2048, self.span.kv_pool_tokens // 2)
 
     # -- sessions ---------------------------------------------------------------
     def make_caches(self, start: int, end: int, width: int) -> SpanCaches:
@@ -295,7 +297,8 @@ class B200ServerEngine:
                 x = keep[0]
             x = x.reshape(batch, tokens, d)
             y = torch.empty((batch, tokens, d), dtype=torch.float32, device=self.device)
-            for chunk in micro_batches(batch, tokens, micro_batch_tokens):
+            for chunk in device_micro_batches(batch, tokens, micro_batch_tokens,
+                                              self.stateless_tokens):
                 nb = chunk.stop - chunk.start
                 xc = x[chunk].contiguous()
                 rec = None
@@ -367,6 +370,20 @@ class _BlockList:
 
     def __iter__(self):
         return (self[i] for i in range(self.span.start, self.span.end))
+
+
+def device_micro_batches(batch: int, tokens: int, micro_batch_tokens: int, device_tokens: int):
+    """Whole-sequence chunks for the GPU: the reference's 1024-token micro-batches
+    bound host memory (SP/server.py:189-194, 216) and its result is micro-batch
+    invariant (T/test_server.py:247-255, array_equal), so the engine runs larger
+    balanced chunks of up to max(micro_batch_tokens, device_tokens) tokens (the
+    prefill GEMM's M); a single long sequence still runs unsplit."""
+    cap = max(micro_batch_tokens, device_tokens)
+    per = max(1, cap // max(tokens, 1))
+    n = -(-batch // per)
+    per = -(-batch // n)                               # balance: 32 x 132 -> 3 x 11/11/10
+    for lo in range(0, batch, per):
+        yield slice(lo, min(lo + per, batch))
 
 
 def micro_batches(batch: int, tokens: int, micro_batch_tokens: int):

@@ -180,6 +180,10 @@ SMALL = {
                              kv_dtype="bf16", seed=7),
     "llama_f32": SpanConfig(n_blocks=2, hidden_dim=256, n_heads=2, n_kv_heads=1, ffn_dim=512,
                             vocab_size=64, max_seq_len=512, family="llama", seed=8),
+    # the 70B attention shape: 8 query heads per kv head, head_dim 128
+    "llama_g8": SpanConfig(n_blocks=2, hidden_dim=1024, n_heads=8, n_kv_heads=1, ffn_dim=2048,
+                           vocab_size=64, max_seq_len=2048, family="llama",
+                           weight_dtype="int8", kv_dtype="bf16", seed=9),
 }
 
 
@@ -262,7 +266,7 @@ def test_tc_pair_gemm_equals_single_cta():
                                               float(np.abs(single).max()))
 
 
-@pytest.mark.parametrize("name", ["llama_int8", "bloom_int8", "llama_bf16"])
+@pytest.mark.parametrize("name", ["llama_int8", "bloom_int8", "llama_bf16", "llama_g8"])
 def test_extended_families_greedy_tokens_match_oracle(name):
     """BASELINE north star: identical greedy tokens to the CPU oracle and
     max-abs logits diff <= 1e-2 — prompt through the prefill path (tcgen05 for
@@ -293,7 +297,7 @@ def test_extended_families_greedy_tokens_match_oracle(name):
     assert worst <= 1e-2, worst
 
 
-@pytest.mark.parametrize("name,width", [("llama_int8", 8), ("bloom_int8", 16)])
+@pytest.mark.parametrize("name,width", [("llama_int8", 8), ("bloom_int8", 16), ("llama_g8", 8)])
 def test_wide_decode_vs_oracle(name, width):
     """Decode with >= 8 rows per step runs its linears on the tcgen05 GEMM
     (one pass over the weights for all rows) and attention on the fused decode
@@ -336,6 +340,36 @@ def test_decode_attention_streamed_subchunks(name):
         _lib.check(eng.lib.sp_span_set_option(eng.span.handle, 5, 0))
     for a, b in zip(*outs):
         assert np.abs(a - b).max() <= 1e-5 * np.abs(b).max()
+
+
+def test_decode_attention_cluster_merge():
+    """70B attention shape (8 query heads per kv head): the DSMEM cluster merge
+    (8 and 16 CTAs per kv head) equals the global last-CTA merge to f32
+    rounding, below and above 1 K positions and across chunk boundaries."""
+    from paper_2312_08361_b200 import _lib
+    cfg = SMALL["llama_g8"]
+    rng = np.random.default_rng(19)
+    d = cfg.hidden_dim
+    x = rng.standard_normal((2, 1100 + 4, d)).astype(np.float32)
+    outs = {}
+    try:
+        for cl in (-1, 8, 16):
+            eng = _engine(cfg)
+            _lib.check(eng.lib.sp_span_set_option(eng.span.handle, 6, cl))
+            c = eng.make_caches(0, cfg.n_blocks, 2)
+            got = [eng.run_cached(0, cfg.n_blocks, c, _blob(x[:, :t0].reshape(-1, d)), 2, t0, False)
+                   .array() for t0 in (200,)]
+            got += [eng.run_cached(0, cfg.n_blocks, c, _blob(x[:, i]), 2, 1, False).array()
+                    for i in range(200, 203)]
+            eng.run_cached(0, cfg.n_blocks, c, _blob(x[:, 203:1100].reshape(-1, d)), 2, 897, False)
+            got += [eng.run_cached(0, cfg.n_blocks, c, _blob(x[:, i]), 2, 1, False).array()
+                    for i in range(1100, 1104)]
+            outs[cl] = got
+    finally:
+        _lib.check(eng.lib.sp_span_set_option(eng.span.handle, 6, 0))
+    for cl in (8, 16):
+        for a, b in zip(outs[cl], outs[-1]):
+            assert np.abs(a - b).max() <= 1e-5 * np.abs(b).max()
 
 
 def test_bf16_tc_prefill_matches_simt():

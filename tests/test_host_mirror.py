@@ -101,3 +101,22 @@ def test_balancer_and_router_vs_live_reference():
         got = mg.find_best_chain(0, nb)
         assert [(h.server_id, h.start, h.end) for h in want.hops] == \
             [(h.server_id, h.start, h.end) for h in got.hops]
+
+
+@pytest.mark.parametrize("batch,tokens,mbt", [(32, 132, 1024), (3, 6, 12), (5, 3000, 1024),
+                                              (1, 1, 1024), (17, 100, 64)])
+def test_device_micro_batches(batch, tokens, mbt):
+    """The GPU forward's whole-sequence chunks: cover every sequence once, in
+    order, never split a sequence, never exceed max(micro_batch_tokens, device
+    cap) tokens unless a single sequence is longer (SP/server.py:189-194), and
+    are balanced (sizes differ by at most one sequence)."""
+    from paper_2312_08361_b200.engine import device_micro_batches
+    cap = 2048
+    chunks = list(device_micro_batches(batch, tokens, mbt, cap))
+    assert [i for c in chunks for i in range(c.start, c.stop)] == list(range(batch))
+    sizes = [c.stop - c.start for c in chunks]
+    assert max(sizes) - min(sizes) <= 1
+    for n in sizes:
+        assert n == 1 or n * tokens <= max(mbt, cap)
+    if batch * tokens <= max(mbt, cap):
+        assert len(chunks) == 1
