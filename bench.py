@@ -231,6 +231,8 @@ def run_b200(args) -> None:
         dist.init_process_group("nccl", device_id=dev)
     peaks = load_peaks()
     cfg = CONFIGS[args.config]()
+    if args.weights:
+        cfg = cfg.with_(weight_dtype=args.weights)
     B = args.batch                                 # rows per session per step
     n_blocks = args.blocks or cfg.n_blocks
     if args.blocks:
@@ -452,7 +454,7 @@ def run_b200(args) -> None:
         # from the committed ncu --set full capture of one block's 4 GEMVs
         traffic, traffic_src = None, None
         try:
-            if args.config != "llama2-70b" or args.batch != 1:
+            if args.config != "llama2-70b" or args.batch != 1 or args.weights:
                 raise ValueError("the committed capture is of the 70B batch-1 GEMVs")
             tj = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)),
                                              "profiles", "gemv_traffic.json")))
@@ -467,6 +469,9 @@ def run_b200(args) -> None:
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": ("int8 (weights x 23-bit (batch<=2) / 15-bit int digit activations, exact int32 tensor-core MMA; "
                       "f32 residual)") if cfg.weight_dtype == "int8" else
+                     ("nf4 (4-bit codes -> 7-bit levels x uint8 block scales, 23-bit int digit "
+                      "activations, exact int32 MMA / int64 sums; f32 residual)")
+                     if cfg.weight_dtype == "nf4" else
                      "bf16 (weights; activations split hi+lo bf16, f32 accumulate)",
             "data": "synthetic (splitmix64 random-init weights per SP/model.py:55-60, N(0,1) "
                     "hidden rows)",
@@ -527,6 +532,8 @@ def main() -> None:
                                                                 "llama2-7b"],
                     help="model shape (BASELINE.json configs; the metric is quoted on llama2-70b)")
     ap.add_argument("--batch", type=int, default=1, help="rows per session per step")
+    ap.add_argument("--weights", default="", choices=["", "int8", "nf4", "bf16"],
+                    help="override the config's weight format (nf4: the paper's 4-bit format)")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":

@@ -19,6 +19,7 @@ in the same structure and dtype rules:
   cos/sin table, GQA, SwiGLU (gate = w1, up = w3 [role 13], down = w2)
 * family "bloom": the toy block with ALiBi biases slope_h * (j - i_abs)
 * weight_dtype "bf16": round-to-nearest-even of the f32 stream values
+* weight_dtype "nf4": see quantize_columns_nf4 (builder's format, parity unpinned)
 * weight_dtype "int8": per output channel ``scale = f32(absmax/127)``,
   ``code = rint(w/scale)`` — the reference codec arithmetic (`SP/quantize.py:44-47`)
   applied column-wise; the effective weight is ``f32(code) * scale``
@@ -108,12 +109,57 @@ def quantize_columns_int8(w: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
     return codes, scales
 
 
+# NF4 (QLoRA, Dettmers et al. 2023: the 16 normal-float levels) on a 1/63 grid:
+# CB7 = rint(63 * NF4_LEVELS).  The reference has no NF4 code (SURVEY.md 8c:
+# parity unpinned); this is the builder's format, chosen so that a block of
+# weights is an exact small integer times one f32 per output channel:
+#   m_r  = max |w| over output channel r,  s_r = f32(m_r / 16065)  (16065 = 63 * 255)
+#   a_j  = max |w| over the 64-wide block j of the channel
+#   q_j  = rint(f32(f32(255 * a_j) / m_r))  in [0, 255]   (double-quantised block scale)
+#   code = argmin_c |f32(w / s_r) - CB7[c] * q_j|, lowest c on ties; q_j = 0 -> level 0
+#   w_eff = f32(f32(CB7[code] * q_j) * s_r)
+NF4_LEVELS = np.array([-1.0, -0.6961928009986877, -0.5250730514526367, -0.39491748809814453,
+                       -0.28444138169288635, -0.18477343022823334, -0.09105003625154495, 0.0,
+                       0.07958029955625534, 0.16093020141124725, 0.24611230194568634,
+                       0.33791524171829224, 0.44070982933044434, 0.5626170039176941,
+                       0.7229568362236023, 1.0])
+CB7 = np.rint(63.0 * NF4_LEVELS).astype(np.int32)     # [-63, -44, ..., 46, 63]
+NF4_ZERO = 7
+
+
+def quantize_columns_nf4(w: np.ndarray) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
+    """w [d_in, d_out] f32 -> codes uint8 [d_out, d_in] (0..15), block scales
+    uint8 [d_out, d_in/64], channel scales f32 [d_out] (format above)."""
+    wt = np.ascontiguousarray(w.T).astype(np.float32)
+    n, k = wt.shape
+    m = np.abs(wt).max(axis=1)
+    s = (m / np.float32(16065.0)).astype(np.float32)
+    a = np.abs(wt.reshape(n, k // 64, 64)).max(axis=2)
+    safe_m = np.where(m > 0, m, np.float32(1.0)).astype(np.float32)
+    q = np.rint((np.float32(255.0) * a) / safe_m[:, None]).astype(np.int32)
+    q[m == 0] = 0
+    safe_s = np.where(s > 0, s, np.float32(1.0)).astype(np.float32)
+    codes = np.empty((n, k), np.uint8)
+    for r0 in range(0, n, 256):                         # bounded memory: 256 channels at a time
+        t = (wt[r0:r0 + 256] / safe_s[r0:r0 + 256, None]).reshape(-1, k // 64, 64)
+        lv = (CB7[None, None, :] * q[r0:r0 + 256, :, None]).astype(np.float32)  # [n, nb, 16]
+        diff = np.abs(t[..., None] - lv[:, :, None, :])                          # f32
+        c = diff.argmin(axis=-1).astype(np.uint8)
+        c[q[r0:r0 + 256] == 0] = NF4_ZERO
+        codes[r0:r0 + 256] = c.reshape(-1, k)
+    return codes, q.astype(np.uint8), s
+
+
 def effective_weight(cfg, w: np.ndarray) -> np.ndarray:
     """The f32 values the GPU multiplies by, for ``cfg.weight_dtype``."""
     if cfg.weight_dtype == "f32":
         return w
     if cfg.weight_dtype == "bf16":
         return to_bf16(w)
+    if cfg.weight_dtype == "nf4":
+        codes, q, s = quantize_columns_nf4(w)
+        ints = (CB7[codes] * np.repeat(q.astype(np.int32), 64, axis=1)).astype(np.float32)
+        return np.ascontiguousarray((ints * s[:, None]).T)
     codes, scales = quantize_columns_int8(w)
     return np.ascontiguousarray((codes.astype(np.float32) * scales[:, None]).T)
 

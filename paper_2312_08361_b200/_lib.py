@@ -20,7 +20,7 @@ SP_ERR_STATE = -4
 SP_ERR_OOM = -5
 
 FAMILY = {"toy": 0, "llama": 1, "bloom": 2}
-WDTYPE = {"f32": 0, "bf16": 1, "int8": 2}
+WDTYPE = {"f32": 0, "bf16": 1, "int8": 2, "nf4": 3}
 KVDTYPE = {"f32": 0, "bf16": 1}
 
 # every symbol include/spanpipe.h declares

@@ -15,7 +15,9 @@ vocab_size / max_seq_len / seed / head_dim`` (`SP/server.py:229, 399, 433,
                   "bloom" — the toy block plus ALiBi attention biases
 * ``n_kv_heads``  GQA key/value heads (default = n_heads)
 * ``ffn_dim``     MLP width (default 4*d)
-* ``weight_dtype`` "f32" | "bf16" | "int8" (per-output-channel absmax/127)
+* ``weight_dtype`` "f32" | "bf16" | "int8" (per-output-channel absmax/127) |
+                  "nf4" (QLoRA NF4 levels on a 1/63 grid, 64-wide blocks with
+                  double-quantised uint8 block scales; oracle/model.py)
 * ``kv_dtype``    "f32" | "bf16"
 
 Weights are always the reference's splitmix64 stream (`SP/model.py:40-60`)
@@ -28,7 +30,7 @@ from __future__ import annotations
 from dataclasses import dataclass, replace
 
 FAMILIES = ("toy", "llama", "bloom")
-WEIGHT_DTYPES = ("f32", "bf16", "int8")
+WEIGHT_DTYPES = ("f32", "bf16", "int8", "nf4")
 KV_DTYPES = ("f32", "bf16")
 
 
@@ -103,11 +105,16 @@ class SpanConfig:
 
     def weight_bytes_per_block(self) -> int:
         """Algorithmic weight bytes one decode step streams per block
-        (codes + per-output-channel f32 scales for int8)."""
+        (codes + per-output-channel f32 scales for int8; nf4: 4-bit codes, one
+        uint8 scale per 64 weights and an f32 scale per output channel)."""
+        elems = sum(a * b for _, a, b in self.block_matrices())
+        chans = sum(b for _, _, b in self.block_matrices())
+        if self.weight_dtype == "nf4":
+            return elems // 2 + elems // 64 + 4 * chans
         elt = {"f32": 4, "bf16": 2, "int8": 1}[self.weight_dtype]
-        n = sum(a * b for _, a, b in self.block_matrices()) * elt
+        n = elems * elt
         if self.weight_dtype == "int8":
-            n += 4 * sum(b for _, _, b in self.block_matrices())
+            n += 4 * chans
         return n
 
     def with_(self, **kw) -> "SpanConfig":

@@ -15,7 +15,7 @@ constexpr int kPageTokens = 64;      // KV page = 64 positions of one block
 constexpr int kCodecBlock = 64;      // SP/quantize.py:15
 
 enum Family { kToy = 0, kLlama = 1, kBloom = 2 };
-enum WDtype { kF32 = 0, kBF16 = 1, kI8 = 2 };
+enum WDtype { kF32 = 0, kBF16 = 1, kI8 = 2, kNF4 = 3 };
 enum KVDtype { kKVF32 = 0, kKVBF16 = 1 };
 
 __device__ __forceinline__ float warp_sum(float v) {
@@ -77,6 +77,35 @@ __host__ __device__ __forceinline__ int64_t cm_offset(int64_t n, int64_t kb, int
   const int64_t g = n >> 7, r8 = (n & 127) >> 3, rr = n & 7;
   const int64_t kt = kb >> 5, kc = (kb & 31) >> 4, b = kb & 15;
   return ((g * (Kbytes >> 5) + kt) * 2 + kc) * 2048 + r8 * 128 + rr * 16 + b;
+}
+
+// NF4 weights (oracle/model.py quantize_columns_nf4): 4-bit codes in units of
+// 128 output channels x 64 k (4 KB, the same unit size as int8), stored in the
+// decode GEMV's mma.m16n8k32 A-fragment order so a lane's 16-byte load holds
+// its two k-steps of one 16-row tile: byte ((t*32 + lane)*16 + s*8 + reg*2 +
+// e/2), low nibble for even e, with t = 16-row tile, lane = g8*4 + t4,
+// reg = h + 2*kc (A register), s = 32-k step.  Block scales (uint8, one per
+// channel per 64 k) follow all codes, 128 per unit ordered [g8][t][h].
+// CB7 = rint(63 * NF4 level); A operand = CB7 + 63 (7-bit, unsigned).
+__host__ __device__ __forceinline__ int64_t nf4_offset(int64_t n, int64_t k, int64_t K, int* nib) {
+  const int64_t unit = (n >> 7) * (K >> 6) + (k >> 6);
+  const int rr = (int)(n & 127), t = rr >> 4, h = (rr >> 3) & 1, g8 = rr & 7;
+  const int kk = (int)(k & 63), st = kk >> 5, kc = (kk >> 4) & 1, t4 = (kk >> 2) & 3, e = kk & 3;
+  *nib = e & 1;
+  return unit * 4096 + (t * 32 + g8 * 4 + t4) * 16 + st * 8 + (h + 2 * kc) * 2 + (e >> 1);
+}
+__host__ __device__ __forceinline__ int64_t nf4_qs_offset(int64_t n, int64_t k, int64_t N, int64_t K) {
+  const int64_t unit = (n >> 7) * (K >> 6) + (k >> 6);
+  const int rr = (int)(n & 127);
+  return N * K / 2 + unit * 128 + (rr & 7) * 16 + (rr >> 4) * 2 + ((rr >> 3) & 1);
+}
+__host__ __device__ __forceinline__ int nf4_cb7(int c) {
+  constexpr int cb[16] = {-63, -44, -33, -25, -18, -12, -6, 0, 5, 10, 16, 21, 28, 35, 46, 63};
+  return cb[c & 15];
+}
+// bytes of an N x K NF4 matrix (codes + block scales)
+__host__ __device__ __forceinline__ int64_t nf4_bytes(int64_t N, int64_t K) {
+  return N * K / 2 + N * K / 64;
 }
 
 // 2^x on the SFU (MUFU.EX2, ~2^-22 relative error): the bf16-class softmax of

@@ -20,6 +20,12 @@ __device__ __forceinline__ float load_w(const LinearArgs& a, int64_t n, int64_t 
   if (a.wdtype == kBF16)
     return __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(
         reinterpret_cast<const uint8_t*>(a.w) + cm_offset(n, 2 * k, 2 * a.K)));
+  if (a.wdtype == kNF4) {   // exact integer CB7 * q; channel scale in the epilogue
+    int nib;
+    const uint8_t* b = reinterpret_cast<const uint8_t*>(a.w);
+    const int code = (b[nf4_offset(n, k, a.K, &nib)] >> (4 * nib)) & 15;
+    return (float)(nf4_cb7(code) * (int)b[nf4_qs_offset(n, k, a.N, a.K)]);
+  }
   int q = (int)reinterpret_cast<const int8_t*>(a.w)[cm_offset(n, k, a.K)];
   return (float)q;  // per-row scale applied in the epilogue
 }
@@ -74,7 +80,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(LinearArgs a) {
       int64_t n = n0 + tx * 4 + j;
       if (n >= a.N) continue;
       float v = acc[i][j];
-      if (a.wdtype == kI8) v *= a.wscale[n];
+      if (a.wdtype == kI8 || a.wdtype == kNF4) v *= a.wscale[n];
       float* dst = a.y + m * a.ldy + n;
       if (a.epi == EPI_RESID) v = a.res[m * a.ldy + n] + v;
       else if (a.epi == EPI_GELU) v = gelu_f(v);

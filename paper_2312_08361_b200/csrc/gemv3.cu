@@ -49,6 +49,28 @@ constexpr int XSLOT = 128;        // per batch row: the unit's activation chunk 
 __host__ __device__ constexpr int stage_bytes(int nt) {
   return UNIT_BYTES + (nt == 1 ? 4 : (nt == 2 ? 8 : 8)) * XSLOT;
 }
+// nf4 (one row per launch): 4 KB of codes (128 channels x 64 k), the unit's
+// 128 uint8 block scales, one row's 64-float activation chunk
+constexpr int NF4_QS = 128, NF4_X = 256;
+__host__ __device__ constexpr int stage_bytes_wt(int wt, int nt) {
+  return wt == kNF4 ? UNIT_BYTES + NF4_QS + NF4_X : stage_bytes(nt);
+}
+// NF4 level bytes (CB7 + 63, common.cuh) for prmt lookups: entries 0-7, 8-15
+constexpr uint32_t kLA0 = 0u | 19u << 8 | 30u << 16 | 38u << 24;
+constexpr uint32_t kLA1 = 45u | 51u << 8 | 57u << 16 | 63u << 24;
+constexpr uint32_t kLB0 = 68u | 73u << 8 | 79u << 16 | 84u << 24;
+constexpr uint32_t kLB1 = 91u | 98u << 8 | 109u << 16 | 126u << 24;
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+// four 4-bit codes (the selector nibbles of `sel`) -> four level bytes: a nibble
+// >= 8 selects, with its msb set, the replicated sign (0) of a table byte in
+// the first lookup, and entry c - 8 of the second (and vice versa)
+__device__ __forceinline__ uint32_t nf4_expand(uint32_t sel) {
+  return prmt(kLA0, kLA1, sel) | prmt(kLB0, kLB1, sel ^ 0x8888u);
+}
 constexpr int STAGES = 3;         // TMA ring depth per warp (units)
 constexpr int RMAX = 8;           // batch rows per launch
 // int8 path: activation code width.  The row is scaled by 2^(kQBits - e)
@@ -154,13 +176,16 @@ __global__ void __launch_bounds__(NW * 32, CTAS_PER_SM)
 gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_total) {
   constexpr int NDIG = ND;
   constexpr int kQBits = 8 * ND - 2;
-  constexpr int KTILE = (WT == kI8) ? 32 : 16;
-  constexpr int COLS = (WT == kI8) ? NDIG : 2;
-  constexpr int XV = (WT == kI8) ? 4 : 2;
-  using XVec = typename std::conditional<WT == kI8, float4, float2>::type;
+  constexpr bool INT = (WT == kI8 || WT == kNF4);   // exact integer digit path
+  constexpr int KTILE = (WT == kI8) ? 32 : (WT == kNF4 ? 64 : 16);
+  constexpr int COLS = INT ? NDIG : 2;
+  constexpr int XV = INT ? 4 : 2;
+  using XVec = typename std::conditional<INT, float4, float2>::type;
+  static_assert(WT != kNF4 || (RM == 1 && NT == 1), "nf4: one row per launch");
+  constexpr int XOFF = UNIT_BYTES + (WT == kNF4 ? NF4_QS : 0);   // activation chunks in a stage
   extern __shared__ __align__(128) uint8_t dyn[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int STAGE_BYTES = stage_bytes(NT);
+  constexpr int STAGE_BYTES = stage_bytes_wt(WT, NT);
   uint8_t* ring = dyn + (size_t)warp * STAGES * STAGE_BYTES;
   WarpSmem* ws_ = reinterpret_cast<WarpSmem*>(dyn + (size_t)NW * STAGES * STAGE_BYTES) + warp;
 
@@ -187,6 +212,7 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
   __syncwarp();
   constexpr int XB = KTILE * 4;
   const uint8_t* wbase = reinterpret_cast<const uint8_t*>(a.w);
+  const uint8_t* qsbase = wbase + (WT == kNF4 ? a.N * a.K / 2 : 0);   // nf4 block scales
   const uint64_t policy = evict_first_policy();
   uint64_t policy_x;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(policy_x));
@@ -198,9 +224,12 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
   if (lane == 0)
     for (int i = 0; i < npre; ++i) {
       const int64_t u = (int64_t)u0 + i;
-      mbar_expect_tx(&ws_->bar[i], UNIT_BYTES + Rn * XB);
+      mbar_expect_tx(&ws_->bar[i], XOFF + Rn * XB);
       tma_load_1d(ring + i * STAGE_BYTES, wbase + u * UNIT_BYTES,
                   UNIT_BYTES, &ws_->bar[i], policy);
+      if constexpr (WT == kNF4)
+        tma_load_1d(ring + i * STAGE_BYTES + UNIT_BYTES, qsbase + u * NF4_QS, NF4_QS,
+                    &ws_->bar[i], policy);
     }
   pdl_trigger();
   pdl_wait();
@@ -237,7 +266,7 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
       // (issued right behind the stats loads, ahead of their reduction)
       const int64_t kt = kt0 + i < KT ? kt0 + i : kt0 + i - KT;
       for (int r = 0; r < (RM == 1 ? 1 : Rn); ++r)
-        tma_load_1d(ring + i * STAGE_BYTES + UNIT_BYTES + r * XSLOT,
+        tma_load_1d(ring + i * STAGE_BYTES + XOFF + r * XSLOT,
                     a.x + (int64_t)(r0 + r) * a.ldx + kt * KTILE, XB, &ws_->bar[i], policy_x);
     }
 #pragma unroll
@@ -262,7 +291,7 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
         bound = m + fabsf(mu) * a.gmax;
       }
       prm_mu[r] = mu;
-      if (WT == kI8) {
+      if (INT) {
         int e = 0;
         if (bound > 0.f) frexpf(bound, &e);          // bound < 2^e
         prm_ds[r] = bound > 0.f ? ldexpf(1.0f, kQBits - e) : 0.f;
@@ -311,12 +340,15 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
   auto issue_next = [&]() {
     // the unit's weights and, alongside, each batch row's activation chunk:
     // both arrive on the same mbarrier (no separate activation-load latency)
-    mbar_expect_tx(&ws_->bar[p_st], UNIT_BYTES + Rn * XB);
+    mbar_expect_tx(&ws_->bar[p_st], XOFF + Rn * XB);
     uint8_t* dstg = ring + p_st * STAGE_BYTES;
     tma_load_1d(dstg, wbase + ((int64_t)p_grp * KT + p_kt) * UNIT_BYTES, UNIT_BYTES,
                 &ws_->bar[p_st], policy);
+    if constexpr (WT == kNF4)
+      tma_load_1d(dstg + UNIT_BYTES, qsbase + ((int64_t)p_grp * KT + p_kt) * NF4_QS, NF4_QS,
+                  &ws_->bar[p_st], policy);
     for (int r = 0; r < (RM == 1 ? 1 : Rn); ++r)
-      tma_load_1d(dstg + UNIT_BYTES + r * XSLOT, a.x + (int64_t)(r0 + r) * a.ldx + p_kt * KTILE,
+      tma_load_1d(dstg + XOFF + r * XSLOT, a.x + (int64_t)(r0 + r) * a.ldx + p_kt * KTILE,
                   XB, &ws_->bar[p_st], policy_x);
     if (++p_kt == KT) { p_kt = 0; ++p_grp; }
     if (++p_st == STAGES) p_st = 0;
@@ -326,11 +358,17 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
 
   // ---- activation side: read from the stage (arrived with the weights) ----
   XVec xc[NT][2], gc[NT][2];
-  constexpr int KOFF = (WT == kI8) ? 16 : 8;
+  constexpr int KOFF = INT ? 16 : 8;
   int c_grp = u0 / KT, c_kt = u0 % KT, c_st = 0;
   uint32_t c_ph = 0;
 
-  using AccT = typename std::conditional<WT == kI8, int, float>::type;
+  using AccT = typename std::conditional<INT, int, float>::type;
+  // nf4: per-unit integer partials times the unit's block scales, in int64
+  long long accl[WT == kNF4 ? RT : 1][4];
+#pragma unroll
+  for (int t = 0; t < (WT == kNF4 ? RT : 1); ++t)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) accl[t][j] = 0;
   AccT acc[RT][NT][4];
 #pragma unroll
   for (int t = 0; t < RT; ++t)
@@ -344,6 +382,57 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
     mbar_wait(&ws_->bar[c_st], c_ph);
     if (i == 0) gtrace(a, 3);
     const uint8_t* stage = ring + c_st * STAGE_BYTES;
+    if constexpr (WT == kNF4) {
+      // ---- nf4 unit: 2 k-steps of 32; B = the row's activation digits ----
+      const float* xs = reinterpret_cast<const float*>(stage + XOFF);
+      uint32_t bb[2][2];
+      const float mu = bmu[0], sc = bsc[0];
+#pragma unroll
+      for (int st = 0; st < 2; ++st) {
+        const float4 v0 = *reinterpret_cast<const float4*>(xs + st * 32 + t4 * 4);
+        const float4 v1 = *reinterpret_cast<const float4*>(xs + st * 32 + 16 + t4 * 4);
+        float v[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+        if (HASG) {
+          const int64_t k0 = (int64_t)c_kt * KTILE + st * 32 + t4 * 4;
+          const float4 g0 = __ldg(reinterpret_cast<const float4*>(a.g + k0));
+          const float4 g1 = __ldg(reinterpret_cast<const float4*>(a.g + k0 + 16));
+          const float g8v[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[j] *= g8v[j];
+        }
+        int q[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float tt = (NORMT == NORM_LN) ? (v[j] - mu) : v[j];
+          q[j] = __float2int_rn(tt * sc);
+        }
+        bb[st][0] = digits4(q[0], q[1], q[2], q[3], bbias[0], bsel_lo[0], 0x5410);
+        bb[st][1] = digits4(q[4], q[5], q[6], q[7], bbias[0], bsel_lo[0], 0x5410);
+      }
+      // the level bytes carry +63 (7-bit, unsigned): subtract 63 * sum(B) per column
+      int off[4] = {0, 0, 0, 0};
+      const uint4 a63 = make_uint4(0x3F3F3F3Fu, 0x3F3F3F3Fu, 0x3F3F3F3Fu, 0x3F3F3F3Fu);
+      mma_s8(off, a63, bb[0][0], bb[0][1]);
+      mma_s8(off, a63, bb[1][0], bb[1][1]);
+      const uint4 qv = *reinterpret_cast<const uint4*>(stage + UNIT_BYTES + (lane >> 2) * 16);
+      const uint32_t qw[4] = {qv.x, qv.y, qv.z, qv.w};
+#pragma unroll
+      for (int t = 0; t < RT; ++t) {
+        const uint4 wv = *reinterpret_cast<const uint4*>(stage + (t * 32 + lane) * 16);
+        int c[4] = {0, 0, 0, 0};
+        mma_s8(c, make_uint4(nf4_expand(wv.x), nf4_expand(wv.x >> 16), nf4_expand(wv.y),
+                             nf4_expand(wv.y >> 16)), bb[0][0], bb[0][1]);
+        mma_s8(c, make_uint4(nf4_expand(wv.z), nf4_expand(wv.z >> 16), nf4_expand(wv.w),
+                             nf4_expand(wv.w >> 16)), bb[1][0], bb[1][1]);
+        // block scales of rows g8 (h = 0) and g8 + 8 (h = 1): bytes 2t, 2t + 1
+        const int q0 = (qw[t >> 1] >> (16 * (t & 1))) & 0xFF;
+        const int q1 = (qw[t >> 1] >> (16 * (t & 1) + 8)) & 0xFF;
+        accl[t][0] += (long long)(c[0] - off[0]) * q0;
+        accl[t][1] += (long long)(c[1] - off[1]) * q0;
+        accl[t][2] += (long long)(c[2] - off[2]) * q1;
+        accl[t][3] += (long long)(c[3] - off[3]) * q1;
+      }
+    } else {
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
       const float* xs = reinterpret_cast<const float*>(stage + UNIT_BYTES + brow[nt] * XSLOT) + t4 * XV;
@@ -402,10 +491,11 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
       for (int t = 0; t < RT; ++t) {
         uint4 wt;
         ldsm_x4(wt, lrow + t * 256);
-        if constexpr (WT == kI8) mma_s8(reinterpret_cast<int*>(acc[t][nt]), wt, b0, b1);
+        if constexpr (INT) mma_s8(reinterpret_cast<int*>(acc[t][nt]), wt, b0, b1);
         else mma_bf16(reinterpret_cast<float*>(acc[t][nt]), wt, b0, b1);
       }
     }
+    }   // int8 / bf16 unit
     __syncwarp();
     if (lane == 0 && p_left > 0) issue_next();
     if (++c_st == STAGES) { c_st = 0; c_ph ^= 1; }
@@ -427,7 +517,15 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
         const int64_t n = grp * 128 + t * 16 + g8 + h * 8;
         for (int r = 0; r < (RM == 1 ? 1 : Rn); ++r) {
           long long D = 0;
-          if constexpr (WT == kI8) {
+          if constexpr (WT == kNF4) {
+#pragma unroll
+            for (int dg = 0; dg < NDIG; ++dg) {
+              const int cw = NDIG * r + dg;
+              long long val = (cw & 1) ? accl[t][1 + 2 * h] : accl[t][2 * h];
+              val = __shfl_sync(0xffffffffu, val, g8 * 4 + (cw >> 1));
+              D += val * (1ll << (8 * (NDIG - 1 - dg)));
+            }
+          } else if constexpr (WT == kI8) {
 #pragma unroll
             for (int dg = 0; dg < NDIG; ++dg) {
               const int c = NDIG * r + dg, nt = c >> 3, cw = c & 7;
@@ -455,6 +553,10 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
       for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[t][nt][j] = 0;
+      if constexpr (WT == kNF4) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) accl[t][j] = 0;
+      }
     }
     __syncwarp();
     int last = 0;
@@ -489,7 +591,7 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
       for (int j = 0; j < 4; ++j) {
         const int row = lane + 32 * j;
         D[j] = (long long)atomicExch(accr + row, 0ull);
-        wsc[j] = (WT == kI8) ? __ldg(a.wscale + grp * 128 + row) : 1.f;
+        wsc[j] = INT ? __ldg(a.wscale + grp * 128 + row) : 1.f;
       }
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -498,7 +600,7 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
         gn[j] = (j < nj && a.g_next) ? __ldg(a.g_next + col) : 1.f;
       }
       auto val_of = [&](int k) {
-        if (WT == kI8) return (float)((double)D[k] * ys * (double)wsc[k]);
+        if (INT) return (float)((double)D[k] * ys * (double)wsc[k]);
         return (float)((double)D[k] * ys);
       };
       float S = 0.f, Q = 0.f, M = 0.f;
@@ -536,10 +638,11 @@ int g_num_sms = 0;
 
 template <int WT, int NT, int NORMT, bool HASG, int ND, int RM, int EP>
 void launch_cfg(const GemvArgs& a, int r0, int rn, cudaStream_t st) {
-  const int KTILE = (WT == kI8) ? 32 : 16;
+  const int KTILE = (WT == kI8) ? 32 : (WT == kNF4 ? 64 : 16);
   const int64_t units = (a.N / 128) * (a.K / KTILE);
   const int grid = g_num_sms * CTAS_PER_SM;
-  const size_t smem = (size_t)NW * STAGES * stage_bytes(NT) + (size_t)NW * sizeof(WarpSmem) + 128;
+  const size_t smem =
+      (size_t)NW * STAGES * stage_bytes_wt(WT, NT) + (size_t)NW * sizeof(WarpSmem) + 128;
   static bool set[kMaxDevices] = {};
   const int dv = current_device();
   if (!set[dv]) {
@@ -600,7 +703,8 @@ void launch_nt2(const GemvArgs& a, int r0, int rn, cudaStream_t st) {
     // span uses — normed input -> STORE / SWIGLU / GELU, raw input -> RESID
     const bool hg = a.g != nullptr;
     if ((a.norm == NORM_NONE) != (a.epi == EPI_RESID)) {   // other pairs: generic kernel
-      launch_norm<WT, NT, ND, RMAX, -1>(a, r0, rn, st);
+      if constexpr (WT != kNF4) launch_norm<WT, NT, ND, RMAX, -1>(a, r0, rn, st);
+      else fprintf(stderr, "nf4 gemv: unsupported (norm, epilogue) pair\n");
       return;
     }
     if (a.norm == NORM_NONE) {
@@ -659,7 +763,11 @@ void launch_gemv3(int wdtype, const GemvArgs& a, cudaStream_t st) {
     // +4 % at batch 1, 2 digits +55 % at batch 4).  SP_GEMV_NDIG overrides.
     static int nd_env = getenv("SP_GEMV_NDIG") ? atoi(getenv("SP_GEMV_NDIG")) : 0;
     const int nd = nd_env ? nd_env : (rn <= 2 ? 3 : kNDig);
-    if (wdtype == kI8) {
+    if (wdtype == kNF4) {
+      // one row per launch (the 4 KB code unit + scales + a 64-float chunk
+      // per stage; two CTAs per SM leave no room for more rows' chunks)
+      for (int r = r0; r < r0 + rn; ++r) launch_nt2<kNF4, 1, 3, 1>(a, r, 1, st);
+    } else if (wdtype == kI8) {
       if (nd == 3) launch_wt<kI8, 3>(a, r0, rn, st);
       else launch_wt<kI8, 2>(a, r0, rn, st);
     } else {

@@ -45,10 +45,11 @@ void launch_dequantize(const int8_t* codes, const float* scales, float* x, int64
                        cudaStream_t st);
 
 void launch_gen_stream(uint64_t stream, int64_t n, double scale, float* dst, cudaStream_t st);
+// nbuf: rows of the destination buffer (nf4: the block scales follow its codes)
 void launch_gen_matrix(int wdtype, uint64_t stream, int64_t K, int64_t N, double scale,
-                       MatPlace place, void* dst, float* scales, cudaStream_t st);
+                       MatPlace place, void* dst, float* scales, cudaStream_t st, int64_t nbuf = 0);
 void launch_read_matrix(int wdtype, const void* src, const float* scales, int64_t K, int64_t N,
-                        MatPlace place, float* dst, cudaStream_t st);
+                        MatPlace place, float* dst, cudaStream_t st, int64_t nbuf = 0);
 
 // decode GEMV for f32 weights (any R; rows independent, batch-invariant)
 void launch_gemv(const LinearArgs& a, cudaStream_t st);

@@ -144,6 +144,12 @@ int wdtype_ktile(int wd) { return wd == kI8 ? 32 : 16; }
 
 int elt_bytes(int wd) { return wd == kF32 ? 4 : (wd == kBF16 ? 2 : 1); }
 
+// algorithmic bytes of one N x K weight matrix (codes + scales)
+double weight_bytes_of(int wd, int64_t N, int64_t K) {
+  if (wd == kNF4) return (double)nf4_bytes(N, K) + 4.0 * N;
+  return (double)N * K * elt_bytes(wd) + (wd == kI8 ? 4.0 * N : 0.0);
+}
+
 int validate(const sp_config* c) {
   if (c->n_blocks < 1 || c->hidden_dim < 1 || c->n_heads < 1) return SP_ERR_ARG;
   if (c->hidden_dim % c->n_heads) return SP_ERR_ARG;
@@ -153,11 +159,13 @@ int validate(const sp_config* c) {
   if (!(hd == 4 || hd == 16 || hd == 32 || hd == 64 || hd == 128)) return SP_ERR_ARG;
   int F = c->ffn_dim ? c->ffn_dim : 4 * c->hidden_dim;
   int d = c->hidden_dim, kv = kvh * hd;
+  if (c->weight_dtype < kF32 || c->weight_dtype > kNF4) return SP_ERR_ARG;
   if (c->weight_dtype != kF32) {
     // core-matrix layout: 128-row groups, K in 32-byte units (common.cuh)
     if (d % 32 || F % 32) return SP_ERR_ARG;
     if ((d + 2 * kv) % 128 || d % 128 || F % 64) return SP_ERR_ARG;
     if (c->family != kLlama && F % 128) return SP_ERR_ARG;
+    if (c->weight_dtype == kNF4 && (d % 64 || F % 64)) return SP_ERR_ARG;   // 64-wide blocks
   } else {
     if (d % 16 || F % 16 || kv % 16) return SP_ERR_ARG;
   }
@@ -334,7 +342,7 @@ struct ProfScope {
 void linear(sp_span* s, int wd, void* w, float* sc, int64_t N, int64_t K, const float* x,
             float* y, int64_t ldy, const float* res, int epi, int64_t R, bool decode,
             cudaStream_t st) {
-  const double wbytes = (double)N * K * elt_bytes(wd) + (wd == kI8 ? 4.0 * N : 0.0);
+  const double wbytes = weight_bytes_of(wd, N, K);
   const double outc = (epi == EPI_SWIGLU) ? N / 2 : N;
   ProfScope ps(s, decode ? PC_GEMV : PC_GEMM, wbytes + 4.0 * R * (K + outc), 2.0 * R * N * K, st);
   LinearArgs a{};
@@ -367,9 +375,8 @@ int run_span_decode_tc(sp_span* s, sp_kv* kv, int b0, int b1, float* y, int widt
   const int64_t d = s->d;
   const int norm = fam == kLlama ? NORM_RMS : NORM_LN;
   const double kv_elt = s->cfg.kv_dtype == kKVBF16 ? 2.0 : 4.0;
-  const double welt = wd == kI8 ? 1.0 : 2.0;
   auto wbytes = [&](int64_t N, int64_t K) {
-    return (double)N * K * welt + (wd == kI8 ? 4.0 * N : 0.0);
+    return weight_bytes_of(wd, N, K);
   };
   if (!gemv_only) {
     ProfScope ps(s, PC_OTHER, 4.0 * R * d, 0, st);
@@ -704,8 +711,12 @@ int sp_span_create(const sp_config* cfg, int32_t start, int32_t end, int32_t dev
   const int64_t d = s->d, F = s->F;
 
   // ---- weights: one allocation per span ----
-  auto mat_bytes = [&](int64_t N, int64_t K) { return align_up((size_t)(N * K * eb), 256); };
-  auto sc_bytes = [&](int64_t N) { return wd == kI8 ? align_up((size_t)N * 4, 256) : 0; };
+  auto mat_bytes = [&](int64_t N, int64_t K) {
+    return align_up(wd == kNF4 ? (size_t)nf4_bytes(N, K) : (size_t)(N * K * eb), 256);
+  };
+  auto sc_bytes = [&](int64_t N) {
+    return (wd == kI8 || wd == kNF4) ? align_up((size_t)N * 4, 256) : 0;
+  };
   size_t per_block = mat_bytes(s->n_qkv, d) + sc_bytes(s->n_qkv) + mat_bytes(d, d) + sc_bytes(d) +
                      mat_bytes(s->n_up, d) + sc_bytes(s->n_up) + mat_bytes(d, F) + sc_bytes(d) +
                      4 * align_up((size_t)d * 4, 256);
@@ -729,17 +740,17 @@ int sp_span_create(const sp_config* cfg, int32_t start, int32_t end, int32_t dev
     W.ln1_g = (float*)take(align_up(d * 4, 256)); W.ln1_b = (float*)take(align_up(d * 4, 256));
     W.ln2_g = (float*)take(align_up(d * 4, 256)); W.ln2_b = (float*)take(align_up(d * 4, 256));
     uint64_t seed = cfg->seed;
-    launch_gen_matrix(wd, stream_seed(seed, b, R_WQ), d, d, scale, MatPlace{0, 1, 0}, W.qkv, W.s_qkv, st);
-    launch_gen_matrix(wd, stream_seed(seed, b, R_WK), d, s->kv, scale, MatPlace{d, 1, 0}, W.qkv, W.s_qkv, st);
-    launch_gen_matrix(wd, stream_seed(seed, b, R_WV), d, s->kv, scale, MatPlace{d + s->kv, 1, 0}, W.qkv, W.s_qkv, st);
-    launch_gen_matrix(wd, stream_seed(seed, b, R_WO), d, d, scale, MatPlace{0, 1, 0}, W.o, W.s_o, st);
+    launch_gen_matrix(wd, stream_seed(seed, b, R_WQ), d, d, scale, MatPlace{0, 1, 0}, W.qkv, W.s_qkv, st, s->n_qkv);
+    launch_gen_matrix(wd, stream_seed(seed, b, R_WK), d, s->kv, scale, MatPlace{d, 1, 0}, W.qkv, W.s_qkv, st, s->n_qkv);
+    launch_gen_matrix(wd, stream_seed(seed, b, R_WV), d, s->kv, scale, MatPlace{d + s->kv, 1, 0}, W.qkv, W.s_qkv, st, s->n_qkv);
+    launch_gen_matrix(wd, stream_seed(seed, b, R_WO), d, d, scale, MatPlace{0, 1, 0}, W.o, W.s_o, st, d);
     if (cfg->family == kLlama) {
-      launch_gen_matrix(wd, stream_seed(seed, b, R_W1), d, F, scale, MatPlace{0, 2, 0}, W.up, W.s_up, st);
-      launch_gen_matrix(wd, stream_seed(seed, b, R_W3), d, F, scale, MatPlace{0, 2, 1}, W.up, W.s_up, st);
+      launch_gen_matrix(wd, stream_seed(seed, b, R_W1), d, F, scale, MatPlace{0, 2, 0}, W.up, W.s_up, st, s->n_up);
+      launch_gen_matrix(wd, stream_seed(seed, b, R_W3), d, F, scale, MatPlace{0, 2, 1}, W.up, W.s_up, st, s->n_up);
     } else {
-      launch_gen_matrix(wd, stream_seed(seed, b, R_W1), d, F, scale, MatPlace{0, 1, 0}, W.up, W.s_up, st);
+      launch_gen_matrix(wd, stream_seed(seed, b, R_W1), d, F, scale, MatPlace{0, 1, 0}, W.up, W.s_up, st, s->n_up);
     }
-    launch_gen_matrix(wd, stream_seed(seed, b, R_W2), F, d, scale, MatPlace{0, 1, 0}, W.down, W.s_down, st);
+    launch_gen_matrix(wd, stream_seed(seed, b, R_W2), F, d, scale, MatPlace{0, 1, 0}, W.down, W.s_down, st, d);
     SP_CUDA_TRY(cudaMemcpy(W.ln1_g, ones.data(), d * 4, cudaMemcpyHostToDevice));
     SP_CUDA_TRY(cudaMemcpy(W.ln2_g, ones.data(), d * 4, cudaMemcpyHostToDevice));
     SP_CUDA_TRY(cudaMemset(W.ln1_b, 0, d * 4));
@@ -828,23 +839,23 @@ int sp_span_read_weight(sp_span* s, int32_t block, int32_t role, float* dst_host
   BlockW& W = s->blocks[block - s->start];
   const int64_t d = s->d, F = s->F;
   void* src = nullptr; float* sc = nullptr; int64_t K = 0, N = 0; MatPlace pl{0, 1, 0};
-  int64_t bufK = 0;
+  int64_t bufK = 0, bufN = 0;
   switch (role) {
-    case R_WQ: src = W.qkv; sc = W.s_qkv; K = d; N = d; pl = {0, 1, 0}; break;
-    case R_WK: src = W.qkv; sc = W.s_qkv; K = d; N = s->kv; pl = {d, 1, 0}; break;
-    case R_WV: src = W.qkv; sc = W.s_qkv; K = d; N = s->kv; pl = {d + s->kv, 1, 0}; break;
-    case R_WO: src = W.o; sc = W.s_o; K = d; N = d; break;
-    case R_W1: src = W.up; sc = W.s_up; K = d; N = F;
+    case R_WQ: src = W.qkv; sc = W.s_qkv; K = d; N = d; pl = {0, 1, 0}; bufN = s->n_qkv; break;
+    case R_WK: src = W.qkv; sc = W.s_qkv; K = d; N = s->kv; pl = {d, 1, 0}; bufN = s->n_qkv; break;
+    case R_WV: src = W.qkv; sc = W.s_qkv; K = d; N = s->kv; pl = {d + s->kv, 1, 0}; bufN = s->n_qkv; break;
+    case R_WO: src = W.o; sc = W.s_o; K = d; N = d; bufN = d; break;
+    case R_W1: src = W.up; sc = W.s_up; K = d; N = F; bufN = s->n_up;
       pl = (s->cfg.family == kLlama) ? MatPlace{0, 2, 0} : MatPlace{0, 1, 0}; break;
     case R_W3: if (s->cfg.family != kLlama) SP_FAIL(SP_ERR_ARG, "no w3");
-      src = W.up; sc = W.s_up; K = d; N = F; pl = {0, 2, 1}; break;
-    case R_W2: src = W.down; sc = W.s_down; K = F; N = d; break;
+      src = W.up; sc = W.s_up; K = d; N = F; pl = {0, 2, 1}; bufN = s->n_up; break;
+    case R_W2: src = W.down; sc = W.s_down; K = F; N = d; bufN = d; break;
     default: SP_FAIL(SP_ERR_ARG, "unknown role");
   }
   (void)bufK;
   float* tmp = nullptr;
   SP_CUDA_TRY(cudaMalloc(&tmp, K * N * sizeof(float)));
-  launch_read_matrix(s->cfg.weight_dtype, src, sc, K, N, pl, tmp, 0);
+  launch_read_matrix(s->cfg.weight_dtype, src, sc, K, N, pl, tmp, 0, bufN);
   SP_CHECK_LAUNCH();
   SP_CUDA_TRY(cudaMemcpy(dst_host, tmp, K * N * sizeof(float), cudaMemcpyDeviceToHost));
   cudaFree(tmp);
@@ -1039,11 +1050,10 @@ int sp_span_decode_gemv_only(sp_span* s, sp_kv* kv, int32_t b0, int32_t b1, floa
   if (!s || !kv || !y) SP_FAIL(SP_ERR_ARG, "null argument");
   if (s->cfg.weight_dtype == kF32) SP_FAIL(SP_ERR_ARG, "tensor-core decode path only");
   SP_CUDA_TRY(cudaSetDevice(s->device));
-  const double welt = s->cfg.weight_dtype == kI8 ? 1.0 : 2.0;
   const int64_t d = s->d;
   double wb = 0;
   const int64_t shapes[4][2] = {{s->n_qkv, d}, {d, d}, {s->n_up, d}, {d, s->F}};
-  for (auto& sh : shapes) wb += (double)sh[0] * sh[1] * welt + (welt == 1.0 ? 4.0 * sh[0] : 0.0);
+  for (auto& sh : shapes) wb += weight_bytes_of(s->cfg.weight_dtype, sh[0], sh[1]);
   if (weight_bytes) *weight_bytes = wb * (b1 - b0);
   return run_span_decode_tc(s, kv, b0, b1, y, width, (cudaStream_t)stream, true);
 }

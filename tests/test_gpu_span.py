@@ -180,6 +180,14 @@ SMALL = {
                              kv_dtype="bf16", seed=7),
     "llama_f32": SpanConfig(n_blocks=2, hidden_dim=256, n_heads=2, n_kv_heads=1, ffn_dim=512,
                             vocab_size=64, max_seq_len=512, family="llama", seed=8),
+    # nf4 weights (oracle/model.py quantize_columns_nf4): decode on the exact
+    # integer GEMV, prefill on the exact-f32 SIMT GEMM over the same levels
+    "llama_nf4": SpanConfig(n_blocks=3, hidden_dim=512, n_heads=4, n_kv_heads=2, ffn_dim=1024,
+                            vocab_size=64, max_seq_len=512, family="llama",
+                            weight_dtype="nf4", kv_dtype="bf16", seed=10),
+    "bloom_nf4": SpanConfig(n_blocks=2, hidden_dim=512, n_heads=4, vocab_size=64,
+                            max_seq_len=512, family="bloom", weight_dtype="nf4",
+                            kv_dtype="bf16", seed=11),
     # the 70B attention shape: 8 query heads per kv head, head_dim 128
     "llama_g8": SpanConfig(n_blocks=2, hidden_dim=1024, n_heads=8, n_kv_heads=1, ffn_dim=2048,
                            vocab_size=64, max_seq_len=2048, family="llama",
@@ -266,7 +274,8 @@ def test_tc_pair_gemm_equals_single_cta():
                                               float(np.abs(single).max()))
 
 
-@pytest.mark.parametrize("name", ["llama_int8", "bloom_int8", "llama_bf16", "llama_g8"])
+@pytest.mark.parametrize("name", ["llama_int8", "bloom_int8", "llama_bf16", "llama_g8",
+                                  "llama_nf4", "bloom_nf4"])
 def test_extended_families_greedy_tokens_match_oracle(name):
     """BASELINE north star: identical greedy tokens to the CPU oracle and
     max-abs logits diff <= 1e-2 — prompt through the prefill path (tcgen05 for
@@ -391,3 +400,27 @@ def test_bf16_tc_prefill_matches_simt():
     assert rel < 2e-3, rel
     split = e_tc.forward(0, cfg.n_blocks, _blob(x), 2, 150, 150, None).array()
     assert np.array_equal(a, split)
+
+
+def test_nf4_decode_rows_independent():
+    """nf4 decode GEMV (one row per launch): a width-3 decode equals three
+    width-1 sessions bit for bit, and the oracle within the decode tolerance."""
+    cfg = SMALL["llama_nf4"]
+    eng = _engine(cfg)
+    rng = np.random.default_rng(29)
+    d = cfg.hidden_dim
+    x = rng.standard_normal((3, 40 + 3, d)).astype(np.float32)
+    c3 = eng.make_caches(0, cfg.n_blocks, 3)
+    eng.run_cached(0, cfg.n_blocks, c3, _blob(x[:, :40].reshape(-1, d)), 3, 40, False)
+    wide = [eng.run_cached(0, cfg.n_blocks, c3, _blob(x[:, i]), 3, 1, False).array()
+            for i in range(40, 43)]
+    for r in range(3):
+        c1 = eng.make_caches(0, cfg.n_blocks, 1)
+        eng.run_cached(0, cfg.n_blocks, c1, _blob(x[r, :40]), 1, 40, False)
+        runner = om.SpanRunner(cfg, 0, cfg.n_blocks)
+        runner.step(x[None, r, :40])
+        for j, i in enumerate(range(40, 43)):
+            one = eng.run_cached(0, cfg.n_blocks, c1, _blob(x[r, i:i + 1]), 1, 1, False).array()
+            assert np.array_equal(one[0], wide[j][r])
+            w = runner.step(x[None, r, i:i + 1])[0]
+            assert np.abs(one - w).max() <= 2e-3 * np.abs(w).max()

@@ -1,5 +1,5 @@
 """GPU weight generation vs the reference recipe (SP/model.py:40-60, 178-199):
-bit-exact f32 streams; bf16/int8 roundings equal to the oracle's."""
+bit-exact f32 streams; bf16/int8/nf4 roundings equal to the oracle's."""
 
 import numpy as np
 import pytest
@@ -41,7 +41,7 @@ def test_toy_span_weights_equal_reference_golden(golden_toy):
             assert np.array_equal(got, golden_toy[f"default__w_{role}_{b}"]), (role, b)
 
 
-@pytest.mark.parametrize("wd", ["bf16", "int8"])
+@pytest.mark.parametrize("wd", ["bf16", "int8", "nf4"])
 def test_rounded_weights_equal_oracle(wd):
     from paper_2312_08361_b200.engine import DeviceSpan
     cfg = SpanConfig(n_blocks=2, hidden_dim=512, n_heads=4, n_kv_heads=2, ffn_dim=1024,
@@ -52,4 +52,18 @@ def test_rounded_weights_equal_oracle(wd):
         w = om.uniform_weights(cfg.seed, 1, role, (a, b), om.weight_scale(cfg))
         ref = om.effective_weight(cfg, w)
         got = span.read_weight(1, role)
+        assert np.array_equal(got.view(np.uint32), ref.view(np.uint32)), role
+
+
+def test_nf4_bloom_gelu_weights_equal_oracle():
+    """nf4 codes, block scales and channel scales for a non-interleaved (GELU)
+    up-projection and K = 4d down-projection (BLOOM family)."""
+    from paper_2312_08361_b200.engine import DeviceSpan
+    cfg = SpanConfig(n_blocks=1, hidden_dim=512, n_heads=4, vocab_size=64, max_seq_len=256,
+                     family="bloom", weight_dtype="nf4", kv_dtype="bf16", seed=4)
+    span = DeviceSpan(cfg, 0, 1)
+    for role, a, b in cfg.block_matrices():
+        w = om.uniform_weights(cfg.seed, 0, role, (a, b), om.weight_scale(cfg))
+        ref = om.effective_weight(cfg, w)
+        got = span.read_weight(0, role)
         assert np.array_equal(got.view(np.uint32), ref.view(np.uint32)), role

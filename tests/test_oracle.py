@@ -166,3 +166,29 @@ def test_oracle_span_forward_backward_matches_reference_golden():
         dxs.append(gc)
     assert np.array_equal(np.concatenate(ys).reshape(-1, d), g["span_y"])
     assert np.array_equal(np.concatenate(dxs).reshape(-1, d), g["span_dx"])
+
+
+def test_nf4_format_properties():
+    """The nf4 weight format (oracle/model.py quantize_columns_nf4; builder's
+    format, parity unpinned): 4-bit codes, uint8 block scales, all-zero
+    channels and blocks map to the zero level, and every weight lands on the
+    nearest level of its block (|w - w_eff| <= half the widest level gap)."""
+    from oracle import model as om
+    rng = np.random.default_rng(3)
+    w = rng.standard_normal((256, 96)).astype(np.float32)
+    w[:, 5] = 0.0                                  # an all-zero channel
+    w[64:128, 7] = 0.0                             # an all-zero block
+    codes, q, s = om.quantize_columns_nf4(w)
+    assert codes.shape == (96, 256) and q.shape == (96, 4) and s.shape == (96,)
+    assert codes.max() <= 15 and q.max() == 255
+    assert (codes[5] == om.NF4_ZERO).all() and s[5] == 0
+    assert q[7, 1] == 0 and (codes[7, 64:128] == om.NF4_ZERO).all()
+
+    class C:
+        weight_dtype = "nf4"
+    eff = om.effective_weight(C, w)
+    assert (eff[:, 5] == 0).all() and (eff[64:128, 7] == 0).all()
+    gap = np.diff(om.CB7).max() / 2 + 0.5           # levels in units of q * s, + rounding
+    bound = (gap * np.repeat(q.astype(np.float32), 64, axis=1) * s[:, None]).T
+    assert (np.abs(eff - w) <= bound * 1.0001 + 1e-12).all()
+    assert list(om.CB7) == [-63, -44, -33, -25, -18, -12, -6, 0, 5, 10, 16, 21, 28, 35, 46, 63]
