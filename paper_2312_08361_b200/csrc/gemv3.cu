@@ -363,12 +363,10 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
   uint32_t c_ph = 0;
 
   using AccT = typename std::conditional<INT, int, float>::type;
-  // nf4: per-unit integer partials times the unit's block scales, in int64
-  long long accl[WT == kNF4 ? RT : 1][4];
-#pragma unroll
-  for (int t = 0; t < (WT == kNF4 ? RT : 1); ++t)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) accl[t][j] = 0;
+  // nf4: acc[t][0] sums (unit partial) x (block scale) in int32; a warp flushes
+  // every kNf4Flush units, the bound that keeps the sum exact:
+  // |partial| <= 64 * 63 * 128, x 255, x 16 < 2^31
+  constexpr int kNf4Flush = 16;
   AccT acc[RT][NT][4];
 #pragma unroll
   for (int t = 0; t < RT; ++t)
@@ -427,10 +425,10 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
         // block scales of rows g8 (h = 0) and g8 + 8 (h = 1): bytes 2t, 2t + 1
         const int q0 = (qw[t >> 1] >> (16 * (t & 1))) & 0xFF;
         const int q1 = (qw[t >> 1] >> (16 * (t & 1) + 8)) & 0xFF;
-        accl[t][0] += (long long)(c[0] - off[0]) * q0;
-        accl[t][1] += (long long)(c[1] - off[1]) * q0;
-        accl[t][2] += (long long)(c[2] - off[2]) * q1;
-        accl[t][3] += (long long)(c[3] - off[3]) * q1;
+        acc[t][0][0] += (c[0] - off[0]) * q0;
+        acc[t][0][1] += (c[1] - off[1]) * q0;
+        acc[t][0][2] += (c[2] - off[2]) * q1;
+        acc[t][0][3] += (c[3] - off[3]) * q1;
       }
     } else {
 #pragma unroll
@@ -504,9 +502,11 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
     const int64_t grp = c_grp;
     const int nkt = c_kt + 1 - seg_kt0;
     const bool grp_end = (c_kt + 1 == KT) || (i + 1 == nunits);
+    const bool chunk_end = (WT == kNF4) && nkt == kNf4Flush;   // exactness bound (above)
     if (++c_kt == KT) { c_kt = 0; ++c_grp; seg_kt0 = 0; }
     if (i + 1 == nunits) gtrace(a, 4);
-    if (!grp_end) continue;
+    if (!grp_end && !chunk_end) continue;
+    if (!grp_end) seg_kt0 = c_kt;                 // nf4 mid-group flush: next segment
     // combine this segment's digit/hi-lo columns per (row, batch row) in registers
     unsigned long long* acc64 = reinterpret_cast<unsigned long long*>(a.ws);
     const int g8 = lane >> 2;
@@ -517,15 +517,7 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
         const int64_t n = grp * 128 + t * 16 + g8 + h * 8;
         for (int r = 0; r < (RM == 1 ? 1 : Rn); ++r) {
           long long D = 0;
-          if constexpr (WT == kNF4) {
-#pragma unroll
-            for (int dg = 0; dg < NDIG; ++dg) {
-              const int cw = NDIG * r + dg;
-              long long val = (cw & 1) ? accl[t][1 + 2 * h] : accl[t][2 * h];
-              val = __shfl_sync(0xffffffffu, val, g8 * 4 + (cw >> 1));
-              D += val * (1ll << (8 * (NDIG - 1 - dg)));
-            }
-          } else if constexpr (WT == kI8) {
+          if constexpr (INT) {
 #pragma unroll
             for (int dg = 0; dg < NDIG; ++dg) {
               const int c = NDIG * r + dg, nt = c >> 3, cw = c & 7;
@@ -553,10 +545,6 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
       for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[t][nt][j] = 0;
-      if constexpr (WT == kNF4) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) accl[t][j] = 0;
-      }
     }
     __syncwarp();
     int last = 0;
