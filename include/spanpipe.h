@@ -51,6 +51,7 @@ extern "C" {
 #define SP_W_F32 0
 #define SP_W_BF16 1
 #define SP_W_I8 2
+#define SP_W_NF4 3   /* 4-bit NF4 levels + uint8 block scales (oracle/model.py) */
 #define SP_KV_F32 0
 #define SP_KV_BF16 1
 
