@@ -297,8 +297,11 @@ class B200ServerEngine:
                 x = keep[0]
             x = x.reshape(batch, tokens, d)
             y = torch.empty((batch, tokens, d), dtype=torch.float32, device=self.device)
-            for chunk in device_micro_batches(batch, tokens, micro_batch_tokens,
-                                              self.stateless_tokens):
+            # chunk cap: the device chunk size, bounded by the KV pages free right
+            # now (a stateless chunk holds ceil(tokens / 64) pages per sequence)
+            fit = max(1, self.span.free_pages // max(1, -(-tokens // 64))) * tokens
+            for chunk in device_micro_batches(batch, tokens, min(micro_batch_tokens, fit),
+                                              min(self.stateless_tokens, fit)):
                 nb = chunk.stop - chunk.start
                 xc = x[chunk].contiguous()
                 rec = None
