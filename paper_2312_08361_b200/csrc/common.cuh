@@ -100,8 +100,10 @@ __host__ __device__ __forceinline__ int64_t nf4_qs_offset(int64_t n, int64_t k, 
   return N * K / 2 + unit * 128 + (rr & 7) * 16 + (rr >> 4) * 2 + ((rr >> 3) & 1);
 }
 __host__ __device__ __forceinline__ int nf4_cb7(int c) {
-  constexpr int cb[16] = {-63, -44, -33, -25, -18, -12, -6, 0, 5, 10, 16, 21, 28, 35, 46, 63};
-  return cb[c & 15];
+  // CB7 + 63 as bytes of two 64-bit words (register shifts, no local-memory table)
+  constexpr unsigned long long lo = 0x3F39332D261E1300ull, hi = 0x7E6D625B544F4944ull;
+  c &= 15;
+  return (int)(((c < 8 ? lo : hi) >> (8 * (c & 7))) & 0xFF) - 63;
 }
 // bytes of an N x K NF4 matrix (codes + block scales)
 __host__ __device__ __forceinline__ int64_t nf4_bytes(int64_t N, int64_t K) {

@@ -98,7 +98,70 @@ __global__ void swiglu_rows_kernel(const float* in, float* out, int64_t R, int64
   out[i] = silu_f(g) * u;
 }
 
+__global__ void gelu_rows_kernel(const float* in, float* out, int64_t n) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = gelu_f(in[i]);
+}
+
+// one warp = one nf4 unit (128 channels x 64 k): the 4 KB of codes are read in
+// their fragment order (lane L, tile t: 16 bytes at (t*32 + L)*16, coalesced),
+// each lane writes 4-byte runs of both int8 planes; 8 lanes (g8) cover 128
+// contiguous bytes of a core-matrix column, so the stores are coalesced too
+__global__ void nf4_split_kernel(const uint8_t* __restrict__ w, const float* __restrict__ sc,
+                                 int64_t N, int64_t K, int8_t* hi, int8_t* lo, float* sc128) {
+  const int64_t unit = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t KT = K >> 6;
+  if (unit >= (N >> 7) * KT) return;
+  const int64_t grp = unit / KT, kt = unit % KT;
+  const int g8 = lane >> 2, t4 = lane & 3;
+  const uint4 qv = *reinterpret_cast<const uint4*>(w + N * K / 2 + unit * 128 + g8 * 16);
+  const uint32_t qw[4] = {qv.x, qv.y, qv.z, qv.w};
+  const uint8_t* base = w + unit * 4096;
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    const uint4 wv = *reinterpret_cast<const uint4*>(base + (t * 32 + lane) * 16);
+    const uint32_t ww[4] = {wv.x, wv.y, wv.z, wv.w};
+#pragma unroll
+    for (int s = 0; s < 2; ++s)
+#pragma unroll
+      for (int reg = 0; reg < 4; ++reg) {
+        const int h = reg & 1, kc = reg >> 1;
+        const uint32_t codes = (ww[2 * s + (reg >> 1)] >> (16 * (reg & 1))) & 0xFFFFu;
+        const int q = (qw[t >> 1] >> (16 * (t & 1) + 8 * h)) & 0xFF;
+        uint32_t ph = 0, pl = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int v = nf4_cb7((codes >> (4 * e)) & 15) * q;          // |v| <= 16065
+          const int vh = (v + 64) >> 7;                                 // floor((v + 64) / 128)
+          ph |= (uint32_t)(uint8_t)(int8_t)vh << (8 * e);
+          pl |= (uint32_t)(uint8_t)(int8_t)(v - vh * 128) << (8 * e);   // [-64, 63]
+        }
+        const int64_t r = grp * 128 + t * 16 + h * 8 + g8;
+        const int64_t k = kt * 64 + s * 32 + kc * 16 + t4 * 4;
+        const int64_t off = cm_offset(r, k, K);
+        *reinterpret_cast<uint32_t*>(hi + off) = ph;
+        *reinterpret_cast<uint32_t*>(lo + off) = pl;
+      }
+  }
+  if (kt == 0)
+    for (int rr = lane; rr < 128; rr += 32) sc128[grp * 128 + rr] = 128.0f * sc[grp * 128 + rr];
+}
+
 }  // namespace
+
+void launch_gelu_rows(const float* in, float* out, int64_t R, int64_t F, cudaStream_t st) {
+  const int64_t n = R * F;
+  if (n == 0) return;
+  gelu_rows_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(in, out, n); count_launch();
+}
+
+void launch_nf4_split(const uint8_t* w, const float* sc, int64_t N, int64_t K, int8_t* hi,
+                      int8_t* lo, float* sc128, cudaStream_t st) {
+  const int64_t warps = (N >> 7) * (K >> 6);
+  nf4_split_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(w, sc, N, K, hi, lo, sc128);
+  count_launch();
+}
 
 void launch_gemm(const LinearArgs& a, cudaStream_t st) {
   dim3 grid((unsigned)((a.N + BN - 1) / BN), (unsigned)((a.R + BM - 1) / BM));

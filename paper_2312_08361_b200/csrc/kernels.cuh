@@ -57,6 +57,11 @@ void launch_gemv(const LinearArgs& a, cudaStream_t st);
 void launch_gemm(const LinearArgs& a, cudaStream_t st);
 // gate/up interleaved [R][2F] -> silu(gate)*up [R][F]
 void launch_swiglu_rows(const float* in, float* out, int64_t R, int64_t F, cudaStream_t st);
+void launch_gelu_rows(const float* in, float* out, int64_t R, int64_t F, cudaStream_t st);
+// nf4 levels of an N x K matrix -> int8 planes hi, lo (hi * 128 + lo = CB7 * q,
+// core-matrix layout) and sc128 = 128 * channel scale
+void launch_nf4_split(const uint8_t* w, const float* sc, int64_t N, int64_t K, int8_t* hi,
+                      int8_t* lo, float* sc128, cudaStream_t st);
 
 // norms: out = LN(x)*g+b  (family toy/bloom) or RMS(x)*g (llama); one row per CTA
 void launch_norm(int family, const float* x, const float* g, const float* b, float* out,

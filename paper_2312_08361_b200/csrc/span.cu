@@ -113,6 +113,11 @@ struct sp_span {
   uint8_t* planes = nullptr;
   int* exps = nullptr;
   bool use_tc_prefill = true;
+  // nf4 prefill: a linear's integer levels split into two int8 planes
+  // (hi * 128 + lo) in core-matrix layout, and 128 x channel scale
+  int64_t nf4_cap = 0;
+  int8_t *nf4_hi = nullptr, *nf4_lo = nullptr;
+  float* nf4_sc = nullptr;
   int64_t attn_ws_floats = 0;
   float* attn_ws = nullptr;
   std::mutex mu;
@@ -224,13 +229,25 @@ int ensure_tc(sp_span* s, int64_t rows) {
   return SP_OK;
 }
 
+int ensure_nf4(sp_span* s) {
+  if (s->nf4_cap) return SP_OK;
+  const int64_t d = s->d;
+  const int64_t cap = std::max(std::max(s->n_qkv * d, d * d), std::max(s->n_up * d, d * s->F));
+  SP_CUDA_TRY(cudaMalloc(&s->nf4_hi, cap));
+  SP_CUDA_TRY(cudaMalloc(&s->nf4_lo, cap));
+  SP_CUDA_TRY(cudaMalloc(&s->nf4_sc, std::max(s->n_qkv, s->n_up) * sizeof(float)));
+  s->nf4_cap = cap;
+  return SP_OK;
+}
+
 bool tc_ok(const sp_span* s) {
   const int wd = s->cfg.weight_dtype;
-  // int8: K multiple of 128 elements (4 x 32-byte units per stage); bf16: 64
-  const int64_t kq = wd == kI8 ? 128 : 64;
-  return (wd == kI8 || wd == kBF16) && s->n_qkv % 256 == 0 && s->d % 256 == 0 &&
+  // int8 / nf4 (as two int8 planes): K multiple of 128 elements (4 x 32-byte
+  // units per stage); bf16: 64
+  const int64_t kq = (wd == kI8 || wd == kNF4) ? 128 : 64;
+  return (wd == kI8 || wd == kBF16 || wd == kNF4) && s->n_qkv % 256 == 0 && s->d % 256 == 0 &&
          s->n_up % 256 == 0 && s->d % kq == 0 && s->F % kq == 0 &&
-         (wd == kI8 || std::max(s->d, s->F) <= 16384);
+         (wd != kBF16 || std::max(s->d, s->F) <= 16384);
 }
 
 int ensure_attn_ws(sp_span* s, int width) {
@@ -473,8 +490,8 @@ int run_span_prefill_tc(sp_span* s, sp_kv* kv, int b0, int b1, float* y, float* 
   at.page_table = kv->d_table; at.max_pages = s->max_pages;
   at.rope_cos = s->rope_cos; at.rope_sin = s->rope_sin; at.alibi = s->alibi;
   at.ctx = s->ctx; at.workspace = s->attn_ws;
-  auto gemm = [&](void* w, float* sc, int64_t N, int64_t K, float* out, int64_t ldy,
-                  const float* res, int epi) {
+  auto gemm1 = [&](void* w, float* sc, int64_t N, int64_t K, float* out, int64_t ldy,
+                   const float* res, int epi) {
     ProfScope ps(s, PC_GEMM, (double)N * K + 4.0 * N + 2.0 * Mp * K + 4.0 * R * ldy,
                  2.0 * R * N * K, st);
     TcGemmArgs g{};
@@ -484,6 +501,29 @@ int run_span_prefill_tc(sp_span* s, sp_kv* kv, int b0, int b1, float* y, float* 
     g.exps = s->exps; g.M = R; g.y = out; g.ldy = ldy; g.res = res; g.epi = epi;
     g.bf16 = bf ? 1 : 0;
     launch_gemm_i8_tc(g, st);
+  };
+  // nf4: W = s * (hi * 128 + lo) exactly (|CB7 * q| <= 16065); two int8 GEMMs on
+  // the same activation planes, the first scaled by 128 s, the second adding
+  // into its output; SwiGLU / GELU applied after the sum
+  const bool nf = s->cfg.weight_dtype == kNF4;
+  if (nf) {
+    rc = ensure_nf4(s);
+    if (rc) return rc;
+  }
+  auto gemm = [&](void* w, float* sc, int64_t N, int64_t K, float* out, int64_t ldy,
+                  const float* res, int epi) {
+    if (!nf) { gemm1(w, sc, N, K, out, ldy, res, epi); return; }
+    {
+      ProfScope ps(s, PC_OTHER, (double)nf4_bytes(N, K) + 2.0 * N * K, 0, st);
+      launch_nf4_split((const uint8_t*)w, sc, N, K, s->nf4_hi, s->nf4_lo, s->nf4_sc, st);
+    }
+    const bool act = (epi == EPI_SWIGLU || epi == EPI_GELU);
+    float* o1 = act ? s->mlp_raw : out;
+    const int64_t ld1 = act ? N : ldy;
+    gemm1(s->nf4_hi, s->nf4_sc, N, K, o1, ld1, res, epi == EPI_RESID ? EPI_RESID : EPI_STORE);
+    gemm1(s->nf4_lo, sc, N, K, o1, ld1, o1, EPI_RESID);
+    if (epi == EPI_SWIGLU) launch_swiglu_rows(s->mlp_raw, out, R, N / 2, st);
+    else if (epi == EPI_GELU) launch_gelu_rows(s->mlp_raw, out, R, N, st);
   };
   auto digit = [&](const float* x, int64_t K, int nm, const float* gg, const float* bb) {
     ProfScope ps(s, PC_OTHER, 4.0 * R * K + 2.0 * Mp * K * eb, 0, st);

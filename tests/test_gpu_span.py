@@ -424,3 +424,25 @@ def test_nf4_decode_rows_independent():
             assert np.array_equal(one[0], wide[j][r])
             w = runner.step(x[None, r, i:i + 1])[0]
             assert np.abs(one - w).max() <= 2e-3 * np.abs(w).max()
+
+
+@pytest.mark.parametrize("name", ["llama_nf4", "bloom_nf4"])
+def test_nf4_tc_prefill_matches_simt(name):
+    """nf4 prefill on the tcgen05 GEMM (levels split exactly into two int8
+    planes, hi * 128 + lo) vs the exact-f32 SIMT GEMM over the same levels, and
+    micro-batch invariance on the tensor-core path."""
+    from paper_2312_08361_b200 import _lib
+    from paper_2312_08361_b200.engine import DeviceSpan, B200ServerEngine
+    cfg = SMALL[name]
+    span_tc = DeviceSpan(cfg, 0, cfg.n_blocks)
+    span_ref = DeviceSpan(cfg, 0, cfg.n_blocks)
+    _lib.check(span_ref.lib.sp_span_set_option(span_ref.handle, 0, 0))
+    e_tc, e_ref = B200ServerEngine(cfg, span=span_tc), B200ServerEngine(cfg, span=span_ref)
+    rng = np.random.default_rng(31)
+    x = rng.standard_normal((2 * 150, cfg.hidden_dim)).astype(np.float32)
+    a = e_tc.forward(0, cfg.n_blocks, _blob(x), 2, 150, 10**9, None).array()
+    b = e_ref.forward(0, cfg.n_blocks, _blob(x), 2, 150, 10**9, None).array()
+    rel = np.abs(a - b).max() / np.abs(b).max()
+    assert rel < 2e-3, rel
+    split = e_tc.forward(0, cfg.n_blocks, _blob(x), 2, 150, 150, None).array()
+    assert np.array_equal(a, split)
