@@ -1,3 +1,5 @@
+#!/bin/bash
+# multi-GPU failover tests and N=2/4 benches (under gpurun --gpus 4)
 timeout -s KILL 600 python -m pytest tests/test_gpu_multi.py -x -q 2>&1 | tail -2
 for n in 2 4; do
 timeout -s KILL 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus $n --no-cpu > gpurun_out/multi_$n.log 2>&1
