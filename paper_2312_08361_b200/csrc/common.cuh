@@ -105,6 +105,23 @@ __host__ __device__ __forceinline__ int nf4_cb7(int c) {
   c &= 15;
   return (int)(((c < 8 ? lo : hi) >> (8 * (c & 7))) & 0xFF) - 63;
 }
+// NF4 level bytes (CB7 + 63, common.cuh) for prmt lookups: entries 0-7, 8-15
+constexpr uint32_t kLA0 = 0u | 19u << 8 | 30u << 16 | 38u << 24;
+constexpr uint32_t kLA1 = 45u | 51u << 8 | 57u << 16 | 63u << 24;
+constexpr uint32_t kLB0 = 68u | 73u << 8 | 79u << 16 | 84u << 24;
+constexpr uint32_t kLB1 = 91u | 98u << 8 | 109u << 16 | 126u << 24;
+__device__ __forceinline__ uint32_t prmt_b32(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+// four 4-bit codes (the selector nibbles of `sel`) -> four level bytes: a nibble
+// >= 8 selects, with its msb set, the replicated sign (0) of a table byte in
+// the first lookup, and entry c - 8 of the second (and vice versa)
+__device__ __forceinline__ uint32_t nf4_expand(uint32_t sel) {
+  return prmt_b32(kLA0, kLA1, sel) | prmt_b32(kLB0, kLB1, sel ^ 0x8888u);
+}
+
 // bytes of an N x K NF4 matrix (codes + block scales)
 __host__ __device__ __forceinline__ int64_t nf4_bytes(int64_t N, int64_t K) {
   return N * K / 2 + N * K / 64;

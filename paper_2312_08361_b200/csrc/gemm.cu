@@ -127,12 +127,13 @@ __global__ void nf4_split_kernel(const uint8_t* __restrict__ w, const float* __r
 #pragma unroll
       for (int reg = 0; reg < 4; ++reg) {
         const int h = reg & 1, kc = reg >> 1;
-        const uint32_t codes = (ww[2 * s + (reg >> 1)] >> (16 * (reg & 1))) & 0xFFFFu;
+        const uint32_t lv = nf4_expand(ww[2 * s + (reg >> 1)] >> (16 * (reg & 1)));  // CB7 + 63
         const int q = (qw[t >> 1] >> (16 * (t & 1) + 8 * h)) & 0xFF;
+        const int q63 = 63 * q;
         uint32_t ph = 0, pl = 0;
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const int v = nf4_cb7((codes >> (4 * e)) & 15) * q;          // |v| <= 16065
+          const int v = (int)((lv >> (8 * e)) & 0xFF) * q - q63;     // CB7 * q, |v| <= 16065
           const int vh = (v + 64) >> 7;                                 // floor((v + 64) / 128)
           ph |= (uint32_t)(uint8_t)(int8_t)vh << (8 * e);
           pl |= (uint32_t)(uint8_t)(int8_t)(v - vh * 128) << (8 * e);   // [-64, 63]

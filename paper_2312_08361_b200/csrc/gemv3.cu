@@ -55,22 +55,6 @@ constexpr int NF4_QS = 128, NF4_X = 256;
 __host__ __device__ constexpr int stage_bytes_wt(int wt, int nt) {
   return wt == kNF4 ? UNIT_BYTES + NF4_QS + NF4_X : stage_bytes(nt);
 }
-// NF4 level bytes (CB7 + 63, common.cuh) for prmt lookups: entries 0-7, 8-15
-constexpr uint32_t kLA0 = 0u | 19u << 8 | 30u << 16 | 38u << 24;
-constexpr uint32_t kLA1 = 45u | 51u << 8 | 57u << 16 | 63u << 24;
-constexpr uint32_t kLB0 = 68u | 73u << 8 | 79u << 16 | 84u << 24;
-constexpr uint32_t kLB1 = 91u | 98u << 8 | 109u << 16 | 126u << 24;
-__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t c) {
-  uint32_t d;
-  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
-  return d;
-}
-// four 4-bit codes (the selector nibbles of `sel`) -> four level bytes: a nibble
-// >= 8 selects, with its msb set, the replicated sign (0) of a table byte in
-// the first lookup, and entry c - 8 of the second (and vice versa)
-__device__ __forceinline__ uint32_t nf4_expand(uint32_t sel) {
-  return prmt(kLA0, kLA1, sel) | prmt(kLB0, kLB1, sel ^ 0x8888u);
-}
 constexpr int STAGES = 3;         // TMA ring depth per warp (units)
 constexpr int RMAX = 8;           // batch rows per launch
 // int8 path: activation code width.  The row is scaled by 2^(kQBits - e)
