@@ -222,6 +222,8 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
   // CTA-wide: 256 threads load the P_in x Rn partials with several loads in
   // flight each, then a fixed-order tree (warp shuffles, then warps in order)
   __shared__ float red_s[NW][RM][3];
+  __shared__ uint32_t nf4_lut[2];
+  if (WT == kNF4 && threadIdx.x == 0) { nf4_lut[0] = kLA0; nf4_lut[1] = kLB0; }
   __shared__ float prm_mu[RM], prm_ds[RM];
   __shared__ double prm_ys[RM];
   {
@@ -359,6 +361,11 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
 #pragma unroll
       for (int j = 0; j < 4; ++j) acc[t][nt][j] = 0;
   int seg_kt0 = c_kt;
+  // nf4 table words in per-thread registers: loaded from shared memory, so
+  // ptxas cannot treat them as uniform constants and re-copy them from uniform
+  // registers before every lookup
+  const uint32_t la0 = WT == kNF4 ? *reinterpret_cast<volatile uint32_t*>(&nf4_lut[0]) : 0u;
+  const uint32_t lb0 = WT == kNF4 ? *reinterpret_cast<volatile uint32_t*>(&nf4_lut[1]) : 0u;
 
   for (int i = 0; i < nunits; ++i) {
     mbar_wait(&ws_->bar[c_st], c_ph);
@@ -366,6 +373,7 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
     const uint8_t* stage = ring + c_st * STAGE_BYTES;
     if constexpr (WT == kNF4) {
       // ---- nf4 unit: 2 k-steps of 32; B = the row's activation digits ----
+
       const float* xs = reinterpret_cast<const float*>(stage + XOFF);
       uint32_t bb[2][2];
       const float mu = bmu[0], sc = bsc[0];
@@ -402,10 +410,21 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
       for (int t = 0; t < RT; ++t) {
         const uint4 wv = *reinterpret_cast<const uint4*>(stage + (t * 32 + lane) * 16);
         int c[4] = {0, 0, 0, 0};
-        mma_s8(c, make_uint4(nf4_expand(wv.x), nf4_expand(wv.x >> 16), nf4_expand(wv.y),
-                             nf4_expand(wv.y >> 16)), bb[0][0], bb[0][1]);
-        mma_s8(c, make_uint4(nf4_expand(wv.z), nf4_expand(wv.z >> 16), nf4_expand(wv.w),
-                             nf4_expand(wv.w >> 16)), bb[1][0], bb[1][1]);
+        // entries 0-7 and 8-15 go to the tensor pipe as two A fragments (each
+        // zero where the other table holds the code) instead of being OR-ed
+        const uint32_t hx = wv.x >> 16, hy = wv.y >> 16, hz = wv.z >> 16, hw = wv.w >> 16;
+        mma_s8(c, make_uint4(prmt_b32(la0, kLA1, wv.x), prmt_b32(la0, kLA1, hx),
+                             prmt_b32(la0, kLA1, wv.y), prmt_b32(la0, kLA1, hy)),
+               bb[0][0], bb[0][1]);
+        mma_s8(c, make_uint4(prmt_b32(lb0, kLB1, wv.x ^ 0x8888u), prmt_b32(lb0, kLB1, hx ^ 0x8888u),
+                             prmt_b32(lb0, kLB1, wv.y ^ 0x8888u), prmt_b32(lb0, kLB1, hy ^ 0x8888u)),
+               bb[0][0], bb[0][1]);
+        mma_s8(c, make_uint4(prmt_b32(la0, kLA1, wv.z), prmt_b32(la0, kLA1, hz),
+                             prmt_b32(la0, kLA1, wv.w), prmt_b32(la0, kLA1, hw)),
+               bb[1][0], bb[1][1]);
+        mma_s8(c, make_uint4(prmt_b32(lb0, kLB1, wv.z ^ 0x8888u), prmt_b32(lb0, kLB1, hz ^ 0x8888u),
+                             prmt_b32(lb0, kLB1, wv.w ^ 0x8888u), prmt_b32(lb0, kLB1, hw ^ 0x8888u)),
+               bb[1][0], bb[1][1]);
         // block scales of rows g8 (h = 0) and g8 + 8 (h = 1): bytes 2t, 2t + 1
         const int q0 = (qw[t >> 1] >> (16 * (t & 1))) & 0xFF;
         const int q1 = (qw[t >> 1] >> (16 * (t & 1) + 8)) & 0xFF;
