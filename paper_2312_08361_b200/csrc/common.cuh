@@ -121,12 +121,6 @@ __device__ __forceinline__ uint32_t prmt_b32(uint32_t a, uint32_t b, uint32_t c)
 __device__ __forceinline__ uint32_t nf4_expand(uint32_t sel) {
   return prmt_b32(kLA0, kLA1, sel) | prmt_b32(kLB0, kLB1, sel ^ 0x8888u);
 }
-// the same with the low table words held in registers by the caller (a prmt
-// takes one immediate; without this the compiler re-materialises the other
-// word before every lookup)
-__device__ __forceinline__ uint32_t nf4_expand_r(uint32_t la0, uint32_t lb0, uint32_t sel) {
-  return prmt_b32(la0, kLA1, sel) | prmt_b32(lb0, kLB1, sel ^ 0x8888u);
-}
 
 // bytes of an N x K NF4 matrix (codes + block scales)
 __host__ __device__ __forceinline__ int64_t nf4_bytes(int64_t N, int64_t K) {
