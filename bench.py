@@ -252,8 +252,8 @@ def run_b200(args) -> None:
         _lib.check(lib.sp_span_set_option(span.handle, 1, 0))
     if os.environ.get("SP_TC_PAIR") == "0":   # A/B switch: single-CTA tcgen05 prefill GEMM
         _lib.check(lib.sp_span_set_option(span.handle, 2, 0))
-    if os.environ.get("SP_ATTN_L2PF") == "0":  # A/B switch: no L2 prefetch of Wo during attention
-        _lib.check(lib.sp_span_set_option(span.handle, 4, 0))
+    if os.environ.get("SP_ATTN_NSUB"):        # A/B switch: decode-attention sub-chunks per CTA
+        _lib.check(lib.sp_span_set_option(span.handle, 5, int(os.environ["SP_ATTN_NSUB"])))
     d = cfg.hidden_dim
     stream = torch.cuda.current_stream(dev)
 
