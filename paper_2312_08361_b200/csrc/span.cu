@@ -231,6 +231,9 @@ int ensure_tc(sp_span* s, int64_t rows) {
 
 int ensure_nf4(sp_span* s) {
   if (s->nf4_cap) return SP_OK;
+  cudaFree(s->nf4_hi); cudaFree(s->nf4_lo); cudaFree(s->nf4_sc);   // after a failed attempt
+  s->nf4_hi = s->nf4_lo = nullptr;
+  s->nf4_sc = nullptr;
   const int64_t d = s->d;
   const int64_t cap = std::max(std::max(s->n_qkv * d, d * d), std::max(s->n_up * d, d * s->F));
   SP_CUDA_TRY(cudaMalloc(&s->nf4_hi, cap));
@@ -864,6 +867,7 @@ int sp_span_destroy(sp_span* s) {
   cudaFree(s->st_norm1); cudaFree(s->st_ctx); cudaFree(s->st_norm2); cudaFree(s->st_mlp);
   cudaFree(s->ws2); cudaFree(s->cnt2); cudaFree(s->attn_part); cudaFree(s->attn_cnt);
   cudaFree(s->planes); cudaFree(s->exps);
+  cudaFree(s->nf4_hi); cudaFree(s->nf4_lo); cudaFree(s->nf4_sc);
   for (auto& r : s->prof_recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : s->ev_pool) cudaEventDestroy(e);
   delete s;
