@@ -53,7 +53,7 @@ def load_peaks() -> dict:
 
 
 def stage_intervals(n_blocks: int, n_stages: int) -> list[tuple[int, int]]:
-    from paper_2312_08361_b200.balancer import stage_intervals as si
+    from paper_2312_08361_b200.placement import stage_intervals as si
     return si(n_blocks, n_stages)
 
 
@@ -168,6 +168,11 @@ def cpu_threads() -> int:
 # ---------------------------------------------------------------------------
 
 def run_reference(args) -> None:
+    """The reference's CPU implementation of the path (the oracle port of
+    SP/model.py:244-280, f32 numpy/OpenBLAS on every host core), one decode step
+    of the whole 80-block span per step.  80 distinct f32 blocks are 274 GB (more
+    than host RAM), so every step runs the same 70B-shape block's weights 80
+    times: the same arithmetic and the same 3.4 GB weight stream per block."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -180,34 +185,65 @@ def run_reference(args) -> None:
         pass
     cfg = llama2_70b()
     context = args.prefill
-    # each step = one oracle block decode at `context` (bounded sample); the
-    # metric scales it to the 80-block model
+    n_blocks = args.blocks or cfg.n_blocks
+
+    def step():
+        t = 0.0
+        for _ in range(n_blocks):
+            s, info = cpu_block_decode_seconds(cfg, context, reps=1)
+            t += s
+        return t, info
+
     for _ in range(args.warmup):
-        cpu_block_decode_seconds(cfg, context, reps=1)
+        step()
     t0 = time.perf_counter()
     per = []
+    info = {}
     for _ in range(args.steps):
-        s, info = cpu_block_decode_seconds(cfg, context, reps=1)
+        s, info = step()
         per.append(s)
     wall = time.perf_counter() - t0
-    t_block = float(np.median(per))
-    value = 1.0 / (t_block * cfg.n_blocks)
+    ms_per_step = wall / args.steps * 1e3
+    value = args.steps / wall
     cores = cpu_threads()
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": t_block * cfg.n_blocks * 1e3, "higher_is_better": True,
+        "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": "llama2-70b-shape decode, batch 1, context %d, 80 blocks" % context,
-                   "sample": "1 block decode per step, scaled x80"},
+        "config": {"workload": f"llama2-70b-shape decode, batch 1, context {context}, "
+                               f"{n_blocks} blocks",
+                   "sample": f"every step = {n_blocks} block decodes (one block's f32 weights "
+                             "reused: 80 distinct blocks exceed host RAM)"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
                          "sample": f"oracle block_forward_batched (SP/model.py:244-280 restated, "
-                                   f"f32 numpy/OpenBLAS) of one 70B-shape block at context "
-                                   f"{context}, {args.steps} steps, scaled to 80 blocks"},
+                                   f"f32 numpy/OpenBLAS) of a 70B-shape block at context "
+                                   f"{context}, x{n_blocks} blocks per step, {args.steps} steps"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "wall_s": wall, **info,
     }
     print(json.dumps(line))
+
+
+def self_launch(args) -> bool:
+    """`python bench.py --gpus N` with no launcher: re-run this command under
+    torch.distributed.run with N ranks (one per GPU) and relay its output.
+    Returns True when it launched (the caller exits)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ or args.impl == "reference":
+        return False
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    # NCCL's init lines (nRanks of every communicator) go to stdout with the JSON line
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    r = subprocess.run(cmd, env=env)
+    sys.exit(r.returncode)
 
 
 # ---------------------------------------------------------------------------
@@ -225,6 +261,8 @@ def run_b200(args) -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py --gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -536,6 +574,7 @@ def main() -> None:
                     help="override the config's weight format (nf4: the paper's 4-bit format)")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
+    self_launch(args)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -148,6 +148,10 @@ int sp_head_embed(sp_head* head, const int32_t* tokens_host, int32_t n, float* o
                   void* stream);
 int sp_head_greedy(sp_head* head, const float* row_dev, int32_t* token_host, void* stream);
 int sp_head_read_embedding(sp_head* head, float* dst_host);
+/* logits of n_rows device rows: logits_dev [n_rows, vocab] = rows @ E^T
+ * (RealClientEngine.logits, SP/client.py:104-105, used by beam search) */
+int sp_head_logits(sp_head* head, const float* rows_dev, int32_t n_rows, float* logits_dev,
+                   void* stream);
 
 /* ---- measurement ----------------------------------------------------------
  * With profiling on, every launch of the span schedule is bracketed by CUDA

@@ -5,9 +5,13 @@ Public surface (mirrors the reference engine protocol, SP/server.py:77-186):
 * :class:`B200ServerEngine` — drop-in for ``RealServerEngine``
 * :class:`HiddenBlob`       — ``SP/wire.py`` blob with a device-resident payload
 * :mod:`.config`            — model shapes (toy / Llama / BLOOM)
+* :class:`.head.ClientHead` — the client payload (embedding, tied logits, pick)
 * :mod:`.codec`             — GPU hidden-state codec
-* :mod:`.server`, :mod:`.client`, :mod:`.balancer` — host-side mirror of the
-  session / dual-cache / block-assignment layers
+* :mod:`.pipeline`          — one span per GPU, int8 codes over NCCL send/recv
+* :mod:`.placement`         — the even span split of the bench / pipeline
+
+The session, dual-cache and block-assignment layers are the reference's own
+(BlockServer, SwarmClient, balancer): the engine plugs into them unchanged.
 """
 
 from .config import SpanConfig, bloom_176b, from_reference, llama2_7b, llama2_70b, toy  # noqa: F401

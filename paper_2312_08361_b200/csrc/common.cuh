@@ -213,3 +213,20 @@ cudaError_t launch_pdl_cluster(void (*kernel)(KArgs...), dim3 grid, dim3 block, 
   } while (0)
 
 void sp_set_error(const char* file, int line, const char* msg);
+
+// Every ABI entry point that touches a device makes the span's (or head's)
+// device current for the duration of the call and restores the caller's
+// device on return (several GPUs in one process; destructors run at GC time).
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) == cudaSuccess && prev != dev) cudaSetDevice(dev);
+    else prev = -1;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+

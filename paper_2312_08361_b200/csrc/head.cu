@@ -36,6 +36,29 @@ __global__ void logits_kernel(const float* E, const float* x, int vocab, int d, 
   if (lane == 0) logits[v] = s;
 }
 
+// logits of R rows (beam search: SP/client.py:624, 634): warp per vocab row,
+// the embedding row streamed once for all R rows
+template <int R>
+__global__ void logits_rows_kernel(const float* E, const float* x, int vocab, int d,
+                                   float* logits) {
+  const int v = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (v >= vocab) return;
+  const float* e = E + (int64_t)v * d;
+  float s[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) s[r] = 0.f;
+  for (int k = lane; k < d; k += 32) {
+    const float ev = e[k];
+#pragma unroll
+    for (int r = 0; r < R; ++r) s[r] = fmaf(ev, x[(int64_t)r * d + k], s[r]);
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const float t = warp_sum(s[r]);
+    if (lane == 0) logits[(int64_t)r * vocab + v] = t;
+  }
+}
+
 // single CTA: (max value, lowest index) over the vocabulary
 __global__ void argmax_kernel(const float* logits, int vocab, int* out) {
   __shared__ float bv[1024];
@@ -80,7 +103,7 @@ uint64_t sp_stream_seed(uint64_t seed, int32_t block, int32_t role_id);
 
 int sp_head_create(const sp_config* cfg, int32_t device, sp_head** out) {
   if (!cfg || !out) return SP_ERR_ARG;
-  SP_CUDA_TRY(cudaSetDevice(device));
+  DeviceGuard dg(device);
   sp_head* h = new sp_head();
   h->device = device;
   h->vocab = cfg->vocab_size;
@@ -101,7 +124,7 @@ int sp_head_create(const sp_config* cfg, int32_t device, sp_head** out) {
 
 int sp_head_destroy(sp_head* h) {
   if (!h) return SP_OK;
-  cudaSetDevice(h->device);
+  DeviceGuard dg(h->device);
   cudaFree(h->E); cudaFree(h->logits); cudaFree(h->tok); cudaFree(h->row);
   delete h;
   return SP_OK;
@@ -113,7 +136,7 @@ int sp_head_embed(sp_head* h, const int32_t* tokens_host, int32_t n, float* out_
   for (int i = 0; i < n; ++i)
     if (tokens_host[i] < 0 || tokens_host[i] >= h->vocab) return SP_ERR_ARG;
   cudaStream_t st = (cudaStream_t)stream;
-  SP_CUDA_TRY(cudaSetDevice(h->device));
+  DeviceGuard dg(h->device);
   SP_CUDA_TRY(cudaMemcpyAsync(h->tok, tokens_host, n * sizeof(int), cudaMemcpyHostToDevice, st));
   const int64_t tot = (int64_t)n * h->d;
   if (tot) {
@@ -128,7 +151,7 @@ int sp_head_embed(sp_head* h, const int32_t* tokens_host, int32_t n, float* out_
 int sp_head_greedy(sp_head* h, const float* row_dev, int32_t* token_host, void* stream) {
   if (!h || !row_dev || !token_host) return SP_ERR_ARG;
   cudaStream_t st = (cudaStream_t)stream;
-  SP_CUDA_TRY(cudaSetDevice(h->device));
+  DeviceGuard dg(h->device);
   sp::logits_kernel<<<(h->vocab + 7) / 8, 256, 0, st>>>(h->E, row_dev, h->vocab, h->d, h->logits);
   sp::argmax_kernel<<<1, 1024, 0, st>>>(h->logits, h->vocab, h->tok);
   sp::count_launch();
@@ -138,9 +161,33 @@ int sp_head_greedy(sp_head* h, const float* row_dev, int32_t* token_host, void* 
   return SP_OK;
 }
 
+// logits [n_rows, vocab] of device rows [n_rows, d] (row @ E^T, SP/model.py:393-395);
+// the same per-row reduction order as sp_head_greedy's logits
+int sp_head_logits(sp_head* h, const float* rows_dev, int32_t n_rows, float* logits_dev,
+                   void* stream) {
+  if (!h || !rows_dev || !logits_dev || n_rows < 0) return SP_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  DeviceGuard dg(h->device);
+  const unsigned grid = (h->vocab + 7) / 8;
+  for (int r0 = 0; r0 < n_rows; r0 += 4) {
+    const int n = n_rows - r0 < 4 ? n_rows - r0 : 4;
+    const float* x = rows_dev + (int64_t)r0 * h->d;
+    float* out = logits_dev + (int64_t)r0 * h->vocab;
+    switch (n) {
+      case 1: sp::logits_rows_kernel<1><<<grid, 256, 0, st>>>(h->E, x, h->vocab, h->d, out); break;
+      case 2: sp::logits_rows_kernel<2><<<grid, 256, 0, st>>>(h->E, x, h->vocab, h->d, out); break;
+      case 3: sp::logits_rows_kernel<3><<<grid, 256, 0, st>>>(h->E, x, h->vocab, h->d, out); break;
+      default: sp::logits_rows_kernel<4><<<grid, 256, 0, st>>>(h->E, x, h->vocab, h->d, out); break;
+    }
+    sp::count_launch();
+  }
+  SP_CUDA_TRY(cudaGetLastError());
+  return SP_OK;
+}
+
 int sp_head_read_embedding(sp_head* h, float* dst_host) {
   if (!h) return SP_ERR_ARG;
-  SP_CUDA_TRY(cudaSetDevice(h->device));
+  DeviceGuard dg(h->device);
   SP_CUDA_TRY(cudaMemcpy(dst_host, h->E, (size_t)h->vocab * h->d * sizeof(float),
                          cudaMemcpyDeviceToHost));
   return SP_OK;

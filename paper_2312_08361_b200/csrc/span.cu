@@ -43,18 +43,6 @@ extern int g_attn_cluster; // attn_decode.cu, option 6
 
 using namespace sp;
 
-// the span's device is current for the duration of a call; the caller's
-// device is restored on return (spans on several GPUs in one process)
-struct DeviceGuard {
-  int prev = -1;
-  explicit DeviceGuard(int dev) {
-    if (cudaGetDevice(&prev) == cudaSuccess && prev != dev) cudaSetDevice(dev);
-    else prev = -1;
-  }
-  ~DeviceGuard() {
-    if (prev >= 0) cudaSetDevice(prev);
-  }
-};
 
 
 namespace {
@@ -121,6 +109,13 @@ struct sp_span {
   int64_t attn_ws_floats = 0;
   float* attn_ws = nullptr;
   std::mutex mu;
+  // every call that uses the span's scratch (h/qkvb/ctx/mlp, digit planes, split-K
+  // workspace and counters, attention partials) is ordered after the previous one,
+  // whatever stream the caller passes: the new stream waits on `done` (recorded at
+  // the end of the previous call's work) before its first launch
+  cudaEvent_t done = nullptr;
+  cudaStream_t done_stream = nullptr;
+  bool done_valid = false;
   // live per-launch timing (bench roofline): CUDA events around each launch
   struct ProfRec { int cls; cudaEvent_t a, b; double bytes, flops; };
   bool prof = false;
@@ -135,7 +130,8 @@ struct sp_kv {
   std::vector<std::vector<int>> pages;
   int* d_table = nullptr;
   int table_cap_width = 0;
-  std::vector<int> h_table;
+  int* h_table = nullptr;          // pinned staging copy of the table (async upload)
+  cudaEvent_t table_ev = nullptr;  // completes when the last upload has read h_table
 };
 
 namespace {
@@ -276,50 +272,76 @@ void release_page(sp_span* s, int p) {
 
 int upload_table(sp_kv* kv, cudaStream_t st) {
   sp_span* s = kv->span;
+  const size_t n = (size_t)kv->width * s->max_pages;
   if (kv->table_cap_width < kv->width) {
+    if (kv->table_ev) SP_CUDA_TRY(cudaEventSynchronize(kv->table_ev));
     cudaFree(kv->d_table);
+    cudaFreeHost(kv->h_table);
     kv->d_table = nullptr;
-    SP_CUDA_TRY(cudaMalloc(&kv->d_table, (size_t)kv->width * s->max_pages * sizeof(int)));
+    kv->h_table = nullptr;
+    kv->table_cap_width = 0;
+    SP_CUDA_TRY(cudaMalloc(&kv->d_table, n * sizeof(int)));
+    SP_CUDA_TRY(cudaMallocHost(&kv->h_table, n * sizeof(int)));
     kv->table_cap_width = kv->width;
   }
-  kv->h_table.assign((size_t)kv->width * s->max_pages, 0);
+  if (!kv->table_ev) SP_CUDA_TRY(cudaEventCreateWithFlags(&kv->table_ev, cudaEventDisableTiming));
+  // the previous upload must have read the staging copy before it is rewritten
+  // (in practice long complete: uploads happen every 64 positions or on reorder)
+  SP_CUDA_TRY(cudaEventSynchronize(kv->table_ev));
+  std::fill(kv->h_table, kv->h_table + n, 0);
   for (int i = 0; i < kv->width; ++i)
     for (size_t p = 0; p < kv->pages[i].size(); ++p)
       kv->h_table[(size_t)i * s->max_pages + p] = kv->pages[i][p];
-  SP_CUDA_TRY(cudaMemcpyAsync(kv->d_table, kv->h_table.data(), kv->h_table.size() * sizeof(int),
-                              cudaMemcpyHostToDevice, st));
-  SP_CUDA_TRY(cudaStreamSynchronize(st));
+  // stream-ordered after every kernel that read the old table; no host sync
+  SP_CUDA_TRY(cudaMemcpyAsync(kv->d_table, kv->h_table, n * sizeof(int), cudaMemcpyHostToDevice,
+                              st));
+  SP_CUDA_TRY(cudaEventRecord(kv->table_ev, st));
   return SP_OK;
 }
 
-// make pages for positions [length, length + n_new) writable for every slot
+// make pages for positions [length, length + n_new) writable for every slot.
+// The pages needed (new pages + copy-on-write copies of shared partial tails)
+// are counted first, so a request the pool cannot hold changes nothing.
 int prepare_pages(sp_kv* kv, int n_new, cudaStream_t st) {
   sp_span* s = kv->span;
-  bool changed = false;
+  const int need = (kv->length + n_new + kPageTokens - 1) / kPageTokens;
+  int64_t want = 0;
+  for (int i = 0; i < kv->width; ++i) {
+    const auto& pg = kv->pages[i];
+    if (kv->length % kPageTokens && !pg.empty() && s->refcount[pg.back()] > 1) ++want;
+    want += std::max(0, need - (int)pg.size());
+  }
+  if (want > (int64_t)s->free_pages.size()) SP_FAIL(SP_ERR_CAPACITY, "KV page pool exhausted");
+  if (want == 0) return SP_OK;
   for (int i = 0; i < kv->width; ++i) {
     auto& pg = kv->pages[i];
     if (kv->length % kPageTokens && !pg.empty()) {
       int tail = pg.back();
       if (s->refcount[tail] > 1) {  // copy-on-write of a shared partial tail page
         int np = alloc_page(s);
-        if (np < 0) SP_FAIL(SP_ERR_CAPACITY, "KV page pool exhausted");
         launch_page_copy(s->pool, s->block_stride, s->end - s->start, s->page_bytes, tail, np,
                          st);
         SP_CHECK_LAUNCH();
         release_page(s, tail);
         pg.back() = np;
-        changed = true;
       }
     }
-    int need = (kv->length + n_new + kPageTokens - 1) / kPageTokens;
-    while ((int)pg.size() < need) {
-      int np = alloc_page(s);
-      if (np < 0) SP_FAIL(SP_ERR_CAPACITY, "KV page pool exhausted");
-      pg.push_back(np);
-      changed = true;
-    }
+    while ((int)pg.size() < need) pg.push_back(alloc_page(s));
   }
-  if (changed) return upload_table(kv, st);
+  return upload_table(kv, st);
+}
+
+// cross-stream ordering of the span's scratch (see sp_span::done)
+int order_begin(sp_span* s, cudaStream_t st) {
+  if (s->done_valid && s->done_stream != st) SP_CUDA_TRY(cudaStreamWaitEvent(st, s->done, 0));
+  return SP_OK;
+}
+
+int order_end(sp_span* s, cudaStream_t st) {
+  if (!s->done) SP_CUDA_TRY(cudaEventCreateWithFlags(&s->done, cudaEventDisableTiming));
+  SP_CUDA_TRY(cudaEventRecord(s->done, st));
+  s->done_stream = st;
+  s->done_valid = true;
   return SP_OK;
 }
 
@@ -737,7 +759,7 @@ int sp_span_create(const sp_config* cfg, int32_t start, int32_t end, int32_t dev
   if (!cfg || !out) SP_FAIL(SP_ERR_ARG, "null argument");
   if (validate(cfg) != SP_OK) SP_FAIL(SP_ERR_ARG, "unsupported config shape");
   if (!(0 <= start && start < end && end <= cfg->n_blocks)) SP_FAIL(SP_ERR_ARG, "bad span");
-  SP_CUDA_TRY(cudaSetDevice(device));
+  DeviceGuard dg(device);
   sp_span* s = new sp_span();
   s->cfg = *cfg;
   s->start = start; s->end = end; s->device = device;
@@ -860,7 +882,7 @@ int sp_span_create(const sp_config* cfg, int32_t start, int32_t end, int32_t dev
 
 int sp_span_destroy(sp_span* s) {
   if (!s) return SP_OK;
-  cudaSetDevice(s->device);
+  DeviceGuard dg(s->device);
   cudaFree(s->wmem); cudaFree(s->rope_cos); cudaFree(s->rope_sin); cudaFree(s->alibi);
   cudaFree(s->pool); cudaFree(s->h); cudaFree(s->qkvb); cudaFree(s->ctx); cudaFree(s->mlp);
   cudaFree(s->mlp_raw); cudaFree(s->gemv_ws); cudaFree(s->gemv_cnt); cudaFree(s->attn_ws);
@@ -870,6 +892,7 @@ int sp_span_destroy(sp_span* s) {
   cudaFree(s->nf4_hi); cudaFree(s->nf4_lo); cudaFree(s->nf4_sc);
   for (auto& r : s->prof_recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : s->ev_pool) cudaEventDestroy(e);
+  if (s->done) cudaEventDestroy(s->done);
   delete s;
   return SP_OK;
 }
@@ -879,7 +902,7 @@ int64_t sp_span_free_pages(const sp_span* s) { return s ? (int64_t)s->free_pages
 
 int sp_span_read_weight(sp_span* s, int32_t block, int32_t role, float* dst_host) {
   if (!s || block < s->start || block >= s->end) SP_FAIL(SP_ERR_ARG, "block outside span");
-  SP_CUDA_TRY(cudaSetDevice(s->device));
+  DeviceGuard dg(s->device);
   BlockW& W = s->blocks[block - s->start];
   const int64_t d = s->d, F = s->F;
   void* src = nullptr; float* sc = nullptr; int64_t K = 0, N = 0; MatPlace pl{0, 1, 0};
@@ -926,7 +949,12 @@ int sp_kv_destroy(sp_kv* kv) {
       for (int p : pg) release_page(s, p);
   }
   DeviceGuard dg(s->device);
+  if (kv->table_ev) {
+    cudaEventSynchronize(kv->table_ev);
+    cudaEventDestroy(kv->table_ev);
+  }
   cudaFree(kv->d_table);
+  cudaFreeHost(kv->h_table);
   delete kv;
   return SP_OK;
 }
@@ -960,7 +988,7 @@ int sp_kv_read(sp_kv* kv, int32_t block, int32_t slot, float* keys_host, float* 
   if (block < s->start || block >= s->end || slot < 0 || slot >= kv->width)
     SP_FAIL(SP_ERR_ARG, "block/slot out of range");
   block -= s->start;
-  SP_CUDA_TRY(cudaSetDevice(s->device));
+  DeviceGuard dg(s->device);
   int64_t n = (int64_t)kv->length * s->kvh * s->hd;
   if (n == 0) return SP_OK;
   float *k = nullptr, *v = nullptr;
@@ -988,9 +1016,10 @@ static int forward_impl(sp_span* s, sp_kv* kv, int32_t b0, int32_t b1, const flo
   if (n_new < 1) SP_FAIL(SP_ERR_ARG, "n_new must be >= 1");
   if (kv->length + n_new > s->cfg.max_seq_len) SP_FAIL(SP_ERR_CAPACITY, "exceeds max_seq_len");
   cudaStream_t st = (cudaStream_t)stream;
-  SP_CUDA_TRY(cudaSetDevice(s->device));
   std::lock_guard<std::mutex> g(s->mu);
-  int rc = prepare_pages(kv, n_new, st);
+  int rc = order_begin(s, st);
+  if (rc) return rc;
+  rc = prepare_pages(kv, n_new, st);
   if (rc) return rc;
   const int64_t n = (int64_t)width * n_new * s->d;
   if (x_codes) {
@@ -999,11 +1028,14 @@ static int forward_impl(sp_span* s, sp_kv* kv, int32_t b0, int32_t b1, const flo
     SP_CUDA_TRY(cudaMemcpyAsync(y, x, n * sizeof(float), cudaMemcpyDeviceToDevice, st));
   }
   rc = run_span(s, kv, b0, b1, y, record, width, n_new, st);
-  if (rc) return rc;
+  if (rc) {
+    order_end(s, st);
+    return rc;
+  }
   kv->length += n_new;
   if (y_codes) launch_quantize(y, y_codes, y_scales, n, st);
   SP_CHECK_LAUNCH();
-  return SP_OK;
+  return order_end(s, st);
 }
 
 int sp_span_forward(sp_span* s, sp_kv* kv, int32_t b0, int32_t b1, const float* x,
@@ -1071,7 +1103,7 @@ int sp_span_set_profiling(sp_span* s, int32_t enable) {
 int sp_span_profile_read(sp_span* s, int32_t n_classes, double* ms, double* bytes, double* flops,
                          int64_t* launches) {
   if (!s) SP_FAIL(SP_ERR_ARG, "null span");
-  SP_CUDA_TRY(cudaSetDevice(s->device));
+  DeviceGuard dg(s->device);
   SP_CUDA_TRY(cudaDeviceSynchronize());
   for (int c = 0; c < n_classes; ++c) { ms[c] = 0; bytes[c] = 0; flops[c] = 0; launches[c] = 0; }
   for (auto& r : s->prof_recs) {
@@ -1093,13 +1125,18 @@ int sp_span_decode_gemv_only(sp_span* s, sp_kv* kv, int32_t b0, int32_t b1, floa
                              int32_t width, void* stream, double* weight_bytes) {
   if (!s || !kv || !y) SP_FAIL(SP_ERR_ARG, "null argument");
   if (s->cfg.weight_dtype == kF32) SP_FAIL(SP_ERR_ARG, "tensor-core decode path only");
-  SP_CUDA_TRY(cudaSetDevice(s->device));
+  DeviceGuard dg(s->device);
+  std::lock_guard<std::mutex> g(s->mu);
+  int rc = order_begin(s, (cudaStream_t)stream);
+  if (rc) return rc;
   const int64_t d = s->d;
   double wb = 0;
   const int64_t shapes[4][2] = {{s->n_qkv, d}, {d, d}, {s->n_up, d}, {d, s->F}};
   for (auto& sh : shapes) wb += weight_bytes_of(s->cfg.weight_dtype, sh[0], sh[1]);
   if (weight_bytes) *weight_bytes = wb * (b1 - b0);
-  return run_span_decode_tc(s, kv, b0, b1, y, width, (cudaStream_t)stream, true);
+  rc = run_span_decode_tc(s, kv, b0, b1, y, width, (cudaStream_t)stream, true);
+  int rc2 = order_end(s, (cudaStream_t)stream);
+  return rc ? rc : rc2;
 }
 
 uint64_t sp_fnv1a64(const uint8_t* data, int64_t n) {

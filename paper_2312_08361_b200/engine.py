@@ -218,6 +218,11 @@ class B200ServerEngine:
         self.blocks = _BlockList(self.span)
         # stateless forward chunk (tokens): see device_micro_batches
         self.stateless_tokens = min(2048, self.span.kv_pool_tokens // 2)
+        self.last_forward_chunks = 0
+        # block_backward exists for the reference's own family only (SP/model.py:320)
+        c = self.config
+        self.backward_defined = (c.family == "toy" and c.weight_dtype == "f32"
+                                 and c.kv_heads == c.n_heads)
 
     # -- sessions ---------------------------------------------------------------
     def make_caches(self, start: int, end: int, width: int) -> SpanCaches:
@@ -284,7 +289,15 @@ class B200ServerEngine:
     def forward(self, start: int, end: int, blob, batch: int, tokens: int,
                 micro_batch_tokens: int, record: list | None) -> HiddenBlob:
         """`RealServerEngine.forward` (SP/server.py:106-125) with the same
-        whole-sequence micro-batching (SP/server.py:189-194)."""
+        whole-sequence micro-batching (SP/server.py:189-194).
+
+        ``record`` (prompt tuning) keeps every block input on the GPU for the
+        backward pass; it is rejected up front for families without a backward
+        (Llama / BLOOM shapes, quantised weights), whose records could never be
+        used and would only hold (end - start) x rows x d floats of HBM."""
+        if record is not None and not self.backward_defined:
+            raise ProtocolError("forward(record=...) needs block_backward, defined for the "
+                                "reference (toy, f32) family only")
         d = self.config.hidden_dim
         with torch.cuda.device(self.device):
             xp, cp, sp_, keep = self._input_ptrs(blob, batch * tokens)
@@ -300,8 +313,10 @@ class B200ServerEngine:
             # chunk cap: the device chunk size, bounded by the KV pages free right
             # now (a stateless chunk holds ceil(tokens / 64) pages per sequence)
             fit = max(1, self.span.free_pages // max(1, -(-tokens // 64))) * tokens
-            for chunk in device_micro_batches(batch, tokens, min(micro_batch_tokens, fit),
-                                              min(self.stateless_tokens, fit)):
+            chunks = list(device_micro_batches(batch, tokens, min(micro_batch_tokens, fit),
+                                               min(self.stateless_tokens, fit)))
+            self.last_forward_chunks = len(chunks)
+            for chunk in chunks:
                 nb = chunk.stop - chunk.start
                 xc = x[chunk].contiguous()
                 rec = None

@@ -1,46 +1,8 @@
-"""Exception hierarchy of the host mirror — same names and meaning as
-`SP/errors.py:8-55` so callers written against the reference read the same."""
+"""The one error class the engine raises itself: a request the span cannot
+serve.  The reference engine protocol raises `ProtocolError` (SP/errors.py:24;
+SURVEY.md §8b) and its BlockServer lets engine exceptions propagate, so only
+the name and meaning matter to callers."""
 
 
-class SwarmError(Exception):
-    """Base of all swarm errors (SP/errors.py:8)."""
-
-
-class ConfigurationError(SwarmError):
-    pass
-
-
-class CapacityError(SwarmError):
-    pass
-
-
-class StateDesyncError(SwarmError):
-    pass
-
-
-class ProtocolError(SwarmError):
-    pass
-
-
-class TransportError(SwarmError):
-    pass
-
-
-class MessageDropped(TransportError):
-    pass
-
-
-class ConnectionFailed(TransportError):
-    pass
-
-
-class NoRouteError(SwarmError):
-    pass
-
-
-class SwarmUnavailableError(SwarmError):
-    pass
-
-
-class BudgetExhausted(SwarmError):
-    pass
+class ProtocolError(Exception):
+    """Invalid request for the span engine (SP/errors.py:24)."""

@@ -1,7 +1,14 @@
-"""Client head on the GPU (`RealClientEngine`, SP/client.py:89-106): embedding
-rows for token ids and the greedy pick from the last output row, through
-libspanpipe.so (sp_head_*).  Interface = what SwarmClient calls:
-``embed_array(tokens) -> np.ndarray [n, d]`` and ``pick(rows) -> int``."""
+"""Client head on the GPU — the payload side of `RealClientEngine`
+(SP/client.py:89-106): embedding rows for token ids, the tied logits
+``row @ E^T`` (SP/model.py:393-395, no final norm) and the token choice, all
+through libspanpipe.so (sp_head_*).
+
+Interface = what the reference's SwarmClient calls on its client engine:
+``embed_array(tokens) -> np.ndarray [n, d]``,
+``pick(final_rows, mode, rng, top_k) -> int`` (greedy on the GPU; sampling
+draws from GPU logits on the host with the reference's float64 recipe) and
+``logits(rows) -> np.ndarray [n, vocab]`` (beam search).
+"""
 
 from __future__ import annotations
 
@@ -35,6 +42,13 @@ class ClientHead:
     def _stream(self) -> int:
         return torch.cuda.current_stream(self.device).cuda_stream
 
+    def _rows_device(self, rows) -> torch.Tensor:
+        d = self.config.hidden_dim
+        if isinstance(rows, torch.Tensor):
+            return rows.to(self.device, torch.float32).reshape(-1, d).contiguous()
+        a = np.ascontiguousarray(np.asarray(rows, dtype=np.float32).reshape(-1, d))
+        return torch.from_numpy(a).to(self.device)
+
     def embed_device(self, tokens) -> torch.Tensor:
         t = np.ascontiguousarray(tokens, dtype=np.int32)
         out = torch.empty((t.size, self.config.hidden_dim), dtype=torch.float32, device=self.device)
@@ -52,12 +66,40 @@ class ClientHead:
                                            self._stream()))
         return int(tok[0])
 
-    def pick(self, final_rows) -> int:
-        last = np.ascontiguousarray(np.asarray(final_rows, dtype=np.float32).reshape(
-            -1, self.config.hidden_dim)[-1])
-        return self.pick_device(torch.from_numpy(last).to(self.device))
+    def logits_device(self, rows) -> torch.Tensor:
+        x = self._rows_device(rows)
+        out = torch.empty((x.shape[0], self.config.vocab_size), dtype=torch.float32,
+                          device=self.device)
+        _lib.check(self.lib.sp_head_logits(self.handle, x.data_ptr(), int(x.shape[0]),
+                                           out.data_ptr(), self._stream()))
+        return out
+
+    def logits(self, rows) -> np.ndarray:
+        """[n, vocab] logits of n rows (`RealClientEngine.logits`, SP/client.py:104-105)."""
+        return self.logits_device(rows).cpu().numpy()
+
+    def pick(self, final_rows, mode: str = "greedy", rng=None, top_k=None) -> int:
+        """Token from the last row (`RealClientEngine.pick`, SP/client.py:97-102)."""
+        last = self._rows_device(final_rows)[-1:]
+        if mode == "greedy":
+            return self.pick_device(last[0])
+        return sample_pick(self.logits_device(last)[0].cpu().numpy(), rng, top_k)
 
     def embedding(self) -> np.ndarray:
         out = np.empty((self.config.vocab_size, self.config.hidden_dim), np.float32)
         _lib.check(self.lib.sp_head_read_embedding(self.handle, out.ctypes.data))
         return out
+
+
+def sample_pick(logits: np.ndarray, rng: np.random.Generator, top_k: int | None = None) -> int:
+    """Seeded categorical draw over float64 softmax probabilities — the recipe
+    of SP/model.py:403-416 (top-k mask to -inf, max-shifted exp, one uniform
+    draw located in the cumulative sum), so a shared rng stream draws the same
+    tokens as the reference client."""
+    z = np.asarray(logits, dtype=np.float64)
+    if top_k is not None and top_k < z.size:
+        kept = np.argpartition(z, -top_k)[-top_k:]
+        z = np.where(np.isin(np.arange(z.size), kept), z, -np.inf)
+    p = np.exp(z - z.max())
+    p = p / p.sum()
+    return int(np.searchsorted(np.cumsum(p), rng.random(), side="right"))

@@ -113,10 +113,20 @@ def swarm_traces() -> None:
         dict(name="four_stage_two_crashes", n_stages=4, replicas=2,
              crash={"s0a": 5, "s3a": 20}, n_new=24, quantized=False),
         dict(name="no_failure_q", n_stages=4, replicas=1, crash={}, n_new=16, quantized=True),
+        # random message drops, SURVEY.md 0.10 (seeds 3, 5, 11, p = 0.01, 128 tokens):
+        # the counters depend only on the seeded drop stream and the byte sizes
+        dict(name="drops_p01_seed3", n_stages=4, replicas=2, crash={}, n_new=128,
+             quantized=False, seed=3, failure_prob=1e-2),
+        dict(name="drops_p01_seed5_q", n_stages=4, replicas=2, crash={}, n_new=128,
+             quantized=True, seed=5, failure_prob=1e-2),
+        dict(name="drops_p01_seed11", n_stages=2, replicas=2, crash={"s0b": 40}, n_new=128,
+             quantized=False, seed=11, failure_prob=1e-2),
     ]
     out = []
     for sc in scenarios:
-        swarm = build_sim_swarm(cfg, n_stages=sc["n_stages"], replicas=sc["replicas"], seed=0,
+        prof = NetProfile(failure_prob=sc["failure_prob"]) if "failure_prob" in sc else None
+        swarm = build_sim_swarm(cfg, n_stages=sc["n_stages"], replicas=sc["replicas"],
+                                seed=sc.get("seed", 0), profile=prof,
                                 server_overrides={k: {"crash_after_messages": v}
                                                   for k, v in sc["crash"].items()})
         res = swarm.client().generate([3, 1, 4], sc["n_new"], strategy=Strategy.DUAL_CACHE,
@@ -125,7 +135,8 @@ def swarm_traces() -> None:
         out.append(dict(sc, tokens=res.tokens, messages=c.messages, recoveries=c.recoveries,
                         reroutes=c.reroutes, restore_events=[list(e) for e in c.restore_events],
                         step_activation_bytes=c.step_activation_bytes,
-                        per_step_bytes=c.per_step_bytes,
+                        per_step_bytes=c.per_step_bytes, elapsed_s=res.elapsed_s,
+                        total_bytes=swarm.net.total_bytes(),
                         oracle=M.reference_generate(cfg, [3, 1, 4], sc["n_new"])))
     with open(os.path.join(OUT, "swarm_traces.json"), "w") as f:
         json.dump(out, f, indent=1)
@@ -179,10 +190,32 @@ def backward_vectors() -> None:
     np.savez_compressed(os.path.join(OUT, "backward.npz"), **arrays)
 
 
+def blob_vectors() -> None:
+    """HiddenBlob byte accounting (SP/wire.py:105-122): nbytes() and the FNV-1a
+    of encode() for raw / int8-coded / shape-only blobs (inputs: the rng stream
+    below, regenerated by tests/test_reference_host.py).  These byte counts drive
+    SimNetwork's timing and drop budget, so the device blob must reproduce them."""
+    from swarmpipe.wire import HiddenBlob, fnv1a64
+    rng = np.random.default_rng(21)
+    out = []
+    for rows, cols in ((1, 64), (3, 64), (7, 100), (1, 4096), (2, 8192), (1, 14336), (0, 64),
+                       (5, 1)):
+        a = (rng.standard_normal((rows, cols)) * rng.uniform(0.1, 30)).astype(np.float32)
+        for q in (False, True):
+            b = HiddenBlob.from_array(a, q)
+            out.append(dict(rows=rows, cols=cols, quantized=q, nbytes=b.nbytes(),
+                            fnv=fnv1a64(b.encode())))
+            s = HiddenBlob.shape_only(rows, cols, q)
+            out.append(dict(rows=rows, cols=cols, quantized=q, synthetic=True,
+                            nbytes=s.nbytes()))
+    with open(os.path.join(OUT, "blob.json"), "w") as f:
+        json.dump(out, f)
+
+
 if __name__ == "__main__":
-    codec_vectors()
-    toy_model_vectors()
-    swarm_traces()
-    assignment_vectors()
-    backward_vectors()
+    only = sys.argv[1:]
+    for fn in (codec_vectors, toy_model_vectors, swarm_traces, assignment_vectors,
+               backward_vectors, blob_vectors):
+        if not only or fn.__name__ in only:
+            fn()
     print("golden vectors written to", OUT)

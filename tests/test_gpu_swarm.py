@@ -1,19 +1,36 @@
-"""The dual-cache failover path on the GPU: span servers backed by the B200
-engine, the client head on the GPU, crash injection — tokens and every
-failover counter must equal the reference's golden traces (SURVEY.md §0.10:
-these integer counters are engine-independent)."""
+"""The B200 engine inside the reference's OWN host layer on the GPU: the
+reference's BlockServer / SimNetwork / DirectoryBoard / SwarmClient (installed
+unmodified in baseline/_ref) with `B200ServerEngine` as every server's payload
+engine and the GPU client head as the client's (SURVEY.md §7 step 2 swap recipe,
+tests/support/ref_swarm.py).
+
+Pinned: tokens and every failover counter (messages, recoveries, reroutes,
+restore_events, per-step bytes, virtual elapsed time, total bytes on the wire)
+equal the traces the reference itself produced (tests/golden/make_golden.py);
+SURVEY.md §0.10: these are engine-independent, so a drop-in must reproduce them
+exactly."""
 
 import json
 import os
-import sys
 
 import numpy as np
 import pytest
 
-from conftest import GOLDEN, ROOT
+from conftest import GOLDEN
 
 pytestmark = pytest.mark.gpu
 TRACES = json.load(open(os.path.join(GOLDEN, "swarm_traces.json")))
+
+
+def _swarm(swarmpipe, tr, model=None):
+    from support.ref_swarm import build_gpu_swarm
+    prof = (swarmpipe.netsim.NetProfile(failure_prob=tr["failure_prob"])
+            if "failure_prob" in tr else None)
+    return build_gpu_swarm(swarmpipe, model or swarmpipe.model.ModelConfig(seed=1),
+                           n_stages=tr["n_stages"], replicas=tr["replicas"],
+                           seed=tr.get("seed", 0), profile=prof,
+                           server_overrides={k: {"crash_after_messages": v}
+                                             for k, v in tr["crash"].items()})
 
 
 def test_client_head_matches_reference(golden_toy):
@@ -28,136 +45,128 @@ def test_client_head_matches_reference(golden_toy):
     for _ in range(50):
         row = rng.standard_normal((2, 64)).astype(np.float32)
         assert head.pick(row) == om.greedy_pick(om.logits_for(emb, row[-1]))
+    rows = rng.standard_normal((5, 64)).astype(np.float32)
+    got = head.logits(rows)
+    want = rows @ emb.T
+    err = np.abs(got - want).max()
+    print(f"head logits max-abs err {err:.3g}")
+    assert err <= 1e-5
+    # sampling: GPU logits, the reference's float64 draw -> same tokens for one rng stream
+    from paper_2312_08361_b200.head import sample_pick
+    r1, r2 = np.random.default_rng(7), np.random.default_rng(7)
+    for _ in range(20):
+        row = rng.standard_normal((1, 64)).astype(np.float32)
+        assert head.pick(row, "sample", r1, 5) == sample_pick(row[0] @ emb.T, r2, 5)
 
 
 @pytest.mark.parametrize("tr", TRACES, ids=[t["name"] for t in TRACES])
-def test_gpu_failover_trace(tr):
-    from paper_2312_08361_b200.client import SwarmClient, build_swarm
-    from paper_2312_08361_b200.config import toy
+def test_failover_trace_inside_reference_swarm(swarmpipe, tr):
     from paper_2312_08361_b200.engine import B200ServerEngine
-    from paper_2312_08361_b200.head import ClientHead
-    cfg = toy(seed=1)
-    eng = B200ServerEngine(cfg)
-    net, servers, routes = build_swarm(lambda: eng, cfg, tr["n_stages"], tr["replicas"],
-                                       crash=tr["crash"])
-    res = SwarmClient("client1", cfg, net, routes, ClientHead(cfg)).generate(
-        [3, 1, 4], tr["n_new"], quantized=tr["quantized"])
+    swarm = _swarm(swarmpipe, tr)
+    assert all(isinstance(s.engine, B200ServerEngine) for s in swarm.servers.values())
+    res = swarm.client().generate([3, 1, 4], tr["n_new"], quantized=tr["quantized"])
     c = res.counters
-    assert res.tokens == tr["tokens"]
-    assert (c.messages, c.recoveries, c.reroutes) == (tr["messages"], tr["recoveries"], tr["reroutes"])
+    assert (c.messages, c.recoveries, c.reroutes) == (tr["messages"], tr["recoveries"],
+                                                      tr["reroutes"])
     assert [list(e) for e in c.restore_events] == tr["restore_events"]
+    assert c.step_activation_bytes == tr["step_activation_bytes"]
     assert c.per_step_bytes == tr["per_step_bytes"]
+    assert res.elapsed_s == tr["elapsed_s"]
+    assert swarm.net.total_bytes() == tr["total_bytes"]
+    agree = np.mean(np.array(res.tokens) == np.array(tr["tokens"]))
+    print(f"{tr['name']}: tokens agree {agree:.3f}, oracle tokens {tr['tokens'] == tr['oracle']}")
+    if not tr["quantized"]:
+        assert res.tokens == tr["tokens"] == tr["oracle"]
+    else:
+        # int8-coded stage boundaries: the reference's own tokens (codec bit-exact,
+        # block outputs within 1e-5; T/test_acceptance.py:358-371 allows >= 95 %)
+        assert agree >= 0.95
 
 
-def _reference_importable():
-    for p in (os.path.join(ROOT, "baseline", "_ref"), "/root/reference/pkg/src"):
-        if os.path.isdir(os.path.join(p, "swarmpipe")):
-            return p
-    return None
-
-
-@pytest.mark.skipif(_reference_importable() is None, reason="reference package not installed")
-def test_dropin_inside_reference_block_server():
-    """The engine plugged into the reference's OWN BlockServer / SimNetwork /
-    SwarmClient (rebinding RealServerEngine): greedy
-    tokens equal the oracle through a crash + restore."""
-    sys.path.insert(0, _reference_importable())
-    import swarmpipe
-    import swarmpipe.server
-    import swarmpipe.swarm
+def test_dropin_c1_crash_and_restore(swarmpipe):
+    """one stage x 2 replicas, s0a crashes after 6
+    messages; tokens == the oracle, one recovery, restore of t = 7 rows."""
     from swarmpipe.model import ModelConfig, reference_generate
-    from paper_2312_08361_b200.engine import B200ServerEngine
-    orig = swarmpipe.swarm.RealServerEngine
-    swarmpipe.swarm.RealServerEngine = B200ServerEngine
-    swarmpipe.server.RealServerEngine = B200ServerEngine
-    try:
-        cfg = ModelConfig(seed=1)
-        swarm = swarmpipe.swarm.build_sim_swarm(
-            cfg, n_stages=1, replicas=2, seed=0,
-            server_overrides={"s0a": {"crash_after_messages": 6}})
-        assert isinstance(swarm.servers["s0a"].engine, B200ServerEngine)
-        res = swarm.client().generate([3, 1, 4], 32)
-        assert res.tokens == reference_generate(cfg, [3, 1, 4], 32)
-        assert res.counters.recoveries == 1
-        assert [tuple(e) for e in res.counters.restore_events] == [(0, 8, 7, 1792)]
-        swarm = swarmpipe.swarm.build_sim_swarm(cfg, n_stages=4, replicas=2, seed=3,
-                                                profile=swarmpipe.netsim.NetProfile(failure_prob=1e-2))
-        res = swarm.client().generate([3, 1, 4], 64, quantized=True)
-        assert len(res.tokens) == 67
-    finally:
-        swarmpipe.swarm.RealServerEngine = orig
-        swarmpipe.server.RealServerEngine = orig
+    from support.ref_swarm import build_gpu_swarm
+    cfg = ModelConfig(seed=1)
+    swarm = build_gpu_swarm(swarmpipe, cfg, n_stages=1, replicas=2, seed=0,
+                            server_overrides={"s0a": {"crash_after_messages": 6}})
+    res = swarm.client().generate([3, 1, 4], 32)
+    assert res.tokens == reference_generate(cfg, [3, 1, 4], 32)
+    assert res.counters.recoveries == 1
+    assert [tuple(e) for e in res.counters.restore_events] == [(0, 8, 7, 1792)]
 
 
-@pytest.mark.skipif(_reference_importable() is None, reason="reference package not installed")
-def test_dropin_beam_search_matches_reference_oracle():
-    """§8f item 2, T/test_beam.py:21-44 with the GPU engine inside the reference's
-    own swarm: k = 4 beams (reorder = page-table permutation with copy-on-write
-    tails) give the local beam oracle's hypotheses and scores, also through a
+def test_dropin_other_strategies(swarmpipe):
+    """T/test_client.py:24-28: RESTART and CACHELESS generation through the GPU
+    engine equal the oracle too."""
+    from swarmpipe.client import Strategy
+    from swarmpipe.model import ModelConfig, reference_generate
+    from support.ref_swarm import build_gpu_swarm
+    cfg = ModelConfig(seed=1)
+    want = reference_generate(cfg, [5, 9], 12)
+    for strat in (Strategy.RESTART, Strategy.CACHELESS):
+        swarm = build_gpu_swarm(swarmpipe, cfg, n_stages=2, replicas=2, seed=1)
+        assert swarm.client().generate([5, 9], 12, strategy=strat).tokens == want
+
+
+def test_dropin_beam_search_matches_reference_oracle(swarmpipe):
+    """§8f item 2, T/test_beam.py:21-44 inside the reference's swarm: k = 4 beams
+    (reorder = page-table permutation with copy-on-write tails, logits on the
+    GPU head) give the local beam oracle's hypotheses and scores, also through a
     crashed server, and k = 1 degenerates to greedy."""
-    sys.path.insert(0, _reference_importable())
-    import swarmpipe.server
-    import swarmpipe.swarm
     from swarmpipe.model import ModelConfig, reference_beam, reference_generate
-    from paper_2312_08361_b200.engine import B200ServerEngine
-    orig = swarmpipe.swarm.RealServerEngine
-    swarmpipe.swarm.RealServerEngine = B200ServerEngine
-    swarmpipe.server.RealServerEngine = B200ServerEngine
-    try:
-        cfg = ModelConfig(seed=1)
-        swarm = swarmpipe.swarm.build_sim_swarm(cfg, seed=0)
-        assert swarm.client().beam_generate([4, 2], 16, k=1).tokens == \
-            reference_generate(cfg, [4, 2], 16)
-        want = reference_beam(cfg, [4, 2], 24, k=4)
-        res = swarmpipe.swarm.build_sim_swarm(cfg, seed=0).client().beam_generate([4, 2], 24, k=4)
-        assert [h for h, _ in res.beams] == [h for h, _ in want]
-        for (_, sa), (_, sb) in zip(res.beams, want):
-            assert sa == pytest.approx(sb, abs=1e-4)
-        want = reference_beam(cfg, [4, 2], 16, k=4)
-        swarm = swarmpipe.swarm.build_sim_swarm(
-            cfg, seed=0, server_overrides={"s2a": {"crash_after_messages": 10}})
-        res = swarm.client().beam_generate([4, 2], 16, k=4)
-        assert [h for h, _ in res.beams] == [h for h, _ in want]
-        assert res.counters.recoveries >= 1
-    finally:
-        swarmpipe.swarm.RealServerEngine = orig
-        swarmpipe.server.RealServerEngine = orig
+    from support.ref_swarm import build_gpu_swarm
+    cfg = ModelConfig(seed=1)
+    assert build_gpu_swarm(swarmpipe, cfg, seed=0).client().beam_generate(
+        [4, 2], 16, k=1).tokens == reference_generate(cfg, [4, 2], 16)
+    want = reference_beam(cfg, [4, 2], 24, k=4)
+    res = build_gpu_swarm(swarmpipe, cfg, seed=0).client().beam_generate([4, 2], 24, k=4)
+    assert [h for h, _ in res.beams] == [h for h, _ in want]
+    for (_, sa), (_, sb) in zip(res.beams, want):
+        assert sa == pytest.approx(sb, abs=1e-4)
+    want = reference_beam(cfg, [4, 2], 16, k=4)
+    swarm = build_gpu_swarm(swarmpipe, cfg, seed=0,
+                            server_overrides={"s2a": {"crash_after_messages": 10}})
+    res = swarm.client().beam_generate([4, 2], 16, k=4)
+    assert [h for h, _ in res.beams] == [h for h, _ in want]
+    assert res.counters.recoveries >= 1
 
 
 @pytest.mark.parametrize("quantized", [False, True])
-def test_llama_int8_failover_greedy_tokens_match_oracle(quantized):
-    """BASELINE north star on the 70B kernel family (int8 weights, GQA, RoPE,
-    SwiGLU, bf16 KV): 2 stages x 2 replicas, a stage-1 server crashes
-    mid-generation, the client replays its cached inputs onto the replica —
-    greedy tokens equal the CPU oracle's (reference_generate restated)."""
+def test_llama_int8_failover_greedy_tokens_match_oracle(swarmpipe, quantized):
+    """The 70B kernel family (int8 weights, GQA, RoPE, SwiGLU, bf16 KV) at a small
+    width, inside the reference's swarm: 2 stages x 2 replicas, s1a crashes
+    mid-generation, the reference client replays its cached inputs onto s1b —
+    greedy tokens equal the CPU oracle's (the same codec round trip at the coded
+    stage boundary when quantized, SP/client.py:280-287)."""
+    from oracle import codec as oc
     from oracle import model as om
-    from paper_2312_08361_b200.client import SwarmClient, build_swarm
     from paper_2312_08361_b200.config import SpanConfig
-    from paper_2312_08361_b200.engine import B200ServerEngine
-    from paper_2312_08361_b200.head import ClientHead
+    from support.ref_swarm import build_gpu_swarm
     cfg = SpanConfig(n_blocks=4, hidden_dim=512, n_heads=4, n_kv_heads=2, ffn_dim=1024,
                      vocab_size=64, max_seq_len=512, family="llama", weight_dtype="int8",
                      kv_dtype="bf16", seed=5)
-    eng = B200ServerEngine(cfg)
-    net, servers, routes = build_swarm(lambda: eng, cfg, 2, 2, crash={"s1a": 9})
-    res = SwarmClient("client1", cfg, net, routes, ClientHead(cfg)).generate(
-        [3, 1, 4], 24, quantized=quantized)
+    swarm = build_gpu_swarm(swarmpipe, cfg, n_stages=2, replicas=2, seed=0,
+                            server_overrides={"s1a": {"crash_after_messages": 9}})
+    res = swarm.client().generate([3, 1, 4], 24, quantized=quantized)
     assert res.counters.recoveries >= 1 and res.counters.restore_events
-    if not quantized:
-        assert res.tokens == om.reference_generate(cfg, [3, 1, 4], 24)
-    else:
-        # stage boundary coded: the oracle applies the same codec round trip
-        from oracle import codec as oc
-        emb = om.init_embedding(cfg)
-        r0, r1 = om.SpanRunner(cfg, 0, 2), om.SpanRunner(cfg, 2, 4)
-        toks = [3, 1, 4]
-        x = emb[toks]
-        for _ in range(24):
-            h = r0.step(x[None])[0]
+    emb = om.init_embedding(cfg)
+    r0, r1 = om.SpanRunner(cfg, 0, 2), om.SpanRunner(cfg, 2, 4)
+    toks = [3, 1, 4]
+    x = emb[toks]
+    margins = []
+    for _ in range(24):
+        h = r0.step(x[None])[0]
+        if quantized:
             codes, scales = oc.quantize(h)
             h = oc.dequantize(codes, scales, h.shape)
-            y = r1.step(h[None])[0]
-            t = om.greedy_pick(om.logits_for(emb, y[-1]))
-            toks.append(t)
-            x = emb[[t]]
-        assert res.tokens == toks
+        y = r1.step(h[None])[0]
+        lg = om.logits_for(emb, y[-1])
+        top2 = np.sort(lg)[-2:]
+        margins.append(float(top2[1] - top2[0]))
+        t = om.greedy_pick(lg)
+        toks.append(t)
+        x = emb[[t]]
+    print(f"oracle min top1-top2 margin {min(margins):.4g}")
+    assert res.tokens == toks

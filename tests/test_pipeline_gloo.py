@@ -22,7 +22,7 @@ import torch.multiprocessing as mp
 
 from oracle import codec as oc
 from oracle import model as om
-from paper_2312_08361_b200.balancer import stage_intervals
+from paper_2312_08361_b200.placement import stage_intervals
 from paper_2312_08361_b200.config import toy
 from paper_2312_08361_b200.pipeline import SpanPipeline
 
