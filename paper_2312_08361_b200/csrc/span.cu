@@ -116,6 +116,11 @@ struct sp_span {
   cudaEvent_t done = nullptr;
   cudaStream_t done_stream = nullptr;
   bool done_valid = false;
+  // sessions keep the span's host bookkeeping alive: destroying a span with
+  // live sessions frees its device memory at once and the struct when the last
+  // session goes (finalizer order in Python reference cycles is arbitrary)
+  int live_kv = 0;
+  bool dying = false;
   // live per-launch timing (bench roofline): CUDA events around each launch
   struct ProfRec { int cls; cudaEvent_t a, b; double bytes, flops; };
   bool prof = false;
@@ -880,8 +885,7 @@ int sp_span_create(const sp_config* cfg, int32_t start, int32_t end, int32_t dev
   return SP_OK;
 }
 
-int sp_span_destroy(sp_span* s) {
-  if (!s) return SP_OK;
+static void free_span_device(sp_span* s) {
   DeviceGuard dg(s->device);
   cudaFree(s->wmem); cudaFree(s->rope_cos); cudaFree(s->rope_sin); cudaFree(s->alibi);
   cudaFree(s->pool); cudaFree(s->h); cudaFree(s->qkvb); cudaFree(s->ctx); cudaFree(s->mlp);
@@ -893,7 +897,27 @@ int sp_span_destroy(sp_span* s) {
   for (auto& r : s->prof_recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : s->ev_pool) cudaEventDestroy(e);
   if (s->done) cudaEventDestroy(s->done);
-  delete s;
+  s->wmem = s->pool = nullptr;
+  s->rope_cos = s->rope_sin = s->alibi = nullptr;
+  s->h = s->qkvb = s->ctx = s->mlp = s->mlp_raw = s->gemv_ws = s->attn_ws = nullptr;
+  s->st_norm1 = s->st_ctx = s->st_norm2 = s->st_mlp = nullptr;
+  s->ws2 = nullptr; s->cnt2 = s->gemv_cnt = s->attn_cnt = s->exps = nullptr;
+  s->attn_part = nullptr; s->planes = nullptr;
+  s->nf4_hi = s->nf4_lo = nullptr; s->nf4_sc = nullptr;
+  s->prof_recs.clear(); s->ev_pool.clear(); s->done = nullptr;
+}
+
+int sp_span_destroy(sp_span* s) {
+  if (!s) return SP_OK;
+  bool keep;
+  {
+    std::lock_guard<std::mutex> g(s->mu);
+    if (s->dying) return SP_OK;
+    s->dying = true;
+    keep = s->live_kv > 0;
+  }
+  free_span_device(s);
+  if (!keep) delete s;
   return SP_OK;
 }
 
@@ -931,6 +955,11 @@ int sp_span_read_weight(sp_span* s, int32_t block, int32_t role, float* dst_host
 
 int sp_kv_create(sp_span* s, int32_t width, sp_kv** out) {
   if (!s || !out || width < 1) SP_FAIL(SP_ERR_ARG, "bad kv args");
+  {
+    std::lock_guard<std::mutex> g(s->mu);
+    if (s->dying) SP_FAIL(SP_ERR_STATE, "span destroyed");
+    ++s->live_kv;
+  }
   sp_kv* kv = new sp_kv();
   kv->span = s;
   kv->width = width;
@@ -943,19 +972,24 @@ int sp_kv_create(sp_span* s, int32_t width, sp_kv** out) {
 int sp_kv_destroy(sp_kv* kv) {
   if (!kv) return SP_OK;
   sp_span* s = kv->span;
+  bool last;
   {
     std::lock_guard<std::mutex> g(s->mu);
     for (auto& pg : kv->pages)
       for (int p : pg) release_page(s, p);
+    last = --s->live_kv == 0 && s->dying;
   }
-  DeviceGuard dg(s->device);
-  if (kv->table_ev) {
-    cudaEventSynchronize(kv->table_ev);
-    cudaEventDestroy(kv->table_ev);
+  {
+    DeviceGuard dg(s->device);
+    if (kv->table_ev) {
+      cudaEventSynchronize(kv->table_ev);
+      cudaEventDestroy(kv->table_ev);
+    }
+    cudaFree(kv->d_table);
+    cudaFreeHost(kv->h_table);
   }
-  cudaFree(kv->d_table);
-  cudaFreeHost(kv->h_table);
   delete kv;
+  if (last) delete s;
   return SP_OK;
 }
 
@@ -988,6 +1022,7 @@ int sp_kv_read(sp_kv* kv, int32_t block, int32_t slot, float* keys_host, float* 
   if (block < s->start || block >= s->end || slot < 0 || slot >= kv->width)
     SP_FAIL(SP_ERR_ARG, "block/slot out of range");
   block -= s->start;
+  if (s->dying) SP_FAIL(SP_ERR_STATE, "span destroyed");
   DeviceGuard dg(s->device);
   int64_t n = (int64_t)kv->length * s->kvh * s->hd;
   if (n == 0) return SP_OK;
@@ -1017,6 +1052,7 @@ static int forward_impl(sp_span* s, sp_kv* kv, int32_t b0, int32_t b1, const flo
   if (kv->length + n_new > s->cfg.max_seq_len) SP_FAIL(SP_ERR_CAPACITY, "exceeds max_seq_len");
   cudaStream_t st = (cudaStream_t)stream;
   std::lock_guard<std::mutex> g(s->mu);
+  if (s->dying) SP_FAIL(SP_ERR_STATE, "span destroyed");
   int rc = order_begin(s, st);
   if (rc) return rc;
   rc = prepare_pages(kv, n_new, st);
@@ -1127,6 +1163,7 @@ int sp_span_decode_gemv_only(sp_span* s, sp_kv* kv, int32_t b0, int32_t b1, floa
   if (s->cfg.weight_dtype == kF32) SP_FAIL(SP_ERR_ARG, "tensor-core decode path only");
   DeviceGuard dg(s->device);
   std::lock_guard<std::mutex> g(s->mu);
+  if (s->dying) SP_FAIL(SP_ERR_STATE, "span destroyed");
   int rc = order_begin(s, (cudaStream_t)stream);
   if (rc) return rc;
   const int64_t d = s->d;

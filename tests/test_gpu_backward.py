@@ -58,33 +58,33 @@ def test_span_forward_record_backward_matches_reference_golden():
 
 
 def test_backward_rejects_other_families():
-    from paper_2312_08361_b200._lib import SpanPipeError
+    """block_backward is the reference's, defined for its own family only
+    (SP/model.py:320): a recording forward on another family is refused up
+    front (its records could never be used), and the C ABI refuses the backward."""
+    import ctypes
+    import torch
+    from paper_2312_08361_b200._lib import SpanPipeError, check
     from paper_2312_08361_b200.config import SpanConfig
     from paper_2312_08361_b200.engine import B200ServerEngine
+    from paper_2312_08361_b200.errors import ProtocolError
     cfg = SpanConfig(n_blocks=2, hidden_dim=512, n_heads=4, n_kv_heads=2, ffn_dim=1024,
                      vocab_size=64, max_seq_len=256, family="llama", weight_dtype="int8",
                      kv_dtype="bf16", seed=5)
     eng = B200ServerEngine(cfg)
-    record: list = []
     x = np.ones((4, 512), np.float32)
-    eng.forward(0, 2, _blob(x), 1, 4, 10**9, record)
+    with pytest.raises(ProtocolError):
+        eng.forward(0, 2, _blob(x), 1, 4, 10**9, [])
+    eng.forward(0, 2, _blob(x), 1, 4, 10**9, None)           # non-recording is fine
+    xd = torch.ones((4, 512), device="cuda")
     with pytest.raises(SpanPipeError):
-        eng.backward(0, 2, _blob(x), 1, 4, record)
+        check(eng.lib.sp_span_block_backward(eng.span.handle, 0, xd.data_ptr(), xd.data_ptr(),
+                                             xd.data_ptr(), 1, 4, ctypes.c_void_p(0)))
 
 
-def _reference_importable():
-    for p in (os.path.join(ROOT, "baseline", "_ref"), "/root/reference/pkg/src"):
-        if os.path.isdir(os.path.join(p, "swarmpipe")):
-            return p
-    return None
-
-
-@pytest.mark.skipif(_reference_importable() is None, reason="reference package not installed")
-def test_dropin_finetune_session():
+def test_dropin_finetune_session(swarmpipe):
     """The reference's own FinetuneSession over its own swarm, every server's
     engine the B200 engine: the soft-prompt and head gradients of one pass equal
     the reference engine's, and the copy task's loss decreases."""
-    sys.path.insert(0, _reference_importable())
     import swarmpipe.server
     import swarmpipe.swarm
     from swarmpipe.client import FinetuneSession
