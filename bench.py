@@ -292,6 +292,8 @@ def run_b200(args) -> None:
         _lib.check(lib.sp_span_set_option(span.handle, 2, 0))
     if os.environ.get("SP_ATTN_NSUB"):        # A/B switch: decode-attention sub-chunks per CTA
         _lib.check(lib.sp_span_set_option(span.handle, 5, int(os.environ["SP_ATTN_NSUB"])))
+    if os.environ.get("SP_ATTN_CLUSTER"):     # A/B switch: decode-attention cluster merge
+        _lib.check(lib.sp_span_set_option(span.handle, 6, int(os.environ["SP_ATTN_CLUSTER"])))
     d = cfg.hidden_dim
     stream = torch.cuda.current_stream(dev)
 

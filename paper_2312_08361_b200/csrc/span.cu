@@ -4,6 +4,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -454,7 +455,10 @@ int run_span_decode_tc(sp_span* s, sp_kv* kv, int b0, int b1, float* y, int widt
     }
     // 2) attention (RoPE, append, page merge)
     at.kv_pool = s->pool + (int64_t)b * s->block_stride;
-    if (!gemv_only) {
+    // timing experiment only (wrong results): SP_DEBUG_SKIP_ATTN=1 measures the
+    // in-stream cost of decode attention
+    static const bool skip_attn = getenv("SP_DEBUG_SKIP_ATTN") != nullptr;
+    if (!gemv_only && !skip_attn) {
       const double kvb = (double)width * (kv->length + 1) * 2 * s->kv * kv_elt;
       ProfScope ps(s, PC_ATTN_DEC, kvb + 4.0 * R * (s->n_qkv + d),
                    4.0 * width * (kv->length + 1) * s->H * s->hd, st);
