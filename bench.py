@@ -507,7 +507,7 @@ def run_b200(args) -> None:
             "ms_per_step": dec_ms / max(steps_done, 1e-9) * (sessions / max(1, world)) * world
             if world > 1 else dec_ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": ("int8 (weights x 23-bit (batch<=2) / 15-bit int digit activations, exact int32 tensor-core MMA; "
+            "dtype": ("int8 (weights x 15-bit int digit activations, exact int32 tensor-core MMA; "
                       "f32 residual)") if cfg.weight_dtype == "int8" else
                      ("nf4 (4-bit codes -> 7-bit levels x uint8 block scales, 23-bit int digit "
                       "activations, exact int32 MMA / int64 sums; f32 residual)")

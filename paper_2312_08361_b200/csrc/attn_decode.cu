@@ -919,7 +919,26 @@ int64_t attn_dec_part_floats(int width, int H, int hd, int max_pages) {
   return (int64_t)width * H * max_pages * (hd + 2);
 }
 
-void launch_attn_decode_fused(const AttnDecArgs& a, cudaStream_t st) {
+namespace {
+// timing experiment only (SP_DEBUG_ATTN_EMPTY=1, wrong results): a trivial
+// dependent kernel with the attention grid, to measure the cost of the kernel
+// boundary itself in the PDL chain
+__global__ void empty_pdl_kernel(int) {
+  pdl_trigger();
+  pdl_wait();
+}
+}  // namespace
+
+bool g_attn_cl = getenv("SP_ATTN_CL") ? atoi(getenv("SP_ATTN_CL")) != 0 : true;
+
+int launch_attn_decode_fused(const AttnDecArgs& a, cudaStream_t st) {
+  static const bool empty = getenv("SP_DEBUG_ATTN_EMPTY") != nullptr;
+  if (empty) {
+    launch_pdl(empty_pdl_kernel, dim3(136), dim3(128), 0, st, 0);
+    count_launch();
+    return a.H;
+  }
+  if (g_attn_cl && attn_dec_cl_ok(a)) return launch_attn_decode_cl(a, st);
   const int G = a.H / a.kvh;
   if (a.kv_dtype == kKVBF16 && G <= 8 && (a.hd == 64 || a.hd == 128)) {
     // group size as a template constant for the shapes we serve (70B: 8,
@@ -934,10 +953,11 @@ void launch_attn_decode_fused(const AttnDecArgs& a, cudaStream_t st) {
     };
     if (a.hd == 128) go(std::integral_constant<int, 128>{});
     else go(std::integral_constant<int, 64>{});
-    return;
+    return a.H;
   }
   if (a.kv_dtype == kKVBF16) dispatch<__nv_bfloat16>(a, st);
   else dispatch<float>(a, st);
+  return a.H;
 }
 
 }  // namespace sp

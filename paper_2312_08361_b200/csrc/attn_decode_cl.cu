@@ -1,0 +1,457 @@
+// Decode attention (n_new == 1) with a thread-block-cluster merge — the
+// default decode attention for a bf16 KV cache (head dim 64 / 128, up to 8
+// query heads per kv head).
+//
+// SP/model.py:263-275 at n = 1: scores = q . k / sqrt(hd) (+ ALiBi), no mask,
+// max-subtracted softmax, ctx = p . v; the new position's k (RoPE'd) and v are
+// appended to the paged cache first (KVCache.append, SP/model.py:163-167).
+//
+// Work split.  One cluster of CL = 8 CTAs per (slot, kv head); CTA rank c holds
+// NW warps, warp w the 32 positions [(s*CL + c)*NW*32 + w*32, +32) of pass s
+// (one pass up to CL*NW*32 positions: 3072 with NW = 12).  Every warp's K/V
+// rows are staged with cp.async BEFORE the programmatic-launch wait (positions
+// < t0 are never rewritten), so after the QKV projection lands only the math
+// remains:
+//   * S^T[16 x 32] = q[16 x hd] . K^T on mma.m16n8k16 (rows 0..G-1 = the kv
+//     group's query heads, q split hi + lo bf16 — two MMAs — against the bf16
+//     cache), online softmax per head in the exp2 domain,
+//   * O[16 x hd] += P[16 x 32] . V (P split hi + lo; the S^T accumulator layout
+//     IS the A-fragment layout of P, no shuffles),
+//   * the NW warp partials merge in a fixed order in shared memory, then the
+//     CL CTA partials merge over distributed shared memory: rank r finalises
+//     outputs [r*G*hd/CL, (r+1)*G*hd/CL) reading its 7 peers in rank order.
+// No global partials, counters or last-CTA merge (the round-1 kernel's serial
+// merge was most of its in-stream cost).  Deterministic: fixed merge orders.
+// Each rank also writes the (sum, sumsq, max|x|) partial of its ctx slice:
+// P_out = kvh * CL partials per row for the O-projection GEMV's prologue.
+#include <cooperative_groups.h>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "common.cuh"
+#include "decode.cuh"
+#include "kernels.cuh"
+
+namespace sp {
+
+namespace cg = cooperative_groups;
+
+namespace {
+
+constexpr int CL = 8;            // CTAs per (slot, kv head)
+constexpr int GM = 8;            // query heads per kv head (rows of the M = 16 tile)
+constexpr int NWMAX = 12;        // warps per CTA
+constexpr float kLog2e = 1.4426950408889634f;
+
+// m16n8k16 with rows 8..15 of A zero (padding): the accumulator pair of those
+// rows goes to a shared scratch pair `z`, so only rows 0..7 hold registers
+__device__ __forceinline__ void mma_top(float* c, float* z, uint32_t a0, uint32_t a2,
+                                        uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(z[0]), "+f"(z[1])
+      : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void ldsm4(uint32_t* r, const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"((uint32_t)__cvta_generic_to_shared(p)));
+}
+__device__ __forceinline__ void ldsm4t(uint32_t* r, const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"((uint32_t)__cvta_generic_to_shared(p)));
+}
+__device__ __forceinline__ void cp16z(void* dst, const void* src, bool ok) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(ok ? 16 : 0));
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+__device__ __forceinline__ void split2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
+  const __nv_bfloat16 h0 = __float2bfloat16_rn(x0), h1 = __float2bfloat16_rn(x1);
+  hi = pack_bf16(__bfloat162float(h0), __bfloat162float(h1));
+  lo = pack_bf16(x0 - __bfloat162float(h0), x1 - __bfloat162float(h1));
+}
+__device__ __forceinline__ float rope_at(const float* x, int dd, int half, const float* cs,
+                                         const float* sn) {
+  const int j = dd % half;
+  const float c = cs[j], s = sn[j];
+  return dd < half ? __fsub_rn(__fmul_rn(x[j], c), __fmul_rn(x[j + half], s))
+                   : __fadd_rn(__fmul_rn(x[j + half], c), __fmul_rn(x[j], s));
+}
+
+// debug (SP_BUILD_TRACE=1 build + SP_ATTN_TRACE=<call>): per-CTA phase times
+__device__ __forceinline__ void cl_mark(const AttnDecArgs& a, int ph) {
+  if (SP_DEV_TRACE && a.trace && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    a.trace[(blockIdx.y * gridDim.x + blockIdx.x) * 12 + ph] = t;
+  }
+}
+
+template <int HD>
+struct Layout {
+  static constexpr int RS = HD + 8;                      // padded bf16 row (ldmatrix banks)
+  static constexpr int KV_WARP = 32 * RS * 2;            // bytes of one warp's K (or V) rows
+  static constexpr int Q_BYTES = 2 * GM * RS * 2;        // q hi, lo
+  static constexpr int OC_BYTES = GM * HD * 4;           // CTA partial O
+  static size_t bytes(int nw) {
+    return (size_t)2 * nw * KV_WARP + Q_BYTES + OC_BYTES + 2 * NWMAX * GM * 4 + 4 * GM * 4 + 256;
+  }
+};
+
+template <int HD>
+__global__ void __launch_bounds__(NWMAX * 32, 1) attn_dec_cl_kernel(AttnDecArgs a) {
+  using L = Layout<HD>;
+  constexpr int RS = L::RS;
+  extern __shared__ __align__(128) uint8_t dsm[];
+  const int NW = blockDim.x >> 5;
+  typedef __nv_bfloat16 Row[RS];
+  Row* Ks = reinterpret_cast<Row*>(dsm);                            // [NW*32]
+  Row* Vs = reinterpret_cast<Row*>(dsm + (size_t)NW * L::KV_WARP);  // [NW*32]
+  Row* Qh = reinterpret_cast<Row*>(dsm + (size_t)2 * NW * L::KV_WARP);   // [GM]
+  Row* Ql = Qh + GM;
+  float* Oc = reinterpret_cast<float*>(dsm + (size_t)2 * NW * L::KV_WARP + L::Q_BYTES);  // [GM][HD]
+  float* mw = Oc + GM * HD;                       // [NWMAX][GM] warp maxima, then factors
+  float* lw = mw + NWMAX * GM;                    // [NWMAX][GM] warp sums
+  float* Mc = lw + NWMAX * GM;                    // [GM] CTA max
+  float* Lc = Mc + GM;                            // [GM] CTA sum
+
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = (int)cluster.block_rank();
+  const int slot = blockIdx.x / a.kvh, kh = blockIdx.x % a.kvh;
+  const int G = a.H / a.kvh;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g8 = lane >> 2, t4 = lane & 3;
+  const int T = a.t0 + 1;
+  const int PC = NW * 32;                          // positions per CTA per pass
+  const int npass = (T + CL * PC - 1) / (CL * PC);
+  const int half = HD / 2;
+  const float* qrow = a.qkv + (int64_t)slot * a.ldqkv;
+  Row* Kw = Ks + warp * 32;
+  Row* Vw = Vs + warp * 32;
+
+  // this warp's 32 K/V rows of pass s (zero-filled past T; the row of t0 is
+  // stale until the append below patches it)
+  auto stage = [&](int s) {
+    const int p0 = (s * CL + rank) * PC + warp * 32;
+    const int nv = max(0, min(32, T - p0));
+    if (nv == 0) return;
+    const int page = a.page_table[slot * a.max_pages + p0 / kPageTokens];
+    const __nv_bfloat16* kb = reinterpret_cast<const __nv_bfloat16*>(a.kv_pool) +
+                              (((int64_t)page * 2 + 0) * a.kvh + kh) * kPageTokens * HD +
+                              (p0 % kPageTokens) * HD;
+    const __nv_bfloat16* vb = kb + (int64_t)a.kvh * kPageTokens * HD;
+    constexpr int CPR = HD / 8;                   // 16-byte chunks per row
+#pragma unroll 4
+    for (int c = lane; c < 32 * CPR; c += 32) {
+      const int r = c / CPR, e = (c % CPR) * 8;
+      const bool ok = r < nv;
+      cp16z(&Kw[r][e], kb + (ok ? r : 0) * HD + e, ok);
+      cp16z(&Vw[r][e], vb + (ok ? r : 0) * HD + e, ok);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  cl_mark(a, 0);
+  stage(0);
+  cl_mark(a, 1);
+  pdl_trigger();
+  pdl_wait();
+  cl_mark(a, 2);
+
+  // ---- q of the kv group (RoPE at t0), hi/lo bf16, rows >= G zero ----
+  const float* cs = a.rope_cos ? a.rope_cos + (int64_t)a.t0 * half : nullptr;
+  const float* sn = a.rope_sin ? a.rope_sin + (int64_t)a.t0 * half : nullptr;
+  for (int i = threadIdx.x; i < GM * HD; i += blockDim.x) {
+    const int g = i / HD, dd = i % HD;
+    float v = 0.f;
+    if (g < G) {
+      const float* q = qrow + (kh * G + g) * HD;
+      v = (a.family == kLlama) ? rope_at(q, dd, half, cs, sn) : q[dd];
+    }
+    const __nv_bfloat16 h = __float2bfloat16_rn(v);
+    Qh[g][dd] = h;
+    Ql[g][dd] = __float2bfloat16_rn(v - __bfloat162float(h));
+  }
+  // the new position: k (RoPE'd) and v appended to the page by the warp that
+  // owns t0 (patched into its staged rows after the wait below)
+  const int app_pass = a.t0 / (CL * PC);
+  const int app_off = a.t0 - app_pass * CL * PC - rank * PC - warp * 32;
+  const bool appender = app_off >= 0 && app_off < 32;
+  __nv_bfloat16 knew[HD / 32], vnew[HD / 32];
+  if (appender) {
+    const int page = a.page_table[slot * a.max_pages + a.t0 / kPageTokens];
+    __nv_bfloat16* kp = reinterpret_cast<__nv_bfloat16*>(a.kv_pool) +
+                        (((int64_t)page * 2 + 0) * a.kvh + kh) * kPageTokens * HD +
+                        (a.t0 % kPageTokens) * HD;
+    __nv_bfloat16* vp = kp + (int64_t)a.kvh * kPageTokens * HD;
+    const float* kn = qrow + a.H * HD + kh * HD;
+    const float* vn = qrow + a.H * HD + a.kvh * HD + kh * HD;
+#pragma unroll
+    for (int u = 0; u < HD / 32; ++u) {
+      const int dd = lane + 32 * u;
+      knew[u] = __float2bfloat16_rn((a.family == kLlama) ? rope_at(kn, dd, half, cs, sn) : kn[dd]);
+      vnew[u] = __float2bfloat16_rn(vn[dd]);
+      kp[dd] = knew[u];
+      vp[dd] = vnew[u];
+    }
+  }
+  __syncthreads();                                 // q visible
+  cl_mark(a, 3);
+
+  const float qscale = kLog2e / sqrtf((float)HD);
+  const float slope_l2 = (a.family == kBloom && g8 < G) ? a.alibi[kh * G + g8] * kLog2e : 0.f;
+
+  float m_run = -INFINITY, l_run = 0.f;            // per head g8 (replicated over t4)
+  float o[HD / 8][2];                              // rows g8 (head), dims i*8 + 2*t4 + j
+  float z[2] = {0.f, 0.f};                         // padding rows' accumulator (discarded)
+#pragma unroll
+  for (int i = 0; i < HD / 8; ++i) o[i][0] = o[i][1] = 0.f;
+
+  for (int s = 0; s < npass; ++s) {
+    const int p0 = (s * CL + rank) * PC + warp * 32;
+    const int nv = max(0, min(32, T - p0));
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncwarp();
+    if (s == 0) cl_mark(a, 4);
+    if (nv > 0) {
+      if (appender && s == app_pass) {
+#pragma unroll
+        for (int u = 0; u < HD / 32; ++u) {
+          Kw[app_off][lane + 32 * u] = knew[u];
+          Vw[app_off][lane + 32 * u] = vnew[u];
+        }
+        __syncwarp();
+      }
+      // ---- S^T[heads x 32 positions] = q . K^T ----
+      float sc[4][2];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) sc[nt][0] = sc[nt][1] = 0.f;
+#pragma unroll
+      for (int ks = 0; ks < HD / 16; ++ks) {
+        // q A fragments of row g8 (rows g8 + 8 are padding)
+        const uint32_t h0 = *reinterpret_cast<const uint32_t*>(&Qh[g8][ks * 16 + 2 * t4]);
+        const uint32_t h2 = *reinterpret_cast<const uint32_t*>(&Qh[g8][ks * 16 + 8 + 2 * t4]);
+        const uint32_t l0 = *reinterpret_cast<const uint32_t*>(&Ql[g8][ks * 16 + 2 * t4]);
+        const uint32_t l2 = *reinterpret_cast<const uint32_t*>(&Ql[g8][ks * 16 + 8 + 2 * t4]);
+#pragma unroll
+        for (int np = 0; np < 2; ++np) {
+          uint32_t kb[4];
+          const int m = lane >> 3;
+          ldsm4(kb, &Kw[np * 16 + (m >> 1) * 8 + (lane & 7)][ks * 16 + (m & 1) * 8]);
+          mma_top(sc[2 * np], z, h0, h2, kb[0], kb[1]);
+          mma_top(sc[2 * np], z, l0, l2, kb[0], kb[1]);
+          mma_top(sc[2 * np + 1], z, h0, h2, kb[2], kb[3]);
+          mma_top(sc[2 * np + 1], z, l0, l2, kb[2], kb[3]);
+        }
+      }
+      // ---- online softmax per head (row g8): positions p0 + nt*8 + 2*t4 + j ----
+      float tmax = -INFINITY;
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int pos = p0 + nt * 8 + 2 * t4 + j;
+          float v = sc[nt][j] * qscale;
+          if (a.family == kBloom) v = fmaf(slope_l2, (float)(pos - a.t0), v);
+          if (pos >= T) v = -INFINITY;
+          sc[nt][j] = v;
+          tmax = fmaxf(tmax, v);
+        }
+      tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 1));
+      tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 2));
+      const float mnew = fmaxf(m_run, tmax);
+      const float alpha = (m_run == -INFINITY) ? 0.f : ex2_approx(m_run - mnew);
+      float psum = 0.f;
+      uint32_t ph[2][2], pl[2][2];                 // [k-step][a0 | a2] of row g8
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        const float p0v = sc[nt][0] == -INFINITY ? 0.f : ex2_approx(sc[nt][0] - mnew);
+        const float p1v = sc[nt][1] == -INFINITY ? 0.f : ex2_approx(sc[nt][1] - mnew);
+        psum += p0v + p1v;
+        // C layout of two n-tiles == A layout of one k16 step (a0: n-tile 2kk, a2: 2kk + 1)
+        split2(p0v, p1v, ph[nt >> 1][nt & 1], pl[nt >> 1][nt & 1]);
+      }
+      psum += __shfl_xor_sync(0xffffffffu, psum, 1);
+      psum += __shfl_xor_sync(0xffffffffu, psum, 2);
+      l_run = l_run * alpha + psum;
+      m_run = mnew;
+#pragma unroll
+      for (int i = 0; i < HD / 8; ++i) { o[i][0] *= alpha; o[i][1] *= alpha; }
+      // ---- O[heads x HD] += P . V ----
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) {
+#pragma unroll
+        for (int dp = 0; dp < HD / 16; ++dp) {
+          uint32_t vb[4];
+          const int m = lane >> 3;
+          ldsm4t(vb, &Vw[kk * 16 + (m & 1) * 8 + (lane & 7)][dp * 16 + (m >> 1) * 8]);
+          mma_top(o[2 * dp], z, ph[kk][0], ph[kk][1], vb[0], vb[1]);
+          mma_top(o[2 * dp], z, pl[kk][0], pl[kk][1], vb[0], vb[1]);
+          mma_top(o[2 * dp + 1], z, ph[kk][0], ph[kk][1], vb[2], vb[3]);
+          mma_top(o[2 * dp + 1], z, pl[kk][0], pl[kk][1], vb[2], vb[3]);
+        }
+      }
+    }
+    if (s + 1 < npass) {
+      __syncwarp();
+      stage(s + 1);                                // this warp's slots are free again
+    }
+  }
+
+  cl_mark(a, 5);
+  // ---- warp partials -> shared (O over this warp's own K rows) ----
+  float* Ow = reinterpret_cast<float*>(Kw);        // [GM][HD] f32 fits 32 K rows
+  __syncwarp();
+  if (g8 < G) {
+#pragma unroll
+    for (int i = 0; i < HD / 8; ++i)
+      *reinterpret_cast<float2*>(Ow + g8 * HD + i * 8 + 2 * t4) = make_float2(o[i][0], o[i][1]);
+    if (t4 == 0) { mw[warp * GM + g8] = m_run; lw[warp * GM + g8] = l_run; }
+  }
+  __syncthreads();
+  // ---- CTA merge over warps (fixed order): factors f_w = exp2(m_w - M) ----
+  if (threadIdx.x < G) {
+    const int g = threadIdx.x;
+    float M = -INFINITY;
+    for (int w = 0; w < NW; ++w) M = fmaxf(M, mw[w * GM + g]);
+    float Ls = 0.f;
+    for (int w = 0; w < NW; ++w) {
+      const float m = mw[w * GM + g];
+      const float f = (m == -INFINITY) ? 0.f : ex2_approx(m - M);
+      mw[w * GM + g] = f;
+      Ls = fmaf(lw[w * GM + g], f, Ls);
+    }
+    Mc[g] = M;
+    Lc[g] = Ls;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < G * HD; i += blockDim.x) {
+    const int g = i / HD;
+    float acc = 0.f;
+    for (int w = 0; w < NW; ++w) {
+      const float f = mw[w * GM + g];
+      if (f != 0.f) acc = fmaf(reinterpret_cast<const float*>(Ks + w * 32)[i], f, acc);
+    }
+    Oc[i] = acc;
+  }
+  cl_mark(a, 6);
+  cluster.sync();                                   // every CTA partial visible cluster-wide
+  cl_mark(a, 7);
+
+  // ---- rank merge over the cluster (fixed rank order) ----
+  // every distributed-shared-memory load of a thread is issued before its
+  // first use (the 8 peers' (max, sum) and O values in flight together: one
+  // DSMEM round trip, not a chain of 16)
+  const int GH = G * HD;
+  const int i0 = rank * GH / CL, i1 = (rank + 1) * GH / CL;
+  float S = 0.f, Q = 0.f, Mx = 0.f;
+  float* ctx = a.ctx + (int64_t)slot * a.H * HD + (int64_t)kh * G * HD;
+  for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+    const int g = i / HD;
+    float pm[CL], pl[CL], po[CL];
+#pragma unroll
+    for (int c = 0; c < CL; ++c) {
+      pm[c] = *cluster.map_shared_rank(&Mc[g], c);
+      pl[c] = *cluster.map_shared_rank(&Lc[g], c);
+      po[c] = *cluster.map_shared_rank(&Oc[i], c);
+    }
+    float M = -INFINITY;
+#pragma unroll
+    for (int c = 0; c < CL; ++c) M = fmaxf(M, pm[c]);
+    float Ls = 0.f, acc = 0.f;
+#pragma unroll
+    for (int c = 0; c < CL; ++c) {
+      const float f = (pm[c] == -INFINITY) ? 0.f : ex2_approx(pm[c] - M);
+      Ls = fmaf(pl[c], f, Ls);
+      acc = fmaf(po[c], f, acc);
+    }
+    const float v = acc / Ls;
+    ctx[i] = v;
+    S += v;
+    Q = fmaf(v, v, Q);
+    Mx = fmaxf(Mx, fabsf(v));
+  }
+  cl_mark(a, 8);
+  if (a.st_out) {
+    // fixed-order block reduction of this rank's slice statistics
+    S = warp_sum(S); Q = warp_sum(Q); Mx = warp_max(Mx);
+    __shared__ float red[NWMAX][3];
+    if (lane == 0) { red[warp][0] = S; red[warp][1] = Q; red[warp][2] = Mx; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      float s2 = 0.f, q2 = 0.f, m2 = 0.f;
+      for (int w = 0; w < NW; ++w) { s2 += red[w][0]; q2 += red[w][1]; m2 = fmaxf(m2, red[w][2]); }
+      a.st_out[(int64_t)(kh * CL + rank) * a.width + slot] = RowStat{s2, q2, m2, 0.f};
+    }
+  }
+  cl_mark(a, 9);
+  cluster.sync();                                   // peers' shared memory read by everyone
+  cl_mark(a, 10);
+}
+
+template <int HD>
+int launch_hd(const AttnDecArgs& a, cudaStream_t st) {
+  const int T = a.t0 + 1;
+  const int nw = max(1, min(NWMAX, (T + CL * 32 - 1) / (CL * 32)));
+  const size_t smem = Layout<HD>::bytes(nw);
+  static bool set[kMaxDevices] = {};
+  const int dv = current_device();
+  if (!set[dv]) {
+    cudaFuncSetAttribute(attn_dec_cl_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)Layout<HD>::bytes(NWMAX));
+    set[dv] = true;
+  }
+  static int trace_call = getenv("SP_ATTN_TRACE") ? atoi(getenv("SP_ATTN_TRACE")) : -1;
+  static int ncall = 0;
+  AttnDecArgs b = a;
+  const dim3 grid(a.width * a.kvh, CL);
+  const bool tr = SP_DEV_TRACE && trace_call >= 0 && ncall++ == trace_call;
+  const size_t tn = (size_t)grid.x * grid.y * 12;
+  unsigned long long* tbuf = nullptr;
+  if (tr) {
+    cudaMalloc(&tbuf, tn * 8);
+    cudaMemsetAsync(tbuf, 0, tn * 8, st);
+    b.trace = tbuf;
+  }
+  launch_pdl_cluster(attn_dec_cl_kernel<HD>, grid, dim3(nw * 32), smem, st, CL, b);
+  count_launch();
+  if (tr) {
+    std::vector<unsigned long long> h(tn);
+    cudaMemcpyAsync(h.data(), tbuf, tn * 8, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    unsigned long long t0 = ~0ull;
+    for (size_t i = 0; i < tn; i += 12) if (h[i] && h[i] < t0) t0 = h[i];
+    fprintf(stderr, "attn_dec_cl T=%d nw=%d phases: start staged waited q cp_done computed "
+            "cta_merged cl_sync merged stats end\n", T, nw);
+    for (size_t i = 0; i < tn; i += 12) {
+      fprintf(stderr, "cta %3zu:", i / 12);
+      for (int p = 0; p < 11; ++p)
+        fprintf(stderr, " %7.2f", h[i + p] ? (double)(h[i + p] - t0) / 1e3 : -1.0);
+      fprintf(stderr, "\n");
+    }
+    cudaFree(tbuf);
+  }
+  return a.kvh * CL;
+}
+
+}  // namespace
+
+// the cluster kernel serves bf16 KV caches with head dim 64 / 128 and up to 8
+// query heads per kv head while one wave of clusters covers the grid
+bool attn_dec_cl_ok(const AttnDecArgs& a) {
+  const int G = a.H / a.kvh;
+  return a.kv_dtype == kKVBF16 && (a.hd == 64 || a.hd == 128) && G <= GM &&
+         (int64_t)a.width * a.kvh * CL <= 4 * 148;
+}
+
+int launch_attn_decode_cl(const AttnDecArgs& a, cudaStream_t st) {
+  return a.hd == 128 ? launch_hd<128>(a, st) : launch_hd<64>(a, st);
+}
+
+}  // namespace sp

@@ -66,7 +66,12 @@ struct AttnDecArgs {
   int nsub;                      // 128-position sub-chunks streamed per CTA (MMA kernel; 0 = 1)
 };
 
-void launch_attn_decode_fused(const AttnDecArgs& a, cudaStream_t st);
+// returns P_out: the number of ctx partial statistics per row written to
+// st_out (the O-projection GEMV's P_in)
+int launch_attn_decode_fused(const AttnDecArgs& a, cudaStream_t st);
+bool attn_dec_cl_ok(const AttnDecArgs& a);              // attn_decode_cl.cu
+int launch_attn_decode_cl(const AttnDecArgs& a, cudaStream_t st);
+extern bool g_attn_cl;                                  // option 7 (default on)
 int64_t attn_dec_part_floats(int width, int H, int hd, int max_pages);
 
 }  // namespace sp

@@ -11,8 +11,8 @@
 //
 // Arithmetic (int8 weights, 70B/BLOOM): exact for the coded input.  The input
 // row is scaled by a power of two 2^(kQBits-e_r) and rounded to an integer
-// q written as ND balanced base-256 digits (23-bit / 3 digits for 1-2 rows,
-// 15-bit / 2 digits for more); the digits of each
+// q written as ND balanced base-256 digits (15-bit / 2 digits for every row
+// count: width-independent numerics); the digits of each
 // batch row are columns of mma.m16n8k32.s8.s8.s32 whose A fragment is the lane's
 // 16-byte weight load (fragment-tiled storage, no conversion).  Digit sums are
 // exact int32, combined in int64; partial sums of a group's k-range are int64
@@ -61,7 +61,7 @@ constexpr int RMAX = 8;           // batch rows per launch
 // (|x| < 2^e) and rounded to an integer |q| <= 2^kQBits written as NDIG
 // balanced int8 digits (MMA columns); 2 digits = 15-bit codes, the precision
 // class of the prefill digit planes, and 4 batch rows per 8-column MMA tile.
-constexpr int kNDig = 2;   // digits for 3+ batch rows (see launch_gemv3)
+constexpr int kNDig = 2;   // digits of the int8 path (see launch_gemv3)
 constexpr double kFix = 4294967296.0;   // bf16 partial fixed point 2^32
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -748,12 +748,13 @@ void launch_gemv3(int wdtype, const GemvArgs& a, cudaStream_t st) {
   }
   for (int r0 = 0; r0 < a.R; r0 += RMAX) {
     const int rn = a.R - r0 < RMAX ? a.R - r0 : RMAX;
-    // activation code width: 23 bits (3 digits) when the rows fit one MMA
-    // column tile anyway (1-2 rows), 15 bits (2 digits, the prefill planes'
-    // class) for 3-8 rows, where it halves the column tiles (measured: 3 digits
-    // +4 % at batch 1, 2 digits +55 % at batch 4).  SP_GEMV_NDIG overrides.
+    // activation code width: 15 bits (2 balanced int8 digits, the precision
+    // class of the prefill digit planes) for every row count, so a row's
+    // result never depends on how many rows share the launch (decode numerics
+    // independent of beam width / batch).  The 3-digit (23-bit) variant is
+    // kept for A/B only (SP_GEMV_NDIG=3): it measured no faster at batch 1.
     static int nd_env = getenv("SP_GEMV_NDIG") ? atoi(getenv("SP_GEMV_NDIG")) : 0;
-    const int nd = nd_env ? nd_env : (rn <= 2 ? 3 : kNDig);
+    const int nd = nd_env ? nd_env : kNDig;
     if (wdtype == kNF4) {
       // one row per launch (the 4 KB code unit + scales + a 64-float chunk
       // per stage; two CTAs per SM leave no room for more rows' chunks)

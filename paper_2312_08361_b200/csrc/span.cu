@@ -122,6 +122,7 @@ struct sp_span {
   // session goes (finalizer order in Python reference cycles is arbitrary)
   int live_kv = 0;
   bool dying = false;
+  int last_p_ctx = 0;             // ctx partial stats the last decode attention wrote
   // live per-launch timing (bench roofline): CUDA events around each launch
   struct ProfRec { int cls; cudaEvent_t a, b; double bytes, flops; };
   bool prof = false;
@@ -199,7 +200,10 @@ int ensure_decode(sp_span* s, int64_t rows) {
   int64_t cap = rows < 8 ? 8 : rows;
   cudaFree(s->st_norm1); cudaFree(s->st_ctx); cudaFree(s->st_norm2); cudaFree(s->st_mlp);
   cudaFree(s->ws2); cudaFree(s->cnt2); cudaFree(s->attn_part); cudaFree(s->attn_cnt);
-  const int64_t P = std::max<int64_t>(std::max<int64_t>(s->d / 64, s->H), s->n_up / 64);
+  // partial-statistics slots per row: the largest producer fan-out (GEMV groups,
+  // decode-attention heads, or kv heads x cluster ranks)
+  const int64_t P = std::max<int64_t>(std::max<int64_t>(s->d / 64, s->H),
+                                      std::max<int64_t>(s->n_up / 64, 8 * (int64_t)s->kvh));
   for (RowStat** b : {&s->st_norm1, &s->st_ctx, &s->st_norm2, &s->st_mlp})
     SP_CUDA_TRY(cudaMalloc(b, P * cap * sizeof(RowStat)));
   int64_t ws = 0, cnt = 0;
@@ -458,15 +462,19 @@ int run_span_decode_tc(sp_span* s, sp_kv* kv, int b0, int b1, float* y, int widt
     // timing experiment only (wrong results): SP_DEBUG_SKIP_ATTN=1 measures the
     // in-stream cost of decode attention
     static const bool skip_attn = getenv("SP_DEBUG_SKIP_ATTN") != nullptr;
+    int p_ctx = s->H;                       // ctx partial statistics per row (O GEMV P_in)
     if (!gemv_only && !skip_attn) {
       const double kvb = (double)width * (kv->length + 1) * 2 * s->kv * kv_elt;
       ProfScope ps(s, PC_ATTN_DEC, kvb + 4.0 * R * (s->n_qkv + d),
                    4.0 * width * (kv->length + 1) * s->H * s->hd, st);
-      launch_attn_decode_fused(at, st);
+      p_ctx = launch_attn_decode_fused(at, st);
+    } else if (gemv_only) {
+      p_ctx = s->last_p_ctx;
     }
+    s->last_p_ctx = p_ctx;
     // 3) x += ctx @ Wo      (stats for norm2)
     g.w = W.o; g.wscale = W.s_o; g.N = d; g.K = d; g.x = s->ctx; g.ldx = d;
-    g.norm = NORM_NONE; g.g = nullptr; g.st_in = s->st_ctx; g.P_in = s->H;
+    g.norm = NORM_NONE; g.g = nullptr; g.st_in = s->st_ctx; g.P_in = p_ctx;
     g.y = y; g.ldy = d; g.res = y; g.epi = EPI_RESID; g.st_out = s->st_norm2;
     g.g_next = s->gains_one ? nullptr : W.ln2_g;
     {
@@ -598,7 +606,11 @@ int run_span_prefill_tc(sp_span* s, sp_kv* kv, int b0, int b1, float* y, float* 
 // on the tcgen05 GEMM (one pass over the weights for all rows, 15-bit digit
 // planes) instead of the GEMV, whose per-unit digit/MMA work makes it
 // latency-bound beyond a few rows; attention stays the fused decode kernel.
-constexpr int kWideDecode = 8;
+// Up to 8 rows (one GEMV launch) every row's result is bit-identical whatever
+// the width (tests/test_gpu_span.py::test_decode_width_invariant); from 9 rows
+// the GEMM computes the same exact integer products of the same 15-bit codes
+// but folds the norm in its own reduction order (last-bit differences).
+constexpr int kWideDecode = 9;
 
 int run_span_decode_wide(sp_span* s, sp_kv* kv, int b0, int b1, float* y, int width,
                          cudaStream_t st) {
@@ -1130,6 +1142,7 @@ int sp_span_set_option(sp_span* s, int32_t option, int32_t value) {
   else if (option == 3) g_attn_hilo = value != 0;
   else if (option == 5) g_attn_nsub = value;
   else if (option == 6) g_attn_cluster = value;
+  else if (option == 7) g_attn_cl = value != 0;
   else SP_FAIL(SP_ERR_ARG, "unknown option");
   return SP_OK;
 }

@@ -54,8 +54,8 @@ def test_full_shape_block_vs_oracle(name):
 
 def test_full_shape_decode_rows_independent():
     """70B int8 block: a width-2 decode equals two width-1 decodes bit for bit
-    (exact integer GEMV partials, fixed-order merges; 1-2 rows share the 23-bit
-    activation code)."""
+    (exact integer GEMV partials, fixed-order merges; one 15-bit activation code
+    for every width)."""
     from paper_2312_08361_b200.engine import B200ServerEngine, DeviceSpan
     cfg = _cfg("llama2-70b-int8")
     eng = B200ServerEngine(cfg, span=DeviceSpan(cfg, 0, 1, kv_pool_tokens=4096))

@@ -333,9 +333,9 @@ def test_extended_families_greedy_tokens_match_oracle(name):
     assert worst <= 1e-2, worst
 
 
-@pytest.mark.parametrize("name,width", [("llama_int8", 8), ("bloom_int8", 16), ("llama_g8", 8)])
+@pytest.mark.parametrize("name,width", [("llama_int8", 9), ("bloom_int8", 16), ("llama_g8", 12)])
 def test_wide_decode_vs_oracle(name, width):
-    """Decode with >= 8 rows per step runs its linears on the tcgen05 GEMM
+    """Decode with >= 9 rows per step runs its linears on the tcgen05 GEMM
     (one pass over the weights for all rows) and attention on the fused decode
     kernel; every row vs the oracle at the decode tolerance."""
     cfg = SMALL[name]
@@ -355,6 +355,35 @@ def test_wide_decode_vs_oracle(name, width):
     assert eng.cache_length(c) == 44
 
 
+@pytest.mark.parametrize("name", ["llama_int8", "bloom_int8", "llama_g8", "llama_bf16"])
+def test_decode_width_invariant(name):
+    """Decode numerics do not depend on the width of the step (SURVEY.md 0.6;
+    T/test_server.py:247-255 pins the same for forward): slot r of a width-3 and
+    of a width-8 session equals a width-1 session on the same rows, bit for bit
+    (one 15-bit activation code for every row count, exact integer GEMV
+    partials, per-row attention)."""
+    cfg = SMALL[name]
+    eng = _engine(cfg)
+    rng = np.random.default_rng(31)
+    d = cfg.hidden_dim
+    x = rng.standard_normal((8, 70 + 3, d)).astype(np.float32)
+    single = []
+    for r in range(8):
+        c1 = eng.make_caches(0, cfg.n_blocks, 1)
+        eng.run_cached(0, cfg.n_blocks, c1, _blob(x[r, :70]), 1, 70, False)
+        single.append([eng.run_cached(0, cfg.n_blocks, c1, _blob(x[r, i:i + 1]), 1, 1,
+                                      False).array()[0] for i in range(70, 73)])
+    for width in (3, 8):
+        cw = eng.make_caches(0, cfg.n_blocks, width)
+        eng.run_cached(0, cfg.n_blocks, cw, _blob(x[:width, :70].reshape(-1, d)), width, 70,
+                       False)
+        for j, i in enumerate(range(70, 73)):
+            out = eng.run_cached(0, cfg.n_blocks, cw, _blob(x[:width, i]), width, 1,
+                                 False).array()
+            for r in range(width):
+                assert np.array_equal(out[r], single[r][j]), (width, r, i)
+
+
 @pytest.mark.parametrize("name", ["bloom_int8", "llama_int8"])
 def test_decode_attention_streamed_subchunks(name):
     """Decode attention streaming several 128-position sub-chunks per CTA with
@@ -366,6 +395,8 @@ def test_decode_attention_streamed_subchunks(name):
     d = cfg.hidden_dim
     x = rng.standard_normal((2, 300 + 5, d)).astype(np.float32)
     outs = []
+    eng = _engine(cfg)
+    _lib.check(eng.lib.sp_span_set_option(eng.span.handle, 7, 0))   # round-1 kernel
     for nsub in (1, 3):
         eng = _engine(cfg)
         _lib.check(eng.lib.sp_span_set_option(eng.span.handle, 5, nsub))
@@ -374,8 +405,11 @@ def test_decode_attention_streamed_subchunks(name):
         outs.append([eng.run_cached(0, cfg.n_blocks, c, _blob(x[:, i]), 2, 1, False).array()
                      for i in range(300, 305)])
         _lib.check(eng.lib.sp_span_set_option(eng.span.handle, 5, 0))
+    _lib.check(eng.lib.sp_span_set_option(eng.span.handle, 7, 1))
+    # f32-rounding differences in ctx, seen through the next GEMV's 15-bit
+    # activation code (resolution 2^-14 of the row maximum)
     for a, b in zip(*outs):
-        assert np.abs(a - b).max() <= 1e-5 * np.abs(b).max()
+        assert np.abs(a - b).max() <= 2e-4 * np.abs(b).max()
 
 
 def test_decode_attention_cluster_merge():
@@ -388,6 +422,8 @@ def test_decode_attention_cluster_merge():
     d = cfg.hidden_dim
     x = rng.standard_normal((2, 1100 + 4, d)).astype(np.float32)
     outs = {}
+    eng = _engine(cfg)
+    _lib.check(eng.lib.sp_span_set_option(eng.span.handle, 7, 0))   # round-1 kernel
     try:
         for cl in (-1, 8, 16):
             eng = _engine(cfg)
@@ -402,10 +438,48 @@ def test_decode_attention_cluster_merge():
                     for i in range(1100, 1104)]
             outs[cl] = got
     finally:
-        _lib.check(eng.lib.sp_span_set_option(eng.span.handle, 6, 0))
+        _lib.check(eng.lib.sp_span_set_option(eng.span.handle, 6, -1))
+        _lib.check(eng.lib.sp_span_set_option(eng.span.handle, 7, 1))
     for cl in (8, 16):
         for a, b in zip(outs[cl], outs[-1]):
-            assert np.abs(a - b).max() <= 1e-5 * np.abs(b).max()
+            assert np.abs(a - b).max() <= 2e-4 * np.abs(b).max()
+
+
+@pytest.mark.parametrize("name,t_pre", [("llama_g8", 70), ("llama_g8", 2040),
+                                        ("llama_int8", 300), ("bloom_int8", 130),
+                                        ("llama_bf16", 65), ("llama_g8_long", 3300)])
+def test_decode_attention_cluster_kernel(name, t_pre):
+    """The default decode attention (8-CTA cluster per kv head, every warp
+    32 positions in parallel, DSMEM merge: attn_decode_cl.cu) against the
+    round-1 kernel (global last-CTA merge, option 7 = 0) and the oracle: the
+    new token's K/V append, page boundaries, GQA 8/2/1, ALiBi, bf16 weights, and
+    more positions than one pass of the cluster holds (> 3072: two passes)."""
+    from paper_2312_08361_b200 import _lib
+    cfg = SMALL[name] if name in SMALL else SMALL["llama_g8"].with_(max_seq_len=4096)
+    rng = np.random.default_rng(23)
+    d = cfg.hidden_dim
+    x = rng.standard_normal((t_pre + 3, d)).astype(np.float32)
+    outs = {}
+    eng = _engine(cfg)
+    try:
+        for v2 in (1, 0):
+            _lib.check(eng.lib.sp_span_set_option(eng.span.handle, 7, v2))
+            c = eng.make_caches(0, cfg.n_blocks, 1)
+            eng.run_cached(0, cfg.n_blocks, c, _blob(x[:t_pre]), 1, t_pre, False)
+            outs[v2] = [eng.run_cached(0, cfg.n_blocks, c, _blob(x[i:i + 1]), 1, 1,
+                                       False).array() for i in range(t_pre, t_pre + 3)]
+    finally:
+        _lib.check(eng.lib.sp_span_set_option(eng.span.handle, 7, 1))
+    runner = om.SpanRunner(cfg, 0, cfg.n_blocks)
+    runner.step(x[None, :t_pre])
+    for j, i in enumerate(range(t_pre, t_pre + 3)):
+        w = runner.step(x[None, i:i + 1])[0]
+        s = np.abs(w).max()
+        e_new, e_old = np.abs(outs[1][j] - w).max() / s, np.abs(outs[0][j] - w).max() / s
+        print(f"{name} T={i + 1}: cluster kernel err {e_new:.2e}, round-1 kernel err {e_old:.2e} "
+              f"(max-abs / max|y|)")
+        assert e_new <= 2e-3
+        assert np.abs(outs[1][j] - outs[0][j]).max() <= 2e-3 * s
 
 
 def test_bf16_tc_prefill_matches_simt():
