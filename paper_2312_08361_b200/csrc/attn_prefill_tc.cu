@@ -1,0 +1,482 @@
+// Prefill / replay causal attention (n_new > 1) on the 5th-gen tensor cores:
+// tcgen05.mma with the score and output tiles in TMEM (bf16 KV cache, head
+// dim 128).
+//
+// SP/model.py:263-275: scores = q . k / sqrt(hd) (+ ALiBi), causal mask for
+// n > 1 (the reference fills -1e30; here -inf, identical after the
+// max-subtracted exp), softmax over cache + new positions, ctx = p . v.
+//
+// CTA = (slot, query head, 128 query rows); keys stream one 64-position page
+// per tile.  Warp roles (10 warps):
+//   * warps 0-7  softmax / epilogue: TMEM lane = query row; the two warps of a
+//                lane quarter split every tile's columns (32 scores, 64 output
+//                dims each) and combine the row maxima through shared memory.
+//                Per tile: tcgen05.ld the scores, scale, mask, online max and
+//                sum (exp2 domain), write P (bf16) to shared memory.  The
+//                output accumulates in TMEM across tiles; it is rescaled
+//                (tcgen05.ld / st) only when a row's maximum grows by more than
+//                2^8 over the one its P values are normalised to, so p <= 256
+//                and most tiles touch no output column.  At the end ctx = O / l.
+//   * warp 8     producer: one lane issues each tile's K and V pages as 2-D
+//                tensor-map TMA loads (cp.async.bulk.tensor, 128-byte swizzle,
+//                [64 keys][64 dims] boxes) from the paged pool: K lands in the
+//                K-major SW128 layout (B operand of S = Q K^T), V in the MN-major
+//                SW128 layout (B operand of O = P V).  3 stages.
+//   * warp 9     TMEM allocator + one elected lane issuing the MMAs:
+//                S_j = (Qhi + Qlo) K_j^T  (M = 128, N = 64, K = 128, f32 in TMEM)
+//                O  += P_j V_j            (M = 128, N = 128, K = 64, in TMEM)
+//                S_{j+1} is issued before O_j, so the tensor pipe works on the
+//                next scores while the softmax warps turn S_j into P_j.
+// TMEM: 2 x 64 score columns (double buffered) + 128 output columns.
+// Q is split hi + lo bf16 (two MMAs) against the bf16 K cache, so the scores
+// carry the cache's rounding, not a bf16 rounding of q; P (in [0, 256]) is
+// bf16 with f32 accumulation.
+// Each query row depends only on its own row: batch / tile invariant.
+#include <cuda.h>   // CUtensorMap (the encoder is fetched from the driver at run time)
+
+#include <cstdio>
+#include <cstdlib>
+#include <mutex>
+#include <unordered_map>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace sp {
+
+bool g_attn_tc = getenv("SP_ATTN_TC") ? atoi(getenv("SP_ATTN_TC")) != 0 : true;  // option 8
+
+namespace {
+
+constexpr int HD = 128;
+constexpr int BQ = 128;                 // query rows per CTA
+constexpr int BK = 64;                  // keys per tile (one page)
+constexpr int NSM = 8;                  // softmax warps: 2 per TMEM lane quarter
+constexpr int NTHREADS = (NSM + 2) * 32;
+constexpr int WP = NSM, WM = NSM + 1;   // producer warp, MMA warp
+constexpr int Q_BYTES = BQ * HD * 2;    // 32 KB per plane (hi, lo)
+constexpr int K_BYTES = BK * HD * 2;    // 16 KB
+constexpr int V_BYTES = BK * HD * 2;    // 16 KB
+constexpr int P_BYTES = BQ * BK * 2;    // 16 KB per plane
+constexpr int STAGE_BYTES = K_BYTES + V_BYTES;
+constexpr int NST = 3;                  // K/V stages
+constexpr int BOX = BK * 64 * 2;        // one [64 keys][64 dims] TMA box (8 KB)
+constexpr int SMEM_BYTES = 2 * Q_BYTES + NST * STAGE_BYTES + 2 * P_BYTES + 1024;
+constexpr int S_COL = 0;                // TMEM columns: S buffers 0..127
+constexpr int O_COL = 128;              //               O 128..255
+constexpr float kRescale = 8.0f;        // log2 growth of a row max that forces an O rescale
+constexpr float kLog2e = 1.4426950408889634f;
+
+// instruction descriptors (kind::f16: bf16 A/B, f32 D)
+constexpr uint32_t kIdescS = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BK >> 3) << 17) |
+                             ((uint32_t)(BQ >> 4) << 24);                       // N = 64, K-major B
+constexpr uint32_t kIdescO = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) |
+                             ((uint32_t)(HD >> 3) << 17) | ((uint32_t)(BQ >> 4) << 24);  // MN-major B
+
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, int n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(su32(b)),
+      "r"(parity)
+      : "memory");
+}
+// UMMA shared-memory descriptor (cute::UMMA::SmemDescriptor, version 1):
+// layout 0 = SWIZZLE_NONE, 2 = SWIZZLE_128B (atoms 1024-byte aligned)
+__device__ __forceinline__ uint64_t sdesc(const void* p, uint32_t lbo, uint32_t sbo,
+                                          uint32_t layout = 0) {
+  uint64_t d = (uint64_t)((su32(p) >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)layout << 61;
+  return d;
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                       uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(su32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                     uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* b) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   su32(b))
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float* v) {
+  const uint32_t* r = reinterpret_cast<const uint32_t*>(v);
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]),
+      "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]),
+      "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]),
+      "r"(r[30]), "r"(r[31])
+      : "memory");
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t bf2(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+// 8 f32 -> 16 bytes of bf16 hi and 16 bytes of bf16 lo (x - hi)
+__device__ __forceinline__ void split8(const float* x, uint4& hi, uint4& lo) {
+  float h[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) h[i] = __bfloat162float(__float2bfloat16_rn(x[i]));
+  hi = make_uint4(bf2(h[0], h[1]), bf2(h[2], h[3]), bf2(h[4], h[5]), bf2(h[6], h[7]));
+  lo = make_uint4(bf2(x[0] - h[0], x[1] - h[1]), bf2(x[2] - h[2], x[3] - h[3]),
+                  bf2(x[4] - h[4], x[5] - h[5]), bf2(x[6] - h[6], x[7] - h[7]));
+}
+// K-major A/B core-matrix layout of a [rows][k] bf16 operand, 16-element k
+// steps: step u = [2 halves][rows/8][8 rows][16 B]; LBO = rows * 16, SBO = 128
+__device__ __forceinline__ int kmajor_off(int row, int chunk, int rows) {
+  return (chunk >> 1) * rows * 32 + (chunk & 1) * rows * 16 + (row >> 3) * 128 + (row & 7) * 16;
+}
+
+__global__ void __launch_bounds__(NTHREADS, 1)
+attn_prefill_tc_kernel(AttnArgs a, const __grid_constant__ CUtensorMap kvmap, int64_t row0) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-byte alignment for the 128-byte-swizzled TMA boxes / UMMA atoms
+  uint8_t* smem = smem_raw + ((1024 - (su32(smem_raw) & 1023)) & 1023);
+  uint8_t* Qhi = smem;
+  uint8_t* Qlo = smem + Q_BYTES;
+  uint8_t* stages = smem + 2 * Q_BYTES;                        // [NST][K box0 box1 | V box0 box1]
+  uint8_t* Pbuf = stages + NST * STAGE_BYTES;                  // [2] bf16 P
+  __shared__ __align__(8) uint64_t kv_full[NST], kv_empty[NST], s_full[2], s_free[2],
+      p_full[2], p_free[2], o_full, q_full;
+  __shared__ uint32_t tmem_base;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = a.H / a.kvh;
+  const int slot = blockIdx.x / a.H, h = blockIdx.x % a.H, kh = h / G;
+  const int q0 = (gridDim.y - 1 - blockIdx.y) * BQ;          // heaviest tiles first
+  const int last_q = min(q0 + BQ, a.n_new) - 1;
+  const int ntiles = (a.t0 + last_q + 1 + BK - 1) / BK;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NST; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_free[i], NSM);
+      mbar_init(&p_full[i], NSM);
+      mbar_init(&p_free[i], 1);
+    }
+    mbar_init(&o_full, 1);
+    mbar_init(&q_full, NSM);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == WM) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     su32(&tmem_base))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tb = tmem_base;
+
+  if (warp == WP) {
+    // ---------------- producer: K / V pages by tensor-map TMA ----------------
+    if (lane == 0) {
+      for (int j = 0; j < ntiles; ++j) {
+        const int st = j % NST;
+        if (j >= NST) mbar_wait(&kv_empty[st], ((j / NST) - 1) & 1);
+        const int page = a.page_table[slot * a.max_pages + j];
+        // rows of the pool viewed as [(page, K|V, kv head, key)][hd]
+        const int64_t rk = row0 + (((int64_t)page * 2 + 0) * a.kvh + kh) * kPageTokens;
+        const int64_t rv = rk + (int64_t)a.kvh * kPageTokens;
+        uint8_t* Ks = stages + st * STAGE_BYTES;
+        mbar_expect_tx(&kv_full[st], STAGE_BYTES);
+        tma_2d(Ks, &kvmap, 0, (int)rk, &kv_full[st]);
+        tma_2d(Ks + BOX, &kvmap, 64, (int)rk, &kv_full[st]);
+        tma_2d(Ks + 2 * BOX, &kvmap, 0, (int)rv, &kv_full[st]);
+        tma_2d(Ks + 3 * BOX, &kvmap, 64, (int)rv, &kv_full[st]);
+      }
+    }
+    __syncwarp();
+  } else if (warp == WM) {
+    // ---------------- MMA issuer ----------------
+    if (lane == 0) {
+      mbar_wait(&q_full, 0);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      auto issue_s = [&](int j) {
+        const int kst = j % NST, st = j & 1;
+        mbar_wait(&kv_full[kst], (j / NST) & 1);
+        if (j >= 2) mbar_wait(&s_free[st], ((j >> 1) - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint8_t* Ks = stages + kst * STAGE_BYTES;
+        const uint32_t d = tb + S_COL + st * BK;
+#pragma unroll
+        for (int u = 0; u < HD / 16; ++u) {
+          // K-major SW128: 16 dims = 32 bytes along the 128-byte swizzle atom row;
+          // dims 64..127 are the second box; 8-row groups 1024 bytes apart
+          const uint64_t bd = sdesc(Ks + (u >> 2) * BOX + (u & 3) * 32, 16, 1024, 2);
+          umma(d, sdesc(Qhi + u * BQ * 32, BQ * 16, 128), bd, kIdescS, u > 0);
+          umma(d, sdesc(Qlo + u * BQ * 32, BQ * 16, 128), bd, kIdescS, 1);
+        }
+        umma_commit(&s_full[st]);
+      };
+      auto issue_o = [&](int j) {
+        const int kst = j % NST, st = j & 1;
+        mbar_wait(&p_full[st], (j >> 1) & 1);    // P_j written (and any O rescale done)
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint8_t* Vs = stages + kst * STAGE_BYTES + K_BYTES;
+        const uint8_t* P = Pbuf + st * P_BYTES;
+#pragma unroll
+        for (int u = 0; u < BK / 16; ++u)
+          // MN-major SW128: 64 dims per 128-byte atom row, the second 64 dims one
+          // box (LBO) further; 16 keys = 2 groups of 8 rows, 1024 bytes apart (SBO)
+          umma(tb + O_COL, sdesc(P + u * BQ * 32, BQ * 16, 128),
+               sdesc(Vs + u * 2048, BOX, 1024, 2), kIdescO, (j | u) ? 1u : 0u);
+        umma_commit(&o_full);                    // O now holds tiles 0..j
+        umma_commit(&p_free[st]);                // P buffer st read
+        umma_commit(&kv_empty[kst]);             // K_j and V_j consumed
+      };
+      issue_s(0);
+      for (int j = 0; j < ntiles; ++j) {
+        if (j + 1 < ntiles) issue_s(j + 1);
+        issue_o(j);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------- softmax / epilogue ----------------
+    // warp w: query rows (TMEM lanes) 32*(w%4) + lane, column half hf = w/4 of
+    // every tile (scores 32*hf.., output dims 64*hf..); the two warps of a row
+    // combine their tile maxima through shared memory (named barrier per pair)
+    __shared__ float red_max[2][BQ][2];
+    __shared__ float red_l[BQ];
+    const int quarter = warp & 3, hf = warp >> 2;
+    const int row = quarter * 32 + lane;
+    const int qi = min(q0 + row, a.n_new - 1);            // rows past n_new: computed, not stored
+    const int qpos = a.t0 + q0 + row;
+    const uint32_t lane_addr = (uint32_t)(quarter * 32) << 16;
+    auto pair_sync = [&]() {
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
+    };
+    // Q row (this warp's 64 dims) -> hi / lo planes (K-major A operand)
+    {
+      const float* qsrc = a.qkv + (int64_t)(slot * a.n_new + qi) * a.ldqkv + h * HD;
+#pragma unroll 4
+      for (int c8 = 0; c8 < HD / 16; ++c8) {
+        const int ch = hf * (HD / 16) + c8;
+        float x[8];
+        const float4 v0 = *reinterpret_cast<const float4*>(qsrc + ch * 8);
+        const float4 v1 = *reinterpret_cast<const float4*>(qsrc + ch * 8 + 4);
+        x[0] = v0.x; x[1] = v0.y; x[2] = v0.z; x[3] = v0.w;
+        x[4] = v1.x; x[5] = v1.y; x[6] = v1.z; x[7] = v1.w;
+        uint4 hi, lo;
+        split8(x, hi, lo);
+        const int off = kmajor_off(row, ch, BQ);
+        *reinterpret_cast<uint4*>(Qhi + off) = hi;
+        *reinterpret_cast<uint4*>(Qlo + off) = lo;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&q_full);
+    }
+    const float qscale = kLog2e / sqrtf((float)HD);
+    const float slope_l2 = (a.family == kBloom) ? a.alibi[h] * kLog2e : 0.f;
+    constexpr int SC = BK / 2;                   // score columns per warp
+    constexpr int OC = HD / 2;                   // output columns per warp
+    float m_used = -INFINITY, l_run = 0.f;       // P_j = exp2(s - m_used); l in the same units
+    for (int j = 0; j < ntiles; ++j) {
+      const int st = j & 1;
+      mbar_wait(&s_full[st], (j >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      float s[SC];
+      tmem_ld32(tb + lane_addr + S_COL + st * BK + hf * SC, s);
+      tmem_wait_ld();
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_free[st]);
+      // scale (log2 e / sqrt(hd)), ALiBi, causal mask, tile max
+      const int kbase = j * BK + hf * SC;
+      const bool unmasked = j * BK + BK - 1 <= a.t0 + q0;   // every row sees every key
+      float tmax = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < SC; ++i) {
+        const int key = kbase + i;
+        float x = s[i] * qscale;
+        if (a.family == kBloom) x = fmaf(slope_l2, (float)(key - qpos), x);
+        if (!unmasked && key > qpos) x = -INFINITY;
+        s[i] = x;
+        tmax = fmaxf(tmax, x);
+      }
+      red_max[st][row][hf] = tmax;
+      pair_sync();
+      tmax = fmaxf(red_max[st][row][0], red_max[st][row][1]);
+      // O rescale only when the row's max outgrows its reference by 2^8
+      // (warp-uniform: tcgen05.ld/st are warp-collective; factor 1 elsewhere)
+      float mnew = m_used;
+      if (j == 0) mnew = tmax;
+      else if (tmax > m_used + kRescale) mnew = tmax;
+      const bool grow = j > 0 && mnew != m_used;
+      if (__any_sync(0xffffffffu, grow)) {
+        const float f = grow ? ex2_approx(m_used - mnew) : 1.f;
+        mbar_wait(&o_full, (j - 1) & 1);         // O holds tiles 0..j-1
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+        for (int c = 0; c < OC / 32; ++c) {
+          float v[32];
+          tmem_ld32(tb + lane_addr + O_COL + hf * OC + c * 32, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] *= f;
+          tmem_st32(tb + lane_addr + O_COL + hf * OC + c * 32, v);
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        l_run *= f;
+      }
+      m_used = mnew;
+      // P_j = exp2(s - m_used) (<= 2^8), bf16, -> shared buffer st, once the
+      // MMA of tile j - 2 has read it
+      if (j >= 2) mbar_wait(&p_free[st], ((j >> 1) - 1) & 1);
+      uint8_t* P = Pbuf + st * P_BYTES;
+      float psum = 0.f;
+#pragma unroll
+      for (int c8 = 0; c8 < SC / 8; ++c8) {
+        float p[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float x = s[c8 * 8 + i];
+          p[i] = (x == -INFINITY) ? 0.f : ex2_approx(x - m_used);
+          psum += p[i];
+        }
+        *reinterpret_cast<uint4*>(P + kmajor_off(row, hf * (SC / 8) + c8, BQ)) =
+            make_uint4(bf2(p[0], p[1]), bf2(p[2], p[3]), bf2(p[4], p[5]), bf2(p[6], p[7]));
+      }
+      l_run += psum;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[st]);
+    }
+    // ---- ctx row = O / l  (l = the two halves' sums, same units) ----
+    if (hf == 1) red_l[row] = l_run;
+    pair_sync();
+    if (hf == 0) red_l[row] += l_run;
+    pair_sync();
+    const float inv = __frcp_rn(red_l[row]);
+    mbar_wait(&o_full, (ntiles - 1) & 1);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    float* dst = a.ctx + (int64_t)(slot * a.n_new + q0 + row) * a.H * HD + h * HD + hf * OC;
+#pragma unroll
+    for (int c = 0; c < OC / 32; ++c) {
+      float v[32];
+      tmem_ld32(tb + lane_addr + O_COL + hf * OC + c * 32, v);
+      tmem_wait_ld();
+      if (q0 + row < a.n_new) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 4)
+          *reinterpret_cast<float4*>(dst + c * 32 + i) =
+              make_float4(v[i] * inv, v[i + 1] * inv, v[i + 2] * inv, v[i + 3] * inv);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == WM)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tb) : "memory");
+}
+
+}  // namespace
+
+namespace {
+// one 2-D tensor map per KV pool: rows = (block, page, K|V, kv head, key), cols = hd
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+const CUtensorMap* pool_map(const void* base, int64_t bytes) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, std::pair<int64_t, CUtensorMap>> maps;
+  static EncodeTiledFn encode = nullptr;
+  std::lock_guard<std::mutex> g(mu);
+  auto it = maps.find(base);
+  if (it != maps.end() && it->second.first == bytes) return &it->second.second;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+            cudaSuccess || !fn)
+      return nullptr;
+    encode = reinterpret_cast<EncodeTiledFn>(fn);
+  }
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {(cuuint64_t)HD, (cuuint64_t)(bytes / (HD * 2))};
+  const cuuint64_t strides[1] = {(cuuint64_t)HD * 2};
+  const cuuint32_t box[2] = {64, (cuuint32_t)BK};
+  const cuuint32_t estr[2] = {1, 1};
+  if (encode(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+      CUDA_SUCCESS)
+    return nullptr;
+  auto& e = maps[base];
+  e = {bytes, m};
+  return &e.second;
+}
+}  // namespace
+
+bool launch_attention_prefill_tc(const AttnArgs& a, cudaStream_t st) {
+  if (!g_attn_tc || a.kv_dtype != kKVBF16 || a.hd != HD || !a.pool_base) return false;
+  const CUtensorMap* map = pool_map(a.pool_base, a.pool_bytes);
+  if (!map) return false;
+  static bool set[kMaxDevices] = {};
+  const int dv = current_device();
+  if (!set[dv]) {
+    cudaFuncSetAttribute(attn_prefill_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         SMEM_BYTES);
+    set[dv] = true;
+  }
+  const int64_t row0 = ((const char*)a.kv_pool - (const char*)a.pool_base) / (HD * 2);
+  dim3 grid(a.width * a.H, (a.n_new + BQ - 1) / BQ);
+  attn_prefill_tc_kernel<<<grid, NTHREADS, SMEM_BYTES, st>>>(a, *map, row0);
+  count_launch();
+  return true;
+}
+
+}  // namespace sp

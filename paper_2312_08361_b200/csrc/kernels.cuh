@@ -82,6 +82,8 @@ struct AttnArgs {
   const float* alibi;            // [H]
   float* ctx;                    // [width*n_new][H*hd]
   float* workspace;              // split partials
+  const void* pool_base;         // the span's whole pool (all blocks): tensor-map base
+  int64_t pool_bytes;
 };
 
 void launch_rope_append(const AttnArgs& a, cudaStream_t st);
@@ -90,6 +92,9 @@ void launch_attention_decode(const AttnArgs& a, cudaStream_t st);
 void launch_attention_prefill(const AttnArgs& a, cudaStream_t st);
 // tensor-core flash prefill (bf16 KV, hd 64/128); false if the shape is unsupported
 bool launch_attention_prefill_mma(const AttnArgs& a, cudaStream_t st);
+// tcgen05 / TMEM flash prefill (bf16 KV, hd 128); false if the shape is unsupported
+bool launch_attention_prefill_tc(const AttnArgs& a, cudaStream_t st);
+extern bool g_attn_tc;    // option 8 (default on)
 
 // KV page copy (copy-on-write of a shared tail page): all blocks of the span
 void launch_page_copy(void* pool, int64_t block_stride_bytes, int n_blocks,

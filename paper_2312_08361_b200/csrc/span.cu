@@ -532,6 +532,7 @@ int run_span_prefill_tc(sp_span* s, sp_kv* kv, int b0, int b1, float* y, float* 
   at.page_table = kv->d_table; at.max_pages = s->max_pages;
   at.rope_cos = s->rope_cos; at.rope_sin = s->rope_sin; at.alibi = s->alibi;
   at.ctx = s->ctx; at.workspace = s->attn_ws;
+  at.pool_base = s->pool; at.pool_bytes = s->block_stride * (s->end - s->start);
   auto gemm1 = [&](void* w, float* sc, int64_t N, int64_t K, float* out, int64_t ldy,
                    const float* res, int epi) {
     ProfScope ps(s, PC_GEMM, (double)N * K + 4.0 * N + 2.0 * Mp * K + 4.0 * R * ldy,
@@ -589,7 +590,8 @@ int run_span_prefill_tc(sp_span* s, sp_kv* kv, int b0, int b1, float* y, float* 
                                             (double)n_new * (n_new + 1) / 2);
       ProfScope ps(s, PC_ATTN_PRE, (double)width * (kv->length + n_new) * 2 * s->kv * kv_elt,
                    4.0 * pairs * s->H * s->hd, st);
-      if (!launch_attention_prefill_mma(at, st)) launch_attention_prefill(at, st);
+      if (!launch_attention_prefill_tc(at, st) && !launch_attention_prefill_mma(at, st))
+        launch_attention_prefill(at, st);
     }
     digit(s->ctx, d, 0, nullptr, nullptr);
     gemm(W.o, W.s_o, d, d, y, d, y, EPI_RESID);
@@ -695,6 +697,7 @@ int run_span(sp_span* s, sp_kv* kv, int b0, int b1, float* y, float* record, int
   at.page_table = kv->d_table; at.max_pages = s->max_pages;
   at.rope_cos = s->rope_cos; at.rope_sin = s->rope_sin; at.alibi = s->alibi;
   at.ctx = s->ctx; at.workspace = s->attn_ws;
+  at.pool_base = s->pool; at.pool_bytes = s->block_stride * (s->end - s->start);
   const int64_t d = s->d, F = s->F;
   const double kv_elt = s->cfg.kv_dtype == kKVBF16 ? 2.0 : 4.0;
   for (int b = b0 - s->start; b < b1 - s->start; ++b) {
@@ -722,7 +725,8 @@ int run_span(sp_span* s, sp_kv* kv, int b0, int b1, float* y, float* record, int
       ProfScope ps(s, decode ? PC_ATTN_DEC : PC_ATTN_PRE, kvbytes + 8.0 * R * d,
                    4.0 * pairs * s->H * s->hd, st);
       if (decode) launch_attention_decode(at, st);
-      else if (!launch_attention_prefill_mma(at, st)) launch_attention_prefill(at, st);
+      else if (!launch_attention_prefill_tc(at, st) && !launch_attention_prefill_mma(at, st))
+        launch_attention_prefill(at, st);
     }
     linear(s, wd, W.o, W.s_o, d, d, s->ctx, y, d, y, EPI_RESID, R, decode, st);
     {
@@ -1143,6 +1147,7 @@ int sp_span_set_option(sp_span* s, int32_t option, int32_t value) {
   else if (option == 5) g_attn_nsub = value;
   else if (option == 6) g_attn_cluster = value;
   else if (option == 7) g_attn_cl = value != 0;
+  else if (option == 8) g_attn_tc = value != 0;
   else SP_FAIL(SP_ERR_ARG, "unknown option");
   return SP_OK;
 }

@@ -482,6 +482,43 @@ def test_decode_attention_cluster_kernel(name, t_pre):
         assert np.abs(outs[1][j] - outs[0][j]).max() <= 2e-3 * s
 
 
+@pytest.mark.parametrize("name", ["llama_g8", "llama_int8", "bloom_int8", "llama_bf16"])
+def test_prefill_attention_tcgen05(name):
+    """Prefill / replay attention on tcgen05 + TMEM (attn_prefill_tc.cu, the
+    default for bf16 KV, hd 128) against the mma.sync FlashAttention kernel
+    with hi/lo Q and P (option 8 off, option 3 on) and the oracle: a 100-token
+    prefill then a 200-token chunk on top of the cache (t0 > 0, causal mask
+    across the page boundary), ragged last query tile."""
+    from paper_2312_08361_b200 import _lib
+    cfg = SMALL[name]
+    rng = np.random.default_rng(37)
+    d = cfg.hidden_dim
+    x = rng.standard_normal((300, d)).astype(np.float32)
+    outs = {}
+    eng = _engine(cfg)
+    try:
+        for tc in (1, 0):
+            _lib.check(eng.lib.sp_span_set_option(eng.span.handle, 8, tc))
+            _lib.check(eng.lib.sp_span_set_option(eng.span.handle, 3, 1 - tc))
+            c = eng.make_caches(0, cfg.n_blocks, 1)
+            a = eng.run_cached(0, cfg.n_blocks, c, _blob(x[:100]), 1, 100, False).array()
+            b = eng.run_cached(0, cfg.n_blocks, c, _blob(x[100:]), 1, 200, False).array()
+            outs[tc] = np.concatenate([a, b])
+    finally:
+        _lib.check(eng.lib.sp_span_set_option(eng.span.handle, 8, 1))
+        _lib.check(eng.lib.sp_span_set_option(eng.span.handle, 3, 0))
+    runner = om.SpanRunner(cfg, 0, cfg.n_blocks)
+    want = np.concatenate([runner.step(x[None, :100])[0], runner.step(x[None, 100:])[0]])
+    s = np.abs(want).max()
+    e_tc = np.abs(outs[1] - want).max() / s
+    e_mma = np.abs(outs[0] - want).max() / s
+    rel = np.abs(outs[1] - want) / (np.abs(want) + 1e-3 * s)
+    print(f"{name} prefill: tcgen05 err {e_tc:.2e}, mma.sync hi/lo err {e_mma:.2e} "
+          f"(max-abs / max|y|); tcgen05 per-element relative p99 {np.percentile(rel, 99):.2e}")
+    assert e_tc <= 2e-3
+    assert np.abs(outs[1] - outs[0]).max() <= 2e-3 * s
+
+
 def test_bf16_tc_prefill_matches_simt():
     """bf16 weights (Llama-2-7B family) on the tcgen05 GEMM (kind::f16, hi/lo
     bf16 activation planes, f32 accumulation) vs the exact-f32 SIMT GEMM, and
