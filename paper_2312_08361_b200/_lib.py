@@ -10,7 +10,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libspanpipe.so")
+LIB_PATH = os.environ.get("SP_LIB_PATH") or os.path.join(HERE, "libspanpipe.so")
 
 SP_OK = 0
 SP_ERR_ARG = -1

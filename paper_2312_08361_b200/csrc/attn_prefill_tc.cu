@@ -1,6 +1,6 @@
 // Prefill / replay causal attention (n_new > 1) on the 5th-gen tensor cores:
-// tcgen05.mma with the score and output tiles in TMEM (bf16 KV cache, head
-// dim 128).
+// tcgen05.mma with both A operands (Q, P) and both accumulators (S, O) in TMEM,
+// K / V pages brought in by tensor-map TMA (bf16 KV cache, head dim 128).
 //
 // SP/model.py:263-275: scores = q . k / sqrt(hd) (+ ALiBi), causal mask for
 // n > 1 (the reference fills -1e30; here -inf, identical after the
@@ -11,27 +11,30 @@
 //   * warps 0-7  softmax / epilogue: TMEM lane = query row; the two warps of a
 //                lane quarter split every tile's columns (32 scores, 64 output
 //                dims each) and combine the row maxima through shared memory.
-//                Per tile: tcgen05.ld the scores, scale, mask, online max and
-//                sum (exp2 domain), write P (bf16) to shared memory.  The
-//                output accumulates in TMEM across tiles; it is rescaled
-//                (tcgen05.ld / st) only when a row's maximum grows by more than
-//                2^8 over the one its P values are normalised to, so p <= 256
-//                and most tiles touch no output column.  At the end ctx = O / l.
+//                Q arrives pre-scaled by log2(e)/sqrt(hd), so the scores leave
+//                the MMA in the exp2 domain.  Per tile: tcgen05.ld the scores,
+//                ALiBi / causal mask (diagonal tiles only), max tree, exp2,
+//                P (bf16) -> TMEM with tcgen05.st.  The output accumulates in
+//                TMEM across tiles and is rescaled (tcgen05.ld / st) only when
+//                a row's maximum grows by more than 2^8 over the one its P
+//                values are normalised to (p <= 256).  At the end ctx = O / l.
 //   * warp 8     producer: one lane issues each tile's K and V pages as 2-D
 //                tensor-map TMA loads (cp.async.bulk.tensor, 128-byte swizzle,
 //                [64 keys][64 dims] boxes) from the paged pool: K lands in the
 //                K-major SW128 layout (B operand of S = Q K^T), V in the MN-major
-//                SW128 layout (B operand of O = P V).  3 stages.
+//                SW128 layout (B operand of O = P V).  5 stages.
 //   * warp 9     TMEM allocator + one elected lane issuing the MMAs:
-//                S_j = (Qhi + Qlo) K_j^T  (M = 128, N = 64, K = 128, f32 in TMEM)
-//                O  += P_j V_j            (M = 128, N = 128, K = 64, in TMEM)
+//                S_j = (Qhi + Qlo) K_j^T  (M = 128, N = 64, K = 128; A in TMEM)
+//                O  += P_j V_j            (M = 128, N = 128, K = 64; A in TMEM)
 //                S_{j+1} is issued before O_j, so the tensor pipe works on the
 //                next scores while the softmax warps turn S_j into P_j.
-// TMEM: 2 x 64 score columns (double buffered) + 128 output columns.
+// TMEM: Q hi/lo 128 columns, S 2 x 64 (double buffered), P 2 x 32, O 128.
 // Q is split hi + lo bf16 (two MMAs) against the bf16 K cache, so the scores
 // carry the cache's rounding, not a bf16 rounding of q; P (in [0, 256]) is
 // bf16 with f32 accumulation.
 // Each query row depends only on its own row: batch / tile invariant.
+// Measured (profiles/r02_attn_prefill_tc.md): the per-tile period is set by the
+// softmax warps (MUFU ex2: 64 per row per tile) and the N = 64 score MMAs.
 #include <cuda.h>   // CUtensorMap (the encoder is fetched from the driver at run time)
 
 #include <cstdio>
@@ -54,16 +57,18 @@ constexpr int BK = 64;                  // keys per tile (one page)
 constexpr int NSM = 8;                  // softmax warps: 2 per TMEM lane quarter
 constexpr int NTHREADS = (NSM + 2) * 32;
 constexpr int WP = NSM, WM = NSM + 1;   // producer warp, MMA warp
-constexpr int Q_BYTES = BQ * HD * 2;    // 32 KB per plane (hi, lo)
 constexpr int K_BYTES = BK * HD * 2;    // 16 KB
 constexpr int V_BYTES = BK * HD * 2;    // 16 KB
-constexpr int P_BYTES = BQ * BK * 2;    // 16 KB per plane
 constexpr int STAGE_BYTES = K_BYTES + V_BYTES;
-constexpr int NST = 3;                  // K/V stages
+constexpr int NST = 5;                  // K/V stages
 constexpr int BOX = BK * 64 * 2;        // one [64 keys][64 dims] TMA box (8 KB)
-constexpr int SMEM_BYTES = 2 * Q_BYTES + NST * STAGE_BYTES + 2 * P_BYTES + 1024;
-constexpr int S_COL = 0;                // TMEM columns: S buffers 0..127
-constexpr int O_COL = 128;              //               O 128..255
+constexpr int SMEM_BYTES = NST * STAGE_BYTES + 1024;
+// TMEM columns (32-bit): the A operands live in TMEM (one column = 2 bf16 of
+// a row): Q hi 0..63, Q lo 64..127; S 2 x 64; P 2 x 32; O 128
+constexpr int Q_COL = 0;
+constexpr int S_COL = 128;
+constexpr int P_COL = 256;
+constexpr int O_COL = 320;
 constexpr float kRescale = 8.0f;        // log2 growth of a row max that forces an O rescale
 constexpr float kLog2e = 1.4426950408889634f;
 
@@ -113,12 +118,13 @@ __device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(su32(bar))
       : "memory");
 }
-__device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
-                                     uint32_t acc) {
+// A operand from TMEM (row = lane, K packed two bf16 per 32-bit column)
+__device__ __forceinline__ void umma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b,
+                                        uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
-      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(b), "r"(idesc), "r"(acc));
 }
 __device__ __forceinline__ void umma_commit(uint64_t* b) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -153,34 +159,36 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float* v) {
       : "memory");
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
 __device__ __forceinline__ uint32_t bf2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
 }
-// 8 f32 -> 16 bytes of bf16 hi and 16 bytes of bf16 lo (x - hi)
-__device__ __forceinline__ void split8(const float* x, uint4& hi, uint4& lo) {
-  float h[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) h[i] = __bfloat162float(__float2bfloat16_rn(x[i]));
-  hi = make_uint4(bf2(h[0], h[1]), bf2(h[2], h[3]), bf2(h[4], h[5]), bf2(h[6], h[7]));
-  lo = make_uint4(bf2(x[0] - h[0], x[1] - h[1]), bf2(x[2] - h[2], x[3] - h[3]),
-                  bf2(x[4] - h[4], x[5] - h[5]), bf2(x[6] - h[6], x[7] - h[7]));
-}
-// K-major A/B core-matrix layout of a [rows][k] bf16 operand, 16-element k
-// steps: step u = [2 halves][rows/8][8 rows][16 B]; LBO = rows * 16, SBO = 128
-__device__ __forceinline__ int kmajor_off(int row, int chunk, int rows) {
-  return (chunk >> 1) * rows * 32 + (chunk & 1) * rows * 16 + (row >> 3) * 128 + (row & 7) * 16;
-}
+// debug (SP_BUILD_TRACE=1 build + SP_ATTN_PF_TRACE=1): per-phase clock sums of
+// softmax warp 0 and the MMA lane of CTA (0, 0), printed by the launcher
+__device__ unsigned long long g_pf_trace[16];
+#define PF_T(slot, t0) \
+  do { if (SP_DEV_TRACE && blockIdx.x == 0 && blockIdx.y == 0) { \
+    const unsigned long long t_ = clock64(); pf_acc[slot] += t_ - (t0); (t0) = t_; } } while (0)
 
 __global__ void __launch_bounds__(NTHREADS, 1)
 attn_prefill_tc_kernel(AttnArgs a, const __grid_constant__ CUtensorMap kvmap, int64_t row0) {
+  unsigned long long pf_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned long long pf_t = SP_DEV_TRACE ? clock64() : 0;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte alignment for the 128-byte-swizzled TMA boxes / UMMA atoms
   uint8_t* smem = smem_raw + ((1024 - (su32(smem_raw) & 1023)) & 1023);
-  uint8_t* Qhi = smem;
-  uint8_t* Qlo = smem + Q_BYTES;
-  uint8_t* stages = smem + 2 * Q_BYTES;                        // [NST][K box0 box1 | V box0 box1]
-  uint8_t* Pbuf = stages + NST * STAGE_BYTES;                  // [2] bf16 P
+  uint8_t* stages = smem;                                      // [NST][K box0 box1 | V box0 box1]
   __shared__ __align__(8) uint64_t kv_full[NST], kv_empty[NST], s_full[2], s_free[2],
       p_full[2], p_free[2], o_full, q_full;
   __shared__ uint32_t tmem_base;
@@ -245,17 +253,20 @@ attn_prefill_tc_kernel(AttnArgs a, const __grid_constant__ CUtensorMap kvmap, in
       auto issue_s = [&](int j) {
         const int kst = j % NST, st = j & 1;
         mbar_wait(&kv_full[kst], (j / NST) & 1);
+        PF_T(3, pf_t);
         if (j >= 2) mbar_wait(&s_free[st], ((j >> 1) - 1) & 1);
+        PF_T(4, pf_t);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint8_t* Ks = stages + kst * STAGE_BYTES;
         const uint32_t d = tb + S_COL + st * BK;
 #pragma unroll
         for (int u = 0; u < HD / 16; ++u) {
           // K-major SW128: 16 dims = 32 bytes along the 128-byte swizzle atom row;
-          // dims 64..127 are the second box; 8-row groups 1024 bytes apart
+          // dims 64..127 are the second box; 8-row groups 1024 bytes apart.
+          // A = Q hi / lo from TMEM: 16 dims = 8 columns
           const uint64_t bd = sdesc(Ks + (u >> 2) * BOX + (u & 3) * 32, 16, 1024, 2);
-          umma(d, sdesc(Qhi + u * BQ * 32, BQ * 16, 128), bd, kIdescS, u > 0);
-          umma(d, sdesc(Qlo + u * BQ * 32, BQ * 16, 128), bd, kIdescS, 1);
+          umma_ts(d, tb + Q_COL + u * 8, bd, kIdescS, u > 0);
+          umma_ts(d, tb + Q_COL + 64 + u * 8, bd, kIdescS, 1);
         }
         umma_commit(&s_full[st]);
       };
@@ -264,22 +275,28 @@ attn_prefill_tc_kernel(AttnArgs a, const __grid_constant__ CUtensorMap kvmap, in
         mbar_wait(&p_full[st], (j >> 1) & 1);    // P_j written (and any O rescale done)
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint8_t* Vs = stages + kst * STAGE_BYTES + K_BYTES;
-        const uint8_t* P = Pbuf + st * P_BYTES;
 #pragma unroll
         for (int u = 0; u < BK / 16; ++u)
           // MN-major SW128: 64 dims per 128-byte atom row, the second 64 dims one
-          // box (LBO) further; 16 keys = 2 groups of 8 rows, 1024 bytes apart (SBO)
-          umma(tb + O_COL, sdesc(P + u * BQ * 32, BQ * 16, 128),
-               sdesc(Vs + u * 2048, BOX, 1024, 2), kIdescO, (j | u) ? 1u : 0u);
+          // box (LBO) further; 16 keys = 2 groups of 8 rows, 1024 bytes apart (SBO).
+          // A = P_j from TMEM: 16 keys = 8 columns
+          umma_ts(tb + O_COL, tb + P_COL + st * (BK / 2) + u * 8,
+                  sdesc(Vs + u * 2048, BOX, 1024, 2), kIdescO, (j | u) ? 1u : 0u);
         umma_commit(&o_full);                    // O now holds tiles 0..j
         umma_commit(&p_free[st]);                // P buffer st read
         umma_commit(&kv_empty[kst]);             // K_j and V_j consumed
       };
+      PF_T(0, pf_t);
       issue_s(0);
+      PF_T(1, pf_t);
       for (int j = 0; j < ntiles; ++j) {
         if (j + 1 < ntiles) issue_s(j + 1);
+        PF_T(1, pf_t);
         issue_o(j);
+        PF_T(2, pf_t);
       }
+      if (SP_DEV_TRACE && blockIdx.x == 0 && blockIdx.y == 0)
+        for (int i = 0; i < 5; ++i) g_pf_trace[8 + i] = pf_acc[i];
     }
     __syncwarp();
   } else {
@@ -297,58 +314,79 @@ attn_prefill_tc_kernel(AttnArgs a, const __grid_constant__ CUtensorMap kvmap, in
     auto pair_sync = [&]() {
       asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
     };
-    // Q row (this warp's 64 dims) -> hi / lo planes (K-major A operand)
+    // Q row (this warp's 64 dims), pre-scaled by log2(e) / sqrt(hd) (scores come
+    // out of the MMA in the exp2 domain), -> hi / lo bf16 pairs in TMEM (the A
+    // operand of S = Q K^T: row = lane, column c = dims 2c, 2c + 1)
+    const float qscale = kLog2e / sqrtf((float)HD);
     {
-      const float* qsrc = a.qkv + (int64_t)(slot * a.n_new + qi) * a.ldqkv + h * HD;
-#pragma unroll 4
-      for (int c8 = 0; c8 < HD / 16; ++c8) {
-        const int ch = hf * (HD / 16) + c8;
-        float x[8];
-        const float4 v0 = *reinterpret_cast<const float4*>(qsrc + ch * 8);
-        const float4 v1 = *reinterpret_cast<const float4*>(qsrc + ch * 8 + 4);
-        x[0] = v0.x; x[1] = v0.y; x[2] = v0.z; x[3] = v0.w;
-        x[4] = v1.x; x[5] = v1.y; x[6] = v1.z; x[7] = v1.w;
-        uint4 hi, lo;
-        split8(x, hi, lo);
-        const int off = kmajor_off(row, ch, BQ);
-        *reinterpret_cast<uint4*>(Qhi + off) = hi;
-        *reinterpret_cast<uint4*>(Qlo + off) = lo;
+      const float* qsrc = a.qkv + (int64_t)(slot * a.n_new + qi) * a.ldqkv + h * HD + hf * 64;
+      float4 qv[16];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) qv[c] = *reinterpret_cast<const float4*>(qsrc + c * 4);
+      uint32_t hi[32], lo[32];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        const float x[4] = {qv[c].x * qscale, qv[c].y * qscale, qv[c].z * qscale,
+                            qv[c].w * qscale};
+        float hh[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) hh[i] = __bfloat162float(__float2bfloat16_rn(x[i]));
+        hi[2 * c] = bf2(hh[0], hh[1]);
+        hi[2 * c + 1] = bf2(hh[2], hh[3]);
+        lo[2 * c] = bf2(x[0] - hh[0], x[1] - hh[1]);
+        lo[2 * c + 1] = bf2(x[2] - hh[2], x[3] - hh[3]);
       }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      tmem_st16(tb + lane_addr + Q_COL + hf * 32, hi);
+      tmem_st16(tb + lane_addr + Q_COL + hf * 32 + 16, hi + 16);
+      tmem_st16(tb + lane_addr + Q_COL + 64 + hf * 32, lo);
+      tmem_st16(tb + lane_addr + Q_COL + 64 + hf * 32 + 16, lo + 16);
+      tmem_wait_st();
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&q_full);
     }
-    const float qscale = kLog2e / sqrtf((float)HD);
     const float slope_l2 = (a.family == kBloom) ? a.alibi[h] * kLog2e : 0.f;
     constexpr int SC = BK / 2;                   // score columns per warp
     constexpr int OC = HD / 2;                   // output columns per warp
     float m_used = -INFINITY, l_run = 0.f;       // P_j = exp2(s - m_used); l in the same units
+    PF_T(7, pf_t);
     for (int j = 0; j < ntiles; ++j) {
       const int st = j & 1;
       mbar_wait(&s_full[st], (j >> 1) & 1);
+      PF_T(0, pf_t);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       float s[SC];
       tmem_ld32(tb + lane_addr + S_COL + st * BK + hf * SC, s);
       tmem_wait_ld();
+      PF_T(1, pf_t);
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&s_free[st]);
-      // scale (log2 e / sqrt(hd)), ALiBi, causal mask, tile max
+      // ALiBi, causal mask (diagonal tiles only), tile max as a 3-input tree
       const int kbase = j * BK + hf * SC;
       const bool unmasked = j * BK + BK - 1 <= a.t0 + q0;   // every row sees every key
-      float tmax = -INFINITY;
+      if (a.family == kBloom) {
 #pragma unroll
-      for (int i = 0; i < SC; ++i) {
-        const int key = kbase + i;
-        float x = s[i] * qscale;
-        if (a.family == kBloom) x = fmaf(slope_l2, (float)(key - qpos), x);
-        if (!unmasked && key > qpos) x = -INFINITY;
-        s[i] = x;
-        tmax = fmaxf(tmax, x);
+        for (int i = 0; i < SC; ++i) s[i] = fmaf(slope_l2, (float)(kbase + i - qpos), s[i]);
       }
+      if (!unmasked) {
+#pragma unroll
+        for (int i = 0; i < SC; ++i) s[i] = (kbase + i > qpos) ? -INFINITY : s[i];
+      }
+      float mx[SC / 4];
+#pragma unroll
+      for (int i = 0; i < SC / 4; ++i)
+        mx[i] = fmaxf(fmaxf(s[4 * i], s[4 * i + 1]), fmaxf(s[4 * i + 2], s[4 * i + 3]));
+#pragma unroll
+      for (int w = SC / 8; w >= 1; w >>= 1)
+#pragma unroll
+        for (int i = 0; i < w; ++i) mx[i] = fmaxf(mx[i], mx[i + w]);
+      float tmax = mx[0];
+      PF_T(2, pf_t);
       red_max[st][row][hf] = tmax;
       pair_sync();
       tmax = fmaxf(red_max[st][row][0], red_max[st][row][1]);
+      PF_T(3, pf_t);
       // O rescale only when the row's max outgrows its reference by 2^8
       // (warp-uniform: tcgen05.ld/st are warp-collective; factor 1 elsewhere)
       float mnew = m_used;
@@ -372,27 +410,35 @@ attn_prefill_tc_kernel(AttnArgs a, const __grid_constant__ CUtensorMap kvmap, in
         l_run *= f;
       }
       m_used = mnew;
-      // P_j = exp2(s - m_used) (<= 2^8), bf16, -> shared buffer st, once the
-      // MMA of tile j - 2 has read it
+      // P_j = exp2(s - m_used) (<= 2^8), bf16, -> TMEM buffer st, once the MMA
+      // of tile j - 2 has read it
+      PF_T(4, pf_t);
       if (j >= 2) mbar_wait(&p_free[st], ((j >> 1) - 1) & 1);
-      uint8_t* P = Pbuf + st * P_BYTES;
-      float psum = 0.f;
+      PF_T(5, pf_t);
+      // p = exp2(s - m) (ex2.approx.ftz(-inf) = +0: masked keys need no test);
+      // four partial sums for instruction-level parallelism
+      float ps4[4] = {0.f, 0.f, 0.f, 0.f};
+      uint32_t pk[SC / 2];
 #pragma unroll
-      for (int c8 = 0; c8 < SC / 8; ++c8) {
-        float p[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const float x = s[c8 * 8 + i];
-          p[i] = (x == -INFINITY) ? 0.f : ex2_approx(x - m_used);
-          psum += p[i];
-        }
-        *reinterpret_cast<uint4*>(P + kmajor_off(row, hf * (SC / 8) + c8, BQ)) =
-            make_uint4(bf2(p[0], p[1]), bf2(p[2], p[3]), bf2(p[4], p[5]), bf2(p[6], p[7]));
+      for (int i = 0; i < SC; i += 2) {
+        const float p0 = ex2_approx(s[i] - m_used);
+        const float p1 = ex2_approx(s[i + 1] - m_used);
+        ps4[(i >> 1) & 3] += p0 + p1;
+        pk[i / 2] = bf2(p0, p1);
       }
+      const float psum = (ps4[0] + ps4[1]) + (ps4[2] + ps4[3]);
+      // P_j -> TMEM (A operand of O += P V): this warp's 32 keys = 16 columns
+      tmem_st16(tb + lane_addr + P_COL + st * (BK / 2) + hf * (SC / 2), pk);
+      tmem_wait_st();
       l_run += psum;
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[st]);
+      PF_T(6, pf_t);
+    }
+    if (SP_DEV_TRACE && blockIdx.x == 0 && blockIdx.y == 0 && warp == 0 && lane == 0) {
+      for (int i = 0; i < 8; ++i) g_pf_trace[i] = pf_acc[i];
+      g_pf_trace[15] = ntiles;
     }
     // ---- ctx row = O / l  (l = the two halves' sums, same units) ----
     if (hf == 1) red_l[row] = l_run;
@@ -476,6 +522,16 @@ bool launch_attention_prefill_tc(const AttnArgs& a, cudaStream_t st) {
   dim3 grid(a.width * a.H, (a.n_new + BQ - 1) / BQ);
   attn_prefill_tc_kernel<<<grid, NTHREADS, SMEM_BYTES, st>>>(a, *map, row0);
   count_launch();
+  static const bool tr = SP_DEV_TRACE && getenv("SP_ATTN_PF_TRACE");
+  if (tr) {
+    unsigned long long h[16];
+    cudaMemcpyFromSymbolAsync(h, g_pf_trace, sizeof(h), 0, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    fprintf(stderr, "attn_pf_tc CTA(0,0) ntiles=%llu softmax clocks: s_wait %llu ld %llu "
+            "scale %llu pair %llu rescale %llu p_free %llu exp_st %llu qload %llu | mma: "
+            "prologue %llu issue_s %llu issue_o(wait P) %llu kv_full %llu s_free %llu\n", h[15],
+            h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7], h[8], h[9], h[10], h[11], h[12]);
+  }
   return true;
 }
 

@@ -897,6 +897,9 @@ int sp_span_create(const sp_config* cfg, int32_t start, int32_t end, int32_t dev
     sp_span_destroy(s);
     SP_FAIL(SP_ERR_OOM, "KV pool allocation failed");
   }
+  // finite contents everywhere: attention tiles read whole pages, and the rows
+  // past a sequence's end (multiplied by zero probabilities) must not be NaN
+  SP_CUDA_TRY(cudaMemset(s->pool, 0, (size_t)s->block_stride * nb));
   s->refcount.assign(s->n_pages, 0);
   for (int64_t i = s->n_pages - 1; i >= 0; --i) s->free_pages.push_back((int)i);
 
