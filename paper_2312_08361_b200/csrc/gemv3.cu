@@ -49,13 +49,18 @@ constexpr int XSLOT = 128;        // per batch row: the unit's activation chunk 
 __host__ __device__ constexpr int stage_bytes(int nt) {
   return UNIT_BYTES + (nt == 1 ? 4 : (nt == 2 ? 8 : 8)) * XSLOT;
 }
-// nf4 (one row per launch): 4 KB of codes (128 channels x 64 k), the unit's
-// 128 uint8 block scales, one row's 64-float activation chunk
+// nf4: 4 KB of codes (128 channels x 64 k), the unit's 128 uint8 block scales,
+// and each batch row's 64-float activation chunk (1 row, or up to 4 rows: the
+// 8 columns of one MMA tile at 2 digits per row)
 constexpr int NF4_QS = 128, NF4_X = 256;
-__host__ __device__ constexpr int stage_bytes_wt(int wt, int nt) {
-  return wt == kNF4 ? UNIT_BYTES + NF4_QS + NF4_X : stage_bytes(nt);
+__host__ __device__ constexpr int stage_bytes_wt(int wt, int nt, int rm = 1) {
+  return wt == kNF4 ? UNIT_BYTES + NF4_QS + (rm == 1 ? 1 : 4) * NF4_X : stage_bytes(nt);
 }
 constexpr int STAGES = 3;         // TMA ring depth per warp (units)
+// multi-row nf4 stages are 5.1 KB: two of them per warp keep two CTAs per SM
+__host__ __device__ constexpr int stages_of(int wt, int rm) {
+  return (wt == kNF4 && rm != 1) ? 2 : STAGES;
+}
 constexpr int RMAX = 8;           // batch rows per launch
 // int8 path: activation code width.  The row is scaled by 2^(kQBits - e)
 // (|x| < 2^e) and rounded to an integer |q| <= 2^kQBits written as NDIG
@@ -165,13 +170,15 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
   constexpr int COLS = INT ? NDIG : 2;
   constexpr int XV = INT ? 4 : 2;
   using XVec = typename std::conditional<INT, float4, float2>::type;
-  static_assert(WT != kNF4 || (RM == 1 && NT == 1), "nf4: one row per launch");
+  static_assert(WT != kNF4 || NT == 1, "nf4: one MMA column tile (up to 4 rows)");
   constexpr int XOFF = UNIT_BYTES + (WT == kNF4 ? NF4_QS : 0);   // activation chunks in a stage
+  constexpr int XS = WT == kNF4 ? NF4_X : XSLOT;                 // bytes per row's chunk
+  constexpr int ST = stages_of(WT, RM);                          // ring depth
   extern __shared__ __align__(128) uint8_t dyn[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int STAGE_BYTES = stage_bytes_wt(WT, NT);
-  uint8_t* ring = dyn + (size_t)warp * STAGES * STAGE_BYTES;
-  WarpSmem* ws_ = reinterpret_cast<WarpSmem*>(dyn + (size_t)NW * STAGES * STAGE_BYTES) + warp;
+  constexpr int STAGE_BYTES = stage_bytes_wt(WT, NT, RM);
+  uint8_t* ring = dyn + (size_t)warp * ST * STAGE_BYTES;
+  WarpSmem* ws_ = reinterpret_cast<WarpSmem*>(dyn + (size_t)NW * ST * STAGE_BYTES) + warp;
 
   const int64_t gw = (int64_t)blockIdx.x * NW + warp;
   // unit indices fit 32 bits (units = N/128 * K/KTILE < 2^31); the slice
@@ -190,7 +197,7 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
 
   gtrace(a, 0);
   if (lane == 0) {
-    for (int st = 0; st < STAGES; ++st) mbar_init(&ws_->bar[st], 1);
+    for (int st = 0; st < ST; ++st) mbar_init(&ws_->bar[st], 1);
     mbar_fence_init();
   }
   __syncwarp();
@@ -201,7 +208,7 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
   uint64_t policy_x;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(policy_x));
   const int nunits = u1 > u0 ? (int)(u1 - u0) : 0;
-  const int npre = nunits < STAGES ? nunits : STAGES;   // the whole ring before the wait
+  const int npre = nunits < ST ? nunits : ST;   // the whole ring before the wait
   // ---- before the dependency: the weights of the first STAGES units (no
   // kernel writes weights), so their DRAM latency overlaps the previous
   // kernel's tail; each stage's barrier also expects its activation bytes ----
@@ -252,7 +259,7 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
       // (issued right behind the stats loads, ahead of their reduction)
       const int64_t kt = kt0 + i < KT ? kt0 + i : kt0 + i - KT;
       for (int r = 0; r < (RM == 1 ? 1 : Rn); ++r)
-        tma_load_1d(ring + i * STAGE_BYTES + XOFF + r * XSLOT,
+        tma_load_1d(ring + i * STAGE_BYTES + XOFF + r * XS,
                     a.x + (int64_t)(r0 + r) * a.ldx + kt * KTILE, XB, &ws_->bar[i], policy_x);
     }
 #pragma unroll
@@ -322,7 +329,7 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
   // ---- TMA producer (lane 0) ----
   // producer state (lane 0): next unit to issue as (group, k-tile, ring stage)
   int p_grp = (u0 + npre) / KT, p_kt = (u0 + npre) % KT;
-  int p_st = npre % STAGES, p_left = nunits - npre;
+  int p_st = npre % ST, p_left = nunits - npre;
   auto issue_next = [&]() {
     // the unit's weights and, alongside, each batch row's activation chunk:
     // both arrive on the same mbarrier (no separate activation-load latency)
@@ -334,10 +341,10 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
       tma_load_1d(dstg + UNIT_BYTES, qsbase + ((int64_t)p_grp * KT + p_kt) * NF4_QS, NF4_QS,
                   &ws_->bar[p_st], policy);
     for (int r = 0; r < (RM == 1 ? 1 : Rn); ++r)
-      tma_load_1d(dstg + XOFF + r * XSLOT, a.x + (int64_t)(r0 + r) * a.ldx + p_kt * KTILE,
+      tma_load_1d(dstg + XOFF + r * XS, a.x + (int64_t)(r0 + r) * a.ldx + p_kt * KTILE,
                   XB, &ws_->bar[p_st], policy_x);
     if (++p_kt == KT) { p_kt = 0; ++p_grp; }
-    if (++p_st == STAGES) p_st = 0;
+    if (++p_st == ST) p_st = 0;
     --p_left;
   };
   __syncwarp();
@@ -374,7 +381,8 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
     if constexpr (WT == kNF4) {
       // ---- nf4 unit: 2 k-steps of 32; B = the row's activation digits ----
 
-      const float* xs = reinterpret_cast<const float*>(stage + XOFF);
+      // this lane's B column = (batch row brow[0], digit bsub[0])
+      const float* xs = reinterpret_cast<const float*>(stage + XOFF + brow[0] * XS);
       uint32_t bb[2][2];
       const float mu = bmu[0], sc = bsc[0];
 #pragma unroll
@@ -499,7 +507,7 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
     }   // int8 / bf16 unit
     __syncwarp();
     if (lane == 0 && p_left > 0) issue_next();
-    if (++c_st == STAGES) { c_st = 0; c_ph ^= 1; }
+    if (++c_st == ST) { c_st = 0; c_ph ^= 1; }
 
     // ---- end of this warp's contribution to a group: flush ----
     const int64_t grp = c_grp;
@@ -633,7 +641,8 @@ void launch_cfg(const GemvArgs& a, int r0, int rn, cudaStream_t st) {
   const int64_t units = (a.N / 128) * (a.K / KTILE);
   const int grid = g_num_sms * CTAS_PER_SM;
   const size_t smem =
-      (size_t)NW * STAGES * stage_bytes_wt(WT, NT) + (size_t)NW * sizeof(WarpSmem) + 128;
+      (size_t)NW * stages_of(WT, RM) * stage_bytes_wt(WT, NT, RM) + (size_t)NW * sizeof(WarpSmem) +
+      128;
   static bool set[kMaxDevices] = {};
   const int dv = current_device();
   if (!set[dv]) {
@@ -756,9 +765,14 @@ void launch_gemv3(int wdtype, const GemvArgs& a, cudaStream_t st) {
     static int nd_env = getenv("SP_GEMV_NDIG") ? atoi(getenv("SP_GEMV_NDIG")) : 0;
     const int nd = nd_env ? nd_env : kNDig;
     if (wdtype == kNF4) {
-      // one row per launch (the 4 KB code unit + scales + a 64-float chunk
-      // per stage; two CTAs per SM leave no room for more rows' chunks)
-      for (int r = r0; r < r0 + rn; ++r) launch_nt2<kNF4, 1, 3, 1>(a, r, 1, st);
+      // one launch per 4 rows (8 MMA columns at 2 digits): the weights stream
+      // once for the batch; the 15-bit code keeps a row's result independent
+      // of the launch's row count
+      for (int q0 = r0; q0 < r0 + rn; q0 += 4) {
+        const int qn = r0 + rn - q0 < 4 ? r0 + rn - q0 : 4;
+        if (qn == 1) launch_nt2<kNF4, 1, 2, 1>(a, q0, 1, st);
+        else launch_nt2<kNF4, 1, 2, 4>(a, q0, qn, st);
+      }
     } else if (wdtype == kI8) {
       if (nd == 3) launch_wt<kI8, 3>(a, r0, rn, st);
       else launch_wt<kI8, 2>(a, r0, rn, st);

@@ -44,12 +44,15 @@ def test_full_shape_block_vs_oracle(name):
     got = eng.run_cached(0, 1, c, _blob(x[:t_pre]), 1, t_pre, False).array()
     want = runner.step(x[None, :t_pre])[0]
     s = np.abs(want).max()
-    assert np.abs(got - want).max() <= 2e-2 * s, np.abs(got - want).max() / s
+    e_pre = np.abs(got - want).max() / s
+    e_dec = []
     for i in range(t_pre, t_pre + n_dec):
         g = eng.run_cached(0, 1, c, _blob(x[i:i + 1]), 1, 1, False).array()
         w = runner.step(x[None, i:i + 1])[0]
-        s = np.abs(w).max()
-        assert np.abs(g - w).max() <= 2e-3 * s, (i, np.abs(g - w).max() / s)
+        e_dec.append(np.abs(g - w).max() / np.abs(w).max())
+    print(f"{name}: prefill err {e_pre:.2e}, decode err max {max(e_dec):.2e} (max-abs / max|y|)")
+    assert e_pre <= 2e-3
+    assert max(e_dec) <= 2e-3
 
 
 def test_full_shape_decode_rows_independent():

@@ -29,6 +29,14 @@ def _blob(a, quantized=False):
     return HiddenBlob.from_array(a, quantized)
 
 
+def _errs(got, want):
+    """(max-abs / max|y|, p99 of the per-element relative error with a 1e-3*max|y|
+    floor): the second shows what the max-abs ratio can hide in small outputs."""
+    s = np.abs(want).max()
+    rel = np.abs(got - want) / (np.abs(want) + 1e-3 * s)
+    return float(np.abs(got - want).max() / s), float(np.percentile(rel, 99))
+
+
 def test_toy_stack_matches_reference_golden(golden_toy):
     """prefill 3 rows then 6 decode rows through all 8 blocks (reference run)."""
     eng = _engine(toy(seed=1))
@@ -234,15 +242,19 @@ def test_extended_families_vs_oracle(name):
     c = eng.make_caches(0, cfg.n_blocks, 1)
     got = eng.run_cached(0, cfg.n_blocks, c, _blob(x[:t_pre]), 1, t_pre, False).array()
     want = runner.step(x[None, :t_pre])[0]
-    tol_pre = 2e-2 if cfg.weight_dtype != "f32" else 1e-4
-    scale = np.abs(want).max()
-    assert np.abs(got - want).max() <= tol_pre * scale, np.abs(got - want).max() / scale
+    # prefill: tcgen05 GEMMs on 15-bit activation digit planes, tcgen05 attention
+    # with hi/lo Q against the bf16 cache (f32 families: exact-f32 SIMT)
+    tol = 2e-3 if cfg.weight_dtype != "f32" else 1e-4
+    e_pre, r_pre = _errs(got, want)
+    errs = []
     for i in range(t_pre, t_pre + n_dec):
         g = eng.run_cached(0, cfg.n_blocks, c, _blob(x[i:i + 1]), 1, 1, False).array()
         w = runner.step(x[None, i:i + 1])[0]
-        tol = 2e-3 if cfg.weight_dtype != "f32" else 1e-4
-        s = np.abs(w).max()
-        assert np.abs(g - w).max() <= tol * s, (i, np.abs(g - w).max() / s)
+        errs.append(_errs(g, w))
+    print(f"{name}: prefill err {e_pre:.2e} (p99 rel {r_pre:.2e}); decode err max "
+          f"{max(e for e, _ in errs):.2e} (p99 rel {max(r for _, r in errs):.2e})")
+    assert e_pre <= tol
+    assert max(e for e, _ in errs) <= tol
 
 
 def test_engine_blocks_params_hash_matches_reference(golden_toy):
