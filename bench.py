@@ -237,8 +237,8 @@ def self_launch(args) -> bool:
         port = sk.getsockname()[1]
     env = dict(os.environ)
     # NCCL's init lines (nRanks of every communicator) go to stdout with the JSON line
-    env.setdefault("NCCL_DEBUG", "INFO")
-    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env["NCCL_DEBUG"] = "INFO"
+    env["NCCL_DEBUG_SUBSYS"] = "INIT"
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
            f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]

@@ -259,8 +259,10 @@ class FailoverRing:
                 rows = [self._rows(j) for j in range(len(msgs))]
                 codes = torch.cat([_split_wire(m, r, self.d)[0] for m, r in zip(msgs, rows)])
                 scales = torch.cat([_split_wire(m, r, self.d)[1] for m, r in zip(msgs, rows)])
-                dist.send(codes.view(torch.uint8).contiguous(), self.spare)
-                dist.send(scales.contiguous(), self.spare)
+                for h in dist.batch_isend_irecv(
+                        [dist.P2POp(dist.isend, codes.view(torch.uint8).contiguous(), self.spare),
+                         dist.P2POp(dist.isend, scales.contiguous(), self.spare)]):
+                    h.wait()
             self.replays.append({"position": pos, "tick": k,
                                  "sessions": sum(1 for c in counts if c),
                                  "rows": [sum(self._rows(j) for j in range(c)) for c in counts],
@@ -277,8 +279,9 @@ class FailoverRing:
                 codes = torch.empty(n_rows * self.d, dtype=torch.uint8, device=self.dev)
                 scales = torch.empty((n_rows * self.d + 63) // 64, dtype=torch.float32,
                                      device=self.dev)
-                dist.recv(codes, 0)
-                dist.recv(scales, 0)
+                for h in dist.batch_isend_irecv([dist.P2POp(dist.irecv, codes, 0),
+                                                  dist.P2POp(dist.irecv, scales, 0)]):
+                    h.wait()
                 codes = codes.view(torch.int8)
                 done = n_rows
                 if pend is not None and pend[0] == s:     # resumed step runs normally
@@ -300,6 +303,24 @@ class FailoverRing:
             self.replays.append({"position": pos, "tick": k,
                                  "replay_s": time.perf_counter() - tr,
                                  "rows": [sum(self._rows(j) for j in range(c)) for c in counts]})
+
+    def warm(self) -> None:
+        """Open the p2p connections a failover would use (client <-> spare, spare <->
+        every span rank) so that a measured replay does not include NCCL's lazy
+        connection set-up.  Collective over all ranks."""
+        dist = self.dist
+        one = torch.zeros(1, device=self.dev)
+        ops = []
+        if self.rank == self.spare:
+            for r in range(self.N):
+                ops.append(dist.P2POp(dist.isend, one, r))
+                ops.append(dist.P2POp(dist.irecv, torch.zeros(1, device=self.dev), r))
+        else:
+            ops.append(dist.P2POp(dist.irecv, torch.zeros(1, device=self.dev), self.spare))
+            ops.append(dist.P2POp(dist.isend, one, self.spare))
+        for h in dist.batch_isend_irecv(ops):
+            h.wait()
+        dist.barrier()
 
     def run(self) -> list[list[int]]:
         self.dropped = False
