@@ -109,7 +109,8 @@ def dram_per_launch(tag: str, name: str) -> list[tuple[str, float, float]]:
 
 TITLES = {
     "gemv": "decode GEMVs of one block (QKV, O, gate/up, down): the dominant kernel",
-    "attn_dec": "decode attention (RoPE + KV append + split-K flash decode, one block)",
+    "attn_dec": "decode attention (RoPE + KV append, 8-CTA cluster flash decode, one block)",
+    "attn_pf": "prefill attention on tcgen05 + TMEM (2048 tokens, one block)",
     "pair_gemm": "prefill tcgen05 CTA-pair GEMM (gate/up, 2048 tokens)",
     "prefill": "prefill attention + digitize (2048 tokens)",
 }

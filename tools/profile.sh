@@ -21,8 +21,10 @@ $T ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.s
     > gpurun_out/ncu_pl.log 2>&1; echo "prefill launch list rc=$?"
 $T ncu --set full --clock-control none --import-source on -k regex:"gemv3" -s 324 -c 4 \
     -o gpurun_out/${TAG}_gemv python bench.py --no-cpu --blocks 8 > gpurun_out/ncu_gemv.log 2>&1; echo "gemv rc=$?"
-$T ncu --set full --clock-control none --import-source on -k regex:"attn_dec_mma" -s 40 -c 1 \
+$T ncu --set full --clock-control none --import-source on -k regex:"attn_dec" -s 40 -c 1 \
     -o gpurun_out/${TAG}_attn_dec python bench.py --no-cpu --blocks 8 > gpurun_out/ncu_ad.log 2>&1; echo "attn_dec rc=$?"
+$T ncu --set full --clock-control none --import-source on -k regex:"attn_prefill_tc" -s 1 -c 1 \
+    -o gpurun_out/${TAG}_attn_pf python bench.py --no-cpu --blocks 1 --steps 2 > gpurun_out/ncu_apf.log 2>&1; echo "attn_pf rc=$?"
 $T ncu --set full --clock-control none --import-source on -k regex:"gemm_i8_tc2" -s 6 -c 1 \
     -o gpurun_out/${TAG}_pair_gemm python bench.py --no-cpu --blocks 1 --steps 2 > gpurun_out/ncu_pg.log 2>&1; echo "pair gemm rc=$?"
 $T ncu --set full --clock-control none --import-source on -k regex:"attn_prefill|digitize_reg" -s 5 -c 2 \
