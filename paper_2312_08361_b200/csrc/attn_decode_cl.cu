@@ -12,11 +12,12 @@
 // rows are staged with cp.async BEFORE the programmatic-launch wait (positions
 // < t0 are never rewritten), so after the QKV projection lands only the math
 // remains:
-//   * S^T[16 x 32] = q[16 x hd] . K^T on mma.m16n8k16 (rows 0..G-1 = the kv
-//     group's query heads, q split hi + lo bf16 — two MMAs — against the bf16
-//     cache), online softmax per head in the exp2 domain,
-//   * O[16 x hd] += P[16 x 32] . V (P split hi + lo; the S^T accumulator layout
-//     IS the A-fragment layout of P, no shuffles),
+//   * S[32 x 8] = K . q^T on mma.m16n8k16 (A = the warp's K rows by ldmatrix,
+//     B columns = the kv group's query heads, q split hi + lo bf16 — two MMAs —
+//     against the bf16 cache), online softmax per head in the exp2 domain,
+//   * O^T[hd x 8] += V^T . P^T (A = V rows transposed by ldmatrix.trans; B = P
+//     split hi + lo, turned from the S accumulator layout into B fragments by
+//     movmatrix.trans) — no padded rows, 64 MMAs per 32 positions,
 //   * the NW warp partials merge in a fixed order in shared memory, then the
 //     CL CTA partials merge over distributed shared memory: rank r finalises
 //     outputs [r*G*hd/CL, (r+1)*G*hd/CL) reading its 7 peers in rank order.
@@ -44,15 +45,19 @@ constexpr int GM = 8;            // query heads per kv head (rows of the M = 16 
 constexpr int NWMAX = 12;        // warps per CTA
 constexpr float kLog2e = 1.4426950408889634f;
 
-// m16n8k16 with rows 8..15 of A zero (padding): the accumulator pair of those
-// rows goes to a shared scratch pair `z`, so only rows 0..7 hold registers
-__device__ __forceinline__ void mma_top(float* c, float* z, uint32_t a0, uint32_t a2,
-                                        uint32_t b0, uint32_t b1) {
+__device__ __forceinline__ void mma16816(float* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
   asm volatile(
       "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
       "{%8,%9}, {%0,%1,%2,%3};"
-      : "+f"(c[0]), "+f"(c[1]), "+f"(z[0]), "+f"(z[1])
-      : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+// transpose of the warp's 8 x 8 b16 matrix fragment (lane (g8, t4) holds row g8,
+// columns 2t4, 2t4 + 1 -> afterwards row g8 of the transpose)
+__device__ __forceinline__ uint32_t movm_trans(uint32_t x) {
+  uint32_t y;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
 }
 __device__ __forceinline__ void ldsm4(uint32_t* r, const void* p) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -205,13 +210,16 @@ __global__ void __launch_bounds__(NWMAX * 32, 1) attn_dec_cl_kernel(AttnDecArgs 
   cl_mark(a, 3);
 
   const float qscale = kLog2e / sqrtf((float)HD);
-  const float slope_l2 = (a.family == kBloom && g8 < G) ? a.alibi[kh * G + g8] * kLog2e : 0.f;
+  // this lane's two heads (B / C columns 2*t4, 2*t4 + 1)
+  const int hA = 2 * t4, hB = 2 * t4 + 1;
+  const float slA = (a.family == kBloom && hA < G) ? a.alibi[kh * G + hA] * kLog2e : 0.f;
+  const float slB = (a.family == kBloom && hB < G) ? a.alibi[kh * G + hB] * kLog2e : 0.f;
 
-  float m_run = -INFINITY, l_run = 0.f;            // per head g8 (replicated over t4)
-  float o[HD / 8][2];                              // rows g8 (head), dims i*8 + 2*t4 + j
-  float z[2] = {0.f, 0.f};                         // padding rows' accumulator (discarded)
+  float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.f, 0.f};   // heads hA, hB
+  // O^T[dims x heads]: dim tile dt, c0/c1 = (dim dt*16 + g8, hA / hB), c2/c3 = (+8)
+  float o[HD / 16][4];
 #pragma unroll
-  for (int i = 0; i < HD / 8; ++i) o[i][0] = o[i][1] = 0.f;
+  for (int i = 0; i < HD / 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
 
   for (int s = 0; s < npass; ++s) {
     const int p0 = (s * CL + rank) * PC + warp * 32;
@@ -228,73 +236,87 @@ __global__ void __launch_bounds__(NWMAX * 32, 1) attn_dec_cl_kernel(AttnDecArgs 
         }
         __syncwarp();
       }
-      // ---- S^T[heads x 32 positions] = q . K^T ----
-      float sc[4][2];
+      // ---- S[32 positions x 8 heads] = K . q^T (A = K rows, B = q hi / lo) ----
+      float sc[2][4];
 #pragma unroll
-      for (int nt = 0; nt < 4; ++nt) sc[nt][0] = sc[nt][1] = 0.f;
+      for (int mt = 0; mt < 2; ++mt) sc[mt][0] = sc[mt][1] = sc[mt][2] = sc[mt][3] = 0.f;
 #pragma unroll
       for (int ks = 0; ks < HD / 16; ++ks) {
-        // q A fragments of row g8 (rows g8 + 8 are padding)
         const uint32_t h0 = *reinterpret_cast<const uint32_t*>(&Qh[g8][ks * 16 + 2 * t4]);
-        const uint32_t h2 = *reinterpret_cast<const uint32_t*>(&Qh[g8][ks * 16 + 8 + 2 * t4]);
+        const uint32_t h1 = *reinterpret_cast<const uint32_t*>(&Qh[g8][ks * 16 + 8 + 2 * t4]);
         const uint32_t l0 = *reinterpret_cast<const uint32_t*>(&Ql[g8][ks * 16 + 2 * t4]);
-        const uint32_t l2 = *reinterpret_cast<const uint32_t*>(&Ql[g8][ks * 16 + 8 + 2 * t4]);
+        const uint32_t l1 = *reinterpret_cast<const uint32_t*>(&Ql[g8][ks * 16 + 8 + 2 * t4]);
 #pragma unroll
-        for (int np = 0; np < 2; ++np) {
-          uint32_t kb[4];
+        for (int mt = 0; mt < 2; ++mt) {
+          uint32_t ka[4];
           const int m = lane >> 3;
-          ldsm4(kb, &Kw[np * 16 + (m >> 1) * 8 + (lane & 7)][ks * 16 + (m & 1) * 8]);
-          mma_top(sc[2 * np], z, h0, h2, kb[0], kb[1]);
-          mma_top(sc[2 * np], z, l0, l2, kb[0], kb[1]);
-          mma_top(sc[2 * np + 1], z, h0, h2, kb[2], kb[3]);
-          mma_top(sc[2 * np + 1], z, l0, l2, kb[2], kb[3]);
+          ldsm4(ka, &Kw[mt * 16 + (m & 1) * 8 + (lane & 7)][ks * 16 + (m >> 1) * 8]);
+          mma16816(sc[mt], ka, h0, h1);
+          mma16816(sc[mt], ka, l0, l1);
         }
       }
-      // ---- online softmax per head (row g8): positions p0 + nt*8 + 2*t4 + j ----
-      float tmax = -INFINITY;
+      // ---- online softmax per head: sc[mt][j] = (position mt*16 + g8 + 8*(j>>1), head 2*t4 + (j&1))
+      float tmA = -INFINITY, tmB = -INFINITY;
 #pragma unroll
-      for (int nt = 0; nt < 4; ++nt)
+      for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          const int pos = p0 + nt * 8 + 2 * t4 + j;
-          float v = sc[nt][j] * qscale;
-          if (a.family == kBloom) v = fmaf(slope_l2, (float)(pos - a.t0), v);
+        for (int j = 0; j < 4; ++j) {
+          const int pos = p0 + mt * 16 + g8 + 8 * (j >> 1);
+          float v = sc[mt][j] * qscale;
+          if (a.family == kBloom) v = fmaf((j & 1) ? slB : slA, (float)(pos - a.t0), v);
           if (pos >= T) v = -INFINITY;
-          sc[nt][j] = v;
-          tmax = fmaxf(tmax, v);
+          sc[mt][j] = v;
+          if (j & 1) tmB = fmaxf(tmB, v); else tmA = fmaxf(tmA, v);
         }
-      tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 1));
-      tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 2));
-      const float mnew = fmaxf(m_run, tmax);
-      const float alpha = (m_run == -INFINITY) ? 0.f : ex2_approx(m_run - mnew);
-      float psum = 0.f;
-      uint32_t ph[2][2], pl[2][2];                 // [k-step][a0 | a2] of row g8
 #pragma unroll
-      for (int nt = 0; nt < 4; ++nt) {
-        const float p0v = sc[nt][0] == -INFINITY ? 0.f : ex2_approx(sc[nt][0] - mnew);
-        const float p1v = sc[nt][1] == -INFINITY ? 0.f : ex2_approx(sc[nt][1] - mnew);
-        psum += p0v + p1v;
-        // C layout of two n-tiles == A layout of one k16 step (a0: n-tile 2kk, a2: 2kk + 1)
-        split2(p0v, p1v, ph[nt >> 1][nt & 1], pl[nt >> 1][nt & 1]);
+      for (int sh = 4; sh <= 16; sh <<= 1) {
+        tmA = fmaxf(tmA, __shfl_xor_sync(0xffffffffu, tmA, sh));
+        tmB = fmaxf(tmB, __shfl_xor_sync(0xffffffffu, tmB, sh));
       }
-      psum += __shfl_xor_sync(0xffffffffu, psum, 1);
-      psum += __shfl_xor_sync(0xffffffffu, psum, 2);
-      l_run = l_run * alpha + psum;
-      m_run = mnew;
+      const float mnA = fmaxf(m_run[0], tmA), mnB = fmaxf(m_run[1], tmB);
+      const float alA = (m_run[0] == -INFINITY) ? 0.f : ex2_approx(m_run[0] - mnA);
+      const float alB = (m_run[1] == -INFINITY) ? 0.f : ex2_approx(m_run[1] - mnB);
+      float psA = 0.f, psB = 0.f;
+      // P^T B fragments (k = positions, n = heads): the S accumulator holds (position g8,
+      // heads 2t4..) pairs; movmatrix.trans turns each 8 x 8 block into (head g8,
+      // positions 2t4..) pairs = the B fragment of the next MMA
+      uint32_t bh[2][2], bl[2][2];
 #pragma unroll
-      for (int i = 0; i < HD / 8; ++i) { o[i][0] *= alpha; o[i][1] *= alpha; }
-      // ---- O[heads x HD] += P . V ----
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {       // positions g8 (hh = 0) or g8 + 8
+          const float pa = ex2_approx(sc[mt][2 * hh] - mnA);       // -inf -> +0
+          const float pb = ex2_approx(sc[mt][2 * hh + 1] - mnB);
+          psA += pa;
+          psB += pb;
+          uint32_t hi, lo;
+          split2(pa, pb, hi, lo);
+          bh[mt][hh] = movm_trans(hi);
+          bl[mt][hh] = movm_trans(lo);
+        }
+#pragma unroll
+      for (int sh = 4; sh <= 16; sh <<= 1) {
+        psA += __shfl_xor_sync(0xffffffffu, psA, sh);
+        psB += __shfl_xor_sync(0xffffffffu, psB, sh);
+      }
+      l_run[0] = l_run[0] * alA + psA;
+      l_run[1] = l_run[1] * alB + psB;
+      m_run[0] = mnA;
+      m_run[1] = mnB;
+#pragma unroll
+      for (int i = 0; i < HD / 16; ++i) {
+        o[i][0] *= alA; o[i][1] *= alB; o[i][2] *= alA; o[i][3] *= alB;
+      }
+      // ---- O^T[dims x heads] += V^T . P^T (A = V rows transposed by ldmatrix) ----
 #pragma unroll
       for (int kk = 0; kk < 2; ++kk) {
 #pragma unroll
-        for (int dp = 0; dp < HD / 16; ++dp) {
-          uint32_t vb[4];
+        for (int dt = 0; dt < HD / 16; ++dt) {
+          uint32_t va[4];
           const int m = lane >> 3;
-          ldsm4t(vb, &Vw[kk * 16 + (m & 1) * 8 + (lane & 7)][dp * 16 + (m >> 1) * 8]);
-          mma_top(o[2 * dp], z, ph[kk][0], ph[kk][1], vb[0], vb[1]);
-          mma_top(o[2 * dp], z, pl[kk][0], pl[kk][1], vb[0], vb[1]);
-          mma_top(o[2 * dp + 1], z, ph[kk][0], ph[kk][1], vb[2], vb[3]);
-          mma_top(o[2 * dp + 1], z, pl[kk][0], pl[kk][1], vb[2], vb[3]);
+          ldsm4t(va, &Vw[kk * 16 + (m >> 1) * 8 + (lane & 7)][dt * 16 + (m & 1) * 8]);
+          mma16816(o[dt], va, bh[kk][0], bh[kk][1]);
+          mma16816(o[dt], va, bl[kk][0], bl[kk][1]);
         }
       }
     }
@@ -308,11 +330,20 @@ __global__ void __launch_bounds__(NWMAX * 32, 1) attn_dec_cl_kernel(AttnDecArgs 
   // ---- warp partials -> shared (O over this warp's own K rows) ----
   float* Ow = reinterpret_cast<float*>(Kw);        // [GM][HD] f32 fits 32 K rows
   __syncwarp();
-  if (g8 < G) {
 #pragma unroll
-    for (int i = 0; i < HD / 8; ++i)
-      *reinterpret_cast<float2*>(Ow + g8 * HD + i * 8 + 2 * t4) = make_float2(o[i][0], o[i][1]);
-    if (t4 == 0) { mw[warp * GM + g8] = m_run; lw[warp * GM + g8] = l_run; }
+  for (int dt = 0; dt < HD / 16; ++dt) {
+    if (hA < G) {
+      Ow[hA * HD + dt * 16 + g8] = o[dt][0];
+      Ow[hA * HD + dt * 16 + g8 + 8] = o[dt][2];
+    }
+    if (hB < G) {
+      Ow[hB * HD + dt * 16 + g8] = o[dt][1];
+      Ow[hB * HD + dt * 16 + g8 + 8] = o[dt][3];
+    }
+  }
+  if (g8 == 0) {
+    if (hA < G) { mw[warp * GM + hA] = m_run[0]; lw[warp * GM + hA] = l_run[0]; }
+    if (hB < G) { mw[warp * GM + hB] = m_run[1]; lw[warp * GM + hB] = l_run[1]; }
   }
   __syncthreads();
   // ---- CTA merge over warps (fixed order): factors f_w = exp2(m_w - M) ----
