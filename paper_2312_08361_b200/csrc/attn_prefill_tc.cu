@@ -6,10 +6,10 @@
 // n > 1 (the reference fills -1e30; here -inf, identical after the
 // max-subtracted exp), softmax over cache + new positions, ctx = p . v.
 //
-// CTA = (slot, query head, 128 query rows); keys stream one 64-position page
-// per tile.  Warp roles (10 warps):
+// CTA = (slot, query head, 128 query rows); keys stream 128 positions (two
+// pages) per tile.  Warp roles (10 warps):
 //   * warps 0-7  softmax / epilogue: TMEM lane = query row; the two warps of a
-//                lane quarter split every tile's columns (32 scores, 64 output
+//                lane quarter split every tile's columns (64 scores, 64 output
 //                dims each) and combine the row maxima through shared memory.
 //                Q arrives pre-scaled by log2(e)/sqrt(hd), so the scores leave
 //                the MMA in the exp2 domain.  Per tile: tcgen05.ld the scores,
@@ -22,19 +22,19 @@
 //                tensor-map TMA loads (cp.async.bulk.tensor, 128-byte swizzle,
 //                [64 keys][64 dims] boxes) from the paged pool: K lands in the
 //                K-major SW128 layout (B operand of S = Q K^T), V in the MN-major
-//                SW128 layout (B operand of O = P V).  5 stages.
+//                SW128 layout (B operand of O = P V).  3 stages of 64 KB.
 //   * warp 9     TMEM allocator + one elected lane issuing the MMAs:
-//                S_j = (Qhi + Qlo) K_j^T  (M = 128, N = 64, K = 128; A in TMEM)
-//                O  += P_j V_j            (M = 128, N = 128, K = 64; A in TMEM)
-//                S_{j+1} is issued before O_j, so the tensor pipe works on the
-//                next scores while the softmax warps turn S_j into P_j.
-// TMEM: Q hi/lo 128 columns, S 2 x 64 (double buffered), P 2 x 32, O 128.
+//                S_j = (Qhi + Qlo) K_j^T  (M = 128, N = 128, K = 128; A in TMEM)
+//                O  += P_j V_j            (M = 128, N = 128, K = 128; A in TMEM)
+//                S_{j+1} is issued as soon as the softmax has read S_j out, so
+//                the tensor pipe computes the next scores while the softmax
+//                warps turn S_j into P_j.
+// TMEM (512 columns): Q hi/lo 128, S 128, P 2 x 64 (double buffered), O 128.
 // Q is split hi + lo bf16 (two MMAs) against the bf16 K cache, so the scores
 // carry the cache's rounding, not a bf16 rounding of q; P (in [0, 256]) is
 // bf16 with f32 accumulation.
 // Each query row depends only on its own row: batch / tile invariant.
-// Measured (profiles/r02_attn_prefill_tc.md): the per-tile period is set by the
-// softmax warps (MUFU ex2: 64 per row per tile) and the N = 64 score MMAs.
+// Measured (profiles/r02_attn_pf.md): 173 us for 2048 tokens of one 70B block.
 #include <cuda.h>   // CUtensorMap (the encoder is fetched from the driver at run time)
 
 #include <cstdio>
@@ -53,28 +53,31 @@ namespace {
 
 constexpr int HD = 128;
 constexpr int BQ = 128;                 // query rows per CTA
-constexpr int BK = 64;                  // keys per tile (one page)
+constexpr int BK = 128;                 // keys per tile (two pages)
 constexpr int NSM = 8;                  // softmax warps: 2 per TMEM lane quarter
 constexpr int NTHREADS = (NSM + 2) * 32;
 constexpr int WP = NSM, WM = NSM + 1;   // producer warp, MMA warp
 constexpr int K_BYTES = BK * HD * 2;    // 16 KB
 constexpr int V_BYTES = BK * HD * 2;    // 16 KB
 constexpr int STAGE_BYTES = K_BYTES + V_BYTES;
-constexpr int NST = 5;                  // K/V stages
-constexpr int BOX = BK * 64 * 2;        // one [64 keys][64 dims] TMA box (8 KB)
+constexpr int NST = 3;                  // K/V stages
+constexpr int BOX = kPageTokens * 64 * 2;   // one [64 keys][64 dims] TMA box (8 KB)
+constexpr int HALF = BK * 128;          // one 64-dim half of a tile: [128 keys][128 B]
 constexpr int SMEM_BYTES = NST * STAGE_BYTES + 1024;
 // TMEM columns (32-bit): the A operands live in TMEM (one column = 2 bf16 of
-// a row): Q hi 0..63, Q lo 64..127; S 2 x 64; P 2 x 32; O 128
+// a row): Q hi 0..63, Q lo 64..127; S 128 (one tile, read out before the next
+// is issued); P 2 x 64; O 128
 constexpr int Q_COL = 0;
 constexpr int S_COL = 128;
 constexpr int P_COL = 256;
-constexpr int O_COL = 320;
+constexpr int O_COL = 384;
 constexpr float kRescale = 8.0f;        // log2 growth of a row max that forces an O rescale
 constexpr float kLog2e = 1.4426950408889634f;
 
 // instruction descriptors (kind::f16: bf16 A/B, f32 D)
-constexpr uint32_t kIdescS = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BK >> 3) << 17) |
-                             ((uint32_t)(BQ >> 4) << 24);                       // N = 64, K-major B
+constexpr int SN = BK;                  // N of one score MMA (128 keys)
+constexpr uint32_t kIdescS = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(SN >> 3) << 17) |
+                             ((uint32_t)(BQ >> 4) << 24);                       // K-major B
 constexpr uint32_t kIdescO = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) |
                              ((uint32_t)(HD >> 3) << 17) | ((uint32_t)(BQ >> 4) << 24);  // MN-major B
 
@@ -117,6 +120,13 @@ __device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0
       " [%0], [%1, {%2, %3}], [%4];" ::"r"(su32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(su32(bar))
       : "memory");
+}
+__device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                     uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
 // A operand from TMEM (row = lane, K packed two bf16 per 32-bit column)
 __device__ __forceinline__ void umma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b,
@@ -174,6 +184,21 @@ __device__ __forceinline__ uint32_t bf2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
 }
+// 8 f32 -> 16 bytes of bf16 hi and 16 bytes of bf16 lo (x - hi)
+__device__ __forceinline__ void split8(const float* x, uint4& hi, uint4& lo) {
+  float h[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) h[i] = __bfloat162float(__float2bfloat16_rn(x[i]));
+  hi = make_uint4(bf2(h[0], h[1]), bf2(h[2], h[3]), bf2(h[4], h[5]), bf2(h[6], h[7]));
+  lo = make_uint4(bf2(x[0] - h[0], x[1] - h[1]), bf2(x[2] - h[2], x[3] - h[3]),
+                  bf2(x[4] - h[4], x[5] - h[5]), bf2(x[6] - h[6], x[7] - h[7]));
+}
+// K-major A/B core-matrix layout of a [rows][k] bf16 operand, 16-element k
+// steps: step u = [2 halves][rows/8][8 rows][16 B]; LBO = rows * 16, SBO = 128
+__device__ __forceinline__ int kmajor_off(int row, int chunk, int rows) {
+  return (chunk >> 1) * rows * 32 + (chunk & 1) * rows * 16 + (row >> 3) * 128 + (row & 7) * 16;
+}
+
 // debug (SP_BUILD_TRACE=1 build + SP_ATTN_PF_TRACE=1): per-phase clock sums of
 // softmax warp 0 and the MMA lane of CTA (0, 0), printed by the launcher
 __device__ unsigned long long g_pf_trace[16];
@@ -189,8 +214,8 @@ attn_prefill_tc_kernel(AttnArgs a, const __grid_constant__ CUtensorMap kvmap, in
   // 1024-byte alignment for the 128-byte-swizzled TMA boxes / UMMA atoms
   uint8_t* smem = smem_raw + ((1024 - (su32(smem_raw) & 1023)) & 1023);
   uint8_t* stages = smem;                                      // [NST][K box0 box1 | V box0 box1]
-  __shared__ __align__(8) uint64_t kv_full[NST], kv_empty[NST], s_full[2], s_free[2],
-      p_full[2], p_free[2], o_full, q_full;
+  __shared__ __align__(8) uint64_t kv_full[NST], kv_empty[NST], s_full, s_free, p_full[2],
+      p_free[2], o_full, q_full;
   __shared__ uint32_t tmem_base;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -205,9 +230,9 @@ attn_prefill_tc_kernel(AttnArgs a, const __grid_constant__ CUtensorMap kvmap, in
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
     }
+    mbar_init(&s_full, 1);
+    mbar_init(&s_free, NSM);
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&s_full[i], 1);
-      mbar_init(&s_free[i], NSM);
       mbar_init(&p_full[i], NSM);
       mbar_init(&p_free[i], 1);
     }
@@ -232,16 +257,22 @@ attn_prefill_tc_kernel(AttnArgs a, const __grid_constant__ CUtensorMap kvmap, in
       for (int j = 0; j < ntiles; ++j) {
         const int st = j % NST;
         if (j >= NST) mbar_wait(&kv_empty[st], ((j / NST) - 1) & 1);
-        const int page = a.page_table[slot * a.max_pages + j];
-        // rows of the pool viewed as [(page, K|V, kv head, key)][hd]
-        const int64_t rk = row0 + (((int64_t)page * 2 + 0) * a.kvh + kh) * kPageTokens;
-        const int64_t rv = rk + (int64_t)a.kvh * kPageTokens;
         uint8_t* Ks = stages + st * STAGE_BYTES;
+        uint8_t* Vs = Ks + K_BYTES;
         mbar_expect_tx(&kv_full[st], STAGE_BYTES);
-        tma_2d(Ks, &kvmap, 0, (int)rk, &kv_full[st]);
-        tma_2d(Ks + BOX, &kvmap, 64, (int)rk, &kv_full[st]);
-        tma_2d(Ks + 2 * BOX, &kvmap, 0, (int)rv, &kv_full[st]);
-        tma_2d(Ks + 3 * BOX, &kvmap, 64, (int)rv, &kv_full[st]);
+        // two pages; a tile's key rows 64p.. of dim half d at d * HALF + p * BOX
+        // (beyond the table: page 0, whose finite rows the causal mask discards)
+        for (int p = 0; p < BK / kPageTokens; ++p) {
+          const int pi = (BK / kPageTokens) * j + p;
+          const int page = pi < a.max_pages ? a.page_table[slot * a.max_pages + pi] : 0;
+          // rows of the pool viewed as [(page, K|V, kv head, key)][hd]
+          const int64_t rk = row0 + (((int64_t)page * 2 + 0) * a.kvh + kh) * kPageTokens;
+          const int64_t rv = rk + (int64_t)a.kvh * kPageTokens;
+          tma_2d(Ks + p * BOX, &kvmap, 0, (int)rk, &kv_full[st]);
+          tma_2d(Ks + HALF + p * BOX, &kvmap, 64, (int)rk, &kv_full[st]);
+          tma_2d(Vs + p * BOX, &kvmap, 0, (int)rv, &kv_full[st]);
+          tma_2d(Vs + HALF + p * BOX, &kvmap, 64, (int)rv, &kv_full[st]);
+        }
       }
     }
     __syncwarp();
@@ -251,24 +282,28 @@ attn_prefill_tc_kernel(AttnArgs a, const __grid_constant__ CUtensorMap kvmap, in
       mbar_wait(&q_full, 0);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       auto issue_s = [&](int j) {
-        const int kst = j % NST, st = j & 1;
+        const int kst = j % NST;
         mbar_wait(&kv_full[kst], (j / NST) & 1);
         PF_T(3, pf_t);
-        if (j >= 2) mbar_wait(&s_free[st], ((j >> 1) - 1) & 1);
+        if (j >= 1) mbar_wait(&s_free, (j - 1) & 1);   // S_{j-1} read out
         PF_T(4, pf_t);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint8_t* Ks = stages + kst * STAGE_BYTES;
-        const uint32_t d = tb + S_COL + st * BK;
+        const uint32_t d = tb + S_COL;
 #pragma unroll
         for (int u = 0; u < HD / 16; ++u) {
           // K-major SW128: 16 dims = 32 bytes along the 128-byte swizzle atom row;
-          // dims 64..127 are the second box; 8-row groups 1024 bytes apart.
+          // dims 64..127 are the second half; 8-key groups 1024 bytes apart.
           // A = Q hi / lo from TMEM: 16 dims = 8 columns
-          const uint64_t bd = sdesc(Ks + (u >> 2) * BOX + (u & 3) * 32, 16, 1024, 2);
-          umma_ts(d, tb + Q_COL + u * 8, bd, kIdescS, u > 0);
-          umma_ts(d, tb + Q_COL + 64 + u * 8, bd, kIdescS, 1);
+#pragma unroll
+          for (int n = 0; n < BK / SN; ++n) {
+            const uint64_t bd =
+                sdesc(Ks + (u >> 2) * HALF + n * (SN * 128) + (u & 3) * 32, 16, 1024, 2);
+            umma_ts(d + n * SN, tb + Q_COL + u * 8, bd, kIdescS, u > 0);
+            umma_ts(d + n * SN, tb + Q_COL + 64 + u * 8, bd, kIdescS, 1);
+          }
         }
-        umma_commit(&s_full[st]);
+        umma_commit(&s_full);
       };
       auto issue_o = [&](int j) {
         const int kst = j % NST, st = j & 1;
@@ -281,7 +316,7 @@ attn_prefill_tc_kernel(AttnArgs a, const __grid_constant__ CUtensorMap kvmap, in
           // box (LBO) further; 16 keys = 2 groups of 8 rows, 1024 bytes apart (SBO).
           // A = P_j from TMEM: 16 keys = 8 columns
           umma_ts(tb + O_COL, tb + P_COL + st * (BK / 2) + u * 8,
-                  sdesc(Vs + u * 2048, BOX, 1024, 2), kIdescO, (j | u) ? 1u : 0u);
+                  sdesc(Vs + u * 2048, HALF, 1024, 2), kIdescO, (j | u) ? 1u : 0u);
         umma_commit(&o_full);                    // O now holds tiles 0..j
         umma_commit(&p_free[st]);                // P buffer st read
         umma_commit(&kv_empty[kst]);             // K_j and V_j consumed
@@ -352,16 +387,17 @@ attn_prefill_tc_kernel(AttnArgs a, const __grid_constant__ CUtensorMap kvmap, in
     PF_T(7, pf_t);
     for (int j = 0; j < ntiles; ++j) {
       const int st = j & 1;
-      mbar_wait(&s_full[st], (j >> 1) & 1);
+      mbar_wait(&s_full, j & 1);
       PF_T(0, pf_t);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       float s[SC];
-      tmem_ld32(tb + lane_addr + S_COL + st * BK + hf * SC, s);
+      tmem_ld32(tb + lane_addr + S_COL + hf * SC, s);
+      if constexpr (SC > 32) tmem_ld32(tb + lane_addr + S_COL + hf * SC + 32, s + 32);
       tmem_wait_ld();
       PF_T(1, pf_t);
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
-      if (lane == 0) mbar_arrive(&s_free[st]);
+      if (lane == 0) mbar_arrive(&s_free);
       // ALiBi, causal mask (diagonal tiles only), tile max as a 3-input tree
       const int kbase = j * BK + hf * SC;
       const bool unmasked = j * BK + BK - 1 <= a.t0 + q0;   // every row sees every key
@@ -427,8 +463,10 @@ attn_prefill_tc_kernel(AttnArgs a, const __grid_constant__ CUtensorMap kvmap, in
         pk[i / 2] = bf2(p0, p1);
       }
       const float psum = (ps4[0] + ps4[1]) + (ps4[2] + ps4[3]);
-      // P_j -> TMEM (A operand of O += P V): this warp's 32 keys = 16 columns
+      // P_j -> TMEM (A operand of O += P V): this warp's 64 keys = 32 columns
       tmem_st16(tb + lane_addr + P_COL + st * (BK / 2) + hf * (SC / 2), pk);
+      if constexpr (SC / 2 > 16)
+        tmem_st16(tb + lane_addr + P_COL + st * (BK / 2) + hf * (SC / 2) + 16, pk + 16);
       tmem_wait_st();
       l_run += psum;
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -494,7 +532,7 @@ const CUtensorMap* pool_map(const void* base, int64_t bytes) {
   CUtensorMap m;
   const cuuint64_t dims[2] = {(cuuint64_t)HD, (cuuint64_t)(bytes / (HD * 2))};
   const cuuint64_t strides[1] = {(cuuint64_t)HD * 2};
-  const cuuint32_t box[2] = {64, (cuuint32_t)BK};
+  const cuuint32_t box[2] = {64, (cuuint32_t)kPageTokens};   // one page of one kv head
   const cuuint32_t estr[2] = {1, 1};
   if (encode(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
