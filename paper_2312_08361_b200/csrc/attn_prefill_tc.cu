@@ -121,13 +121,6 @@ __device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(su32(bar))
       : "memory");
 }
-__device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
-                                     uint32_t acc) {
-  asm volatile(
-      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
-      "l"(a), "l"(b), "r"(idesc), "r"(acc));
-}
 // A operand from TMEM (row = lane, K packed two bf16 per 32-bit column)
 __device__ __forceinline__ void umma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b,
                                         uint32_t idesc, uint32_t acc) {
@@ -184,21 +177,6 @@ __device__ __forceinline__ uint32_t bf2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
 }
-// 8 f32 -> 16 bytes of bf16 hi and 16 bytes of bf16 lo (x - hi)
-__device__ __forceinline__ void split8(const float* x, uint4& hi, uint4& lo) {
-  float h[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) h[i] = __bfloat162float(__float2bfloat16_rn(x[i]));
-  hi = make_uint4(bf2(h[0], h[1]), bf2(h[2], h[3]), bf2(h[4], h[5]), bf2(h[6], h[7]));
-  lo = make_uint4(bf2(x[0] - h[0], x[1] - h[1]), bf2(x[2] - h[2], x[3] - h[3]),
-                  bf2(x[4] - h[4], x[5] - h[5]), bf2(x[6] - h[6], x[7] - h[7]));
-}
-// K-major A/B core-matrix layout of a [rows][k] bf16 operand, 16-element k
-// steps: step u = [2 halves][rows/8][8 rows][16 B]; LBO = rows * 16, SBO = 128
-__device__ __forceinline__ int kmajor_off(int row, int chunk, int rows) {
-  return (chunk >> 1) * rows * 32 + (chunk & 1) * rows * 16 + (row >> 3) * 128 + (row & 7) * 16;
-}
-
 // debug (SP_BUILD_TRACE=1 build + SP_ATTN_PF_TRACE=1): per-phase clock sums of
 // softmax warp 0 and the MMA lane of CTA (0, 0), printed by the launcher
 __device__ unsigned long long g_pf_trace[16];
@@ -225,6 +203,16 @@ attn_prefill_tc_kernel(AttnArgs a, const __grid_constant__ CUtensorMap kvmap, in
   const int last_q = min(q0 + BQ, a.n_new) - 1;
   const int ntiles = (a.t0 + last_q + 1 + BK - 1) / BK;
 
+  // softmax warps: this row's 64 q values are loaded first of all, so their
+  // latency overlaps the barrier / TMEM set-up and the first K/V loads
+  float4 qv[16];
+  if (warp < NSM) {
+    const int row_ = (warp & 3) * 32 + lane;
+    const int qi_ = min(q0 + row_, a.n_new - 1);
+    const float* qsrc = a.qkv + (int64_t)(slot * a.n_new + qi_) * a.ldqkv + h * HD + (warp >> 2) * 64;
+#pragma unroll
+    for (int c = 0; c < 16; ++c) qv[c] = __ldcs(reinterpret_cast<const float4*>(qsrc + c * 4));
+  }
   if (threadIdx.x == 0) {
     for (int i = 0; i < NST; ++i) {
       mbar_init(&kv_full[i], 1);
@@ -343,7 +331,6 @@ attn_prefill_tc_kernel(AttnArgs a, const __grid_constant__ CUtensorMap kvmap, in
     __shared__ float red_l[BQ];
     const int quarter = warp & 3, hf = warp >> 2;
     const int row = quarter * 32 + lane;
-    const int qi = min(q0 + row, a.n_new - 1);            // rows past n_new: computed, not stored
     const int qpos = a.t0 + q0 + row;
     const uint32_t lane_addr = (uint32_t)(quarter * 32) << 16;
     auto pair_sync = [&]() {
@@ -354,10 +341,6 @@ attn_prefill_tc_kernel(AttnArgs a, const __grid_constant__ CUtensorMap kvmap, in
     // operand of S = Q K^T: row = lane, column c = dims 2c, 2c + 1)
     const float qscale = kLog2e / sqrtf((float)HD);
     {
-      const float* qsrc = a.qkv + (int64_t)(slot * a.n_new + qi) * a.ldqkv + h * HD + hf * 64;
-      float4 qv[16];
-#pragma unroll
-      for (int c = 0; c < 16; ++c) qv[c] = *reinterpret_cast<const float4*>(qsrc + c * 4);
       uint32_t hi[32], lo[32];
 #pragma unroll
       for (int c = 0; c < 16; ++c) {
