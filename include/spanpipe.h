@@ -152,6 +152,12 @@ int sp_head_read_embedding(sp_head* head, float* dst_host);
  * (RealClientEngine.logits, SP/client.py:104-105, used by beam search) */
 int sp_head_logits(sp_head* head, const float* rows_dev, int32_t n_rows, float* logits_dev,
                    void* stream);
+/* one beam-search selection step (beam_select, SP/model.py:470-491) on device
+ * logits [w, vocab]: float64 log-softmax per row, candidates scores[r] + logp,
+ * the k (<= 16) best ranked by score desc, parent asc, token asc; results to host */
+int sp_beam_select(const float* logits_dev, const double* scores_host, int32_t w, int32_t vocab,
+                   int32_t k, int32_t* parents_host, int32_t* tokens_host, double* new_scores_host,
+                   void* stream);
 
 /* ---- measurement ----------------------------------------------------------
  * With profiling on, every launch of the span schedule is bracketed by CUDA

@@ -32,7 +32,7 @@ EXPORTS = (
     "sp_span_forward", "sp_span_forward_stateless", "sp_fnv1a64",
     "sp_span_set_profiling", "sp_span_profile_read", "sp_kernel_launches",
     "sp_span_decode_gemv_only", "sp_head_create", "sp_head_destroy", "sp_head_embed",
-    "sp_head_greedy", "sp_head_read_embedding", "sp_span_set_option", "sp_span_block_backward", "sp_head_logits",
+    "sp_head_greedy", "sp_head_read_embedding", "sp_span_set_option", "sp_span_block_backward", "sp_head_logits", "sp_beam_select",
 )
 
 
@@ -100,6 +100,7 @@ def load() -> ctypes.CDLL:
         "sp_head_greedy": (I32, [P, P, P, P]),
         "sp_head_read_embedding": (I32, [P, P]),
         "sp_head_logits": (I32, [P, P, I32, P, P]),
+        "sp_beam_select": (I32, [P, P, I32, I32, I32, P, P, P, P]),
         "sp_span_set_option": (I32, [P, I32, I32]),
     }
     for name in EXPORTS:

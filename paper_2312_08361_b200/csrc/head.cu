@@ -86,6 +86,96 @@ __global__ void argmax_kernel(const float* logits, int vocab, int* out) {
   if (threadIdx.x == 0) *out = bi[0];
 }
 
+// ---- beam selection (SP/model.py:470-491) -----------------------------------
+// row log-sum-exp in float64 like the reference: z = logit - max, lse = log(sum exp z)
+__global__ void beam_lse_kernel(const float* logits, int vocab, double* mx, double* lse) {
+  __shared__ double red[1024];
+  const float* l = logits + (int64_t)blockIdx.x * vocab;
+  double m = -INFINITY;
+  for (int v = threadIdx.x; v < vocab; v += blockDim.x) m = fmax(m, (double)l[v]);
+  red[threadIdx.x] = m;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + s]);
+    __syncthreads();
+  }
+  m = red[0];
+  __syncthreads();
+  double acc = 0.0;
+  for (int v = threadIdx.x; v < vocab; v += blockDim.x) acc += exp((double)l[v] - m);
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {           // fixed-order tree
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) { mx[blockIdx.x] = m; lse[blockIdx.x] = log(red[0]); }
+}
+
+constexpr int KMAX = 16;
+struct Cand { double s; int i; };
+// ranking of SP/model.py:485-488: score descending, then (parent, token)
+// ascending = flat index ascending
+__device__ __forceinline__ bool better(const Cand& a, const Cand& b) {
+  return a.s > b.s || (a.s == b.s && a.i < b.i);
+}
+
+// one CTA: every thread keeps its own top-k, warps then the block merge them by
+// k rounds of a shuffle arg-best
+__global__ void __launch_bounds__(1024) beam_topk_kernel(const float* logits, const double* scores,
+                                                         const double* mx, const double* lse,
+                                                         int w, int vocab, int k, int* parents,
+                                                         int* tokens, double* out_scores) {
+  __shared__ Cand wl[32][KMAX];
+  Cand top[KMAX];
+#pragma unroll
+  for (int j = 0; j < KMAX; ++j) top[j] = Cand{-INFINITY, 0x7fffffff};
+  const int n = w * vocab;
+  for (int f = threadIdx.x; f < n; f += blockDim.x) {
+    const int r = f / vocab;
+    const double z = (double)logits[f] - mx[r];
+    const Cand c{scores[r] + (z - lse[r]), f};
+    if (!better(c, top[k - 1])) continue;
+    int j = k - 1;                                    // insertion into the sorted list
+    while (j > 0 && better(c, top[j - 1])) { top[j] = top[j - 1]; --j; }
+    top[j] = c;
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  auto warp_merge = [&](Cand* list, Cand* out) {     // list: this lane's sorted k; out: warp's k
+    int head = 0;
+    for (int j = 0; j < k; ++j) {
+      Cand c = head < k ? list[head] : Cand{-INFINITY, 0x7fffffff};
+      Cand b = c;
+      int who = lane;
+      for (int off = 16; off > 0; off >>= 1) {
+        const double os = __shfl_xor_sync(0xffffffffu, b.s, off);
+        const int oi = __shfl_xor_sync(0xffffffffu, b.i, off);
+        const int ow = __shfl_xor_sync(0xffffffffu, who, off);
+        if (better(Cand{os, oi}, b)) { b = Cand{os, oi}; who = ow; }
+      }
+      if (lane == who) ++head;
+      if (lane == 0) out[j] = b;
+    }
+  };
+  warp_merge(top, wl[warp]);
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = blockDim.x >> 5;
+    Cand mine[KMAX];
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j)
+      mine[j] = (lane < nw && j < k) ? wl[lane][j] : Cand{-INFINITY, 0x7fffffff};
+    __shared__ Cand fin[KMAX];
+    warp_merge(mine, fin);
+    __syncwarp();
+    if (lane < k) {
+      parents[lane] = fin[lane].i / vocab;
+      tokens[lane] = fin[lane].i % vocab;
+      out_scores[lane] = fin[lane].s;
+    }
+  }
+}
+
 }  // namespace
 }  // namespace sp
 
@@ -182,6 +272,37 @@ int sp_head_logits(sp_head* h, const float* rows_dev, int32_t n_rows, float* log
     sp::count_launch();
   }
   SP_CUDA_TRY(cudaGetLastError());
+  return SP_OK;
+}
+
+// SP/model.py:470-491 on the GPU: log-softmax of each row (float64), candidates
+// scores[r] + logp, the k best by (score desc, parent asc, token asc)
+int sp_beam_select(const float* logits_dev, const double* scores_host, int32_t w, int32_t vocab,
+                   int32_t k, int32_t* parents_host, int32_t* tokens_host, double* new_scores_host,
+                   void* stream) {
+  if (!logits_dev || !scores_host || w < 1 || vocab < 1 || k < 1 || k > sp::KMAX ||
+      (int64_t)w * vocab < k || (int64_t)w * vocab > (1ll << 31) - 1)
+    return SP_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  double* buf = nullptr;           // scores, mx, lse, out_scores
+  int* ibuf = nullptr;             // parents, tokens
+  SP_CUDA_TRY(cudaMallocAsync(&buf, (3 * (size_t)w + sp::KMAX) * sizeof(double), st));
+  SP_CUDA_TRY(cudaMallocAsync(&ibuf, 2 * sp::KMAX * sizeof(int), st));
+  SP_CUDA_TRY(cudaMemcpyAsync(buf, scores_host, w * sizeof(double), cudaMemcpyHostToDevice, st));
+  sp::beam_lse_kernel<<<w, 1024, 0, st>>>(logits_dev, vocab, buf + w, buf + 2 * w);
+  sp::beam_topk_kernel<<<1, 1024, 0, st>>>(logits_dev, buf, buf + w, buf + 2 * w, w, vocab, k,
+                                           ibuf, ibuf + sp::KMAX, buf + 3 * w);
+  sp::count_launch();
+  sp::count_launch();
+  SP_CUDA_TRY(cudaGetLastError());
+  SP_CUDA_TRY(cudaMemcpyAsync(parents_host, ibuf, k * sizeof(int), cudaMemcpyDeviceToHost, st));
+  SP_CUDA_TRY(cudaMemcpyAsync(tokens_host, ibuf + sp::KMAX, k * sizeof(int),
+                              cudaMemcpyDeviceToHost, st));
+  SP_CUDA_TRY(cudaMemcpyAsync(new_scores_host, buf + 3 * w, k * sizeof(double),
+                              cudaMemcpyDeviceToHost, st));
+  SP_CUDA_TRY(cudaFreeAsync(buf, st));
+  SP_CUDA_TRY(cudaFreeAsync(ibuf, st));
+  SP_CUDA_TRY(cudaStreamSynchronize(st));
   return SP_OK;
 }
 

@@ -85,6 +85,10 @@ class ClientHead:
             return self.pick_device(last[0])
         return sample_pick(self.logits_device(last)[0].cpu().numpy(), rng, top_k)
 
+    def beam_select_device(self, scores, logits_dev: torch.Tensor, k: int):
+        """`beam_select` (SP/model.py:470-491) on device logits [w, vocab]."""
+        return beam_select_device(scores, logits_dev, k)
+
     def embedding(self) -> np.ndarray:
         out = np.empty((self.config.vocab_size, self.config.hidden_dim), np.float32)
         _lib.check(self.lib.sp_head_read_embedding(self.handle, out.ctypes.data))
@@ -103,3 +107,30 @@ def sample_pick(logits: np.ndarray, rng: np.random.Generator, top_k: int | None 
     p = np.exp(z - z.max())
     p = p / p.sum()
     return int(np.searchsorted(np.cumsum(p), rng.random(), side="right"))
+
+
+def beam_select_device(scores, logits_dev: torch.Tensor, k: int):
+    """One beam-search selection step on the GPU (sp_beam_select): float64
+    log-softmax of each row, candidates scores[r] + logp, the k best ranked by
+    (score desc, parent asc, token asc) — SP/model.py:470-491.  Returns
+    (parents, tokens, new_scores) like the reference."""
+    lib = _lib.load()
+    lg = logits_dev.to(torch.float32).contiguous()
+    w, vocab = int(lg.shape[0]), int(lg.shape[1])
+    sc = np.ascontiguousarray(np.asarray(scores, dtype=np.float64).reshape(w))
+    par = np.zeros(k, np.int32)
+    tok = np.zeros(k, np.int32)
+    out = np.zeros(k, np.float64)
+    stream = torch.cuda.current_stream(lg.device).cuda_stream
+    with torch.cuda.device(lg.device):
+        _lib.check(lib.sp_beam_select(lg.data_ptr(), sc.ctypes.data, w, vocab, k, par.ctypes.data,
+                                      tok.ctypes.data, out.ctypes.data, stream))
+    return par.tolist(), tok.tolist(), out
+
+
+def beam_select(scores, all_logits, k: int, device: int = 0):
+    """Drop-in for the reference's `beam_select(scores, all_logits, k)` with host
+    logits (uploaded to the GPU first)."""
+    lg = torch.from_numpy(np.ascontiguousarray(all_logits, dtype=np.float32)).to(
+        torch.device("cuda", device))
+    return beam_select_device(scores, lg, k)

@@ -133,6 +133,45 @@ def test_dropin_beam_search_matches_reference_oracle(swarmpipe):
     assert res.counters.recoveries >= 1
 
 
+def test_gpu_beam_select_matches_reference(swarmpipe):
+    """§8f item 2: beam_select (SP/model.py:470-491) on the GPU — float64
+    log-softmax, candidate ranking by (score desc, parent asc, token asc) — gives
+    the reference's parents and tokens, scores to 1e-12, also with exact ties."""
+    from swarmpipe.model import beam_select as ref_select
+    from paper_2312_08361_b200.head import beam_select
+    rng = np.random.default_rng(3)
+    for w, vocab, k in ((1, 256, 4), (4, 32000, 4), (3, 1000, 16), (8, 250, 8)):
+        logits = (rng.standard_normal((w, vocab)) * 3).astype(np.float32)
+        scores = rng.standard_normal(w) * 2
+        p, t, s = beam_select(scores, logits, k)
+        rp, rt, rs = ref_select(scores, logits, k)
+        assert p == list(rp) and t == list(rt)
+        assert np.allclose(s, rs, rtol=0, atol=1e-12)
+    # ties: equal scores and repeated logits -> parent asc, then token asc
+    logits = np.tile(np.round(rng.standard_normal((1, 64)), 0).astype(np.float32), (4, 1))
+    scores = np.zeros(4)
+    p, t, s = beam_select(scores, logits, 12)
+    rp, rt, rs = ref_select(scores, logits, 12)
+    assert p == list(rp) and t == list(rt)
+
+
+def test_dropin_beam_search_with_gpu_beam_select(swarmpipe, monkeypatch):
+    """The reference's own SwarmClient.beam_generate with its selection step
+    swapped for the GPU one (and the GPU engine / head): hypotheses and scores of
+    the local beam oracle (T/test_beam.py:21-44)."""
+    import swarmpipe.client as rc
+    from swarmpipe.model import ModelConfig, reference_beam
+    from paper_2312_08361_b200.head import beam_select
+    from support.ref_swarm import build_gpu_swarm
+    cfg = ModelConfig(seed=1)
+    want = reference_beam(cfg, [4, 2], 20, k=4)        # the oracle, before the swap
+    monkeypatch.setattr(rc.M, "beam_select", beam_select)
+    res = build_gpu_swarm(swarmpipe, cfg, seed=0).client().beam_generate([4, 2], 20, k=4)
+    assert [h for h, _ in res.beams] == [h for h, _ in want]
+    for (_, sa), (_, sb) in zip(res.beams, want):
+        assert sa == pytest.approx(sb, abs=1e-4)
+
+
 @pytest.mark.parametrize("quantized", [False, True])
 def test_llama_int8_failover_greedy_tokens_match_oracle(swarmpipe, quantized):
     """The 70B kernel family (int8 weights, GQA, RoPE, SwiGLU, bf16 KV) at a small
