@@ -232,17 +232,33 @@ def self_launch(args) -> bool:
     if args.gpus <= 1 or "WORLD_SIZE" in os.environ or args.impl == "reference":
         return False
     import socket
-    with socket.socket() as sk:
-        sk.bind(("127.0.0.1", 0))
-        port = sk.getsockname()[1]
     env = dict(os.environ)
-    # NCCL's init lines (nRanks of every communicator) go to stdout with the JSON line
+    # NCCL's init lines (nRanks of every communicator) go to stdout ahead of the
+    # JSON line, which is printed last (NCCL's teardown lines are relayed first)
     env["NCCL_DEBUG"] = "INFO"
     env["NCCL_DEBUG_SUBSYS"] = "INIT"
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
-           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
-           f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
-    r = subprocess.run(cmd, env=env)
+    for _attempt in range(3):
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+               f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        r = subprocess.run(cmd, env=env, stdout=subprocess.PIPE, stderr=subprocess.PIPE,
+                           text=True)
+        if r.returncode != 0 and "EADDRINUSE" in r.stderr:
+            continue                                   # rendezvous port raced: new port
+        break
+    lines = r.stdout.splitlines()
+    result = [ln for ln in lines if ln.startswith('{"metric"') or ln.startswith('{"impl"')]
+    for ln in lines:
+        if ln not in result:
+            print(ln)
+    sys.stderr.write(r.stderr)
+    sys.stderr.flush()
+    for ln in result:
+        print(ln)
+    sys.stdout.flush()
     sys.exit(r.returncode)
 
 
@@ -470,6 +486,7 @@ def run_b200(args) -> None:
         e2e_t = torch.tensor([time.perf_counter() - t0], device=dev)
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
         e2e_s = float(e2e_t.item())
+        pipe.verify()          # every received hop passed its relay checksum (raises if not)
         e2e = {"value": args.steps * sessions / max(1, world) / e2e_s, "unit": UNIT,
                "h2d_bytes_per_step": 4 * B * d, "d2h_bytes_per_step": 4 * B * d,
                "note": "per tick: rank 0 H2D of one input row, last rank D2H of one output "
@@ -520,6 +537,10 @@ def run_b200(args) -> None:
                                    f"{world} GPU(s), {sessions} session(s) in flight",
                        "span_per_gpu": [start, end], "prefill_tokens": args.prefill,
                        "batch": B,
+                       "wire": ({"bytes_per_hop": pipe.wire_bytes_per_token,
+                                 "relay_checksum": pipe.check is not None,
+                                 "codec": "int8 codes + f32 scales per 64 (SP/quantize.py)"}
+                                if world > 1 else None),
                        "l2": f"inputs larger than L2 ({span.weight_bytes / 1e9:.1f} GB weights "
                              f"per GPU)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -27,6 +27,9 @@
  *                                T/test_server.py:173-178)
  *   sp_fnv1a64               <- fnv1a64 / RealServerEngine.blob_checksum
  *                                SP/wire.py:39-44, SP/server.py:141-142
+ *   sp_content_hash(_verify) <- the relay checksum stamp / check of BlockServer._step
+ *                                (SP/server.py:388-393, 413-426) for the device-resident
+ *                                span-to-span wire
  */
 #ifndef SPANPIPE_H_
 #define SPANPIPE_H_
@@ -190,6 +193,18 @@ int64_t sp_kernel_launches(void);
 /* FNV-1a 64 over host bytes — SP/wire.py:39-44 (relay checksums,
  * SP/server.py:141-142); host-side helper */
 uint64_t sp_fnv1a64(const uint8_t* data, int64_t n);
+
+/* Content hash of n bytes of DEVICE memory, computed in `stream` with no host
+ * synchronisation: H = (n + sum_i (w_i + 1) r^(i+1)) mod 2^61-1 over the
+ * little-endian u32 words w_i (zero-padded tail), r = 0x0A3B1C5D7E9F2468 mod p
+ * (definition: csrc/hash.cu; restatement: oracle/content_hash.py).
+ * sp_content_hash writes H to *hash_out (device).  sp_content_hash_verify
+ * compares H with *expect (device) and sets *mismatch (device int32) to 1 when
+ * they differ (sticky: never cleared) — the relay-checksum check of
+ * SP/server.py:388-393 done in the stream of the receiving span. */
+int sp_content_hash(const void* data, int64_t n, uint64_t* hash_out, void* stream);
+int sp_content_hash_verify(const void* data, int64_t n, const uint64_t* expect, int32_t* mismatch,
+                           void* stream);
 
 #ifdef __cplusplus
 }

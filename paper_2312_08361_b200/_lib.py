@@ -30,6 +30,7 @@ EXPORTS = (
     "sp_span_weight_bytes", "sp_span_free_pages", "sp_span_read_weight", "sp_kv_create",
     "sp_kv_destroy", "sp_kv_length", "sp_kv_width", "sp_kv_reorder", "sp_kv_read",
     "sp_span_forward", "sp_span_forward_stateless", "sp_fnv1a64",
+    "sp_content_hash", "sp_content_hash_verify",
     "sp_span_set_profiling", "sp_span_profile_read", "sp_kernel_launches",
     "sp_span_decode_gemv_only", "sp_head_create", "sp_head_destroy", "sp_head_embed",
     "sp_head_greedy", "sp_head_read_embedding", "sp_span_set_option", "sp_span_block_backward", "sp_head_logits", "sp_beam_select",
@@ -90,6 +91,8 @@ def load() -> ctypes.CDLL:
         "sp_span_forward_stateless": (I32, [P, I32, I32, P, P, P, I32, I32, P]),
         "sp_span_block_backward": (I32, [P, I32, P, P, P, I32, I32, P]),
         "sp_fnv1a64": (ctypes.c_uint64, [P, I64]),
+        "sp_content_hash": (I32, [P, I64, P, P]),
+        "sp_content_hash_verify": (I32, [P, I64, P, P, P]),
         "sp_span_set_profiling": (I32, [P, I32]),
         "sp_span_profile_read": (I32, [P, I32, P, P, P, P]),
         "sp_kernel_launches": (I64, []),

@@ -22,6 +22,9 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxe
 # code would otherwise sit in the hot kernels' instruction footprint
 if os.environ.get("SP_BUILD_TRACE") == "1":
     FLAGS = FLAGS + ["-DSP_DEV_TRACE=1"]
+    # separate library + objects (load with SP_LIB_PATH=.../libspanpipe_trace.so)
+    OUT = os.path.join(HERE, "libspanpipe_trace.so")
+    OBJ = os.path.join(HERE, "_obj_trace")
 
 
 def sources() -> list[str]:

@@ -1,0 +1,154 @@
+// Device-side content hash of wire payloads ("a
+// GPU-side content hash over int8 codes").  The reference hashes relayed
+// activations with FNV-1a 64 on the host (SP/wire.py:39-44, checked at
+// SP/server.py:388-393 and stamped at :413-426); FNV-1a is a strict byte chain
+// (no parallel decomposition), so the span-to-span wire of the NCCL pipeline
+// uses a polynomial hash instead, computed and verified on the GPU in the
+// stream, with no host round trip:
+//
+//   words  w_i = little-endian u32 of bytes [4i, 4i + 4) (zero-padded tail),
+//          m   = ceil(n / 4),  p = 2^61 - 1,  r = kRadix (below)
+//   H(b)   = ( n + sum_{i < m} (w_i + 1) * r^(i + 1) )  mod p
+//
+// Every term is independent, and the sum is exact modular arithmetic, so any
+// reduction order gives the same 61-bit value (deterministic, order-free):
+// thread t of T takes words t, t + T, ... with powers r^(t+1) * (r^T)^j.
+// Restated in oracle/content_hash.py (test infrastructure).  Distinct payloads
+// of one length collide with probability <= m / p (a polynomial of degree m).
+// HBM-bound: n bytes read once; one launch (last-block reduction).
+#include <cstdint>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace sp {
+
+namespace {
+
+constexpr uint64_t kP = (1ull << 61) - 1;
+constexpr uint64_t kRadix = 0x0A3B1C5D7E9F2468ull % kP;
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ uint64_t mulmod(uint64_t a, uint64_t b) {   // a, b < p
+  const uint64_t lo = a * b, hi = __umul64hi(a, b);                     // hi < 2^58
+  uint64_t s = (lo & kP) + (lo >> 61) + (hi << 3);                      // 2^64 = 8 (mod p)
+  s = (s & kP) + (s >> 61);
+  return s >= kP ? s - kP : s;
+}
+__device__ __forceinline__ uint64_t addmod(uint64_t a, uint64_t b) {
+  const uint64_t s = a + b;
+  return s >= kP ? s - kP : s;
+}
+__device__ uint64_t powmod(uint64_t b, uint64_t e) {
+  uint64_t r = 1;
+  while (e) {
+    if (e & 1) r = mulmod(r, b);
+    b = mulmod(b, b);
+    e >>= 1;
+  }
+  return r;
+}
+
+// partial sums per CTA; the last CTA to finish adds them in CTA order, adds n
+// and either stores the hash or compares it with *expect (sticky mismatch flag)
+__global__ void __launch_bounds__(kThreads) content_hash_kernel(
+    const uint8_t* __restrict__ data, int64_t n, uint64_t* part, unsigned* done, uint64_t* out,
+    const uint64_t* expect, int* mismatch) {
+  const int64_t m = (n + 3) / 4;
+  const int64_t T = (int64_t)gridDim.x * kThreads;
+  const int64_t t = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  const bool aligned = (reinterpret_cast<uintptr_t>(data) & 3) == 0;
+  uint64_t acc = 0;
+  if (t < m) {
+    uint64_t pw = powmod(kRadix, (uint64_t)t + 1);
+    const uint64_t step = powmod(kRadix, (uint64_t)T);
+    for (int64_t i = t; i < m; i += T) {
+      uint32_t w;
+      if (aligned && 4 * i + 4 <= n) {
+        w = __ldg(reinterpret_cast<const uint32_t*>(data) + i);
+      } else {
+        w = 0;
+        for (int k = 0; k < 4 && 4 * i + k < n; ++k) w |= (uint32_t)data[4 * i + k] << (8 * k);
+      }
+      acc = addmod(acc, mulmod((uint64_t)w + 1, pw));
+      pw = mulmod(pw, step);
+    }
+  }
+  // CTA sum (modular: any order gives the same value)
+  for (int o = 16; o > 0; o >>= 1) acc = addmod(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+  __shared__ uint64_t ws[kThreads / 32];
+  __shared__ bool last;
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t s = 0;
+    for (int w = 0; w < kThreads / 32; ++w) s = addmod(s, ws[w]);
+    part[blockIdx.x] = s;
+    __threadfence();
+    last = atomicAdd(done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    uint64_t h = (uint64_t)n % kP;
+    for (unsigned b = 0; b < gridDim.x; ++b) h = addmod(h, *((volatile uint64_t*)part + b));
+    if (mismatch) {
+      if (h != *expect) atomicOr(mismatch, 1);
+    } else {
+      *out = h;
+    }
+  }
+}
+
+int content_hash(const void* data, int64_t n, uint64_t* out, const uint64_t* expect,
+                 int* mismatch, cudaStream_t st) {
+  // run on the device that holds the result word (several GPUs per process)
+  cudaPointerAttributes pa{};
+  SP_CUDA_TRY(cudaPointerGetAttributes(&pa, out ? (const void*)out : (const void*)mismatch));
+  if (pa.type != cudaMemoryTypeDevice) {
+    sp_set_error(__FILE__, __LINE__, "content hash: result pointer is not device memory");
+    return SP_ERR_ARG;
+  }
+  DeviceGuard dg(pa.device);
+  const int64_t m = (n + 3) / 4;
+  // >= 8 words per thread, at most 4 CTAs per SM of a 148-SM B200
+  int64_t grid = (m + kThreads * 8 - 1) / (kThreads * 8);
+  if (grid < 1) grid = 1;
+  if (grid > 592) grid = 592;
+  void* ws = nullptr;
+  const size_t wbytes = (size_t)grid * 8 + 16;
+  SP_CUDA_TRY(cudaMallocAsync(&ws, wbytes, st));
+  unsigned* done = reinterpret_cast<unsigned*>(static_cast<uint8_t*>(ws) + grid * 8);
+  SP_CUDA_TRY(cudaMemsetAsync(done, 0, 4, st));
+  content_hash_kernel<<<(unsigned)grid, kThreads, 0, st>>>(
+      static_cast<const uint8_t*>(data), n, static_cast<uint64_t*>(ws), done, out, expect,
+      mismatch);
+  count_launch();
+  SP_CUDA_TRY(cudaGetLastError());
+  SP_CUDA_TRY(cudaFreeAsync(ws, st));
+  return SP_OK;
+}
+
+}  // namespace
+}  // namespace sp
+
+extern "C" {
+
+int sp_content_hash(const void* data, int64_t n, uint64_t* hash_out, void* stream) {
+  if (n < 0 || (n > 0 && !data) || !hash_out) {
+    sp_set_error(__FILE__, __LINE__, "sp_content_hash: bad arguments");
+    return SP_ERR_ARG;
+  }
+  return sp::content_hash(data, n, hash_out, nullptr, nullptr, (cudaStream_t)stream);
+}
+
+int sp_content_hash_verify(const void* data, int64_t n, const uint64_t* expect, int32_t* mismatch,
+                           void* stream) {
+  if (n < 0 || (n > 0 && !data) || !expect || !mismatch) {
+    sp_set_error(__FILE__, __LINE__, "sp_content_hash_verify: bad arguments");
+    return SP_ERR_ARG;
+  }
+  return sp::content_hash(data, n, nullptr, expect, mismatch, (cudaStream_t)stream);
+}
+
+}  // extern "C"

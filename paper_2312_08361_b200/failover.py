@@ -23,6 +23,12 @@ missing rank dead (ban, SP/client.py:346-347) and publishes the route of the
 tick.  p2p ops of a tick are posted only after its route is known, so no
 collective is ever held open on a dropped rank.
 
+Relay checksum (SP/server.py:388-393, 413-426): every coded wire (hop, relay
+copy, replayed history) carries a content hash of its codes + scales, stamped
+by the sender and verified by every receiver on the GPU (`relay.py`); a
+mismatch raises ProtocolError("desync: relay checksum mismatch") at the tick
+it is received.
+
 Failover (`_replace_failed_stage` + `_restore`, SP/client.py:340-384,
 SP/server.py:429-450): the client sends the spare, per session, the dropped
 span's whole input history — the coded rows it cached — and the spare replays
@@ -41,6 +47,7 @@ import torch
 
 from .blob import HiddenBlob
 from .placement import stage_intervals
+from .relay import WireCheck, split_wire, wire_layout
 
 
 class SwarmUnavailableError(RuntimeError):
@@ -74,16 +81,6 @@ class Membership:
         return self.dead
 
 
-def _wire_len(rows: int, d: int) -> int:
-    n = rows * d
-    return n + 4 * ((n + 63) // 64)
-
-
-def _split_wire(w: torch.Tensor, rows: int, d: int):
-    n = rows * d
-    return w[:n].view(torch.int8), w[n:].view(torch.float32)
-
-
 class FailoverRing:
     """Greedy generation of `n_sessions` sessions through an N-span ring with a
     spare rank.  `engine` = the span engine of this rank (`run_cached`,
@@ -92,7 +89,7 @@ class FailoverRing:
 
     def __init__(self, engine, head, cfg, rank: int, world: int, device: torch.device,
                  prefixes: list[list[int]], n_new: int, store=None, drop: tuple | None = None,
-                 detect_timeout_s: float = 2.0, store_prefix: str = "fo"):
+                 detect_timeout_s: float = 2.0, store_prefix: str = "fo", checksum=None):
         import torch.distributed as dist
         self.dist = dist
         if world < 3:
@@ -122,6 +119,11 @@ class FailoverRing:
         self.final_rows = {}                     # rank 0: session -> final f32 row
         self.replays: list[dict] = []
         self._span_of = None
+        # relay checksum: None = on for a CUDA device, False = off, or a checker
+        # object with stamp / verify / raise_if_mismatch (CPU tests)
+        if checksum is None:
+            checksum = WireCheck(device) if device.type == "cuda" else False
+        self.check = checksum or None
         self._bind_position()
 
     # -- schedule ---------------------------------------------------------------
@@ -137,6 +139,22 @@ class FailoverRing:
 
     def _rows(self, j: int) -> int:
         return self.P if j == 0 else 1
+
+    def _layout(self, rows: int):
+        return wire_layout(rows, self.d, self.check is not None)
+
+    def _new_wire(self, rows: int) -> torch.Tensor:
+        return torch.zeros(self._layout(rows)[2], dtype=torch.uint8, device=self.dev)
+
+    def _stamp(self, w: torch.Tensor, rows: int) -> None:
+        if self.check is not None:
+            payload, off, _ = self._layout(rows)
+            self.check.stamp(w, payload, off)
+
+    def _verify(self, w: torch.Tensor, rows: int) -> None:
+        if self.check is not None:
+            payload, off, _ = self._layout(rows)
+            self.check.verify(w, payload, off)
 
     @property
     def n_ticks(self) -> int:
@@ -158,15 +176,16 @@ class FailoverRing:
             toks = self.prefixes[s] if j == 0 else [self.tokens[s][-1]]
             blob = HiddenBlob.from_device(self.head.embed_device(toks))
         else:
-            c, sc = _split_wire(wire_in, rows, self.d)
+            c, sc = split_wire(wire_in, rows, self.d)
             blob = HiddenBlob(rows, self.d, dev_codes=c, dev_scales=sc)
         out = self.eng.run_cached(a, b, self.caches[s], blob, 1, rows, not last)
         if last:
             return out.dev[-1].contiguous()
-        w = torch.empty(_wire_len(rows, self.d), dtype=torch.uint8, device=self.dev)
-        n = rows * self.d
-        w[:n].view(torch.int8).copy_(out.dev_codes)
-        w[n:].view(torch.float32).copy_(out.dev_scales)
+        w = self._new_wire(rows)
+        c, sc = split_wire(w, rows, self.d)
+        c.copy_(out.dev_codes)
+        sc.copy_(out.dev_scales)
+        self._stamp(w, rows)
         return w
 
     def step(self, k: int) -> None:
@@ -200,8 +219,7 @@ class FailoverRing:
             w = self._work(self.pos - 1, k)
             if w is not None:
                 s, j = w
-                buf = torch.empty(_wire_len(self._rows(j), self.d), dtype=torch.uint8,
-                                  device=self.dev)
+                buf = self._new_wire(self._rows(j))
                 ops.append(dist.P2POp(dist.irecv, buf, self.pos2rank[self.pos - 1]))
                 recvs.append(("in", s, j, buf))
         if self.pos == 0:
@@ -215,13 +233,17 @@ class FailoverRing:
                 w = self._work(p, k)
                 if w is not None:
                     s, j = w
-                    buf = torch.empty(_wire_len(self._rows(j), self.d), dtype=torch.uint8,
-                                      device=self.dev)
+                    buf = self._new_wire(self._rows(j))
                     ops.append(dist.P2POp(dist.irecv, buf, self.pos2rank[p]))
                     recvs.append(("hist", s, j, buf, p + 1))
         if ops:
             for h in dist.batch_isend_irecv(ops):
                 h.wait()
+        for r in recvs:                               # relay checksums (in the stream)
+            if r[0] != "final":
+                self._verify(r[3], self._rows(r[2]))
+        if self.check is not None and any(r[0] != "final" for r in recvs):
+            self.check.raise_if_mismatch()
         for r in recvs:
             if r[0] == "in":
                 self.pending[(r[1], r[2])] = r[3]
@@ -257,11 +279,14 @@ class FailoverRing:
                 if not msgs:
                     continue
                 rows = [self._rows(j) for j in range(len(msgs))]
-                codes = torch.cat([_split_wire(m, r, self.d)[0] for m, r in zip(msgs, rows)])
-                scales = torch.cat([_split_wire(m, r, self.d)[1] for m, r in zip(msgs, rows)])
-                for h in dist.batch_isend_irecv(
-                        [dist.P2POp(dist.isend, codes.view(torch.uint8).contiguous(), self.spare),
-                         dist.P2POp(dist.isend, scales.contiguous(), self.spare)]):
+                # the history as ONE wire of sum(rows) rows (codes, scales, hash)
+                n_rows = sum(rows)
+                hw = self._new_wire(n_rows)
+                hc, hs = split_wire(hw, n_rows, self.d)
+                torch.cat([split_wire(m, r, self.d)[0] for m, r in zip(msgs, rows)], out=hc)
+                torch.cat([split_wire(m, r, self.d)[1] for m, r in zip(msgs, rows)], out=hs)
+                self._stamp(hw, n_rows)
+                for h in dist.batch_isend_irecv([dist.P2POp(dist.isend, hw, self.spare)]):
                     h.wait()
             self.replays.append({"position": pos, "tick": k,
                                  "sessions": sum(1 for c in counts if c),
@@ -276,22 +301,21 @@ class FailoverRing:
                     continue
                 rows = [self._rows(j) for j in range(counts[s])]
                 n_rows = sum(rows)
-                codes = torch.empty(n_rows * self.d, dtype=torch.uint8, device=self.dev)
-                scales = torch.empty((n_rows * self.d + 63) // 64, dtype=torch.float32,
-                                     device=self.dev)
-                for h in dist.batch_isend_irecv([dist.P2POp(dist.irecv, codes, 0),
-                                                  dist.P2POp(dist.irecv, scales, 0)]):
+                hw = self._new_wire(n_rows)
+                for h in dist.batch_isend_irecv([dist.P2POp(dist.irecv, hw, 0)]):
                     h.wait()
-                codes = codes.view(torch.int8)
+                self._verify(hw, n_rows)
+                if self.check is not None:
+                    self.check.raise_if_mismatch()
+                codes, scales = split_wire(hw, n_rows, self.d)
                 done = n_rows
                 if pend is not None and pend[0] == s:     # resumed step runs normally
                     r_last = rows[-1]
                     done = n_rows - r_last
-                    w = torch.empty(_wire_len(r_last, self.d), dtype=torch.uint8,
-                                    device=self.dev)
-                    w[:r_last * self.d].view(torch.int8).copy_(codes[done * self.d:])
-                    w[r_last * self.d:].view(torch.float32).copy_(
-                        scales[done * self.d // 64:])
+                    w = self._new_wire(r_last)
+                    wc, ws = split_wire(w, r_last, self.d)
+                    wc.copy_(codes[done * self.d:])
+                    ws.copy_(scales[done * self.d // 64:])
                     self.pending[(s, pend[1])] = w
                 if done:
                     blob = HiddenBlob(done, self.d, dev_codes=codes[:done * self.d],

@@ -10,6 +10,11 @@ to rank 0 (the client side: only stage->stage boundaries are coded,
 Each tick ends with ONE grouped p2p (send this tick's output, receive next
 tick's input), so the ring never deadlocks and the host never blocks.
 With N == 1 this degenerates to plain autoregressive stepping of one session.
+
+Relay checksum (SP/server.py:388-393, 413-426): every coded hop carries a
+content hash of its codes + scales (`relay.py`), stamped by the sender and
+verified by the receiver on the GPU before its span consumes the input; a
+mismatch is raised by `verify()` (or at the next tick with `strict=True`).
 """
 
 from __future__ import annotations
@@ -17,11 +22,13 @@ from __future__ import annotations
 import torch
 
 from . import _lib
+from .relay import WireCheck, wire_layout
 
 
 class SpanPipeline:
     def __init__(self, engine, start: int, end: int, caches: list, rank: int, world: int, d: int,
-                 device: torch.device, seed: int = 7, width: int = 1):
+                 device: torch.device, seed: int = 7, width: int = 1, checksum=None,
+                 strict: bool = False):
         self.eng, self.lib = engine, getattr(engine, "lib", None)
         self.start, self.end = start, end
         self.caches = caches
@@ -35,12 +42,19 @@ class SpanPipeline:
         self.init_rows = torch.randn(max(1, world), w, d, device=device, generator=g)
         self.y = torch.empty(w, d, device=device)
         self.ring_in = torch.empty(w, d, device=device)            # rank 0: from the last rank
-        self.out_wire = torch.empty(n + 4 * n_sc, dtype=torch.uint8, device=device)
-        self.in_wire = torch.empty(n + 4 * n_sc, dtype=torch.uint8, device=device)
+        # relay checksum: None = on for a CUDA device, False = off, or a checker
+        # object with stamp / verify / raise_if_mismatch (CPU tests)
+        if checksum is None:
+            checksum = WireCheck(device) if device.type == "cuda" and world > 1 else False
+        self.check = checksum or None
+        self.strict = strict
+        self.payload, self.hash_off, total = wire_layout(w, d, self.check is not None)
+        self.out_wire = torch.zeros(total, dtype=torch.uint8, device=device)
+        self.in_wire = torch.zeros(total, dtype=torch.uint8, device=device)
         self.out_codes = self.out_wire[:n].view(torch.int8)
-        self.out_scales = self.out_wire[n:].view(torch.float32)
+        self.out_scales = self.out_wire[n:n + 4 * n_sc].view(torch.float32)
         self.in_codes = self.in_wire[:n].view(torch.int8)
-        self.in_scales = self.in_wire[n:].view(torch.float32)
+        self.in_scales = self.in_wire[n:n + 4 * n_sc].view(torch.float32)
         if world == 1:
             self.y.copy_(self.init_rows[0])
 
@@ -73,7 +87,11 @@ class SpanPipeline:
                 x = self.init_rows[s] if k < N else self.ring_in
                 self._forward(s, x, False, True)
             else:
+                if self.check is not None and self.strict:
+                    self.check.raise_if_mismatch()
                 self._forward(s, None, True, not last)
+            if not last:
+                self._stamp()
         ops = []
         if active:
             if last:
@@ -88,7 +106,22 @@ class SpanPipeline:
         if ops:
             for w in dist.batch_isend_irecv(ops):
                 w.wait()
+        if r > 0 and k >= r - 1:
+            self._verify_in()
         self.k += 1
+
+    def _stamp(self) -> None:
+        if self.check is not None:
+            self.check.stamp(self.out_wire, self.payload, self.hash_off)
+
+    def _verify_in(self) -> None:
+        if self.check is not None:
+            self.check.verify(self.in_wire, self.payload, self.hash_off)
+
+    def verify(self) -> None:
+        """Raise ProtocolError if any received hop failed its relay checksum."""
+        if self.check is not None:
+            self.check.raise_if_mismatch()
 
     def step_api(self, host_rows) -> None:
         """One tick through the public engine API (`run_cached`): rank 0 takes its
@@ -114,6 +147,7 @@ class SpanPipeline:
             else:
                 self.out_codes.copy_(out.dev_codes)
                 self.out_scales.copy_(out.dev_scales)
+                self._stamp()
         import torch.distributed as dist
         ops = []
         if active:
@@ -127,6 +161,8 @@ class SpanPipeline:
         if ops:
             for w in dist.batch_isend_irecv(ops):
                 w.wait()
+        if r > 0 and k >= r - 1:
+            self._verify_in()
         self.k += 1
 
     @property

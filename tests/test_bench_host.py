@@ -11,14 +11,15 @@ import pytest
 from conftest import ROOT
 
 
-def test_self_launch_builds_torchrun_command(monkeypatch):
+def test_self_launch_builds_torchrun_command(monkeypatch, capsys):
     sys.path.insert(0, ROOT)
     import bench
     seen = {}
 
-    def fake_run(cmd, env=None):
+    def fake_run(cmd, env=None, **kw):
         seen["cmd"], seen["env"] = cmd, env
-        return subprocess.CompletedProcess(cmd, 0)
+        out = "NCCL INFO comm 0x1 rank 0 nranks 4\n{\"metric\": \"m\"}\nNCCL INFO Destroy COMPLETE\n"
+        return subprocess.CompletedProcess(cmd, 0, stdout=out, stderr="")
 
     monkeypatch.setattr(subprocess, "run", fake_run)
     monkeypatch.delenv("WORLD_SIZE", raising=False)
@@ -27,6 +28,9 @@ def test_self_launch_builds_torchrun_command(monkeypatch):
     with pytest.raises(SystemExit) as e:
         bench.self_launch(args)
     assert e.value.code == 0
+    # the JSON line is relayed last, after NCCL's init / teardown lines
+    out = capsys.readouterr().out.splitlines()
+    assert out[-1] == '{"metric": "m"}' and out[0].startswith("NCCL INFO")
     cmd = seen["cmd"]
     assert cmd[1:3] == ["-m", "torch.distributed.run"]
     assert "--nproc-per-node=4" in cmd and "--master-addr=127.0.0.1" in cmd

@@ -26,7 +26,9 @@ from oracle import codec as oc
 from oracle import model as om
 from paper_2312_08361_b200.blob import HiddenBlob
 from paper_2312_08361_b200.config import toy
+from paper_2312_08361_b200.errors import ProtocolError
 from paper_2312_08361_b200.placement import stage_intervals
+from support.wirecheck import OracleWireCheck
 
 P, T = 3, 10
 
@@ -72,7 +74,7 @@ def _prefixes(n, vocab):
     return [[int(t) for t in rng.integers(0, vocab, P)] for _ in range(n)]
 
 
-def _worker(rank, world, port, out_dir, drop):
+def _worker(rank, world, port, out_dir, drop, corrupt=None):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -82,13 +84,19 @@ def _worker(rank, world, port, out_dir, drop):
         eng = OracleSpanEngine(cfg)
         head = OracleHead(cfg) if rank == 0 else None
         res = {}
-        for tag, dr in (("clean", None), ("fail", drop)):
+        runs = (("clean", None), ("fail", drop)) if corrupt is None else (("corrupt", None),)
+        for tag, dr in runs:
+            chk = OracleWireCheck(corrupt[1:] if corrupt and corrupt[0] == rank else ())
             ring = FailoverRing(eng, head, cfg, rank, world, torch.device("cpu"),
                                 _prefixes(world - 1, cfg.vocab_size), T, drop=dr,
-                                detect_timeout_s=1.0, store_prefix=tag)
-            toks = ring.run()
-            res[tag] = (toks, ring.replays)
-            dist.barrier()
+                                detect_timeout_s=1.0, store_prefix=tag, checksum=chk)
+            try:
+                toks = ring.run()
+            except ProtocolError as e:
+                toks = str(e)
+            res[tag] = (toks, ring.replays, chk.stamped, chk.verified)
+            if corrupt is None:
+                dist.barrier()
         np.save(os.path.join(out_dir, f"r{rank}.npy"), np.array(res, dtype=object),
                 allow_pickle=True)
     finally:
@@ -125,8 +133,8 @@ def test_failover_ring_tokens_equal_clean_run_and_oracle(tmp_path, world, drop):
     mp.spawn(_worker, args=(world, _free_port(), str(tmp_path), drop), nprocs=world, join=True)
     cfg = toy(seed=1)
     res = [np.load(tmp_path / f"r{r}.npy", allow_pickle=True).item() for r in range(world)]
-    clean, _ = res[0]["clean"]
-    failed, client_replays = res[0]["fail"]
+    clean = res[0]["clean"][0]
+    failed, client_replays = res[0]["fail"][:2]
     prefixes = _prefixes(world - 1, cfg.vocab_size)
     for s, p in enumerate(prefixes):
         want = _oracle_tokens(cfg, p, world - 1)
@@ -139,3 +147,20 @@ def test_failover_ring_tokens_equal_clean_run_and_oracle(tmp_path, world, drop):
     assert client_replays[0]["position"] == pos and spare[0]["position"] == pos
     assert spare[0]["rows"] == client_replays[0]["rows"] and sum(spare[0]["rows"]) > 0
     assert res[world - 1]["clean"][1] == []              # the spare idles without a failure
+    # relay checksums: hops, relay copies and the replayed history all verified
+    assert all(res[r]["fail"][2] > 0 for r in range(world - 2))      # coded senders
+    assert all(res[r]["fail"][3] > 0 for r in range(1, world))       # receivers + spare
+
+
+def test_failover_ring_refuses_corrupted_hop(tmp_path):
+    """A byte flipped on the client span's second coded hop (after its stamp):
+    the next span refuses it at that tick with the reference's desync error
+    (SP/server.py:388-393) and leaves the ring; the client then treats it as
+    failed and the spare takes its position (the run completes)."""
+    world = 3
+    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path), None, (0, 1)), nprocs=world,
+             join=True)
+    res = [np.load(tmp_path / f"r{r}.npy", allow_pickle=True).item() for r in range(world)]
+    assert res[1]["corrupt"][0] == "desync: relay checksum mismatch"
+    assert isinstance(res[0]["corrupt"][0], list)            # the client finished
+    assert [r["position"] for r in res[0]["corrupt"][1]] == [1]   # ... after a failover

@@ -195,3 +195,17 @@ def test_nf4_format_properties():
     bound = (gap * np.repeat(q.astype(np.float32), 64, axis=1) * s[:, None]).T
     assert (np.abs(eff - w) <= bound * 1.0001 + 1e-12).all()
     assert list(om.CB7) == [-63, -44, -33, -25, -18, -12, -6, 0, 5, 10, 16, 21, 28, 35, 46, 63]
+
+
+def test_content_hash_restatement_forms_agree():
+    """oracle/content_hash.py: the power-sum form (the GPU's decomposition) equals
+    Horner's rule; length is part of the hash (zero padding is not a collision);
+    FNV-1a 64 restatement equals the reference vectors (SP/wire.py:39-44)."""
+    import os
+    from oracle.content_hash import content_hash, content_hash_horner, fnv1a64
+    for n in (0, 1, 3, 4, 5, 17, 64, 1000):
+        d = os.urandom(n)
+        assert content_hash(d) == content_hash_horner(d)
+    assert content_hash(b"\0") != content_hash(b"\0\0") != content_hash(b"")
+    assert fnv1a64(b"") == 0xCBF29CE484222325
+    assert fnv1a64(b"a") == 0xAF63DC4C8601EC8C

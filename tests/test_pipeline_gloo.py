@@ -8,7 +8,10 @@ runs over NCCL; only `_forward` is swapped.
 
 Pinned: every output row of the last stage equals a single-process run of the
 same session (span 0 -> codec round trip -> ... -> last span -> feedback), bit
-for bit, and each rank advances exactly the session the schedule names.
+for bit, and each rank advances exactly the session the schedule names.  Every
+coded hop carries the relay checksum (stamped by the sender, verified by the
+receiver — the plumbing of relay.WireCheck with the oracle hash); a corrupted
+hop is refused with the reference's "relay checksum mismatch" desync.
 """
 
 import os
@@ -24,17 +27,19 @@ from oracle import codec as oc
 from oracle import model as om
 from paper_2312_08361_b200.placement import stage_intervals
 from paper_2312_08361_b200.config import toy
+from paper_2312_08361_b200.errors import ProtocolError
 from paper_2312_08361_b200.pipeline import SpanPipeline
+from support.wirecheck import OracleWireCheck
 
 
 class OraclePipeline(SpanPipeline):
     """SpanPipeline whose span function is the CPU oracle (one SpanRunner per
     session = that session's KV caches on this rank)."""
 
-    def __init__(self, cfg, start, end, rank, world):
+    def __init__(self, cfg, start, end, rank, world, corrupt=()):
         runners = [om.SpanRunner(cfg, start, end, width=1) for _ in range(max(1, world))]
         super().__init__(None, start, end, runners, rank, world, cfg.hidden_dim,
-                         torch.device("cpu"))
+                         torch.device("cpu"), checksum=OracleWireCheck(corrupt))
         self.log = []          # (tick, session, y) of every forward on this rank
 
     def _forward(self, session, x, coded_input, quantize_out):
@@ -52,16 +57,25 @@ class OraclePipeline(SpanPipeline):
         self.log.append((self.k, session, y.copy()))
 
 
-def _worker(rank, world, ticks, port, out_dir):
+def _worker(rank, world, ticks, port, out_dir, corrupt=None):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         cfg = toy(seed=1)
         start, end = stage_intervals(cfg.n_blocks, world)[rank]
-        pipe = OraclePipeline(cfg, start, end, rank, world)
+        bad = corrupt[1:] if corrupt and corrupt[0] == rank else ()
+        pipe = OraclePipeline(cfg, start, end, rank, world, bad)
         for _ in range(ticks):
             pipe.step()
+        try:
+            pipe.verify()
+            verdict = "ok"
+        except ProtocolError as e:
+            verdict = str(e)
+        np.save(os.path.join(out_dir, f"check{rank}.npy"),
+                np.array([verdict, pipe.check.stamped, pipe.check.verified], dtype=object),
+                allow_pickle=True)
         np.save(os.path.join(out_dir, f"log{rank}.npy"),
                 np.array([(k, s, y) for k, s, y in pipe.log], dtype=object), allow_pickle=True)
         np.save(os.path.join(out_dir, f"init{rank}.npy"), pipe.init_rows.numpy())
@@ -106,6 +120,22 @@ def test_pipeline_matches_single_process(tmp_path, world):
                     h = oc.dequantize(codes, scales, (1, d))
             assert np.array_equal(g, h)
             x = h
+    # relay checksums: every coded hop stamped by its sender, verified by its receiver
+    checks = [np.load(tmp_path / f"check{r}.npy", allow_pickle=True) for r in range(world)]
+    assert all(c[0] == "ok" for c in checks)
+    for r in range(world - 1):
+        assert checks[r][1] == ticks - r and checks[r + 1][2] == ticks - r
+
+
+def test_pipeline_refuses_corrupted_hop(tmp_path):
+    """A byte flipped on rank 1's third coded hop (after the stamp) is detected by
+    rank 2 (SP/server.py:388-393: Error("desync", "relay checksum mismatch"));
+    every other receiver stays clean."""
+    world, ticks = 4, 9
+    mp.spawn(_worker, args=(world, ticks, _free_port(), str(tmp_path), (1, 2)), nprocs=world,
+             join=True)
+    checks = [np.load(tmp_path / f"check{r}.npy", allow_pickle=True) for r in range(world)]
+    assert [c[0] for c in checks] == ["ok", "ok", "desync: relay checksum mismatch", "ok"]
 
 
 @pytest.mark.parametrize("world", [2, 4, 8])
