@@ -219,6 +219,8 @@ class B200ServerEngine:
         # stateless forward chunk (tokens): see device_micro_batches
         self.stateless_tokens = min(2048, self.span.kv_pool_tokens // 2)
         self.last_forward_chunks = 0
+        self._staging = []            # pinned host slots for row uploads: [tensor, event]
+        self._stage_next = 0
         # block_backward exists for the reference's own family only (SP/model.py:320)
         c = self.config
         self.backward_defined = (c.family == "toy" and c.weight_dtype == "f32"
@@ -253,8 +255,31 @@ class B200ServerEngine:
             s = torch.from_numpy(np.ascontiguousarray(q.scales, np.float32)).to(self.device)
             return 0, c.data_ptr(), s.data_ptr(), (c, s)
         a = np.ascontiguousarray(blob.array(), dtype=np.float32).reshape(rows, d)
-        x = torch.from_numpy(a).to(self.device)
+        x = self._upload(a)
         return x.data_ptr(), 0, 0, (x,)
+
+    def _upload(self, a: np.ndarray) -> torch.Tensor:
+        """Host rows -> HBM without blocking the host on the stream: the rows are
+        copied into a pinned staging slot (a ring of 4; a slot is rewritten only
+        after its previous copy has completed) and moved by an asynchronous H2D
+        copy ordered in the span's stream (a pageable `.to(device)` would wait
+        for every kernel already queued — the previous step)."""
+        nb = a.nbytes
+        if len(self._staging) < 4:
+            self._staging.append([None, torch.cuda.Event()])
+        slot = self._staging[self._stage_next % len(self._staging)]
+        self._stage_next += 1
+        if slot[0] is None or slot[0].numel() < nb:
+            slot[1].synchronize()
+            slot[0] = torch.empty(max(nb, 1 << 16), dtype=torch.uint8, pin_memory=True)
+        else:
+            slot[1].synchronize()
+        host = slot[0][:nb].view(torch.float32).view(a.shape)
+        host.numpy()[...] = a
+        x = torch.empty(a.shape, dtype=torch.float32, device=self.device)
+        x.copy_(host, non_blocking=True)
+        slot[1].record(torch.cuda.current_stream(self.device))
+        return x
 
     def run_cached(self, start: int, end: int, caches: SpanCaches, blob, width: int, n_new: int,
                    quantized: bool) -> HiddenBlob:
