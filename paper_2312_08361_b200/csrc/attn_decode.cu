@@ -938,6 +938,7 @@ int launch_attn_decode_fused(const AttnDecArgs& a, cudaStream_t st) {
     count_launch();
     return a.H;
   }
+  if (attn_dec_mha_ok(a)) return launch_attn_decode_mha(a, st);
   if (g_attn_cl && attn_dec_cl_ok(a)) return launch_attn_decode_cl(a, st);
   const int G = a.H / a.kvh;
   if (a.kv_dtype == kKVBF16 && G <= 8 && (a.hd == 64 || a.hd == 128)) {

@@ -72,6 +72,9 @@ int launch_attn_decode_fused(const AttnDecArgs& a, cudaStream_t st);
 bool attn_dec_cl_ok(const AttnDecArgs& a);              // attn_decode_cl.cu
 int launch_attn_decode_cl(const AttnDecArgs& a, cudaStream_t st);
 extern bool g_attn_cl;                                  // option 7 (default on)
+bool attn_dec_mha_ok(const AttnDecArgs& a);             // attn_decode_mha.cu
+int launch_attn_decode_mha(const AttnDecArgs& a, cudaStream_t st);
+extern bool g_attn_mha;                                 // option 9 (default on)
 int64_t attn_dec_part_floats(int width, int H, int hd, int max_pages);
 
 }  // namespace sp

@@ -1151,6 +1151,7 @@ int sp_span_set_option(sp_span* s, int32_t option, int32_t value) {
   else if (option == 6) g_attn_cluster = value;
   else if (option == 7) g_attn_cl = value != 0;
   else if (option == 8) g_attn_tc = value != 0;
+  else if (option == 9) g_attn_mha = value != 0;
   else SP_FAIL(SP_ERR_ARG, "unknown option");
   return SP_OK;
 }

@@ -494,6 +494,63 @@ def test_decode_attention_cluster_kernel(name, t_pre):
         assert np.abs(outs[1][j] - outs[0][j]).max() <= 2e-3 * s
 
 
+@pytest.mark.parametrize("name,t_pre", [("bloom_int8", 70), ("bloom_int8", 450),
+                                         ("llama_bf16", 300), ("bloom_long", 2040),
+                                         ("bloom_long", 4100)])
+def test_decode_attention_mha_kernel(name, t_pre):
+    """Multi-head decode attention (one query head per kv head: attn_decode_mha.cu,
+    option 9) against the MMA / cluster kernels (option 9 off) and the oracle:
+    one chunk (T <= 512), 3 and 4 chunks merged by the last CTA, 1024-position
+    chunks past 4 K, ALiBi and RoPE, the new token's K/V append."""
+    from paper_2312_08361_b200 import _lib
+    cfg = SMALL[name] if name in SMALL else SMALL["bloom_int8"].with_(max_seq_len=4608, seed=12)
+    rng = np.random.default_rng(29)
+    d = cfg.hidden_dim
+    x = rng.standard_normal((t_pre + 3, d)).astype(np.float32)
+    outs = {}
+    eng = _engine(cfg)
+    try:
+        for v in (1, 0):
+            _lib.check(eng.lib.sp_span_set_option(eng.span.handle, 9, v))
+            c = eng.make_caches(0, cfg.n_blocks, 1)
+            eng.run_cached(0, cfg.n_blocks, c, _blob(x[:t_pre]), 1, t_pre, False)
+            outs[v] = [eng.run_cached(0, cfg.n_blocks, c, _blob(x[i:i + 1]), 1, 1,
+                                      False).array() for i in range(t_pre, t_pre + 3)]
+    finally:
+        _lib.check(eng.lib.sp_span_set_option(eng.span.handle, 9, 1))
+    runner = om.SpanRunner(cfg, 0, cfg.n_blocks)
+    runner.step(x[None, :t_pre])
+    for j, i in enumerate(range(t_pre, t_pre + 3)):
+        w = runner.step(x[None, i:i + 1])[0]
+        s = np.abs(w).max()
+        e_new, e_old = np.abs(outs[1][j] - w).max() / s, np.abs(outs[0][j] - w).max() / s
+        print(f"{name} T={i + 1}: mha kernel err {e_new:.2e}, mma kernel err {e_old:.2e} "
+              f"(max-abs / max|y|)")
+        assert e_new <= 2e-3
+        assert np.abs(outs[1][j] - outs[0][j]).max() <= 2e-3 * s
+
+
+def test_decode_attention_mha_batch_rows_independent():
+    """The batched MHA decode (many (row, head) pairs per step) gives every row
+    exactly what it gets stepped alone (width 8: the widest step whose linears
+    run on the decode GEMV; wider steps switch the linears to the tcgen05 GEMM)."""
+    cfg = SMALL["bloom_int8"]
+    eng = _engine(cfg)
+    rng = np.random.default_rng(41)
+    d = cfg.hidden_dim
+    x = rng.standard_normal((8, 400 + 2, d)).astype(np.float32)
+    cw = eng.make_caches(0, cfg.n_blocks, 8)
+    eng.run_cached(0, cfg.n_blocks, cw, _blob(x[:, :400].reshape(-1, d)), 8, 400, False)
+    outs = [eng.run_cached(0, cfg.n_blocks, cw, _blob(x[:, i]), 8, 1, False).array()
+            for i in (400, 401)]
+    for r in (0, 3, 7):
+        c1 = eng.make_caches(0, cfg.n_blocks, 1)
+        eng.run_cached(0, cfg.n_blocks, c1, _blob(x[r, :400]), 1, 400, False)
+        for j, i in enumerate((400, 401)):
+            one = eng.run_cached(0, cfg.n_blocks, c1, _blob(x[r, i:i + 1]), 1, 1, False).array()
+            assert np.array_equal(one[0], outs[j][r]), (r, i)
+
+
 @pytest.mark.parametrize("name", ["llama_g8", "llama_int8", "bloom_int8", "llama_bf16"])
 def test_prefill_attention_tcgen05(name):
     """Prefill / replay attention on tcgen05 + TMEM (attn_prefill_tc.cu, the
