@@ -177,9 +177,10 @@ int sp_span_set_profiling(sp_span* span, int32_t enable);
  * 6 = decode-attention cluster merge for 8 query heads per kv head
  * (-1 = global last-CTA merge, the default; 0 = auto; 8 or 16 = cluster size);
  * 7 = decode attention on the 8-CTA cluster kernel (default 1); 8 = prefill
- * attention on tcgen05 (default 1); 9 = batched multi-head decode attention
- * (one query head per kv head, >= one wave of (row, head) pairs; default 1).
- * Option 0 is per span; options 1-9 are kernel-selection switches shared by
+ * attention on tcgen05 (default 1); 9 = multi-head decode attention
+ * (one query head per kv head; default 1); 10 = wide decode (9..32 rows) GEMM
+ * with the weights as the MMA's A operand (default 1; 0 = the token-tile GEMM,
+ * bit-identical).  Option 0 is per span; options 1-10 are kernel-selection switches shared by
  * every span in the process (set them before concurrent use). */
 int sp_span_set_option(sp_span* span, int32_t option, int32_t value);
 int sp_span_profile_read(sp_span* span, int32_t n_classes, double* ms, double* bytes,

@@ -79,6 +79,15 @@ __host__ __device__ __forceinline__ int64_t cm_offset(int64_t n, int64_t kb, int
   return ((g * (Kbytes >> 5) + kt) * 2 + kc) * 2048 + r8 * 128 + rr * 16 + b;
 }
 
+// the same layout with rt-row tiles instead of 128 (rt a multiple of 8): the
+// wide-decode digit planes use rt = 16 / 32 so a tile's rows are contiguous
+__host__ __device__ __forceinline__ int64_t cm_offset_rt(int64_t n, int64_t kb, int64_t Kbytes,
+                                                         int rt) {
+  const int64_t g = n / rt, r8 = (n % rt) >> 3, rr = n & 7;
+  const int64_t kt = kb >> 5, kc = (kb & 31) >> 4, b = kb & 15;
+  return ((g * (Kbytes >> 5) + kt) * 2 + kc) * (int64_t)(rt * 16) + r8 * 128 + rr * 16 + b;
+}
+
 // NF4 weights (oracle/model.py quantize_columns_nf4): 4-bit codes in units of
 // 128 output channels x 64 k (4 KB, the same unit size as int8), stored in the
 // decode GEMV's mma.m16n8k32 A-fragment order so a lane's 16-byte load holds

@@ -127,6 +127,15 @@ __device__ __forceinline__ void tmem_ld32_nw(uint32_t taddr, int* v) {
         "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
       : "r"(taddr));
 }
+__device__ __forceinline__ void tmem_ld16_nw(uint32_t taddr, int* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
 __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
@@ -236,25 +245,57 @@ __device__ __forceinline__ void finish_tile(const TcGemmArgs& a, int mt, int ng0
   const int rows = (int)min((int64_t)BM, a.M - (int64_t)mt * BM);
   const bool swiglu = a.epi == EPI_SWIGLU;
   const int outs = swiglu ? 64 : 128;                // outputs per weight group
+  const int total = rows * NGRP * outs;
   long long* ws = a.ws;
-  for (int i = threadIdx.x; i < rows * NGRP * outs; i += blockDim.x) {
-    const int r = i / (NGRP * outs), rem = i % (NGRP * outs), j = rem / outs, c = rem % outs;
-    const int64_t m = (int64_t)mt * BM + r;
-    const float ys = ldexpf(1.0f, a.exps[m] - 14);
-    const int64_t n0 = (int64_t)(ng0 + j) * 128;
-    long long* wr = ws + m * a.N + n0;
-    if (swiglu) {
-      const float gd = __fmul_rn(__fmul_rn((float)__ldcg(wr + c), ys), __ldg(a.wscale + n0 + c));
-      const float ud = __fmul_rn(__fmul_rn((float)__ldcg(wr + 64 + c), ys), __ldg(a.wscale + n0 + 64 + c));
-      wr[c] = 0;
-      wr[64 + c] = 0;
-      a.y[m * a.ldy + (ng0 + j) * 64 + c] = __fmul_rn(__fdividef(gd, __fadd_rn(1.0f, __expf(-gd))), ud);
-    } else {
-      float v = __fmul_rn(__fmul_rn((float)__ldcg(wr + c), ys), __ldg(a.wscale + n0 + c));
-      wr[c] = 0;
-      if (a.epi == EPI_RESID) v = __fadd_rn(v, a.res[m * a.ldy + n0 + c]);
-      else if (a.epi == EPI_GELU) v = gelu_f(v);
-      a.y[m * a.ldy + n0 + c] = v;
+  // 8 outputs per thread per pass with every load issued before the first use
+  // (one L2 round trip per pass instead of one per output: this tail runs on
+  // the critical path of every split-K GEMM)
+  constexpr int U = 8;
+  for (int i0 = threadIdx.x; i0 < total; i0 += U * blockDim.x) {
+    long long g0[U], g1[U];
+    float wg[U], wu[U], rv[U], ys[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = i0 + u * blockDim.x;
+      g0[u] = g1[u] = 0;
+      wg[u] = wu[u] = rv[u] = 0.f;
+      ys[u] = 1.f;
+      if (i >= total) continue;
+      const int r = i / (NGRP * outs), rem = i % (NGRP * outs), j = rem / outs, c = rem % outs;
+      const int64_t m = (int64_t)mt * BM + r;
+      const int64_t n0 = (int64_t)(ng0 + j) * 128;
+      const long long* wr = ws + m * a.N + n0;
+      ys[u] = ldexpf(1.0f, a.exps[m] - 14);
+      g0[u] = __ldcg(wr + c);
+      wg[u] = __ldg(a.wscale + n0 + c);
+      if (swiglu) {
+        g1[u] = __ldcg(wr + 64 + c);
+        wu[u] = __ldg(a.wscale + n0 + 64 + c);
+      } else if (a.epi == EPI_RESID) {
+        rv[u] = a.res[m * a.ldy + n0 + c];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = i0 + u * blockDim.x;
+      if (i >= total) continue;
+      const int r = i / (NGRP * outs), rem = i % (NGRP * outs), j = rem / outs, c = rem % outs;
+      const int64_t m = (int64_t)mt * BM + r;
+      const int64_t n0 = (int64_t)(ng0 + j) * 128;
+      long long* wr = ws + m * a.N + n0;
+      if (swiglu) {
+        const float gd = __fmul_rn(__fmul_rn((float)g0[u], ys[u]), wg[u]);
+        const float ud = __fmul_rn(__fmul_rn((float)g1[u], ys[u]), wu[u]);
+        wr[c] = 0;
+        wr[64 + c] = 0;
+        a.y[m * a.ldy + (ng0 + j) * 64 + c] = __fmul_rn(__fdividef(gd, __fadd_rn(1.0f, __expf(-gd))), ud);
+      } else {
+        float v = __fmul_rn(__fmul_rn((float)g0[u], ys[u]), wg[u]);
+        wr[c] = 0;
+        if (a.epi == EPI_RESID) v = __fadd_rn(v, rv[u]);
+        else if (a.epi == EPI_GELU) v = gelu_f(v);
+        a.y[m * a.ldy + n0 + c] = v;
+      }
     }
   }
 }
@@ -558,7 +599,7 @@ __global__ void __launch_bounds__(256) digitize_kernel(const float* __restrict__
                                                        int64_t M, int64_t K, int norm,
                                                        const float* g, const float* b,
                                                        uint8_t* planes, int64_t plane_stride,
-                                                       int* exps) {
+                                                       int* exps, int rt) {
   __shared__ float sh[3][9];
   const int64_t m = blockIdx.x;
   const float* xr = x + m * ldx;
@@ -613,7 +654,7 @@ __global__ void __launch_bounds__(256) digitize_kernel(const float* __restrict__
       d1[i] = (int8_t)lo;
       d0[i] = (int8_t)((q - lo) >> 8);
     }
-    const int64_t off = cm_offset(m, k0, K);
+    const int64_t off = cm_offset_rt(m, k0, K, rt);
     *reinterpret_cast<uint4*>(planes + off) = *reinterpret_cast<uint4*>(d0);
     *reinterpret_cast<uint4*>(planes + plane_stride + off) = *reinterpret_cast<uint4*>(d1);
   }
@@ -628,7 +669,7 @@ __global__ void __launch_bounds__(NT) digitize_reg_kernel(const float* __restric
                                                           const float* __restrict__ g,
                                                           const float* __restrict__ b,
                                                           uint8_t* planes, int64_t plane_stride,
-                                                          int* exps) {
+                                                          int* exps, int rt) {
   constexpr int NW = NT / 32;
   __shared__ float red[3][NW];
   const int64_t m = blockIdx.x;
@@ -727,7 +768,7 @@ __global__ void __launch_bounds__(NT) digitize_reg_kernel(const float* __restric
       d1[i] = (int8_t)lo;
       d0[i] = (int8_t)((qv - lo) >> 8);
     }
-    const int64_t off = cm_offset(m, (int64_t)c * 16, K);
+    const int64_t off = cm_offset_rt(m, (int64_t)c * 16, K, rt);
     *reinterpret_cast<uint4*>(planes + off) = *reinterpret_cast<uint4*>(d0);
     *reinterpret_cast<uint4*>(planes + plane_stride + off) = *reinterpret_cast<uint4*>(d1);
   }
@@ -821,21 +862,21 @@ bool g_tc_pair = true;
 
 void launch_digitize(const float* x, int64_t ldx, int64_t M, int64_t K, int norm, const float* g,
                      const float* b, uint8_t* planes, int64_t plane_stride, int* exps,
-                     cudaStream_t st) {
+                     cudaStream_t st, int rt) {
   // padding rows of the planes are never written: a tile's rows are
   // independent in the MMA and the GEMM epilogue drops rows >= M
   const unsigned grid = (unsigned)M;
   const bool al = (K % 16 == 0) && (ldx % 4 == 0);
   if (al && K <= 256 * 16 * 2)
-    digitize_reg_kernel<256, 2><<<grid, 256, 0, st>>>(x, ldx, M, K, norm, g, b, planes, plane_stride, exps);
+    digitize_reg_kernel<256, 2><<<grid, 256, 0, st>>>(x, ldx, M, K, norm, g, b, planes, plane_stride, exps, rt);
   else if (al && K <= 256 * 16 * 4)
-    digitize_reg_kernel<256, 4><<<grid, 256, 0, st>>>(x, ldx, M, K, norm, g, b, planes, plane_stride, exps);
+    digitize_reg_kernel<256, 4><<<grid, 256, 0, st>>>(x, ldx, M, K, norm, g, b, planes, plane_stride, exps, rt);
   else if (al && K <= 512 * 16 * 4)
-    digitize_reg_kernel<512, 4><<<grid, 512, 0, st>>>(x, ldx, M, K, norm, g, b, planes, plane_stride, exps);
+    digitize_reg_kernel<512, 4><<<grid, 512, 0, st>>>(x, ldx, M, K, norm, g, b, planes, plane_stride, exps, rt);
   else if (al && K <= 1024 * 16 * 4)
-    digitize_reg_kernel<1024, 4><<<grid, 1024, 0, st>>>(x, ldx, M, K, norm, g, b, planes, plane_stride, exps);
+    digitize_reg_kernel<1024, 4><<<grid, 1024, 0, st>>>(x, ldx, M, K, norm, g, b, planes, plane_stride, exps, rt);
   else
-    digitize_kernel<<<grid, 256, 0, st>>>(x, ldx, M, K, norm, g, b, planes, plane_stride, exps);
+    digitize_kernel<<<grid, 256, 0, st>>>(x, ldx, M, K, norm, g, b, planes, plane_stride, exps, rt);
   count_launch();
 }
 
@@ -875,6 +916,222 @@ void launch_pair(const TcGemmArgs& a, cudaStream_t st) {
               (h[i + 2] - t0) / 1e3, (h[i + 3] - t0) / 1e3);
     cudaFree(b.trace);
   }
+}
+
+
+// ---- wide decode (9..32 token rows, split-K): weights as the A operand -------
+// The single-CTA kernel above puts the tokens on the MMA's M = 128 rows, so at
+// decode widths of 9-32 rows 75-93 % of every MMA multiplies padding and the
+// tensor pipe (fed at 8 KB of shared memory per MMA) becomes the limit: BLOOM
+// batch 16 measured 77.6 % tensor-pipe active at 55 % of the HBM rate.  Here
+// the operands swap: A = one 128-channel weight unit (the same core-matrix
+// bytes, K-major), B = the NR token rows of the digit planes (N = NR = 16 or
+// 32; the planes are digitised in NR-row core-matrix tiles, so a stage's rows
+// are one contiguous copy per plane), D in
+// TMEM with lane = output channel and column = token row.  Same exact integer
+// products, same scaling and rounding sequence in the epilogue as
+// epilogue_group / finish_tile, so the outputs are bit-identical to the
+// single-CTA kernel's.  3 stages of 32 KB weights + NR KB of planes, two CTAs
+// per SM; split-K over the int64 workspace as above.
+template <int NR>
+struct WideCfg {
+  static constexpr int XU = NR * 32;                       // one plane unit: NR rows x 32 B
+  static constexpr int W_BYTES = NGRP * KU * UNIT;         // 32 KB
+  static constexpr int X_BYTES = 2 * KU * XU;
+  static constexpr int STAGE = W_BYTES + X_BYTES;
+  static constexpr int NST = 3;
+  static constexpr int SMEM = NST * STAGE;
+  static constexpr int TCOLS = 2 * NGRP * NR;              // D columns: (plane, group, row)
+  static constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) |
+                                    ((uint32_t)(NR >> 3) << 17) | ((128u >> 4) << 24);
+};
+static_assert(NGRP * 32 * 128 * 4 <= WideCfg<32>::SMEM && NGRP * 16 * 128 * 4 <= WideCfg<16>::SMEM,
+              "the epilogue tile fits the drained stage ring");
+
+__device__ __forceinline__ void mma_i8_id(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                          uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+template <int NR, int EP>
+__global__ void __launch_bounds__(256, 2) gemm_i8_wide_kernel(TcGemmArgs a) {
+  using C = WideCfg<NR>;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ __align__(8) uint64_t full[C::NST], empty[C::NST], tmem_full;
+  __shared__ uint32_t tmem_base;
+  __shared__ int last_cta;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ng0 = blockIdx.y * NGRP;
+  const int64_t KT = a.K >> 5;
+  const int KBT = (int)(KT / KU);
+  const int S = a.ksplit > 1 ? a.ksplit : 1;
+  const int kb0 = (int)((int64_t)blockIdx.z * KBT / S), kb1 = (int)((int64_t)(blockIdx.z + 1) * KBT / S);
+  const int KB = kb1 - kb0;
+  const int M = (int)a.M;                                  // <= NR
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::NST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    mbar_init(&tmem_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tmem_base)), "n"(C::TCOLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tbase = tmem_base;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer ----------------
+    const uint8_t* wb = reinterpret_cast<const uint8_t*>(a.w);
+    for (int kb = 0; kb < KB; ++kb) {
+      const int s = kb % C::NST;
+      if (kb >= C::NST) mbar_wait(&empty[s], ((kb / C::NST) - 1) & 1);
+      uint8_t* st = smem + (size_t)s * C::STAGE;
+      mbar_expect_tx(&full[s], C::STAGE);
+      for (int j = 0; j < NGRP; ++j) {
+        const int64_t ub = ((int64_t)(ng0 + j) * KT + (int64_t)(kb0 + kb) * KU) * UNIT;
+        tma_load_1d(st + j * KU * UNIT, wb + ub, KU * UNIT, &full[s]);
+      }
+      // the planes are digitised with NR-row tiles (launch_digitize rt = NR):
+      // a stage's KU units of one plane are KU * NR * 32 contiguous bytes
+      for (int p = 0; p < 2; ++p)
+        tma_load_1d(st + C::W_BYTES + p * KU * C::XU,
+                    a.planes + p * a.plane_stride + (int64_t)(kb0 + kb) * KU * C::XU, KU * C::XU,
+                    &full[s]);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer: D[channel][row] += W . X^T ----------------
+    for (int kb = 0; kb < KB; ++kb) {
+      const int s = kb % C::NST;
+      mbar_wait(&full[s], (kb / C::NST) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint8_t* st = smem + (size_t)s * C::STAGE;
+#pragma unroll
+      for (int u = 0; u < KU; ++u)
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+          const uint64_t bd = umma_desc(st + C::W_BYTES + (p * KU + u) * C::XU, NR * 16, 128);
+#pragma unroll
+          for (int j = 0; j < NGRP; ++j) {
+            const uint64_t ad = umma_desc(st + j * KU * UNIT + u * UNIT, 2048, 128);
+            mma_i8_id(tbase + (uint32_t)((p * NGRP + j) * NR), ad, bd, C::IDESC, (kb | u) ? 1u : 0u);
+          }
+        }
+      mma_commit(&empty[s]);
+    }
+    mma_commit(&tmem_full);
+  } else if (warp >= 4) {
+    // ---------------- epilogue: thread = output channel ----------------
+    const int q = warp - 4, ch = q * 32 + lane;
+    const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
+    mbar_wait(&tmem_full, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    float* tile = reinterpret_cast<float*>(smem);           // [NGRP][NR][128] (stages are drained)
+    for (int j = 0; j < NGRP; ++j) {
+      int d0[NR], d1[NR];
+#pragma unroll
+      for (int c = 0; c < NR; c += 16) {
+        tmem_ld16_nw(tbase + lane_addr + (uint32_t)((0 * NGRP + j) * NR + c), d0 + c);
+        tmem_ld16_nw(tbase + lane_addr + (uint32_t)((1 * NGRP + j) * NR + c), d1 + c);
+      }
+      tmem_wait_ld();
+      const int64_t n = (int64_t)(ng0 + j) * 128 + ch;
+      if (S == 1) {
+        const float wsc = __ldg(a.wscale + n);
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+          if (r >= M) break;
+          const float ys = ldexpf(1.0f, a.exps[r] - 14);
+          tile[(j * NR + r) * 128 + ch] =
+              __fmul_rn(__fmul_rn((float)((long long)d0[r] * 256 + d1[r]), ys), wsc);
+        }
+      } else {
+        unsigned long long* ws = reinterpret_cast<unsigned long long*>(a.ws);
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+          if (r >= M) break;
+          atomicAdd(ws + (int64_t)r * a.N + n, (unsigned long long)((long long)d0[r] * 256 + d1[r]));
+        }
+      }
+    }
+    if (S == 1) {
+      asm volatile("bar.sync 1, 128;" ::: "memory");       // the 4 epilogue warps
+      const int t = threadIdx.x - 128;
+      const int epi = EP >= 0 ? EP : a.epi;
+      if (epi == EPI_SWIGLU) {
+        for (int i = t; i < NGRP * M * 64; i += 128) {
+          const int j = i / (M * 64), r = (i / 64) % M, c = i % 64;
+          const float gd = tile[(j * NR + r) * 128 + c], ud = tile[(j * NR + r) * 128 + 64 + c];
+          a.y[(int64_t)r * a.ldy + (ng0 + j) * 64 + c] =
+              __fmul_rn(__fdividef(gd, __fadd_rn(1.0f, __expf(-gd))), ud);
+        }
+      } else {
+        for (int i = t; i < NGRP * M * 128; i += 128) {
+          const int j = i / (M * 128), r = (i / 128) % M, c = i % 128;
+          const int64_t col = (int64_t)(ng0 + j) * 128 + c;
+          float v = tile[(j * NR + r) * 128 + c];
+          if (epi == EPI_RESID) v = __fadd_rn(v, a.res[(int64_t)r * a.ldy + col]);
+          else if (epi == EPI_GELU) v = gelu_f(v);
+          a.y[(int64_t)r * a.ldy + col] = v;
+        }
+      }
+    } else {
+      __threadfence();
+    }
+  }
+  if (S > 1) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int* cnt = a.counters + blockIdx.y;
+      const int old = atomicAdd(cnt, 1);
+      last_cta = (old == S - 1);
+      if (last_cta) { __threadfence(); *cnt = 0; }
+    }
+    __syncthreads();
+    if (last_cta) finish_tile(a, 0, ng0);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 2)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "n"(C::TCOLS)
+                 : "memory");
+}
+
+template <int NR, int EP>
+void launch_wide_t(const TcGemmArgs& b, dim3 grid, cudaStream_t st) {
+  static bool set[kMaxDevices] = {};
+  const int dv = current_device();
+  if (!set[dv]) {
+    cudaFuncSetAttribute(gemm_i8_wide_kernel<NR, EP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         WideCfg<NR>::SMEM);
+    set[dv] = true;
+  }
+  gemm_i8_wide_kernel<NR, EP><<<grid, 256, WideCfg<NR>::SMEM, st>>>(b);
+}
+
+template <int NR>
+void launch_wide_nr(const TcGemmArgs& b, dim3 grid, cudaStream_t st) {
+  switch (b.epi) {
+    case EPI_STORE: launch_wide_t<NR, EPI_STORE>(b, grid, st); break;
+    case EPI_RESID: launch_wide_t<NR, EPI_RESID>(b, grid, st); break;
+    case EPI_SWIGLU: launch_wide_t<NR, EPI_SWIGLU>(b, grid, st); break;
+    default: launch_wide_t<NR, EPI_GELU>(b, grid, st); break;
+  }
+}
+
+bool g_tc_wide = getenv("SP_TC_WIDE") ? atoi(getenv("SP_TC_WIDE")) != 0 : true;
+
+int wide_rows(int64_t M) {
+  if (!g_tc_wide) return 0;
+  return M <= 16 ? 16 : (M <= 32 ? 32 : 0);
 }
 
 template <bool BF, int EP>
@@ -923,6 +1180,22 @@ void launch_gemm_i8_tc(const TcGemmArgs& a, cudaStream_t st) {
     };
     if (a.bf16) go(std::true_type{});
     else go(std::false_type{});
+    return;
+  }
+  if (!a.bf16 && a.ws && a.counters && wide_rows(a.M)) {
+    // wide decode: weights on the MMA's M side (gemm_i8_wide_kernel); split K
+    // as far as every CTA stays resident (two per SM): no second wave
+    TcGemmArgs b = a;
+    const int tiles = (int)(a.N / (128 * NGRP));
+    const int kbt = (int)(a.K / 32 / KU);
+    int S = (2 * 148) / tiles;                // every CTA resident at once (2 per SM)
+    if (S > kbt / 4) S = kbt / 4;
+    if (S < 1) S = 1;
+    b.ksplit = S;
+    const dim3 grid(1u, (unsigned)tiles, (unsigned)S);
+    if (wide_rows(a.M) == 16) launch_wide_nr<16>(b, grid, st);
+    else launch_wide_nr<32>(b, grid, st);
+    count_launch();
     return;
   }
   TcGemmArgs b = a;

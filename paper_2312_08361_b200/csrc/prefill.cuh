@@ -27,13 +27,16 @@ struct TcGemmArgs {
   int bf16;                 // bf16 weights and hi/lo bf16 planes (K counted in bytes)
 };
 
+extern bool g_tc_wide;    // option 10: wide-decode GEMM with the weights on the MMA's M side
+
 // token rows of the digit planes: padded to the 256-token CTA-pair tile
 inline int64_t tc_rows(int64_t M) { return (M + 255) / 256 * 256; }
 int64_t tc_plane_bytes(int64_t M, int64_t K);
 extern bool g_tc_pair;    // sp_span_set_option(.., 2, ..): CTA-pair tcgen05 GEMM (default on)
 void launch_digitize(const float* x, int64_t ldx, int64_t M, int64_t K, int norm, const float* g,
                      const float* b, uint8_t* planes, int64_t plane_stride, int* exps,
-                     cudaStream_t st);
+                     cudaStream_t st, int rt = 128);   // rt: rows per core-matrix tile
+int wide_rows(int64_t M);   // row tile of the wide-decode GEMM for M rows (0 = not used)
 void launch_gemm_i8_tc(const TcGemmArgs& a, cudaStream_t st);
 // bf16 operand planes (hi, lo) for bf16 weights; K <= 16384
 void launch_digitize_bf16(const float* x, int64_t ldx, int64_t M, int64_t K, int norm,

@@ -649,7 +649,8 @@ int run_span_decode_wide(sp_span* s, sp_kv* kv, int b0, int b1, float* y, int wi
   auto digit = [&](const float* x, int64_t K, int nm, const float* gg, const float* bb) {
     ProfScope ps(s, PC_OTHER, 4.0 * R * K + 2.0 * Mp * K * eb, 0, st);
     if (bf) launch_digitize_bf16(x, K, R, K, nm, gg, bb, s->planes, Mp * K * eb, st);
-    else launch_digitize(x, K, R, K, nm, gg, bb, s->planes, Mp * K, s->exps, st);
+    else launch_digitize(x, K, R, K, nm, gg, bb, s->planes, Mp * K, s->exps, st,
+                         wide_rows(R) ? wide_rows(R) : 128);   // the GEMM's row tile
   };
   for (int b = b0 - s->start; b < b1 - s->start; ++b) {
     BlockW& W = s->blocks[b];
@@ -1152,6 +1153,7 @@ int sp_span_set_option(sp_span* s, int32_t option, int32_t value) {
   else if (option == 7) g_attn_cl = value != 0;
   else if (option == 8) g_attn_tc = value != 0;
   else if (option == 9) g_attn_mha = value != 0;
+  else if (option == 10) g_tc_wide = value != 0;
   else SP_FAIL(SP_ERR_ARG, "unknown option");
   return SP_OK;
 }

@@ -345,7 +345,33 @@ def test_extended_families_greedy_tokens_match_oracle(name):
     assert worst <= 1e-2, worst
 
 
-@pytest.mark.parametrize("name,width", [("llama_int8", 9), ("bloom_int8", 16), ("llama_g8", 12)])
+@pytest.mark.parametrize("name,width", [("llama_int8", 12), ("bloom_int8", 16), ("llama_int8", 32)])
+def test_wide_decode_weight_side_gemm_bit_identical(name, width):
+    """The wide-decode GEMM with the weights on the MMA's M side (option 10:
+    N = 16 / 32 token rows, split-K) gives exactly the token-tile GEMM's output
+    (same exact integer products, same scaling and rounding)."""
+    from paper_2312_08361_b200 import _lib
+    cfg = SMALL[name]
+    rng = np.random.default_rng(53)
+    d = cfg.hidden_dim
+    x = rng.standard_normal((width, 30 + 2, d)).astype(np.float32)
+    outs = {}
+    eng = _engine(cfg)
+    try:
+        for v in (1, 0):
+            _lib.check(eng.lib.sp_span_set_option(eng.span.handle, 10, v))
+            c = eng.make_caches(0, cfg.n_blocks, width)
+            eng.run_cached(0, cfg.n_blocks, c, _blob(x[:, :30].reshape(-1, d)), width, 30, False)
+            outs[v] = [eng.run_cached(0, cfg.n_blocks, c, _blob(x[:, i]), width, 1, False).array()
+                       for i in (30, 31)]
+    finally:
+        _lib.check(eng.lib.sp_span_set_option(eng.span.handle, 10, 1))
+    for a, b in zip(outs[1], outs[0]):
+        assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("name,width", [("llama_int8", 9), ("bloom_int8", 16), ("llama_g8", 12),
+                                        ("llama_int8", 24), ("bloom_int8", 32)])
 def test_wide_decode_vs_oracle(name, width):
     """Decode with >= 9 rows per step runs its linears on the tcgen05 GEMM
     (one pass over the weights for all rows) and attention on the fused decode
