@@ -475,12 +475,14 @@ def run_b200(args) -> None:
                                 ).pin_memory().numpy()
         for _ in range(args.warmup):
             pipe.step_api(host_rows)
+        pipe.finish_api()
         torch.cuda.synchronize()
         dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(args.steps):
             pipe.step_api(host_rows)
+        pipe.finish_api()          # the last tick's result read to the host (last rank)
         torch.cuda.synchronize()
         dist.barrier()
         e2e_t = torch.tensor([time.perf_counter() - t0], device=dev)
@@ -490,7 +492,8 @@ def run_b200(args) -> None:
         e2e = {"value": args.steps * sessions / max(1, world) / e2e_s, "unit": UNIT,
                "h2d_bytes_per_step": 4 * B * d, "d2h_bytes_per_step": 4 * B * d,
                "note": "per tick: rank 0 H2D of one input row, last rank D2H of one output "
-                       "row; wall clock max over ranks"}
+                       "row (HiddenBlob.array_async, collected at the next tick; all inside "
+                       "the timed region); wall clock max over ranks"}
 
     # ---- roofline of the dominant kernel (decode GEMV) ----
     achieved = wbytes.value / (gemv_ms / 1e3) / 1e9

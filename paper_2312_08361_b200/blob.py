@@ -121,6 +121,27 @@ class HiddenBlob:
                 "cpu").numpy().reshape(self.rows, self.cols)
         return self.data
 
+    def array_async(self) -> "PendingRows":
+        """Start the device->host copy of the decoded rows without waiting for
+        the stream: the copy lands in pinned memory behind the kernels already
+        queued, and ``.result()`` waits for it (an extension of `array()` for
+        callers that pipeline several sessions, e.g. the multi-GPU ring)."""
+        if self.synthetic:
+            raise ProtocolError("synthetic blob carries no data")
+        if self.dev is None and self.dev_codes is None:
+            return PendingRows(self.array(), None)
+        import torch
+        if self.dev is not None:
+            src = self.dev
+        else:
+            from . import codec
+            src = codec.dequantize_device(self.dev_codes, self.dev_scales, self.rows * self.cols)
+        host = torch.empty((self.rows, self.cols), dtype=torch.float32, pin_memory=True)
+        host.copy_(src.reshape(self.rows, self.cols), non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(src.device))
+        return PendingRows(host, ev)
+
     def device_codes(self, device=None):
         """(codes, scales) as device tensors (uploaded if host-held)."""
         if self.dev_codes is None:
@@ -165,3 +186,16 @@ class HiddenBlob:
         where = "device" if (self.dev is not None or self.dev_codes is not None) else "host"
         kind = "synthetic" if self.synthetic else ("int8" if self.is_quantized else "f32")
         return f"HiddenBlob({self.rows}x{self.cols}, {kind}, {where})"
+
+
+class PendingRows:
+    """A device->host read in flight (`HiddenBlob.array_async`)."""
+
+    def __init__(self, host, event):
+        self._host, self._event = host, event
+
+    def result(self) -> np.ndarray:
+        if self._event is None:
+            return self._host
+        self._event.synchronize()
+        return self._host.numpy()

@@ -142,7 +142,12 @@ class SpanPipeline:
             out = self.eng.run_cached(self.start, self.end, self.caches[s], blob, self.width, 1,
                                       not last)
             if last:
-                self.host_out = out.array()               # the step's result on the host
+                # the step's result to the host: the read is started now and
+                # collected at the next tick, so this rank's host keeps the ring
+                # fed instead of idling on its own stream (finish_api() collects
+                # the last one)
+                self.finish_api()
+                self._pending = out.array_async()
                 self.y.copy_(out.dev)
             else:
                 self.out_codes.copy_(out.dev_codes)
@@ -164,6 +169,14 @@ class SpanPipeline:
         if r > 0 and k >= r - 1:
             self._verify_in()
         self.k += 1
+
+    def finish_api(self):
+        """Collect the outstanding device->host read of step_api (last rank)."""
+        p = getattr(self, "_pending", None)
+        if p is not None:
+            self.host_out = p.result()
+            self._pending = None
+        return getattr(self, "host_out", None)
 
     @property
     def wire_bytes_per_token(self) -> int:

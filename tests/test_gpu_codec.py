@@ -81,3 +81,18 @@ def test_large_roundtrip_size_independent():
     assert torch.equal(c, c2) and torch.equal(s, s2)
     bound = (s / 1.0).repeat_interleave(64)[: x.numel()]
     assert bool(((back - x).abs() <= bound * 0.501 + 1e-6).all())
+
+
+def test_array_async_equals_array():
+    """HiddenBlob.array_async (pinned, non-blocking device->host read) returns
+    exactly what array() returns, for raw and int8-coded device blobs."""
+    import torch
+    from paper_2312_08361_b200 import codec
+    from paper_2312_08361_b200.blob import HiddenBlob
+    rng = np.random.default_rng(5)
+    x = torch.from_numpy(rng.standard_normal((3, 8192)).astype(np.float32)).cuda()
+    raw = HiddenBlob.from_device(x)
+    assert np.array_equal(raw.array_async().result(), x.cpu().numpy())
+    c, s = codec.quantize_device(x)
+    coded = HiddenBlob(3, 8192, dev_codes=c, dev_scales=s)
+    assert np.array_equal(coded.array_async().result(), coded.array())
