@@ -412,6 +412,8 @@ attn_prefill_tc_kernel(AttnArgs a, const __grid_constant__ CUtensorMap kvmap, in
       if (j == 0) mnew = tmax;
       else if (tmax > m_used + kRescale) mnew = tmax;
       const bool grow = j > 0 && mnew != m_used;
+      // P buffer st free = O_{j-2} complete: also bounds o_full's phase below
+      if (j >= 2) mbar_wait(&p_free[st], ((j >> 1) - 1) & 1);
       if (__any_sync(0xffffffffu, grow)) {
         const float f = grow ? ex2_approx(m_used - mnew) : 1.f;
         mbar_wait(&o_full, (j - 1) & 1);         // O holds tiles 0..j-1
@@ -432,7 +434,6 @@ attn_prefill_tc_kernel(AttnArgs a, const __grid_constant__ CUtensorMap kvmap, in
       // P_j = exp2(s - m_used) (<= 2^8), bf16, -> TMEM buffer st, once the MMA
       // of tile j - 2 has read it
       PF_T(4, pf_t);
-      if (j >= 2) mbar_wait(&p_free[st], ((j >> 1) - 1) & 1);
       PF_T(5, pf_t);
       // p = exp2(s - m) (ex2.approx.ftz(-inf) = +0: masked keys need no test);
       // four partial sums for instruction-level parallelism
@@ -467,7 +468,9 @@ attn_prefill_tc_kernel(AttnArgs a, const __grid_constant__ CUtensorMap kvmap, in
     if (hf == 0) red_l[row] += l_run;
     pair_sync();
     const float inv = __frcp_rn(red_l[row]);
-    mbar_wait(&o_full, (ntiles - 1) & 1);
+    // every O MMA done = the last tile's P buffer released (one phase past the
+    // one waited at that tile: an unambiguous parity wait)
+    mbar_wait(&p_free[(ntiles - 1) & 1], ((ntiles - 1) >> 1) & 1);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     float* dst = a.ctx + (int64_t)(slot * a.n_new + q0 + row) * a.H * HD + h * HD + hf * OC;
 #pragma unroll
