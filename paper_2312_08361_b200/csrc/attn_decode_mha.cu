@@ -24,10 +24,10 @@
 //     sumsq, max|x|) partial for the O-projection GEMV are written once.
 // Bytes per launch: K+V of the visible positions (2 * T * H * hd * 2) + q/ctx.
 // A (row, head) pair's positions are cut into chunks of a size that depends on
-// the sequence length only (mha_chunk: >= T/4, 128..1024), one CTA each; with
+// the sequence length only (mha_chunk: >= T/16, 128..1024), one CTA each; with
 // several chunks the last-arriving CTA merges the chunk partials in ascending
 // order.  So a row's arithmetic is the same at every width (batch invariant)
-// and batch 1 still spreads over ~4 CTAs per head.
+// and batch 1 still spreads over up to 16 CTAs per head.
 #include <cstdint>
 
 #include "common.cuh"
@@ -63,15 +63,15 @@ __device__ __forceinline__ float rope_at(const float* x, int dd, int half, const
                    : __fadd_rn(__fmul_rn(x[j + half], c), __fmul_rn(x[j], s));
 }
 
-// positions per CTA: a power of two >= T/4 in [128, 1024] — a function of the
+// positions per CTA: a power of two >= T/div in [128, 1024] — a function of the
 // sequence length only, so a row's arithmetic never depends on the step's width
-__host__ __device__ __forceinline__ int mha_chunk(int T) {
+__host__ __device__ __forceinline__ int mha_chunk(int T, int div) {
   int ch = 128;
-  while (ch < 1024 && 4 * ch < T) ch *= 2;
+  while (ch < 1024 && div * ch < T) ch *= 2;
   return ch;
 }
 
-__global__ void __launch_bounds__(NW * 32, 3) attn_dec_mha_kernel(AttnDecArgs a) {
+__global__ void __launch_bounds__(NW * 32, 3) attn_dec_mha_kernel(AttnDecArgs a, int div) {
   __shared__ __align__(16) float qs[HD];
   __shared__ __align__(16) float wo[NW][HD];
   __shared__ float wm[NW], wl[NW], cf[32];
@@ -80,11 +80,28 @@ __global__ void __launch_bounds__(NW * 32, 3) attn_dec_mha_kernel(AttnDecArgs a)
   const int slot = blockIdx.x / a.kvh, kh = blockIdx.x % a.kvh;   // one query head: h = kh
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int T = a.t0 + 1;
-  const int CH = mha_chunk(T);
+  const int CH = mha_chunk(T, div);
   const int nchunk = (T + CH - 1) / CH;
   const int chunk = blockIdx.y;
   if (chunk >= nchunk) return;
   const int half = HD / 2;
+  const int* ptab = a.page_table + slot * a.max_pages;
+  const __nv_bfloat16* pool = reinterpret_cast<const __nv_bfloat16*>(a.kv_pool);
+  const int b0 = chunk * (CH / 32), b1 = min((chunk + 1) * (CH / 32), (T + 31) / 32);
+  auto block_k = [&](int b) {          // K rows of 32-position block b (V follows kvh pages on)
+    const int page = ptab[(b * 32) / kPageTokens];
+    return pool + (((int64_t)page * 2 + 0) * a.kvh + kh) * kPageTokens * HD +
+           ((b * 32) % kPageTokens) * HD;
+  };
+  // before the dependency wait (page tables and cached rows are not written by
+  // the kernels of this chain; L2 is coherent with the append below): the
+  // warp's first two K/V blocks stream into L2 under the QKV projection's tail
+  if (lane == 0)
+    for (int b = b0 + warp, n = 0; b < b1 && n < 2; b += NW, ++n) {
+      const __nv_bfloat16* kb = block_k(b);
+      l2_prefetch(kb, 32 * HD * 2);
+      l2_prefetch(kb + (int64_t)a.kvh * kPageTokens * HD, 32 * HD * 2);
+    }
   pdl_trigger();
   pdl_wait();                          // q / k_new / v_new come from the QKV projection
 
@@ -118,25 +135,17 @@ __global__ void __launch_bounds__(NW * 32, 3) attn_dec_mha_kernel(AttnDecArgs a)
     for (int e = 0; e < 8; ++e) qreg[c * 8 + e] = qs[c * 64 + (lane & 7) * 8 + e];
   const float qscale = kLog2e / sqrtf((float)HD);
   const float slope = (a.family == kBloom) ? a.alibi[kh] * kLog2e : 0.f;
-  const __nv_bfloat16* pool = reinterpret_cast<const __nv_bfloat16*>(a.kv_pool);
-  const int* ptab = a.page_table + slot * a.max_pages;
   float m = -INFINITY, l = 0.f;        // warp-uniform max, per-lane partial sum
   float o[4] = {0.f, 0.f, 0.f, 0.f};   // dims 4*lane .. 4*lane + 3
-  const int b0 = chunk * (CH / 32), b1 = min((chunk + 1) * (CH / 32), (T + 31) / 32);
   for (int b = b0 + warp; b < b1; b += NW) {
     // a 32-position block lies inside one 64-position page (allocated: it holds b*32 < T)
-    const int page = ptab[(b * 32) / kPageTokens];
-    const __nv_bfloat16* kblk = pool + (((int64_t)page * 2 + 0) * a.kvh + kh) * kPageTokens * HD +
-                                ((b * 32) % kPageTokens) * HD;
+    const __nv_bfloat16* kblk = block_k(b);
     const __nv_bfloat16* vblk = kblk + (int64_t)a.kvh * kPageTokens * HD;
-    // the warp's next block (K and V: 8 KB contiguous each) streams into L2
-    // under this block's arithmetic, so HBM stays busy between the register
-    // loads of consecutive blocks
-    if (lane == 0 && b + NW < b1) {
-      const int bn = b + NW;
-      const int pn = ptab[(bn * 32) / kPageTokens];
-      const __nv_bfloat16* kn = pool + (((int64_t)pn * 2 + 0) * a.kvh + kh) * kPageTokens * HD +
-                                ((bn * 32) % kPageTokens) * HD;
+    // the warp's block after next (K and V: 8 KB contiguous each) streams into
+    // L2 under this block's arithmetic, so HBM stays busy between the register
+    // loads of consecutive blocks (the first two were requested before the wait)
+    if (lane == 0 && b + 2 * NW < b1) {
+      const __nv_bfloat16* kn = block_k(b + 2 * NW);
       l2_prefetch(kn, 32 * HD * 2);
       l2_prefetch(kn + (int64_t)a.kvh * kPageTokens * HD, 32 * HD * 2);
     }
@@ -278,6 +287,10 @@ __global__ void __launch_bounds__(NW * 32, 3) attn_dec_mha_kernel(AttnDecArgs a)
 }  // namespace
 
 bool g_attn_mha = getenv("SP_ATTN_MHA") ? atoi(getenv("SP_ATTN_MHA")) != 0 : true;
+// chunk length >= T / div (128..1024 positions); measured (div 4 / 8 / 16):
+// Llama-2-7B batch 1 at 1 K positions 312 / 336 / 346 steps/s (the cluster
+// kernel: 341), BLOOM batch 16 at 2 K 163.0 / 160.4 / 159.2 per 8 blocks
+static int g_mha_div = getenv("SP_MHA_DIV") ? atoi(getenv("SP_MHA_DIV")) : 16;
 
 bool attn_dec_mha_ok(const AttnDecArgs& a) {
   // one query head per kv head, bf16 cache, hd 128; every width (the per-row
@@ -285,13 +298,13 @@ bool attn_dec_mha_ok(const AttnDecArgs& a) {
   // smallest size must fit the partial buffers (max_pages) and one warp's merge
   const int T = a.t0 + 1;
   return g_attn_mha && a.kv_dtype == kKVBF16 && a.hd == HD && a.H == a.kvh &&
-         (T + mha_chunk(T) - 1) / mha_chunk(T) <= 32;
+         (T + mha_chunk(T, g_mha_div) - 1) / mha_chunk(T, g_mha_div) <= 32;
 }
 
 int launch_attn_decode_mha(const AttnDecArgs& a, cudaStream_t st) {
   const int T = a.t0 + 1;
-  const dim3 grid(a.width * a.kvh, (T + mha_chunk(T) - 1) / mha_chunk(T));
-  launch_pdl(attn_dec_mha_kernel, grid, dim3(NW * 32), 0, st, a);
+  const dim3 grid(a.width * a.kvh, (T + mha_chunk(T, g_mha_div) - 1) / mha_chunk(T, g_mha_div));
+  launch_pdl(attn_dec_mha_kernel, grid, dim3(NW * 32), 0, st, a, g_mha_div);
   count_launch();
   return a.H;                          // P_out: one partial per head
 }
