@@ -37,8 +37,10 @@
 // Measured (profiles/r02_attn_pf.md): 173 us for 2048 tokens of one 70B block.
 #include <cuda.h>   // CUtensorMap (the encoder is fetched from the driver at run time)
 
+#include <array>
 #include <cstdio>
 #include <cstdlib>
+#include <list>
 #include <mutex>
 #include <unordered_map>
 
@@ -495,18 +497,25 @@ attn_prefill_tc_kernel(AttnArgs a, const __grid_constant__ CUtensorMap kvmap, in
 }  // namespace
 
 namespace {
-// one 2-D tensor map per KV pool: rows = (block, page, K|V, kv head, key), cols = hd
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-const CUtensorMap* pool_map(const void* base, int64_t bytes) {
+}  // namespace
+
+// one 2-D tensor map per (KV pool, head dim, box rows): rows = (block, page,
+// K|V, kv head, key), cols = hd; boxes of [box_rows keys][64 dims], 128-byte
+// swizzle (prefill attention: a page per box; decode attention: 32 keys)
+const CUtensorMap* kv_pool_map(const void* base, int64_t bytes, int hd, int box_rows) {
   static std::mutex mu;
-  static std::unordered_map<const void*, std::pair<int64_t, CUtensorMap>> maps;
+  // std::list: the returned pointers stay valid as further maps are added
+  static std::unordered_map<const void*, std::list<std::pair<std::array<int64_t, 3>,
+                                                              CUtensorMap>>> maps;
   static EncodeTiledFn encode = nullptr;
   std::lock_guard<std::mutex> g(mu);
-  auto it = maps.find(base);
-  if (it != maps.end() && it->second.first == bytes) return &it->second.second;
+  auto& v = maps[base];
+  for (auto& e : v)
+    if (e.first[0] == bytes && e.first[1] == hd && e.first[2] == box_rows) return &e.second;
   if (!encode) {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -516,24 +525,22 @@ const CUtensorMap* pool_map(const void* base, int64_t bytes) {
     encode = reinterpret_cast<EncodeTiledFn>(fn);
   }
   CUtensorMap m;
-  const cuuint64_t dims[2] = {(cuuint64_t)HD, (cuuint64_t)(bytes / (HD * 2))};
-  const cuuint64_t strides[1] = {(cuuint64_t)HD * 2};
-  const cuuint32_t box[2] = {64, (cuuint32_t)kPageTokens};   // one page of one kv head
+  const cuuint64_t dims[2] = {(cuuint64_t)hd, (cuuint64_t)(bytes / (hd * 2))};
+  const cuuint64_t strides[1] = {(cuuint64_t)hd * 2};
+  const cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
   const cuuint32_t estr[2] = {1, 1};
   if (encode(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
       CUDA_SUCCESS)
     return nullptr;
-  auto& e = maps[base];
-  e = {bytes, m};
-  return &e.second;
+  v.push_back({{bytes, hd, box_rows}, m});
+  return &v.back().second;
 }
-}  // namespace
 
 bool launch_attention_prefill_tc(const AttnArgs& a, cudaStream_t st) {
   if (!g_attn_tc || a.kv_dtype != kKVBF16 || a.hd != HD || !a.pool_base) return false;
-  const CUtensorMap* map = pool_map(a.pool_base, a.pool_bytes);
+  const CUtensorMap* map = kv_pool_map(a.pool_base, a.pool_bytes, HD, kPageTokens);
   if (!map) return false;
   static bool set[kMaxDevices] = {};
   const int dv = current_device();

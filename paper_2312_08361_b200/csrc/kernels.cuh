@@ -1,5 +1,6 @@
 // Kernel launch interfaces shared between the kernel files and the span runtime.
 #pragma once
+#include <cuda.h>   // CUtensorMap (tensor-map TMA of the KV pool)
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -95,6 +96,9 @@ bool launch_attention_prefill_mma(const AttnArgs& a, cudaStream_t st);
 // tcgen05 / TMEM flash prefill (bf16 KV, hd 128); false if the shape is unsupported
 bool launch_attention_prefill_tc(const AttnArgs& a, cudaStream_t st);
 extern bool g_attn_tc;    // option 8 (default on)
+// 2-D tensor map over a span's KV pool (cols = hd, bf16, 128-byte swizzle,
+// [box_rows][64] boxes); cached per pool; null if the driver entry point is missing
+const CUtensorMap* kv_pool_map(const void* base, int64_t bytes, int hd, int box_rows);
 
 // KV page copy (copy-on-write of a shared tail page): all blocks of the span
 void launch_page_copy(void* pool, int64_t block_stride_bytes, int n_blocks,
