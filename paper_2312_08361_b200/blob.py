@@ -121,11 +121,13 @@ class HiddenBlob:
                 "cpu").numpy().reshape(self.rows, self.cols)
         return self.data
 
-    def array_async(self) -> "PendingRows":
+    def array_async(self, out=None) -> "PendingRows":
         """Start the device->host copy of the decoded rows without waiting for
         the stream: the copy lands in pinned memory behind the kernels already
         queued, and ``.result()`` waits for it (an extension of `array()` for
-        callers that pipeline several sessions, e.g. the multi-GPU ring)."""
+        callers that pipeline several sessions, e.g. the multi-GPU ring).
+        ``out``: a pinned f32 [rows, cols] host tensor to copy into (reused
+        buffers avoid a pinned allocation per call)."""
         if self.synthetic:
             raise ProtocolError("synthetic blob carries no data")
         if self.dev is None and self.dev_codes is None:
@@ -136,7 +138,8 @@ class HiddenBlob:
         else:
             from . import codec
             src = codec.dequantize_device(self.dev_codes, self.dev_scales, self.rows * self.cols)
-        host = torch.empty((self.rows, self.cols), dtype=torch.float32, pin_memory=True)
+        host = out if out is not None else torch.empty((self.rows, self.cols),
+                                                       dtype=torch.float32, pin_memory=True)
         host.copy_(src.reshape(self.rows, self.cols), non_blocking=True)
         ev = torch.cuda.Event()
         ev.record(torch.cuda.current_stream(src.device))

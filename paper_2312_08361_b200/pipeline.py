@@ -147,7 +147,13 @@ class SpanPipeline:
                 # fed instead of idling on its own stream (finish_api() collects
                 # the last one)
                 self.finish_api()
-                self._pending = out.array_async()
+                if not hasattr(self, "_host_bufs"):      # two pinned result buffers, alternated
+                    self._host_bufs = [torch.empty((self.width, self.d), dtype=torch.float32,
+                                                   pin_memory=True) for _ in range(2)]
+                    self._host_i = 0
+                buf = self._host_bufs[self._host_i]
+                self._host_i ^= 1
+                self._pending = out.array_async(out=buf)
                 self.y.copy_(out.dev)
             else:
                 self.out_codes.copy_(out.dev_codes)
@@ -174,7 +180,7 @@ class SpanPipeline:
         """Collect the outstanding device->host read of step_api (last rank)."""
         p = getattr(self, "_pending", None)
         if p is not None:
-            self.host_out = p.result()
+            self.host_out = p.result().copy()      # the buffer is reused two ticks later
             self._pending = None
         return getattr(self, "host_out", None)
 
