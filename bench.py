@@ -387,12 +387,16 @@ def run_b200(args) -> None:
     for _ in range(args.warmup + (world if world > 1 else 0)):
         pipe.step()
     torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
     launches0 = lib.sp_kernel_launches()
     clocks = ClockSampler(local).start()
     time.sleep(0.3)
+    # the barrier comes after the clock sampler's start-up (a subprocess: its
+    # duration differs per rank), so every rank enters the timed ticks together;
+    # otherwise the first rank's events also time its wait for the last one
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):

@@ -15,8 +15,12 @@
 // thread t of T takes words t, t + T, ... with powers r^(t+1) * (r^T)^j.
 // Restated in oracle/content_hash.py (test infrastructure).  Distinct payloads
 // of one length collide with probability <= m / p (a polynomial of degree m).
-// HBM-bound: n bytes read once; one launch (last-block reduction).
+// HBM-bound: n bytes read once; one launch (last-block reduction), a
+// persistent workspace per (device, stream).
 #include <cstdint>
+#include <map>
+#include <mutex>
+#include <utility>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -97,7 +101,26 @@ __global__ void __launch_bounds__(kThreads) content_hash_kernel(
     } else {
       *out = h;
     }
+    *done = 0;                       // the workspace is reused by the next call on this stream
   }
+}
+
+// one workspace (CTA partials + arrival counter, zero at rest) per (device,
+// stream): calls on one stream are ordered, so they can share it; no
+// allocation or memset per call (stream-ordered allocations may return memory
+// to the driver at synchronisation points and re-map it on the next call)
+constexpr int kMaxGrid = 592;
+void* workspace(int dev, cudaStream_t st) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, void*> ws;
+  std::lock_guard<std::mutex> g(mu);
+  auto it = ws.find({dev, st});
+  if (it != ws.end()) return it->second;
+  void* p = nullptr;
+  if (cudaMalloc(&p, (size_t)kMaxGrid * 8 + 16) != cudaSuccess) return nullptr;
+  if (cudaMemset(p, 0, (size_t)kMaxGrid * 8 + 16) != cudaSuccess) return nullptr;
+  ws[{dev, st}] = p;
+  return p;
 }
 
 int content_hash(const void* data, int64_t n, uint64_t* out, const uint64_t* expect,
@@ -114,18 +137,18 @@ int content_hash(const void* data, int64_t n, uint64_t* out, const uint64_t* exp
   // >= 8 words per thread, at most 4 CTAs per SM of a 148-SM B200
   int64_t grid = (m + kThreads * 8 - 1) / (kThreads * 8);
   if (grid < 1) grid = 1;
-  if (grid > 592) grid = 592;
-  void* ws = nullptr;
-  const size_t wbytes = (size_t)grid * 8 + 16;
-  SP_CUDA_TRY(cudaMallocAsync(&ws, wbytes, st));
-  unsigned* done = reinterpret_cast<unsigned*>(static_cast<uint8_t*>(ws) + grid * 8);
-  SP_CUDA_TRY(cudaMemsetAsync(done, 0, 4, st));
+  if (grid > kMaxGrid) grid = kMaxGrid;
+  void* ws = workspace(pa.device, st);
+  if (!ws) {
+    sp_set_error(__FILE__, __LINE__, "content hash: workspace allocation failed");
+    return SP_ERR_OOM;
+  }
+  unsigned* done = reinterpret_cast<unsigned*>(static_cast<uint8_t*>(ws) + kMaxGrid * 8);
   content_hash_kernel<<<(unsigned)grid, kThreads, 0, st>>>(
       static_cast<const uint8_t*>(data), n, static_cast<uint64_t*>(ws), done, out, expect,
       mismatch);
   count_launch();
   SP_CUDA_TRY(cudaGetLastError());
-  SP_CUDA_TRY(cudaFreeAsync(ws, st));
   return SP_OK;
 }
 
