@@ -9,9 +9,9 @@
 // Work split.  One cluster of CL = 8 CTAs per (slot, kv head); CTA rank c holds
 // NW warps, warp w the 32 positions [(s*CL + c)*NW*32 + w*32, +32) of pass s
 // (one pass up to CL*NW*32 positions: 3072 with NW = 12).  Every warp's K/V
-// rows are staged by tensor-map TMA (one lane, four boxes, 128-byte swizzle)
-// BEFORE the programmatic-launch wait (positions < t0 are never rewritten), so
-// after the QKV projection lands only the math remains:
+// rows are staged with cp.async BEFORE the programmatic-launch wait (positions
+// < t0 are never rewritten), so after the QKV projection lands only the math
+// remains:
 //   * S[32 x 8] = K . q^T on mma.m16n8k16 (A = the warp's K rows by ldmatrix,
 //     B columns = the kv group's query heads, q split hi + lo bf16 — two MMAs —
 //     against the bf16 cache), online softmax per head in the exp2 domain,
@@ -69,36 +69,10 @@ __device__ __forceinline__ void ldsm4t(uint32_t* r, const void* p) {
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
                : "r"((uint32_t)__cvta_generic_to_shared(p)));
 }
-__device__ __forceinline__ uint32_t su32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* b, int n) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra WAIT_%=;\n}" ::"r"(su32(b)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0, int c1,
-                                       uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3}], [%4];" ::"r"(su32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(su32(bar))
-      : "memory");
-}
-// byte offset of element (row r, dim d) in a warp's K or V buffer: [hd/64 halves]
-// x [32 rows][128 B], 128-byte TMA swizzle (16-byte chunk ^ row % 8)
-__device__ __forceinline__ int swz(int r, int d) {
-  return (d >> 6) * 4096 + r * 128 + ((((d & 63) >> 3) ^ (r & 7)) << 4) + (d & 7) * 2;
+__device__ __forceinline__ void cp16z(void* dst, const void* src, bool ok) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(ok ? 16 : 0));
 }
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
@@ -128,28 +102,24 @@ __device__ __forceinline__ void cl_mark(const AttnDecArgs& a, int ph) {
 
 template <int HD>
 struct Layout {
-  static constexpr int RS = HD + 8;                      // padded bf16 row (q: ldmatrix-free)
-  static constexpr int KV_WARP = 32 * HD * 2;            // one warp's K (or V) rows, swizzled
+  static constexpr int RS = HD + 8;                      // padded bf16 row (ldmatrix banks)
+  static constexpr int KV_WARP = 32 * RS * 2;            // bytes of one warp's K (or V) rows
   static constexpr int Q_BYTES = 2 * GM * RS * 2;        // q hi, lo
   static constexpr int OC_BYTES = GM * HD * 4;           // CTA partial O
   static size_t bytes(int nw) {
-    return (size_t)2 * nw * KV_WARP + Q_BYTES + OC_BYTES + 2 * NWMAX * GM * 4 + 4 * GM * 4 + 256 +
-           1024;                                         // + alignment of the TMA boxes
+    return (size_t)2 * nw * KV_WARP + Q_BYTES + OC_BYTES + 2 * NWMAX * GM * 4 + 4 * GM * 4 + 256;
   }
 };
 
 template <int HD>
-__global__ void __launch_bounds__(NWMAX * 32, 1)
-attn_dec_cl_kernel(AttnDecArgs a, const __grid_constant__ CUtensorMap kvmap, int64_t row0) {
+__global__ void __launch_bounds__(NWMAX * 32, 1) attn_dec_cl_kernel(AttnDecArgs a) {
   using L = Layout<HD>;
   constexpr int RS = L::RS;
-  extern __shared__ __align__(1024) uint8_t dsm_raw[];
-  uint8_t* dsm = dsm_raw + ((1024 - (su32(dsm_raw) & 1023)) & 1023);   // 1 KB-aligned boxes
-  __shared__ __align__(8) uint64_t kv_bar[NWMAX];
+  extern __shared__ __align__(128) uint8_t dsm[];
   const int NW = blockDim.x >> 5;
   typedef __nv_bfloat16 Row[RS];
-  uint8_t* Ks = dsm;                                                // [NW][KV_WARP]
-  uint8_t* Vs = dsm + (size_t)NW * L::KV_WARP;                      // [NW][KV_WARP]
+  Row* Ks = reinterpret_cast<Row*>(dsm);                            // [NW*32]
+  Row* Vs = reinterpret_cast<Row*>(dsm + (size_t)NW * L::KV_WARP);  // [NW*32]
   Row* Qh = reinterpret_cast<Row*>(dsm + (size_t)2 * NW * L::KV_WARP);   // [GM]
   Row* Ql = Qh + GM;
   float* Oc = reinterpret_cast<float*>(dsm + (size_t)2 * NW * L::KV_WARP + L::Q_BYTES);  // [GM][HD]
@@ -168,32 +138,29 @@ attn_dec_cl_kernel(AttnDecArgs a, const __grid_constant__ CUtensorMap kvmap, int
   const int npass = (T + CL * PC - 1) / (CL * PC);
   const int half = HD / 2;
   const float* qrow = a.qkv + (int64_t)slot * a.ldqkv;
-  uint8_t* Kw = Ks + (size_t)warp * L::KV_WARP;
-  uint8_t* Vw = Vs + (size_t)warp * L::KV_WARP;
+  Row* Kw = Ks + warp * 32;
+  Row* Vw = Vs + warp * 32;
 
-  // this warp's 32 K/V rows of pass s: tensor-map TMA boxes of [32 keys][64
-  // dims] (128-byte swizzle) from lane 0, completion on the warp's mbarrier.
-  // Rows past T come in as whatever the page holds (zero at pool creation or
-  // finite earlier rows): their scores are masked, their P is 0.  The row of
-  // t0 is stale until the append below patches it.
-  if (lane == 0) {
-    mbar_init(&kv_bar[warp], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncwarp();
+  // this warp's 32 K/V rows of pass s (zero-filled past T; the row of t0 is
+  // stale until the append below patches it)
   auto stage = [&](int s) {
     const int p0 = (s * CL + rank) * PC + warp * 32;
-    if (p0 >= T || lane != 0) return;
+    const int nv = max(0, min(32, T - p0));
+    if (nv == 0) return;
     const int page = a.page_table[slot * a.max_pages + p0 / kPageTokens];
-    const int64_t rk = row0 + (((int64_t)page * 2 + 0) * a.kvh + kh) * kPageTokens +
-                       (p0 % kPageTokens);
-    const int64_t rv = rk + (int64_t)a.kvh * kPageTokens;
-    mbar_expect_tx(&kv_bar[warp], 2 * L::KV_WARP);
-#pragma unroll
-    for (int hh = 0; hh < HD / 64; ++hh) {
-      tma_2d(Kw + hh * 4096, &kvmap, hh * 64, (int)rk, &kv_bar[warp]);
-      tma_2d(Vw + hh * 4096, &kvmap, hh * 64, (int)rv, &kv_bar[warp]);
+    const __nv_bfloat16* kb = reinterpret_cast<const __nv_bfloat16*>(a.kv_pool) +
+                              (((int64_t)page * 2 + 0) * a.kvh + kh) * kPageTokens * HD +
+                              (p0 % kPageTokens) * HD;
+    const __nv_bfloat16* vb = kb + (int64_t)a.kvh * kPageTokens * HD;
+    constexpr int CPR = HD / 8;                   // 16-byte chunks per row
+#pragma unroll 4
+    for (int c = lane; c < 32 * CPR; c += 32) {
+      const int r = c / CPR, e = (c % CPR) * 8;
+      const bool ok = r < nv;
+      cp16z(&Kw[r][e], kb + (ok ? r : 0) * HD + e, ok);
+      cp16z(&Vw[r][e], vb + (ok ? r : 0) * HD + e, ok);
     }
+    asm volatile("cp.async.commit_group;" ::: "memory");
   };
   cl_mark(a, 0);
   stage(0);
@@ -257,15 +224,15 @@ attn_dec_cl_kernel(AttnDecArgs a, const __grid_constant__ CUtensorMap kvmap, int
   for (int s = 0; s < npass; ++s) {
     const int p0 = (s * CL + rank) * PC + warp * 32;
     const int nv = max(0, min(32, T - p0));
-    if (nv > 0) mbar_wait(&kv_bar[warp], s & 1);   // this pass's K / V landed
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncwarp();
     if (s == 0) cl_mark(a, 4);
     if (nv > 0) {
       if (appender && s == app_pass) {
 #pragma unroll
         for (int u = 0; u < HD / 32; ++u) {
-          *reinterpret_cast<__nv_bfloat16*>(Kw + swz(app_off, lane + 32 * u)) = knew[u];
-          *reinterpret_cast<__nv_bfloat16*>(Vw + swz(app_off, lane + 32 * u)) = vnew[u];
+          Kw[app_off][lane + 32 * u] = knew[u];
+          Vw[app_off][lane + 32 * u] = vnew[u];
         }
         __syncwarp();
       }
@@ -283,7 +250,7 @@ attn_dec_cl_kernel(AttnDecArgs a, const __grid_constant__ CUtensorMap kvmap, int
         for (int mt = 0; mt < 2; ++mt) {
           uint32_t ka[4];
           const int m = lane >> 3;
-          ldsm4(ka, Kw + swz(mt * 16 + (m & 1) * 8 + (lane & 7), ks * 16 + (m >> 1) * 8));
+          ldsm4(ka, &Kw[mt * 16 + (m & 1) * 8 + (lane & 7)][ks * 16 + (m >> 1) * 8]);
           mma16816(sc[mt], ka, h0, h1);
           mma16816(sc[mt], ka, l0, l1);
         }
@@ -347,7 +314,7 @@ attn_dec_cl_kernel(AttnDecArgs a, const __grid_constant__ CUtensorMap kvmap, int
         for (int dt = 0; dt < HD / 16; ++dt) {
           uint32_t va[4];
           const int m = lane >> 3;
-          ldsm4t(va, Vw + swz(kk * 16 + (m >> 1) * 8 + (lane & 7), dt * 16 + (m & 1) * 8));
+          ldsm4t(va, &Vw[kk * 16 + (m >> 1) * 8 + (lane & 7)][dt * 16 + (m & 1) * 8]);
           mma16816(o[dt], va, bh[kk][0], bh[kk][1]);
           mma16816(o[dt], va, bl[kk][0], bl[kk][1]);
         }
@@ -355,14 +322,13 @@ attn_dec_cl_kernel(AttnDecArgs a, const __grid_constant__ CUtensorMap kvmap, int
     }
     if (s + 1 < npass) {
       __syncwarp();
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       stage(s + 1);                                // this warp's slots are free again
     }
   }
 
   cl_mark(a, 5);
   // ---- warp partials -> shared (O over this warp's own K rows) ----
-  float* Ow = reinterpret_cast<float*>(Kw);        // [GM][HD] f32 fits the warp's K buffer
+  float* Ow = reinterpret_cast<float*>(Kw);        // [GM][HD] f32 fits 32 K rows
   __syncwarp();
 #pragma unroll
   for (int dt = 0; dt < HD / 16; ++dt) {
@@ -401,7 +367,7 @@ attn_dec_cl_kernel(AttnDecArgs a, const __grid_constant__ CUtensorMap kvmap, int
     float acc = 0.f;
     for (int w = 0; w < NW; ++w) {
       const float f = mw[w * GM + g];
-      if (f != 0.f) acc = fmaf(reinterpret_cast<const float*>(Ks + (size_t)w * L::KV_WARP)[i], f, acc);
+      if (f != 0.f) acc = fmaf(reinterpret_cast<const float*>(Ks + w * 32)[i], f, acc);
     }
     Oc[i] = acc;
   }
@@ -484,9 +450,7 @@ int launch_hd(const AttnDecArgs& a, cudaStream_t st) {
     cudaMemsetAsync(tbuf, 0, tn * 8, st);
     b.trace = tbuf;
   }
-  const CUtensorMap* map = kv_pool_map(a.pool_base, a.pool_bytes, HD, 32);
-  const int64_t row0 = ((const char*)a.kv_pool - (const char*)a.pool_base) / (HD * 2);
-  launch_pdl_cluster(attn_dec_cl_kernel<HD>, grid, dim3(nw * 32), smem, st, CL, b, *map, row0);
+  launch_pdl_cluster(attn_dec_cl_kernel<HD>, grid, dim3(nw * 32), smem, st, CL, b);
   count_launch();
   if (tr) {
     std::vector<unsigned long long> h(tn);
@@ -513,8 +477,7 @@ int launch_hd(const AttnDecArgs& a, cudaStream_t st) {
 // query heads per kv head while one wave of clusters covers the grid
 bool attn_dec_cl_ok(const AttnDecArgs& a) {
   const int G = a.H / a.kvh;
-  return a.kv_dtype == kKVBF16 && (a.hd == 64 || a.hd == 128) && G <= GM && a.pool_base &&
-         kv_pool_map(a.pool_base, a.pool_bytes, a.hd, 32) &&
+  return a.kv_dtype == kKVBF16 && (a.hd == 64 || a.hd == 128) && G <= GM &&
          (int64_t)a.width * a.kvh * CL <= 4 * 148;
 }
 
