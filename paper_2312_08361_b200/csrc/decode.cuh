@@ -64,8 +64,6 @@ struct AttnDecArgs {
   RowStat* st_out;               // [H][width] partial stats of ctx (P = H)
   unsigned long long* trace;     // debug (SP_ATTN_TRACE): per-CTA phase timestamps, or null
   int nsub;                      // 128-position sub-chunks streamed per CTA (MMA kernel; 0 = 1)
-  const void* pool_base;         // the span's whole KV pool (tensor-map base; null = none)
-  int64_t pool_bytes;
 };
 
 // returns P_out: the number of ctx partial statistics per row written to

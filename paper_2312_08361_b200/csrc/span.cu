@@ -444,7 +444,6 @@ int run_span_decode_tc(sp_span* s, sp_kv* kv, int b0, int b1, float* y, int widt
   at.page_table = kv->d_table; at.max_pages = s->max_pages;
   at.rope_cos = s->rope_cos; at.rope_sin = s->rope_sin; at.alibi = s->alibi;
   at.ctx = s->ctx; at.part = s->attn_part; at.counters = s->attn_cnt; at.st_out = s->st_ctx;
-  at.pool_base = s->pool; at.pool_bytes = s->block_stride * (s->end - s->start);
   for (int b = b0 - s->start; b < b1 - s->start; ++b) {
     BlockW& W = s->blocks[b];
     const bool last = (b == b1 - s->start - 1);
@@ -637,7 +636,6 @@ int run_span_decode_wide(sp_span* s, sp_kv* kv, int b0, int b1, float* y, int wi
   at.page_table = kv->d_table; at.max_pages = s->max_pages;
   at.rope_cos = s->rope_cos; at.rope_sin = s->rope_sin; at.alibi = s->alibi;
   at.ctx = s->ctx; at.part = s->attn_part; at.counters = s->attn_cnt; at.st_out = nullptr;
-  at.pool_base = s->pool; at.pool_bytes = s->block_stride * (s->end - s->start);
   auto gemm = [&](void* w, float* sc, int64_t N, int64_t K, float* out, int64_t ldy,
                   const float* res, int epi) {
     ProfScope ps(s, PC_GEMV, (double)N * K + 4.0 * N + 2.0 * Mp * K + 4.0 * R * ldy,
