@@ -583,6 +583,9 @@ def run_b200(args) -> None:
             "decode_breakdown_ms_per_tick_evented": {k: dec_prof[i]["ms"] / ticks for i, k in
                                                      enumerate(["gemv", "gemm", "attn_decode",
                                                                 "attn_prefill", "other"])},
+            "decode_breakdown_note": "a second pass with CUDA events around every launch "
+                                     "(event-inflated: the sum exceeds ms_per_step; it only "
+                                     "apportions the step)",
             "e2e": e2e, "cpu_baseline": cpu, "clocks": clk, "gpu_launches": int(launches),
             "weight_gen_s": t_gen, "weight_bytes_per_gpu": span.weight_bytes,
         }
