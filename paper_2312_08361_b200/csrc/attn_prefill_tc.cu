@@ -439,16 +439,35 @@ attn_prefill_tc_kernel(AttnArgs a, const __grid_constant__ CUtensorMap kvmap, in
       PF_T(5, pf_t);
       // p = exp2(s - m) (ex2.approx.ftz(-inf) = +0: masked keys need no test);
       // four partial sums for instruction-level parallelism
-      float ps4[4] = {0.f, 0.f, 0.f, 0.f};
+      // (paired f32 arithmetic, FADD2: the softmax warps are issue-bound)
+      uint64_t acc2[4] = {0, 0, 0, 0};
       uint32_t pk[SC / 2];
+      uint64_t mm;
+      asm("mov.b64 %0, {%1, %1};" : "=l"(mm) : "f"(m_used));
 #pragma unroll
       for (int i = 0; i < SC; i += 2) {
-        const float p0 = ex2_approx(s[i] - m_used);
-        const float p1 = ex2_approx(s[i + 1] - m_used);
-        ps4[(i >> 1) & 3] += p0 + p1;
+        uint64_t x2, d2;
+        asm("mov.b64 %0, {%1, %2};" : "=l"(x2) : "f"(s[i]), "f"(s[i + 1]));
+        asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d2) : "l"(x2), "l"(mm));
+        float d0, d1;
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(d0), "=f"(d1) : "l"(d2));
+        const float p0 = ex2_approx(d0);
+        const float p1 = ex2_approx(d1);
+        uint64_t p2;
+        asm("mov.b64 %0, {%1, %2};" : "=l"(p2) : "f"(p0), "f"(p1));
+        asm("add.rn.f32x2 %0, %0, %1;" : "+l"(acc2[(i >> 1) & 3]) : "l"(p2));
         pk[i / 2] = bf2(p0, p1);
       }
-      const float psum = (ps4[0] + ps4[1]) + (ps4[2] + ps4[3]);
+      float psum;
+      {
+        uint64_t t01, t23, t;
+        asm("add.rn.f32x2 %0, %1, %2;" : "=l"(t01) : "l"(acc2[0]), "l"(acc2[1]));
+        asm("add.rn.f32x2 %0, %1, %2;" : "=l"(t23) : "l"(acc2[2]), "l"(acc2[3]));
+        asm("add.rn.f32x2 %0, %1, %2;" : "=l"(t) : "l"(t01), "l"(t23));
+        float a0, a1;
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(a0), "=f"(a1) : "l"(t));
+        psum = a0 + a1;
+      }
       // P_j -> TMEM (A operand of O += P V): this warp's 64 keys = 32 columns
       tmem_st16(tb + lane_addr + P_COL + st * (BK / 2) + hf * (SC / 2), pk);
       if constexpr (SC / 2 > 16)
