@@ -402,7 +402,10 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const float tt = (NORMT == NORM_LN) ? (v[j] - mu) : v[j];
-          q[j] = __float2int_rn(tt * sc);
+          // rint(tt * sc) by the 1.5 * 2^23 shift (sc is a power of two, so the
+          // product is exact and this equals __float2int_rn(tt * sc), |q| < 2^22):
+          // FFMA + integer add instead of FMUL + F2I on the slower conversion pipe
+          q[j] = __float_as_int(fmaf(tt, sc, 12582912.0f)) - 0x4B400000;
         }
         bb[st][0] = digits4(q[0], q[1], q[2], q[3], bbias[0], bsel_lo[0], 0x5410);
         bb[st][1] = digits4(q[4], q[5], q[6], q[7], bbias[0], bsel_lo[0], 0x5410);
@@ -417,7 +420,8 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
 #pragma unroll
       for (int t = 0; t < RT; ++t) {
         const uint4 wv = *reinterpret_cast<const uint4*>(stage + (t * 32 + lane) * 16);
-        int c[4] = {0, 0, 0, 0};
+        // the -63 * sum(B) level offset seeds the accumulator (no per-tile subtraction)
+        int c[4] = {-off[0], -off[1], -off[2], -off[3]};
         // entries 0-7 and 8-15 go to the tensor pipe as two A fragments (each
         // zero where the other table holds the code) instead of being OR-ed
         const uint32_t hx = wv.x >> 16, hy = wv.y >> 16, hz = wv.z >> 16, hw = wv.w >> 16;
@@ -436,10 +440,10 @@ gemv3_kernel(GemvArgs a, int r0, int Rn, int Rs, int64_t units, int64_t warps_to
         // block scales of rows g8 (h = 0) and g8 + 8 (h = 1): bytes 2t, 2t + 1
         const int q0 = (qw[t >> 1] >> (16 * (t & 1))) & 0xFF;
         const int q1 = (qw[t >> 1] >> (16 * (t & 1) + 8)) & 0xFF;
-        acc[t][0][0] += (c[0] - off[0]) * q0;
-        acc[t][0][1] += (c[1] - off[1]) * q0;
-        acc[t][0][2] += (c[2] - off[2]) * q1;
-        acc[t][0][3] += (c[3] - off[3]) * q1;
+        acc[t][0][0] += c[0] * q0;
+        acc[t][0][1] += c[1] * q0;
+        acc[t][0][2] += c[2] * q1;
+        acc[t][0][3] += c[3] * q1;
       }
     } else {
 #pragma unroll
