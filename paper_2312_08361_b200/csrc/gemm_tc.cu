@@ -19,6 +19,7 @@
 // * Warp roles: warp 0 = TMA producer (one lane), warp 1 = MMA issuer (one
 //   lane), warp 2 = TMEM allocator, warps 4..7 = epilogue (tcgen05.ld, scale,
 //   residual / GELU / SwiGLU, store).  3-stage smem ring of 64 KB stages.
+#include <cooperative_groups.h>
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -774,6 +775,133 @@ __global__ void __launch_bounds__(NT) digitize_reg_kernel(const float* __restric
   }
 }
 
+
+// few-row digitize (wide decode, M <= 32 rows): one row per thread-block
+// cluster of CL CTAs (grid (CL, M)), each CTA holding 1/CL of the row in
+// registers; the row's sums and maximum are combined over distributed shared
+// memory in rank order (every CTA gets the same totals), so a 57 K-element
+// row is read by 8 SMs at once instead of one CTA streaming it alone.
+template <int NCH>
+__global__ void __launch_bounds__(256) digitize_cl_kernel(const float* __restrict__ x, int64_t ldx,
+                                                         int64_t M, int64_t K, int norm,
+                                                         const float* __restrict__ g,
+                                                         const float* __restrict__ b,
+                                                         uint8_t* planes, int64_t plane_stride,
+                                                         int* exps, int rt) {
+  namespace cgx = cooperative_groups;
+  constexpr int NT = 256, NW = NT / 32;
+  cgx::cluster_group cluster = cgx::this_cluster();
+  const int CL = (int)cluster.num_blocks(), rank = (int)cluster.block_rank();
+  __shared__ float red[NW];
+  __shared__ float part[3];                        // this CTA's (sum, centred sumsq, amax)
+  const int64_t m = blockIdx.y;
+  const float* xr = x + m * ldx;
+  const int nchunk = (int)(K >> 4);
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  float v[NCH][16];
+#pragma unroll
+  for (int j = 0; j < NCH; ++j) {
+    const int c = (rank + CL * j) * NT + t;
+    if (c < nchunk) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float4 f = __ldcs(reinterpret_cast<const float4*>(xr + (int64_t)c * 16) + q);
+        v[j][4 * q] = f.x; v[j][4 * q + 1] = f.y; v[j][4 * q + 2] = f.z; v[j][4 * q + 3] = f.w;
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 16; ++e) v[j][e] = 0.f;
+    }
+  }
+  // cluster-wide reduction of one value (sum or max), rank order
+  auto csum = [&](float a, int slot, bool is_max) {
+    a = is_max ? warp_max(a) : warp_sum(a);
+    if (lane == 0) red[warp] = a;
+    __syncthreads();
+    if (t == 0) {
+      float r = is_max ? 0.f : 0.f;
+      for (int w = 0; w < NW; ++w) r = is_max ? fmaxf(r, red[w]) : r + red[w];
+      part[slot] = r;
+    }
+    cluster.sync();
+    float r = 0.f;
+    for (int c = 0; c < CL; ++c) {
+      const float pv = *cluster.map_shared_rank(&part[slot], c);
+      r = is_max ? fmaxf(r, pv) : r + pv;
+    }
+    return r;
+  };
+  float s = 0.f, s2 = 0.f;
+#pragma unroll
+  for (int j = 0; j < NCH; ++j)
+#pragma unroll
+    for (int e = 0; e < 16; ++e) { s += v[j][e]; s2 = fmaf(v[j][e], v[j][e], s2); }
+  if (norm != 0) {
+    float mu = 0.f, rstd;
+    if (norm == 2) {
+      mu = csum(s, 0, false) / (float)K;
+      float q2 = 0.f;
+#pragma unroll
+      for (int j = 0; j < NCH; ++j) {
+        const int c = (rank + CL * j) * NT + t;
+        if (c < nchunk)
+#pragma unroll
+          for (int e = 0; e < 16; ++e) { const float d = v[j][e] - mu; q2 = fmaf(d, d, q2); }
+      }
+      rstd = 1.0f / sqrtf(csum(q2, 1, false) / (float)K + 1e-5f);
+    } else {
+      rstd = 1.0f / sqrtf(csum(s2, 1, false) / (float)K + 1e-5f);
+    }
+#pragma unroll
+    for (int j = 0; j < NCH; ++j) {
+      const int c = (rank + CL * j) * NT + t;
+      if (c >= nchunk) continue;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float4 gg = __ldg(reinterpret_cast<const float4*>(g + (int64_t)c * 16) + q);
+        const float gq[4] = {gg.x, gg.y, gg.z, gg.w};
+        float bq[4] = {0.f, 0.f, 0.f, 0.f};
+        if (norm == 2) {
+          const float4 bb = __ldg(reinterpret_cast<const float4*>(b + (int64_t)c * 16) + q);
+          bq[0] = bb.x; bq[1] = bb.y; bq[2] = bb.z; bq[3] = bb.w;
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          float& vv = v[j][4 * q + e];
+          vv = (norm == 1) ? vv * rstd * gq[e] : (vv - mu) * rstd * gq[e] + bq[e];
+        }
+      }
+    }
+  }
+  float amax = 0.f;
+#pragma unroll
+  for (int j = 0; j < NCH; ++j)
+#pragma unroll
+    for (int e = 0; e < 16; ++e) amax = fmaxf(amax, fabsf(v[j][e]));
+  amax = csum(amax, 2, true);
+  int e2 = 0;
+  if (amax > 0.f) frexpf(amax, &e2);                 // |v| < 2^e
+  const float sc = amax > 0.f ? ldexpf(1.0f, 14 - e2) : 0.f;
+  if (t == 0 && rank == 0) exps[m] = e2;
+#pragma unroll
+  for (int j = 0; j < NCH; ++j) {
+    const int c = (rank + CL * j) * NT + t;
+    if (c >= nchunk) continue;
+    __align__(16) int8_t d0[16], d1[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int qv = __float2int_rn(v[j][i] * sc);    // |q| <= 2^14
+      const int lo = (int)(int8_t)(qv & 0xFF);
+      d1[i] = (int8_t)lo;
+      d0[i] = (int8_t)((qv - lo) >> 8);
+    }
+    const int64_t off = cm_offset_rt(m, (int64_t)c * 16, K, rt);
+    *reinterpret_cast<uint4*>(planes + off) = *reinterpret_cast<uint4*>(d0);
+    *reinterpret_cast<uint4*>(planes + plane_stride + off) = *reinterpret_cast<uint4*>(d1);
+  }
+  cluster.sync();                                  // peers' partials read before exit
+}
+
 // bf16 operands for the tcgen05 GEMM (bf16 weights, Llama-2-7B): the
 // (normalised) row as hi = bf16(x) and lo = bf16(x - hi) planes in the same
 // core-matrix layout (16-byte rows = 8 elements); no exponent
@@ -867,6 +995,33 @@ void launch_digitize(const float* x, int64_t ldx, int64_t M, int64_t K, int norm
   // independent in the MMA and the GEMM epilogue drops rows >= M
   const unsigned grid = (unsigned)M;
   const bool al = (K % 16 == 0) && (ldx % 4 == 0);
+  static const bool cl_ok = getenv("SP_DIGITIZE_CL") ? atoi(getenv("SP_DIGITIZE_CL")) != 0 : true;
+  if (cl_ok && al && M <= 32 && K > 256 * 16 * 2 && K <= 8 * 256 * 16 * 4) {
+    // few rows (wide decode): a cluster of CL CTAs per row, 256 threads x 2-4 chunks each
+    const int64_t nchunk = K / 16;
+    int CLN = (int)((nchunk + 256 * 2 - 1) / (256 * 2));
+    const bool four = CLN > 8;
+    if (four) CLN = (int)((nchunk + 256 * 4 - 1) / (256 * 4));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)CLN, (unsigned)M);
+    cfg.blockDim = dim3(256);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CLN;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (four)
+      cudaLaunchKernelEx(&cfg, digitize_cl_kernel<4>, x, ldx, M, K, norm, g, b, planes,
+                         plane_stride, exps, rt);
+    else
+      cudaLaunchKernelEx(&cfg, digitize_cl_kernel<2>, x, ldx, M, K, norm, g, b, planes,
+                         plane_stride, exps, rt);
+    count_launch();
+    return;
+  }
   if (al && K <= 256 * 16 * 2)
     digitize_reg_kernel<256, 2><<<grid, 256, 0, st>>>(x, ldx, M, K, norm, g, b, planes, plane_stride, exps, rt);
   else if (al && K <= 256 * 16 * 4)
