@@ -310,6 +310,8 @@ def run_b200(args) -> None:
         _lib.check(lib.sp_span_set_option(span.handle, 5, int(os.environ["SP_ATTN_NSUB"])))
     if os.environ.get("SP_ATTN_CLUSTER"):     # A/B switch: decode-attention cluster merge
         _lib.check(lib.sp_span_set_option(span.handle, 6, int(os.environ["SP_ATTN_CLUSTER"])))
+    if args.wide_from:                        # option 11 (throughput setting: 3)
+        _lib.check(lib.sp_span_set_option(span.handle, 11, args.wide_from))
     d = cfg.hidden_dim
     stream = torch.cuda.current_stream(dev)
 
@@ -547,7 +549,7 @@ def run_b200(args) -> None:
                                    f"{B}, context {args.prefill}+, {n_blocks} blocks over "
                                    f"{world} GPU(s), {sessions} session(s) in flight",
                        "span_per_gpu": [start, end], "prefill_tokens": args.prefill,
-                       "batch": B,
+                       "batch": B, "wide_from": args.wide_from or 9,
                        "wire": ({"bytes_per_hop": pipe.wire_bytes_per_token,
                                  "relay_checksum": pipe.check is not None,
                                  "codec": "int8 codes + f32 scales per 64 (SP/quantize.py)"}
@@ -610,6 +612,9 @@ def main() -> None:
     ap.add_argument("--weights", default="", choices=["", "int8", "nf4", "bf16"],
                     help="override the config's weight format (nf4: the paper's 4-bit format)")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--wide-from", type=int, default=0,
+                    help="option 11: decode rows per step from which the linears run on the "
+                         "tcgen05 GEMM (0 = library default 9; 3 = throughput setting)")
     args = ap.parse_args()
     self_launch(args)
     if args.impl == "reference":

@@ -604,7 +604,7 @@ int run_span_prefill_tc(sp_span* s, sp_kv* kv, int b0, int b1, float* y, float* 
   return SP_OK;
 }
 
-// Wide decode (n_new == 1, width >= kWideDecode rows, int8): the linears run
+// Wide decode (n_new == 1, width >= g_wide_from rows, int8): the linears run
 // on the tcgen05 GEMM (one pass over the weights for all rows, 15-bit digit
 // planes) instead of the GEMV, whose per-unit digit/MMA work makes it
 // latency-bound beyond a few rows; attention stays the fused decode kernel.
@@ -612,7 +612,11 @@ int run_span_prefill_tc(sp_span* s, sp_kv* kv, int b0, int b1, float* y, float* 
 // the width (tests/test_gpu_span.py::test_decode_width_invariant); from 9 rows
 // the GEMM computes the same exact integer products of the same 15-bit codes
 // but folds the norm in its own reduction order (last-bit differences).
-constexpr int kWideDecode = 9;
+// option 11: the row count from which decode takes the GEMM path (default 9 keeps
+// every step of 1-8 rows bit-identical per row; from 3 rows the GEMM path is
+// faster: BLOOM-176B shape batch 8 125.6 -> 207.1, 70B batch 8 253.9 -> 501.8
+// steps/s per 8 blocks; steps of >= 3 rows then agree with each other bit for bit)
+int g_wide_from = getenv("SP_WIDE_FROM") ? atoi(getenv("SP_WIDE_FROM")) : 9;
 
 int run_span_decode_wide(sp_span* s, sp_kv* kv, int b0, int b1, float* y, int width,
                          cudaStream_t st) {
@@ -675,7 +679,7 @@ int run_span_decode_wide(sp_span* s, sp_kv* kv, int b0, int b1, float* y, int wi
 
 int run_span(sp_span* s, sp_kv* kv, int b0, int b1, float* y, float* record, int width,
              int n_new, cudaStream_t st) {
-  if (n_new == 1 && width >= kWideDecode && tc_ok(s) && s->cfg.weight_dtype == kI8 &&
+  if (n_new == 1 && width >= (g_wide_from > 1 ? g_wide_from : 2) && tc_ok(s) && s->cfg.weight_dtype == kI8 &&
       s->use_tc_prefill && !record)
     return run_span_decode_wide(s, kv, b0, b1, y, width, st);
   if (n_new == 1 && s->cfg.weight_dtype != kF32 && !record)
@@ -1154,6 +1158,7 @@ int sp_span_set_option(sp_span* s, int32_t option, int32_t value) {
   else if (option == 8) g_attn_tc = value != 0;
   else if (option == 9) g_attn_mha = value != 0;
   else if (option == 10) g_tc_wide = value != 0;
+  else if (option == 11) g_wide_from = value;
   else SP_FAIL(SP_ERR_ARG, "unknown option");
   return SP_OK;
 }
