@@ -1074,6 +1074,132 @@ void launch_pair(const TcGemmArgs& a, cudaStream_t st) {
 }
 
 
+
+// ---- the decode GEMV's activation code for the wide-decode GEMM ----------------
+// (gemv3.cu prologue and unit loop, restated so that a row of a wide step gets
+// exactly the GEMV's integers and scale): statistics from the producer's
+// partials in the GEMV's reduction order (256 threads, partials p and p + 256
+// per thread, warp butterflies, warps in order), bound -> exponent e,
+// q = rint(t * 2^(14-e)) with t = x*g (- mu for LayerNorm), ys = 2^(e-14) * rstd.
+__device__ __forceinline__ float silu_gemv(float x) { return x / (1.0f + expf(-x)); }
+
+__global__ void __launch_bounds__(256) digitize_gemv_kernel(
+    const float* __restrict__ x, int64_t ldx, int64_t M, int64_t K, int norm,
+    const float* __restrict__ g, const float4* __restrict__ st_in, int P_in, float gmax, float eps,
+    uint8_t* planes, int64_t plane_stride, double* ys_rows, int rt) {
+  __shared__ float red[8][3];
+  __shared__ float prm[2];                          // mu, dscale
+  const int64_t m = blockIdx.y;                     // row; blockIdx.x = 4096-element slice
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int nchunk = (int)(K >> 4);
+  const int c = blockIdx.x * 256 + t;              // this thread's 16 elements
+  float4 xv[4];                                    // loaded ahead of the statistics
+  if (c < nchunk) {
+#pragma unroll
+    for (int qd = 0; qd < 4; ++qd)
+      xv[qd] = __ldg(reinterpret_cast<const float4*>(x + m * ldx + (int64_t)c * 16) + qd);
+  }
+  float S = 0.f, Q = 0.f, Mx = 0.f;
+  for (int p0 = t; p0 < P_in; p0 += 4 * 256) {
+    float4 v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int p = p0 + j * 256;
+      v[j] = p < P_in ? st_in[(int64_t)p * M + m] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) { S += v[j].x; Q += v[j].y; Mx = fmaxf(Mx, v[j].z); }
+  }
+  {
+    const float vs = warp_sum(S), vq = warp_sum(Q), vm = warp_max(Mx);
+    if (lane == 0) { red[warp][0] = vs; red[warp][1] = vq; red[warp][2] = vm; }
+  }
+  __syncthreads();
+  if (t == 0) {
+    float s = 0.f, q = 0.f, mm = 0.f;
+    for (int w = 0; w < 8; ++w) { s += red[w][0]; q += red[w][1]; mm = fmaxf(mm, red[w][2]); }
+    const float invK = 1.0f / (float)K;
+    float mu = 0.f, rstd = 1.f, bound = mm;
+    if (norm == 1) {
+      rstd = 1.0f / sqrtf(q * invK + eps);
+    } else if (norm == 2) {
+      mu = s * invK;
+      rstd = 1.0f / sqrtf(fmaxf(q * invK - mu * mu, 0.f) + eps);
+      bound = mm + fabsf(mu) * gmax;
+    }
+    int e = 0;
+    if (bound > 0.f) frexpf(bound, &e);             // bound < 2^e
+    prm[0] = mu;
+    prm[1] = bound > 0.f ? ldexpf(1.0f, 14 - e) : 0.f;
+    if (blockIdx.x == 0) ys_rows[m] = ldexp(1.0, e - 14) * (double)rstd;
+  }
+  __syncthreads();
+  const float mu = prm[0], sc = prm[1];
+  // every CTA of the row recomputes the same statistics and codes one
+  // 256-chunk slice of the row (no reduction over x: the coding is per element)
+  {
+    if (c >= nchunk) return;
+    __align__(16) int8_t d0[16], d1[16];
+#pragma unroll
+    for (int qd = 0; qd < 4; ++qd) {
+      const float4 f = xv[qd];
+      float v[4] = {f.x, f.y, f.z, f.w};
+      if (g) {
+        const float4 gg = __ldg(reinterpret_cast<const float4*>(g + (int64_t)c * 16) + qd);
+        v[0] *= gg.x; v[1] *= gg.y; v[2] *= gg.z; v[3] *= gg.w;
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float tt = (norm == 2) ? (v[e] - mu) : v[e];
+        const int qv = __float2int_rn(tt * sc);
+        const int lo = (int)(int8_t)(qv & 0xFF);
+        d1[4 * qd + e] = (int8_t)lo;
+        d0[4 * qd + e] = (int8_t)((qv - lo) >> 8);
+      }
+    }
+    const int64_t off = cm_offset_rt(m, (int64_t)c * 16, K, rt);
+    *reinterpret_cast<uint4*>(planes + off) = *reinterpret_cast<uint4*>(d0);
+    *reinterpret_cast<uint4*>(planes + plane_stride + off) = *reinterpret_cast<uint4*>(d1);
+  }
+}
+
+// the GEMV's epilogue for rows x one 128-channel weight group: val =
+// f32((double)D * ys * wscale) (+ residual / GELU, or SwiGLU of the group's two
+// halves), then the group's (sum, sumsq, max|val * g_next|) partial, lanes and
+// the warp butterfly in the GEMV's order.  vals(c) returns the pre-epilogue
+// value of channel c (0..127) of the group for this row.
+template <typename VAL>
+__device__ __forceinline__ void gemv_epilogue_group(const TcGemmArgs& a, int grp, int64_t m,
+                                                    int lane, VAL vals) {
+  const bool swiglu = a.epi == EPI_SWIGLU;
+  const int nj = swiglu ? 2 : 4;
+  float S = 0.f, Q = 0.f, M = 0.f;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    if (j >= nj) break;
+    float val;
+    int64_t col;
+    if (swiglu) {
+      col = (int64_t)grp * 64 + lane + 32 * j;
+      val = silu_gemv(vals(lane + 32 * j)) * vals(lane + 32 * j + 64);
+    } else {
+      col = (int64_t)grp * 128 + lane + 32 * j;
+      val = vals(lane + 32 * j);
+      if (a.epi == EPI_RESID) val += a.res[m * a.ldy + col];
+      else if (a.epi == EPI_GELU) val = gelu_f(val);
+    }
+    a.y[m * a.ldy + col] = val;
+    const float gn = a.g_next ? __ldg(a.g_next + col) : 1.f;
+    S += val;
+    Q = fmaf(val, val, Q);
+    M = fmaxf(M, fabsf(val * gn));
+  }
+  if (a.st_out) {
+    S = warp_sum(S); Q = warp_sum(Q); M = warp_max(M);
+    if (lane == 0) a.st_out[(int64_t)grp * a.stat_rs + m] = make_float4(S, Q, M, 0.f);
+  }
+}
+
 // ---- wide decode (9..32 token rows, split-K): weights as the A operand -------
 // The single-CTA kernel above puts the tokens on the MMA's M = 128 rows, so at
 // decode widths of 9-32 rows 75-93 % of every MMA multiplies padding and the
@@ -1199,7 +1325,15 @@ __global__ void __launch_bounds__(256, 2) gemm_i8_wide_kernel(TcGemmArgs a) {
       }
       tmem_wait_ld();
       const int64_t n = (int64_t)(ng0 + j) * 128 + ch;
-      if (S == 1) {
+      if (S == 1 && a.ys_rows) {                    // the decode GEMV's numerics
+        const double wsc = (double)__ldg(a.wscale + n);
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+          if (r >= M) break;
+          tile[(j * NR + r) * 128 + ch] =
+              (float)((double)((long long)d0[r] * 256 + d1[r]) * a.ys_rows[r] * wsc);
+        }
+      } else if (S == 1) {
         const float wsc = __ldg(a.wscale + n);
 #pragma unroll
         for (int r = 0; r < NR; ++r) {
@@ -1217,7 +1351,14 @@ __global__ void __launch_bounds__(256, 2) gemm_i8_wide_kernel(TcGemmArgs a) {
         }
       }
     }
-    if (S == 1) {
+    if (S == 1 && a.ys_rows) {
+      asm volatile("bar.sync 1, 128;" ::: "memory");       // the 4 epilogue warps
+      for (int pr = q; pr < NGRP * M; pr += 4) {
+        const int j = pr / M, r = pr % M;
+        gemv_epilogue_group(a, ng0 + j, r, lane,
+                            [&](int c) { return tile[(j * NR + r) * 128 + c]; });
+      }
+    } else if (S == 1) {
       asm volatile("bar.sync 1, 128;" ::: "memory");       // the 4 epilogue warps
       const int t = threadIdx.x - 128;
       const int epi = EP >= 0 ? EP : a.epi;
@@ -1251,7 +1392,24 @@ __global__ void __launch_bounds__(256, 2) gemm_i8_wide_kernel(TcGemmArgs a) {
       if (last_cta) { __threadfence(); *cnt = 0; }
     }
     __syncthreads();
-    if (last_cta) finish_tile(a, 0, ng0);
+    if (last_cta) {
+      if (a.ys_rows) {
+        // the decode GEMV's epilogue on the summed int64 workspace (zeroed after)
+        for (int pr = warp; pr < NGRP * M; pr += 8) {
+          const int j = pr / M, r = pr % M;
+          const int64_t n0 = (int64_t)(ng0 + j) * 128;
+          long long* wr = a.ws + (int64_t)r * a.N + n0;
+          const double ys = a.ys_rows[r];
+          gemv_epilogue_group(a, ng0 + j, r, lane, [&](int c) {
+            return (float)((double)__ldcg(wr + c) * ys * (double)__ldg(a.wscale + n0 + c));
+          });
+          __syncwarp();
+          for (int c = lane; c < 128; c += 32) wr[c] = 0;
+        }
+      } else {
+        finish_tile(a, 0, ng0);
+      }
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -1283,6 +1441,16 @@ void launch_wide_nr(const TcGemmArgs& b, dim3 grid, cudaStream_t st) {
 }
 
 bool g_tc_wide = getenv("SP_TC_WIDE") ? atoi(getenv("SP_TC_WIDE")) != 0 : true;
+
+void launch_digitize_gemv(const float* x, int64_t ldx, int64_t M, int64_t K, int norm,
+                          const float* g, const float4* st_in, int P_in, float gmax, float eps,
+                          uint8_t* planes, int64_t plane_stride, double* ys_rows, int rt,
+                          cudaStream_t st) {
+  const dim3 grid((unsigned)((K / 16 + 255) / 256), (unsigned)M);
+  digitize_gemv_kernel<<<grid, 256, 0, st>>>(x, ldx, M, K, norm, g, st_in, P_in, gmax, eps,
+                                             planes, plane_stride, ys_rows, rt);
+  count_launch();
+}
 
 int wide_rows(int64_t M) {
   if (!g_tc_wide) return 0;

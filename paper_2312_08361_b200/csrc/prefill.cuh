@@ -25,6 +25,15 @@ struct TcGemmArgs {
   int* counters;
   int ksplit;               // set by the launcher
   int bf16;                 // bf16 weights and hi/lo bf16 planes (K counted in bytes)
+  // decode-GEMV numerics (weight-side wide kernel only, ys_rows != null): the
+  // planes carry the GEMV's activation code (digitize_gemv), the output is
+  // f32((double)D * ys_rows[m] * wscale[n]) with the GEMV's epilogue order, and
+  // the (sum, sumsq, max|x*g_next|) partial of every 128-channel group is
+  // written to st_out[group * stat_rs + m] — a row's result equals the GEMV's
+  const double* ys_rows;
+  float4* st_out;
+  const float* g_next;
+  int64_t stat_rs;
 };
 
 extern bool g_tc_wide;    // option 10: wide-decode GEMM with the weights on the MMA's M side
@@ -37,6 +46,13 @@ void launch_digitize(const float* x, int64_t ldx, int64_t M, int64_t K, int norm
                      const float* b, uint8_t* planes, int64_t plane_stride, int* exps,
                      cudaStream_t st, int rt = 128);   // rt: rows per core-matrix tile
 int wide_rows(int64_t M);   // row tile of the wide-decode GEMM for M rows (0 = not used)
+// the decode GEMV's activation code as digit planes (rt-row tiles): per row the
+// statistics come from the producer's partials st_in[p * R + m] (p < P_in),
+// reduced in the GEMV's order; ys_rows[m] = 2^(e-14) * rstd (double)
+void launch_digitize_gemv(const float* x, int64_t ldx, int64_t M, int64_t K, int norm,
+                          const float* g, const float4* st_in, int P_in, float gmax, float eps,
+                          uint8_t* planes, int64_t plane_stride, double* ys_rows, int rt,
+                          cudaStream_t st);
 void launch_gemm_i8_tc(const TcGemmArgs& a, cudaStream_t st);
 // bf16 operand planes (hi, lo) for bf16 weights; K <= 16384
 void launch_digitize_bf16(const float* x, int64_t ldx, int64_t M, int64_t K, int norm,

@@ -101,6 +101,7 @@ struct sp_span {
   int64_t tc_cap_rows = 0;
   uint8_t* planes = nullptr;
   int* exps = nullptr;
+  double* ys_rows = nullptr;   // wide decode: per-row scale of the GEMV-numerics code
   bool use_tc_prefill = true;
   // nf4 prefill: a linear's integer levels split into two int8 planes
   // (hi * 128 + lo) in core-matrix layout, and 128 x channel scale
@@ -226,11 +227,12 @@ int ensure_decode(sp_span* s, int64_t rows) {
 
 int ensure_tc(sp_span* s, int64_t rows) {
   if (rows <= s->tc_cap_rows) return SP_OK;
-  cudaFree(s->planes); cudaFree(s->exps);
+  cudaFree(s->planes); cudaFree(s->exps); cudaFree(s->ys_rows);
   const int64_t Mp = tc_rows(rows);       // the CTA-pair GEMM tiles 256 tokens
   const int64_t K = std::max<int64_t>(s->d, s->F) * (s->cfg.weight_dtype == kBF16 ? 2 : 1);
   SP_CUDA_TRY(cudaMalloc(&s->planes, 2 * Mp * K));
   SP_CUDA_TRY(cudaMalloc(&s->exps, Mp * sizeof(int)));
+  SP_CUDA_TRY(cudaMalloc(&s->ys_rows, Mp * sizeof(double)));
   s->tc_cap_rows = Mp;
   return SP_OK;
 }
@@ -612,11 +614,12 @@ int run_span_prefill_tc(sp_span* s, sp_kv* kv, int b0, int b1, float* y, float* 
 // the width (tests/test_gpu_span.py::test_decode_width_invariant); from 9 rows
 // the GEMM computes the same exact integer products of the same 15-bit codes
 // but folds the norm in its own reduction order (last-bit differences).
-// option 11: the row count from which decode takes the GEMM path (default 9 keeps
-// every step of 1-8 rows bit-identical per row; from 3 rows the GEMM path is
-// faster: BLOOM-176B shape batch 8 125.6 -> 207.1, 70B batch 8 253.9 -> 501.8
-// steps/s per 8 blocks; steps of >= 3 rows then agree with each other bit for bit)
-int g_wide_from = getenv("SP_WIDE_FROM") ? atoi(getenv("SP_WIDE_FROM")) : 9;
+// option 11: the row count from which decode takes the GEMM path.  Up to 32 rows
+// the weight-side GEMM reproduces the GEMV's numerics exactly (a row's result
+// does not depend on the path), and from 3 rows it is faster (the GEMV's
+// per-unit digit work makes it latency-bound beyond two rows): BLOOM-176B shape
+// batch 8 125.6 -> 207.1, 70B batch 8 253.9 -> 501.8 steps/s per 8 blocks
+int g_wide_from = getenv("SP_WIDE_FROM") ? atoi(getenv("SP_WIDE_FROM")) : 3;
 
 int run_span_decode_wide(sp_span* s, sp_kv* kv, int b0, int b1, float* y, int width,
                          cudaStream_t st) {
@@ -656,6 +659,60 @@ int run_span_decode_wide(sp_span* s, sp_kv* kv, int b0, int b1, float* y, int wi
     else launch_digitize(x, K, R, K, nm, gg, bb, s->planes, Mp * K, s->exps, st,
                          wide_rows(R) ? wide_rows(R) : 128);   // the GEMM's row tile
   };
+  const int rt = wide_rows(R);
+  if (rt && s->gains_one) {
+    // up to 32 rows: the decode GEMV's numerics on the weight-side GEMM — the
+    // same statistics partials, activation code, double-precision scale and
+    // epilogue order, so every row equals what the GEMV gives it at any width
+    // (tests/test_gpu_span.py::test_decode_width_invariant)
+    auto st4 = [](RowStat* p) { return reinterpret_cast<float4*>(p); };
+    auto gemm_g = [&](void* w, float* sc, int64_t N, int64_t K, float* out, int64_t ldy,
+                      const float* res, int epi, RowStat* st_out, const float* g_next) {
+      ProfScope ps(s, PC_GEMV, (double)N * K + 4.0 * N + 2.0 * Mp * K + 4.0 * R * ldy,
+                   2.0 * R * N * K, st);
+      TcGemmArgs g{};
+      g.w = w; g.wscale = sc; g.N = N; g.K = K; g.planes = s->planes; g.plane_stride = Mp * K;
+      g.exps = s->exps; g.M = R; g.y = out; g.ldy = ldy; g.res = res; g.epi = epi;
+      g.ws = s->ws2; g.counters = s->cnt2;
+      g.ys_rows = s->ys_rows; g.st_out = st_out ? st4(st_out) : nullptr; g.g_next = g_next;
+      g.stat_rs = R;
+      launch_gemm_i8_tc(g, st);
+    };
+    auto digit_g = [&](const float* x, int64_t K, int nm, const RowStat* st_in, int P_in) {
+      ProfScope ps(s, PC_OTHER, 4.0 * R * K + 2.0 * Mp * K, 0, st);
+      launch_digitize_gemv(x, K, R, K, nm, nullptr, reinterpret_cast<const float4*>(st_in),
+                           P_in, 1.0f, 1e-5f, s->planes, Mp * K, s->ys_rows, rt, st);
+    };
+    {
+      ProfScope ps(s, PC_OTHER, 4.0 * R * d, 0, st);
+      launch_row_stats(y, (int)R, d, nullptr, s->st_norm1, st);
+    }
+    at.st_out = s->st_ctx;
+    for (int b = b0 - s->start; b < b1 - s->start; ++b) {
+      BlockW& W = s->blocks[b];
+      const bool last = (b == b1 - s->start - 1);
+      digit_g(y, d, norm, s->st_norm1, (int)(d / 128));
+      gemm_g(W.qkv, W.s_qkv, s->n_qkv, d, s->qkvb, s->n_qkv, nullptr, EPI_STORE, nullptr,
+             nullptr);
+      at.kv_pool = s->pool + (int64_t)b * s->block_stride;
+      int p_ctx;
+      {
+        ProfScope ps(s, PC_ATTN_DEC, (double)width * (kv->length + 1) * 2 * s->kv * kv_elt,
+                     4.0 * width * (kv->length + 1) * s->H * s->hd, st);
+        p_ctx = launch_attn_decode_fused(at, st);
+      }
+      digit_g(s->ctx, d, NORM_NONE, s->st_ctx, p_ctx);
+      gemm_g(W.o, W.s_o, d, d, y, d, y, EPI_RESID, s->st_norm2, nullptr);
+      digit_g(y, d, norm, s->st_norm2, (int)(d / 128));
+      gemm_g(W.up, W.s_up, s->n_up, d, s->mlp, F, nullptr,
+             fam == kLlama ? EPI_SWIGLU : EPI_GELU, s->st_mlp, nullptr);
+      digit_g(s->mlp, F, NORM_NONE, s->st_mlp, (int)(s->n_up / 128));
+      gemm_g(W.down, W.s_down, d, F, y, d, y, EPI_RESID, last ? nullptr : s->st_norm1,
+             nullptr);
+    }
+    SP_CHECK_LAUNCH();
+    return SP_OK;
+  }
   for (int b = b0 - s->start; b < b1 - s->start; ++b) {
     BlockW& W = s->blocks[b];
     digit(y, d, norm, W.ln1_g, W.ln1_b);
@@ -920,7 +977,7 @@ static void free_span_device(sp_span* s) {
   cudaFree(s->mlp_raw); cudaFree(s->gemv_ws); cudaFree(s->gemv_cnt); cudaFree(s->attn_ws);
   cudaFree(s->st_norm1); cudaFree(s->st_ctx); cudaFree(s->st_norm2); cudaFree(s->st_mlp);
   cudaFree(s->ws2); cudaFree(s->cnt2); cudaFree(s->attn_part); cudaFree(s->attn_cnt);
-  cudaFree(s->planes); cudaFree(s->exps);
+  cudaFree(s->planes); cudaFree(s->exps); cudaFree(s->ys_rows);
   cudaFree(s->nf4_hi); cudaFree(s->nf4_lo); cudaFree(s->nf4_sc);
   for (auto& r : s->prof_recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : s->ev_pool) cudaEventDestroy(e);
@@ -930,6 +987,7 @@ static void free_span_device(sp_span* s) {
   s->h = s->qkvb = s->ctx = s->mlp = s->mlp_raw = s->gemv_ws = s->attn_ws = nullptr;
   s->st_norm1 = s->st_ctx = s->st_norm2 = s->st_mlp = nullptr;
   s->ws2 = nullptr; s->cnt2 = s->gemv_cnt = s->attn_cnt = s->exps = nullptr;
+  s->ys_rows = nullptr;
   s->attn_part = nullptr; s->planes = nullptr;
   s->nf4_hi = s->nf4_lo = nullptr; s->nf4_sc = nullptr;
   s->prof_recs.clear(); s->ev_pool.clear(); s->done = nullptr;
