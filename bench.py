@@ -549,7 +549,7 @@ def run_b200(args) -> None:
                                    f"{B}, context {args.prefill}+, {n_blocks} blocks over "
                                    f"{world} GPU(s), {sessions} session(s) in flight",
                        "span_per_gpu": [start, end], "prefill_tokens": args.prefill,
-                       "batch": B, "wide_from": args.wide_from or 9,
+                       "batch": B, "wide_from": args.wide_from or 3,
                        "wire": ({"bytes_per_hop": pipe.wire_bytes_per_token,
                                  "relay_checksum": pipe.check is not None,
                                  "codec": "int8 codes + f32 scales per 64 (SP/quantize.py)"}
@@ -614,7 +614,7 @@ def main() -> None:
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--wide-from", type=int, default=0,
                     help="option 11: decode rows per step from which the linears run on the "
-                         "tcgen05 GEMM (0 = library default 9; 3 = throughput setting)")
+                         "weight-side tcgen05 GEMM (0 = library default 3)")
     args = ap.parse_args()
     self_launch(args)
     if args.impl == "reference":

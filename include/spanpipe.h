@@ -181,9 +181,9 @@ int sp_span_set_profiling(sp_span* span, int32_t enable);
  * (one query head per kv head; default 1); 10 = wide decode (9..32 rows) GEMM
  * with the weights as the MMA's A operand (default 1; 0 = the token-tile GEMM,
  * bit-identical); 11 = the row count from which decode runs its linears on the
- * tcgen05 GEMM instead of the GEMV (default 9: steps of 1-8 rows are
- * bit-identical per row; 3 is fastest for batched decode).  Option 0 is per
- * span; options 1-11 are kernel-selection switches shared by
+ * weight-side tcgen05 GEMM instead of the GEMV (default 3; up to 32 rows the
+ * GEMM reproduces the GEMV's numerics, so rows are bit-identical either way).
+ * Option 0 is per span; options 1-11 are kernel-selection switches shared by
  * every span in the process (set them before concurrent use). */
 int sp_span_set_option(sp_span* span, int32_t option, int32_t value);
 int sp_span_profile_read(sp_span* span, int32_t n_classes, double* ms, double* bytes,
