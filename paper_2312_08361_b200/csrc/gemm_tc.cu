@@ -1173,6 +1173,15 @@ __device__ __forceinline__ void gemv_epilogue_group(const TcGemmArgs& a, int grp
                                                     int lane, VAL vals) {
   const bool swiglu = a.epi == EPI_SWIGLU;
   const int nj = swiglu ? 2 : 4;
+  // every input of the lane first (the group's values, residuals): one round
+  // trip instead of a load -> store chain per output (res may alias y)
+  float v[4], rv[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) v[i] = vals(lane + 32 * i);
+  if (!swiglu && a.epi == EPI_RESID) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) rv[i] = a.res[m * a.ldy + (int64_t)grp * 128 + lane + 32 * i];
+  }
   float S = 0.f, Q = 0.f, M = 0.f;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
@@ -1181,11 +1190,11 @@ __device__ __forceinline__ void gemv_epilogue_group(const TcGemmArgs& a, int grp
     int64_t col;
     if (swiglu) {
       col = (int64_t)grp * 64 + lane + 32 * j;
-      val = silu_gemv(vals(lane + 32 * j)) * vals(lane + 32 * j + 64);
+      val = silu_gemv(v[j]) * v[j + 2];
     } else {
       col = (int64_t)grp * 128 + lane + 32 * j;
-      val = vals(lane + 32 * j);
-      if (a.epi == EPI_RESID) val += a.res[m * a.ldy + col];
+      val = v[j];
+      if (a.epi == EPI_RESID) val += rv[j];
       else if (a.epi == EPI_GELU) val = gelu_f(val);
     }
     a.y[m * a.ldy + col] = val;
