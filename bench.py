@@ -565,7 +565,11 @@ def run_b200(args) -> None:
                          "avg_launch_us": gemv_ms / gemv_launches * 1e3,
                          "bytes_per_launch": wbytes.value / gemv_launches,
                          "how": f"{gemv_launches} launches (4 per block) back to back x {reps}, "
-                                "CUDA events on the launching stream"},
+                                "CUDA events on the launching stream",
+                         "note": (None if B < (args.wide_from or 3) else
+                                  "at this batch the decode linears run on the weight-side "
+                                  "tcgen05 GEMM (option 11); this GEMV-only figure is not the "
+                                  "step's kernel — see step_roofline")},
             "step_roofline": {"bytes_per_tick": step_bytes / ticks,
                               "achieved_gbs": step_bytes / ticks / (rank_ms_per_tick / 1e3) / 1e9,
                               "note": "all algorithmic bytes of a step (weights+KV+activations) "

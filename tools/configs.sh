@@ -13,5 +13,7 @@ run --weights nf4
 run --config llama2-7b --prefill 128
 run --config bloom-176b --blocks 8
 run --config bloom-176b --batch 16 --blocks 8
+run --config bloom-176b --batch 8 --blocks 8
 run --batch 16 --blocks 8
+run --batch 8 --blocks 8
 run --config bloom-176b --weights nf4
