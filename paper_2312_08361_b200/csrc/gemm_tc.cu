@@ -1209,9 +1209,9 @@ __device__ __forceinline__ void gemv_epilogue_group(const TcGemmArgs& a, int grp
   }
 }
 
-// ---- wide decode (9..32 token rows, split-K): weights as the A operand -------
+// ---- wide decode (3..32 token rows, split-K): weights as the A operand -------
 // The single-CTA kernel above puts the tokens on the MMA's M = 128 rows, so at
-// decode widths of 9-32 rows 75-93 % of every MMA multiplies padding and the
+// decode widths of 3-32 rows 75-98 % of every MMA multiplies padding and the
 // tensor pipe (fed at 8 KB of shared memory per MMA) becomes the limit: BLOOM
 // batch 16 measured 77.6 % tensor-pipe active at 55 % of the HBM rate.  Here
 // the operands swap: A = one 128-channel weight unit (the same core-matrix

@@ -409,7 +409,7 @@ def test_wide_decode_token_tile_gemm(name, width):
 @pytest.mark.parametrize("name,width", [("llama_int8", 9), ("bloom_int8", 16), ("llama_g8", 12),
                                         ("llama_int8", 24), ("bloom_int8", 32), ("llama_int8", 40)])
 def test_wide_decode_vs_oracle(name, width):
-    """Decode with >= 9 rows per step runs its linears on the tcgen05 GEMM
+    """Decode with >= 3 rows per step (option 11) runs its linears on the tcgen05 GEMM
     (one pass over the weights for all rows: weight-side up to 32 rows, the
     token-tile split-K GEMM beyond) and attention on the fused decode kernel;
     every row vs the oracle at the decode tolerance."""
