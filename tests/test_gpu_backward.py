@@ -120,3 +120,89 @@ def test_dropin_finetune_session(swarmpipe):
     finally:
         swarmpipe.swarm.RealServerEngine = orig
         swarmpipe.server.RealServerEngine = orig
+
+
+def _gpu_block_backward(eng, b, x, dy):
+    """sp_span_block_backward on [batch, t, d] f32 arrays -> dx (numpy)."""
+    import torch
+    from paper_2312_08361_b200 import _lib
+    batch, t, d = x.shape
+    xd = torch.from_numpy(np.ascontiguousarray(x.reshape(-1, d))).cuda()
+    dyd = torch.from_numpy(np.ascontiguousarray(dy.reshape(-1, d))).cuda()
+    dx = torch.empty_like(xd)
+    _lib.check(eng.lib.sp_span_block_backward(eng.span.handle, b, xd.data_ptr(), dyd.data_ptr(),
+                                              dx.data_ptr(), batch, t, 0))
+    torch.cuda.synchronize()
+    return dx.cpu().numpy().reshape(batch, t, d)
+
+
+def test_block_backward_zero_grad_out():
+    """T/test_model.py:151-156: a zero output gradient gives exactly zero."""
+    from paper_2312_08361_b200.config import toy
+    from paper_2312_08361_b200.engine import B200ServerEngine
+    eng = B200ServerEngine(toy(seed=3))
+    x = np.random.default_rng(0).standard_normal((2, 4, 64)).astype(np.float32)
+    dx = _gpu_block_backward(eng, 1, x, np.zeros_like(x))
+    assert not dx.any()
+
+
+def test_block_backward_params_untouched():
+    """T/test_model.py:158-164: the backward only reads the block's weights."""
+    from paper_2312_08361_b200.config import toy
+    from paper_2312_08361_b200.engine import B200ServerEngine
+    cfg = toy(seed=3)
+    eng = B200ServerEngine(cfg)
+    roles = [r for r, _, _ in cfg.block_matrices()]
+    before = {r: eng.span.read_weight(0, r).copy() for r in roles}
+    rng = np.random.default_rng(1)
+    x = rng.standard_normal((1, 6, 64)).astype(np.float32)
+    _gpu_block_backward(eng, 0, x, rng.standard_normal(x.shape).astype(np.float32))
+    for r in roles:
+        assert np.array_equal(eng.span.read_weight(0, r), before[r]), r
+
+
+def _forward_f64(p, x, n_heads):
+    """The toy block (SP/model.py:244-280) in float64 on [1, t, d] — the
+    finite-difference loss of T/test_model.py:166-192."""
+    import oracle.model as om
+    f8 = {k: np.asarray(v, np.float64) for k, v in p.items()}
+    t, d = x.shape[1], x.shape[2]
+    hd = d // n_heads
+    h = om.ln(x, f8["ln1_g"], f8["ln1_b"])
+    q, k, v = (om._split_heads(h @ f8[w], n_heads) for w in ("wq", "wk", "wv"))
+    s = np.einsum("bhid,bhjd->bhij", q, k) / np.sqrt(hd)
+    s = np.where(np.triu(np.ones((t, t), bool), 1), -1e30, s)
+    e = np.exp(s - s.max(axis=-1, keepdims=True))
+    x1 = x + om._merge_heads((e / e.sum(axis=-1, keepdims=True)) @ v) @ f8["wo"]
+    return x1 + om.gelu(om.ln(x1, f8["ln2_g"], f8["ln2_b"]) @ f8["w1"]) @ f8["w2"]
+
+
+def test_block_backward_matches_finite_differences():
+    """T/test_model.py:166-192: the GPU gradient against central differences
+    (eps 1e-3) of a float64 forward, worst relative error <= 1e-4 over trials."""
+    sys.path.insert(0, ROOT)
+    import oracle.model as om
+    from paper_2312_08361_b200.config import toy
+    from paper_2312_08361_b200.engine import B200ServerEngine
+    eps, worst = 1e-3, 0.0
+    for trial in range(4):
+        cfg = toy(seed=trial, n_blocks=1)
+        eng = B200ServerEngine(cfg)
+        p = om.init_block(cfg, 0)
+        rng = np.random.default_rng(100 + trial)
+        x = rng.standard_normal((1, 4, 64)).astype(np.float32)
+        gy = rng.standard_normal((1, 4, 64)).astype(np.float32)
+        got = _gpu_block_backward(eng, 0, x, gy)
+        g8 = gy.astype(np.float64)
+        fd = np.zeros(x.shape)
+        for i in range(4):
+            for j in range(64):
+                up = x.astype(np.float64)
+                dn = up.copy()
+                up[0, i, j] += eps
+                dn[0, i, j] -= eps
+                fd[0, i, j] = ((g8 * _forward_f64(p, up, cfg.n_heads)).sum()
+                               - (g8 * _forward_f64(p, dn, cfg.n_heads)).sum()) / (2 * eps)
+        worst = max(worst, np.abs(got - fd).max() / max(np.abs(fd).max(), 1e-12))
+    print(f"worst relative gradient error vs finite differences {worst:.3g}")
+    assert worst <= 1e-4, worst
