@@ -43,6 +43,7 @@ namespace {
 constexpr int CL = 8;            // CTAs per (slot, kv head)
 constexpr int GM = 8;            // query heads per kv head (rows of the M = 16 tile)
 constexpr int NWMAX = 12;        // warps per CTA
+constexpr int kMinWarps = 4;     // q preparation and merges run on >= 4 warps
 constexpr float kLog2e = 1.4426950408889634f;
 
 __device__ __forceinline__ void mma16816(float* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
@@ -83,13 +84,6 @@ __device__ __forceinline__ void split2(float x0, float x1, uint32_t& hi, uint32_
   hi = pack_bf16(__bfloat162float(h0), __bfloat162float(h1));
   lo = pack_bf16(x0 - __bfloat162float(h0), x1 - __bfloat162float(h1));
 }
-__device__ __forceinline__ float rope_at(const float* x, int dd, int half, const float* cs,
-                                         const float* sn) {
-  const int j = dd % half;
-  const float c = cs[j], s = sn[j];
-  return dd < half ? __fsub_rn(__fmul_rn(x[j], c), __fmul_rn(x[j + half], s))
-                   : __fadd_rn(__fmul_rn(x[j + half], c), __fmul_rn(x[j], s));
-}
 
 // debug (SP_BUILD_TRACE=1 build + SP_ATTN_TRACE=<call>): per-CTA phase times
 __device__ __forceinline__ void cl_mark(const AttnDecArgs& a, int ph) {
@@ -123,7 +117,7 @@ __global__ void __launch_bounds__(NWMAX * 32, 1) attn_dec_cl_kernel(AttnDecArgs 
   Row* Qh = reinterpret_cast<Row*>(dsm + (size_t)2 * NW * L::KV_WARP);   // [GM]
   Row* Ql = Qh + GM;
   float* Oc = reinterpret_cast<float*>(dsm + (size_t)2 * NW * L::KV_WARP + L::Q_BYTES);  // [GM][HD]
-  float* mw = Oc + GM * HD;                       // [NWMAX][GM] warp maxima, then factors
+  float* mw = Oc + GM * HD;                       // [NWMAX][GM] warp maxima
   float* lw = mw + NWMAX * GM;                    // [NWMAX][GM] warp sums
   float* Mc = lw + NWMAX * GM;                    // [GM] CTA max
   float* Lc = Mc + GM;                            // [GM] CTA sum
@@ -170,18 +164,43 @@ __global__ void __launch_bounds__(NWMAX * 32, 1) attn_dec_cl_kernel(AttnDecArgs 
   cl_mark(a, 2);
 
   // ---- q of the kv group (RoPE at t0), hi/lo bf16, rows >= G zero ----
+  // (g, j < half) pairs; every load of a thread is issued before the first
+  // store (one L2 round trip, not one per pair)
   const float* cs = a.rope_cos ? a.rope_cos + (int64_t)a.t0 * half : nullptr;
   const float* sn = a.rope_sin ? a.rope_sin + (int64_t)a.t0 * half : nullptr;
-  for (int i = threadIdx.x; i < GM * HD; i += blockDim.x) {
-    const int g = i / HD, dd = i % HD;
-    float v = 0.f;
-    if (g < G) {
-      const float* q = qrow + (kh * G + g) * HD;
-      v = (a.family == kLlama) ? rope_at(q, dd, half, cs, sn) : q[dd];
+  const bool llama = a.family == kLlama;
+  {
+    constexpr int QI = GM * HD / 2 / (kMinWarps * 32);
+    float x0[QI], x1[QI], c0[QI], s0[QI];
+#pragma unroll
+    for (int u = 0; u < QI; ++u) {
+      const int i = threadIdx.x + u * blockDim.x, g = i / half, j = i % half;
+      x0[u] = x1[u] = 0.f;
+      c0[u] = 1.f;
+      s0[u] = 0.f;
+      if (i < GM * half && g < G) {
+        const float* q = qrow + (kh * G + g) * HD;
+        x0[u] = q[j];
+        x1[u] = q[j + half];
+        if (llama) { c0[u] = cs[j]; s0[u] = sn[j]; }
+      }
     }
-    const __nv_bfloat16 h = __float2bfloat16_rn(v);
-    Qh[g][dd] = h;
-    Ql[g][dd] = __float2bfloat16_rn(v - __bfloat162float(h));
+#pragma unroll
+    for (int u = 0; u < QI; ++u) {
+      const int i = threadIdx.x + u * blockDim.x, g = i / half, j = i % half;
+      if (i < GM * half) {
+        float v0 = x0[u], v1 = x1[u];
+        if (llama) {
+          v0 = __fsub_rn(__fmul_rn(x0[u], c0[u]), __fmul_rn(x1[u], s0[u]));
+          v1 = __fadd_rn(__fmul_rn(x1[u], c0[u]), __fmul_rn(x0[u], s0[u]));
+        }
+        const __nv_bfloat16 h0 = __float2bfloat16_rn(v0), h1 = __float2bfloat16_rn(v1);
+        Qh[g][j] = h0;
+        Qh[g][j + half] = h1;
+        Ql[g][j] = __float2bfloat16_rn(v0 - __bfloat162float(h0));
+        Ql[g][j + half] = __float2bfloat16_rn(v1 - __bfloat162float(h1));
+      }
+    }
   }
   // the new position: k (RoPE'd) and v appended to the page by the warp that
   // owns t0 (patched into its staged rows after the wait below)
@@ -197,11 +216,24 @@ __global__ void __launch_bounds__(NWMAX * 32, 1) attn_dec_cl_kernel(AttnDecArgs 
     __nv_bfloat16* vp = kp + (int64_t)a.kvh * kPageTokens * HD;
     const float* kn = qrow + a.H * HD + kh * HD;
     const float* vn = qrow + a.H * HD + a.kvh * HD + kh * HD;
+    float kv_[HD / 32], kr_[HD / 32], vv_[HD / 32], ck[HD / 32], sk[HD / 32];
+#pragma unroll
+    for (int u = 0; u < HD / 32; ++u) {
+      const int dd = lane + 32 * u, j = dd % half;
+      kv_[u] = kn[dd];
+      kr_[u] = kn[dd < half ? dd + half : dd - half];
+      vv_[u] = vn[dd];
+      if (llama) { ck[u] = cs[j]; sk[u] = sn[j]; }
+    }
 #pragma unroll
     for (int u = 0; u < HD / 32; ++u) {
       const int dd = lane + 32 * u;
-      knew[u] = __float2bfloat16_rn((a.family == kLlama) ? rope_at(kn, dd, half, cs, sn) : kn[dd]);
-      vnew[u] = __float2bfloat16_rn(vn[dd]);
+      float kx = kv_[u];
+      if (llama)   // rope_at: x[j] c - x[j+half] s  /  x[j+half] c + x[j] s
+        kx = dd < half ? __fsub_rn(__fmul_rn(kv_[u], ck[u]), __fmul_rn(kr_[u], sk[u]))
+                       : __fadd_rn(__fmul_rn(kv_[u], ck[u]), __fmul_rn(kr_[u], sk[u]));
+      knew[u] = __float2bfloat16_rn(kx);
+      vnew[u] = __float2bfloat16_rn(vv_[u]);
       kp[dd] = knew[u];
       vp[dd] = vnew[u];
     }
@@ -346,30 +378,30 @@ __global__ void __launch_bounds__(NWMAX * 32, 1) attn_dec_cl_kernel(AttnDecArgs 
     if (hB < G) { mw[warp * GM + hB] = m_run[1]; lw[warp * GM + hB] = l_run[1]; }
   }
   __syncthreads();
-  // ---- CTA merge over warps (fixed order): factors f_w = exp2(m_w - M) ----
-  if (threadIdx.x < G) {
-    const int g = threadIdx.x;
+  // ---- CTA merge over warps (fixed order): factors f_w = exp2(m_w - M),
+  // recomputed by every thread for its own head (no serial factor phase);
+  // four consecutive outputs (one head) per thread ----
+  for (int i4 = threadIdx.x; i4 < G * HD / 4; i4 += blockDim.x) {
+    const int g = i4 * 4 / HD;
     float M = -INFINITY;
     for (int w = 0; w < NW; ++w) M = fmaxf(M, mw[w * GM + g]);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     float Ls = 0.f;
+#pragma unroll 3
     for (int w = 0; w < NW; ++w) {
       const float m = mw[w * GM + g];
       const float f = (m == -INFINITY) ? 0.f : ex2_approx(m - M);
-      mw[w * GM + g] = f;
       Ls = fmaf(lw[w * GM + g], f, Ls);
+      if (f != 0.f) {
+        const float4 o = reinterpret_cast<const float4*>(Ks + w * 32)[i4];
+        acc.x = fmaf(o.x, f, acc.x);
+        acc.y = fmaf(o.y, f, acc.y);
+        acc.z = fmaf(o.z, f, acc.z);
+        acc.w = fmaf(o.w, f, acc.w);
+      }
     }
-    Mc[g] = M;
-    Lc[g] = Ls;
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < G * HD; i += blockDim.x) {
-    const int g = i / HD;
-    float acc = 0.f;
-    for (int w = 0; w < NW; ++w) {
-      const float f = mw[w * GM + g];
-      if (f != 0.f) acc = fmaf(reinterpret_cast<const float*>(Ks + w * 32)[i], f, acc);
-    }
-    Oc[i] = acc;
+    reinterpret_cast<float4*>(Oc)[i4] = acc;
+    if (i4 * 4 % HD == 0) { Mc[g] = M; Lc[g] = Ls; }
   }
   cl_mark(a, 6);
   cluster.sync();                                   // every CTA partial visible cluster-wide
@@ -408,6 +440,8 @@ __global__ void __launch_bounds__(NWMAX * 32, 1) attn_dec_cl_kernel(AttnDecArgs 
     Q = fmaf(v, v, Q);
     Mx = fmaxf(Mx, fabsf(v));
   }
+  // (relaxed: the DSMEM loads have returned — their values are used above)
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
   cl_mark(a, 8);
   if (a.st_out) {
     // fixed-order block reduction of this rank's slice statistics
@@ -422,14 +456,16 @@ __global__ void __launch_bounds__(NWMAX * 32, 1) attn_dec_cl_kernel(AttnDecArgs 
     }
   }
   cl_mark(a, 9);
-  cluster.sync();                                   // peers' shared memory read by everyone
+  // peers' shared memory read by everyone before any CTA exits (arrived right
+  // after this CTA's last DSMEM read, above)
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
   cl_mark(a, 10);
 }
 
 template <int HD>
 int launch_hd(const AttnDecArgs& a, cudaStream_t st) {
   const int T = a.t0 + 1;
-  const int nw = max(1, min(NWMAX, (T + CL * 32 - 1) / (CL * 32)));
+  const int nw = max(kMinWarps, min(NWMAX, (T + CL * 32 - 1) / (CL * 32)));
   const size_t smem = Layout<HD>::bytes(nw);
   static bool set[kMaxDevices] = {};
   const int dv = current_device();
